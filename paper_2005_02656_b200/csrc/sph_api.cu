@@ -1,0 +1,589 @@
+// sph_api.cu -- the extern "C" boundary declared in include/sph.h: validation,
+// scratch ownership, phase sequencing, grid geometry, error state, profiling.
+// Every step of the method runs in the kernels of sfc_sort.cu / physics.cu.
+#include <algorithm>
+#include <cmath>
+#include <cstring>
+#include <string>
+
+#include "sph_internal.cuh"
+
+using namespace sphb;
+
+namespace {
+
+sph_status fail(sph_ctx* c, sph_status st, const std::string& msg) {
+  if (c->status == SPH_OK) {
+    c->status = st;
+    c->err = msg;
+  }
+  return c->status;
+}
+
+#define CK(call)                                                                              \
+  do {                                                                                        \
+    cudaError_t e_ = (call);                                                                  \
+    if (e_ != cudaSuccess)                                                                    \
+      return fail(c, SPH_ERR_CUDA, std::string(#call) + ": " + cudaGetErrorString(e_));       \
+  } while (0)
+
+#define CKL()                                                                                 \
+  do {                                                                                        \
+    cudaError_t e_ = cudaGetLastError();                                                      \
+    if (e_ != cudaSuccess)                                                                    \
+      return fail(c, SPH_ERR_CUDA, std::string("kernel launch: ") + cudaGetErrorString(e_));  \
+  } while (0)
+
+// ---- B_n of Eq. 6: 1 / (4 pi int_0^2 [sinc(pi v/2)]^n v^2 dv).
+// Composite 8-point Gauss-Legendre in long double (independent of the oracle's
+// Simpson rule).
+long double sinc_pow_ld(long double v, int n) {
+  if (v >= 2.0L) return 0.0L;
+  long double x = 0.5L * 3.141592653589793238462643383279502884L * v;
+  long double s = x == 0.0L ? 1.0L : std::sin(x) / x;
+  long double r = 1.0L;
+  for (int k = 0; k < n; ++k) r *= s;
+  return r;
+}
+
+double kernel_norm(int n) {
+  static const long double gx[8] = {-0.960289856497536231683560868569473L, -0.796666477413626739591553936475830L,
+                                    -0.525532409916328985817739049189246L, -0.183434642495649804939476142360184L,
+                                    0.183434642495649804939476142360184L,  0.525532409916328985817739049189246L,
+                                    0.796666477413626739591553936475830L,  0.960289856497536231683560868569473L};
+  static const long double gw[8] = {0.101228536290376259152531354309962L, 0.222381034453374470544355994426241L,
+                                    0.313706645877887287337962201986601L, 0.362683783378361982965150449277196L,
+                                    0.362683783378361982965150449277196L, 0.313706645877887287337962201986601L,
+                                    0.222381034453374470544355994426241L, 0.101228536290376259152531354309962L};
+  const int panels = 4000;
+  long double acc = 0.0L, hw = 1.0L / panels;  // panel half-width (2 / panels / 2)
+  for (int p = 0; p < panels; ++p) {
+    long double mid = (2.0L * p + 1.0L) * hw;
+    for (int k = 0; k < 8; ++k) {
+      long double v = mid + hw * gx[k];
+      acc += gw[k] * hw * sinc_pow_ld(v, n) * v * v;
+    }
+  }
+  return (double)(1.0L / (4.0L * 3.141592653589793238462643383279502884L * acc));
+}
+
+// Maclaurin coefficients of sinc(pi sqrt(t)/2) = sum_k (-1)^k (pi^2/4)^k t^k / (2k+1)!
+void sinc_coeffs(double* poly, double* dpoly) {
+  const long double q = 3.141592653589793238462643383279502884L * 3.141592653589793238462643383279502884L / 4.0L;
+  long double ck = 1.0L;
+  long double c[kPolyTerms];
+  for (int k = 0; k < kPolyTerms; ++k) {
+    c[k] = ck;
+    ck = -ck * q / ((2.0L * (k + 1)) * (2.0L * (k + 1) + 1.0L));
+  }
+  for (int k = 0; k < kPolyTerms; ++k) poly[k] = (double)c[k];
+  for (int k = 0; k < kPolyTerms - 1; ++k) dpoly[k] = (double)((k + 1) * c[k + 1]);
+  dpoly[kPolyTerms - 1] = 0.0;
+}
+
+int bits_for(uint64_t v) {  // number of bits to hold values 0..v
+  int b = 0;
+  while (b < 64 && (v >> b)) ++b;
+  return b;
+}
+
+struct Phase {
+  sph_ctx* c;
+  int ph;
+  cudaEvent_t a = nullptr, b = nullptr;
+  Phase(sph_ctx* c_, int ph_) : c(c_), ph(ph_) {
+    if (c->prof) {
+      cudaEventCreate(&a);
+      cudaEventCreate(&b);
+      cudaEventRecord(a, c->stream);
+    }
+  }
+  void done(int launches) {
+    c->launches += launches;
+    c->phase_launches[ph] += launches;
+    if (c->prof) {
+      cudaEventRecord(b, c->stream);
+      c->pending.push_back({ph, a, b});
+      a = b = nullptr;
+    }
+  }
+  ~Phase() {
+    if (a) cudaEventDestroy(a);
+    if (b) cudaEventDestroy(b);
+  }
+};
+
+template <class T>
+sph_status dalloc(sph_ctx* c, T** p, size_t count) {
+  CK(cudaMalloc((void**)p, sizeof(T) * (count ? count : 1)));
+  return SPH_OK;
+}
+
+sph_status choose_grid(sph_ctx* c, const double* bb) {
+  const sph_params& q = c->prm;
+  const int64_t n = c->P.n;
+  Grid& g = c->grid;
+  const double hmean = bb[7] / (double)n;
+  if (!(hmean > 0.0) || !std::isfinite(hmean) || !std::isfinite(bb[6]))
+    return fail(c, SPH_ERR_NUMERIC, "non-finite or non-positive smoothing lengths");
+  for (int d = 0; d < 3; ++d) {
+    if (!std::isfinite(bb[d]) || !std::isfinite(bb[3 + d]))
+      return fail(c, SPH_ERR_NUMERIC, "non-finite particle positions");
+    if (q.periodic[d] && (bb[d] < q.box_lo[d] || bb[3 + d] >= q.box_hi[d]))
+      return fail(c, SPH_ERR_CONFIG, "particle outside the periodic box in dim " + std::to_string(d));
+  }
+  double edge = q.cell_factor * 2.0 * hmean;
+  for (int attempt = 0; attempt < 200; ++attempt) {
+    int64_t ncell = 1;
+    for (int d = 0; d < 3; ++d) {
+      double lo = q.periodic[d] ? q.box_lo[d] : bb[d];
+      double ext = q.periodic[d] ? q.box_hi[d] - q.box_lo[d] : bb[3 + d] - bb[d];
+      double ncd = std::floor(ext / edge);
+      int nc = ncd < 1.0 ? 1 : (ncd > 2097151.0 ? 2097151 : (int)ncd);
+      g.lo[d] = lo;
+      g.nc[d] = nc;
+      g.inv[d] = ext > 0.0 ? (double)nc / ext : 0.0;
+      g.L[d] = q.box_hi[d] - q.box_lo[d];
+      g.periodic[d] = q.periodic[d];
+      ncell *= nc;
+    }
+    g.ncell = ncell;
+    if (ncell <= c->s.max_cells) break;
+    edge *= 1.25;
+  }
+  if (g.ncell > c->s.max_cells) return fail(c, SPH_ERR_CAPACITY, "search grid too large");
+  int mx = std::max(g.nc[0], std::max(g.nc[1], g.nc[2]));
+  g.cbits = bits_for((uint64_t)(mx - 1));
+  g.idbits = bits_for((uint64_t)bb[8]);
+  if (3 * g.cbits + g.idbits > 64)
+    return fail(c, SPH_ERR_CONFIG, "Morton key + id exceed 64 bits");
+  return SPH_OK;
+}
+
+sph_status drain_profile(sph_ctx* c) {
+  for (auto& e : c->pending) {
+    float ms = 0.f;
+    cudaEventSynchronize(e.b);
+    cudaEventElapsedTime(&ms, e.a, e.b);
+    c->phase_ms[e.ph] += ms;
+    cudaEventDestroy(e.a);
+    cudaEventDestroy(e.b);
+  }
+  c->pending.clear();
+  return SPH_OK;
+}
+
+}  // namespace
+
+extern "C" {
+
+int sph_abi_version(void) { return SPH_ABI_VERSION; }
+
+const char* sph_error_string(const sph_ctx* c) {
+  if (!c) return "null context";
+  return c->status == SPH_OK ? "ok" : c->err.c_str();
+}
+
+sph_status sph_init(const sph_params* prm, int64_t capacity, sph_ctx** out) {
+  if (!out) return SPH_ERR_CONFIG;
+  *out = nullptr;
+  if (!prm || prm->abi_version != SPH_ABI_VERSION) return SPH_ERR_CONFIG;
+  double nexp = prm->sinc_n;
+  if (!(nexp >= 3.0 && nexp <= 9.0 && nexp == std::floor(nexp))) return SPH_ERR_CONFIG;
+  if (capacity < 1 || capacity > 0xffffffffLL) return SPH_ERR_CONFIG;
+  if (prm->nranks != 1) return SPH_ERR_CONFIG;  // multi-rank context: see sph_dist.cu
+  for (int d = 0; d < 3; ++d)
+    if (prm->periodic[d] && !(prm->box_hi[d] > prm->box_lo[d])) return SPH_ERR_CONFIG;
+  if (prm->eos != SPH_EOS_LINEAR && prm->eos != SPH_EOS_IDEAL) return SPH_ERR_CONFIG;
+
+  sph_ctx* c = new sph_ctx();
+  c->prm = *prm;
+  if (c->prm.max_neighbors <= 0) c->prm.max_neighbors = 512;
+  if (!(c->prm.cell_factor > 0.0)) c->prm.cell_factor = 1.0;
+  c->maxn = c->prm.max_neighbors;
+  c->cap = capacity;
+  c->stream = (cudaStream_t)prm->stream;
+  int dev = 0;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&c->num_sms, cudaDevAttrMultiProcessorCount, dev);
+
+  Phys& ph = c->phys;
+  ph.n = (int)nexp;
+  ph.B = kernel_norm(ph.n);
+  sinc_coeffs(ph.poly, ph.dpoly);
+  ph.eos = prm->eos;
+  ph.omega_mode = prm->omega_mode;
+  ph.alpha = prm->alpha_av;
+  ph.c0 = prm->c0;
+  ph.rho0 = prm->rho0;
+  ph.gamma = prm->gamma;
+  ph.courant = prm->courant;
+  ph.dt_growth = prm->dt_growth;
+  ph.n_target = prm->n_target;
+  ph.h_min = prm->h_min;
+  ph.h_max = prm->h_max;
+  ph.u_floor = prm->u_floor;
+  for (int d = 0; d < 3; ++d) {
+    ph.periodic[d] = prm->periodic[d];
+    ph.box_lo[d] = prm->box_lo[d];
+    ph.box_hi[d] = prm->box_hi[d];
+    ph.L[d] = prm->box_hi[d] - prm->box_lo[d];
+  }
+
+  Scratch& s = c->s;
+  const int64_t cap = capacity;
+  const int64_t nblk_rs = (cap + 4095) / 4096;
+  s.max_cells = std::max<int64_t>(1 << 16, 2 * cap);
+  sph_status st = SPH_OK;
+#define AL(p, n)                               \
+  if ((st = dalloc(c, &(p), (size_t)(n))) != SPH_OK) { \
+    sph_ctx* cc = c;                           \
+    *out = cc;                                 \
+    return st;                                 \
+  }
+  AL(s.keys, cap);
+  AL(s.keys_alt, cap);
+  AL(s.idx, cap);
+  AL(s.idx_alt, cap);
+  AL(s.hist, 256 * nblk_rs);
+  AL(s.scan_tmp, (256 * nblk_rs) / 8192 + 64);
+  AL(s.gather, 13 * cap);
+  AL(s.gather_id, cap);
+  AL(s.cell_start, s.max_cells);
+  AL(s.cell_end, s.max_cells);
+  AL(s.nbr, cap * (int64_t)c->maxn);
+  AL(s.ncount, cap);
+  AL(s.nbr_maxcount, 1);
+  AL(s.wB, cap);
+  AL(s.ih2, cap);
+  AL(s.vol, cap);
+  AL(s.rinv, cap);
+  AL(s.X, cap);
+  AL(s.red, (int64_t)c->num_sms * 64 * 9);
+  AL(s.bbox, 16);
+  AL(s.dts, DT_SLOTS);
+  AL(s.cnt, kCounters);
+  AL(s.diag, 8);
+#undef AL
+  cudaMemsetAsync(s.cnt, 0, sizeof(unsigned long long) * kCounters, c->stream);
+  cudaMemsetAsync(s.dts, 0, sizeof(double) * DT_SLOTS, c->stream);
+  cudaMemsetAsync(s.ncount, 0, sizeof(uint32_t) * cap, c->stream);
+  {
+    double inf = INFINITY;
+    unsigned long long bits;
+    memcpy(&bits, &inf, 8);
+    cudaMemcpyAsync(s.dts + DT_RAW_BITS, &bits, 8, cudaMemcpyHostToDevice, c->stream);
+    cudaStreamSynchronize(c->stream);
+  }
+  cudaError_t e = cudaGetLastError();
+  if (e != cudaSuccess) {
+    fail(c, SPH_ERR_CUDA, cudaGetErrorString(e));
+    *out = c;
+    return SPH_ERR_CUDA;
+  }
+  *out = c;
+  return SPH_OK;
+}
+
+sph_status sph_attach(sph_ctx* c, const sph_particles* p) {
+  if (!c || !p) return SPH_ERR_CONFIG;
+  if (c->status != SPH_OK) return c->status;
+  if (p->n < 0 || p->n > c->cap || p->capacity < p->n)
+    return fail(c, SPH_ERR_CAPACITY, "n exceeds the context capacity");
+  const void* ptrs[] = {p->id, p->x, p->y, p->z, p->vx, p->vy, p->vz, p->h, p->m, p->u, p->rho,
+                        p->omega, p->p, p->c, p->c11, p->c12, p->c13, p->c22, p->c23, p->c33,
+                        p->ax, p->ay, p->az, p->du, p->vsig, p->vhx, p->vhy, p->vhz, p->du_prev};
+  for (const void* q : ptrs)
+    if (!q) return fail(c, SPH_ERR_CONFIG, "null particle array");
+  c->P = *p;
+  c->attached = true;
+  c->first = true;
+  c->stage = 0;
+  c->steps = 0;
+  return SPH_OK;
+}
+
+sph_status sph_find_neighbors(sph_ctx* c) {
+  if (!c) return SPH_ERR_CONFIG;
+  if (c->status != SPH_OK) return c->status;
+  if (!c->attached) return fail(c, SPH_ERR_STATE, "no particles attached");
+  const int64_t n = c->P.n;
+  c->stage = 0;
+  if (n == 0) {
+    c->nbr_total = c->nbr_max = 0;
+    c->stage = 1;
+    return SPH_OK;
+  }
+  double bb[16];
+  {
+    Phase ph(c, SPH_PH_BBOX);
+    int k = launch_bbox(c);
+    CKL();
+    ph.done(k);
+  }
+  CK(cudaMemcpyAsync(bb, c->s.bbox, 9 * sizeof(double), cudaMemcpyDeviceToHost, c->stream));
+  CK(cudaStreamSynchronize(c->stream));
+  if (choose_grid(c, bb) != SPH_OK) return c->status;
+  const int nbits = 3 * c->grid.cbits + c->grid.idbits;
+  {
+    Phase ph(c, SPH_PH_KEYS);
+    int k = launch_keys(c);
+    CKL();
+    ph.done(k);
+  }
+  const uint32_t* perm = nullptr;
+  {
+    Phase ph(c, SPH_PH_SORT);
+    int k = launch_sort(c, nbits, &perm);
+    CKL();
+    ph.done(k);
+  }
+  {
+    Phase ph(c, SPH_PH_PERMUTE);
+    int k = launch_permute(c, perm);
+    CKL();
+    ph.done(k);
+  }
+  {
+    Phase ph(c, SPH_PH_CELLS);
+    int k = launch_cells(c);
+    CKL();
+    ph.done(k);
+  }
+  CK(cudaMemsetAsync(c->s.nbr_maxcount, 0, sizeof(unsigned int), c->stream));
+  {
+    Phase ph(c, SPH_PH_NEIGHBORS);
+    int k = launch_neighbors(c);
+    CKL();
+    ph.done(k);
+  }
+  unsigned int mc = 0;
+  CK(cudaMemcpyAsync(&mc, c->s.nbr_maxcount, sizeof(unsigned int), cudaMemcpyDeviceToHost,
+                     c->stream));
+  CK(cudaStreamSynchronize(c->stream));
+  if (mc > (unsigned)c->maxn)
+    return fail(c, SPH_ERR_CAPACITY, "a neighbour row holds " + std::to_string(mc) +
+                                         " entries > max_neighbors = " + std::to_string(c->maxn));
+  c->stage = 1;
+  return SPH_OK;
+}
+
+sph_status sph_get_neighbors(sph_ctx* c, int64_t* offsets, int64_t* ids, int64_t cap) {
+  if (!c || !offsets) return SPH_ERR_CONFIG;
+  if (c->status != SPH_OK) return c->status;
+  if (c->stage < 1) return fail(c, SPH_ERR_STATE, "sph_get_neighbors before sph_find_neighbors");
+  const int64_t n = c->P.n;
+  std::vector<uint32_t> cnt(n > 0 ? n : 1);
+  std::vector<int64_t> id(n > 0 ? n : 1);
+  CK(cudaStreamSynchronize(c->stream));
+  if (n) {
+    CK(cudaMemcpy(cnt.data(), c->s.ncount, sizeof(uint32_t) * n, cudaMemcpyDeviceToHost));
+    CK(cudaMemcpy(id.data(), c->P.id, sizeof(int64_t) * n, cudaMemcpyDeviceToHost));
+  }
+  offsets[0] = 0;
+  for (int64_t i = 0; i < n; ++i) offsets[i + 1] = offsets[i] + cnt[i];
+  if (offsets[n] > cap) return SPH_ERR_CAPACITY;  // not sticky: caller retries with room
+  if (!ids) return SPH_OK;
+  const int64_t chunk = 1 << 14;
+  std::vector<uint32_t> rows((size_t)chunk * c->maxn);
+  for (int64_t r0 = 0; r0 < n; r0 += chunk) {
+    int64_t nr = std::min(chunk, n - r0);
+    CK(cudaMemcpy(rows.data(), c->s.nbr + (size_t)r0 * c->maxn, sizeof(uint32_t) * nr * c->maxn,
+                  cudaMemcpyDeviceToHost));
+    for (int64_t i = 0; i < nr; ++i)
+      for (uint32_t k = 0; k < cnt[r0 + i]; ++k)
+        ids[offsets[r0 + i] + k] = id[rows[(size_t)i * c->maxn + k]];
+  }
+  return SPH_OK;
+}
+
+sph_status sph_density(sph_ctx* c) {
+  if (!c) return SPH_ERR_CONFIG;
+  if (c->status != SPH_OK) return c->status;
+  if (c->stage < 1) return fail(c, SPH_ERR_STATE, "sph_density before sph_find_neighbors");
+  if (c->P.n) {
+    Phase ph(c, SPH_PH_DENSITY);
+    int k = launch_density(c);
+    CKL();
+    ph.done(k);
+  }
+  c->stage = 2;
+  return SPH_OK;
+}
+
+sph_status sph_iad(sph_ctx* c) {
+  if (!c) return SPH_ERR_CONFIG;
+  if (c->status != SPH_OK) return c->status;
+  if (c->stage < 2) return fail(c, SPH_ERR_STATE, "sph_iad before sph_density");
+  if (c->P.n) {
+    Phase ph(c, SPH_PH_IAD);
+    int k = launch_iad(c);
+    CKL();
+    ph.done(k);
+  }
+  c->stage = 3;
+  return SPH_OK;
+}
+
+sph_status sph_momentum_energy(sph_ctx* c, double* dt_out) {
+  if (!c) return SPH_ERR_CONFIG;
+  if (c->status != SPH_OK) return c->status;
+  if (c->stage < 3) return fail(c, SPH_ERR_STATE, "sph_momentum_energy before sph_iad");
+  {
+    Phase ph(c, SPH_PH_MOMENTUM);
+    int k = c->P.n ? launch_momentum(c) : 0;
+    k += launch_dt_finalize(c);
+    CKL();
+    ph.done(k);
+  }
+  c->stage = 4;
+  if (dt_out) {
+    double dts[DT_SLOTS];
+    CK(cudaMemcpyAsync(dts, c->s.dts, sizeof(dts), cudaMemcpyDeviceToHost, c->stream));
+    CK(cudaStreamSynchronize(c->stream));
+    *dt_out = dts[DT_CUR];
+    if (!std::isfinite(dts[DT_CUR]) || !(dts[DT_CUR] > 0.0))
+      return fail(c, SPH_ERR_NUMERIC, "non-finite or non-positive dt");
+  }
+  return SPH_OK;
+}
+
+sph_status sph_advance(sph_ctx* c) {
+  if (!c) return SPH_ERR_CONFIG;
+  if (c->status != SPH_OK) return c->status;
+  if (c->stage < 4) return fail(c, SPH_ERR_STATE, "sph_advance before sph_momentum_energy");
+  if (c->P.n) {
+    Phase ph(c, SPH_PH_UPDATE);
+    int k = launch_update(c);
+    CKL();
+    ph.done(k);
+  }
+  c->first = false;
+  c->steps++;
+  c->stage = 0;
+  return SPH_OK;
+}
+
+sph_status sph_step(sph_ctx* c, double* dt_out) {
+  sph_status st;
+  if ((st = sph_find_neighbors(c)) != SPH_OK) return st;
+  if ((st = sph_density(c)) != SPH_OK) return st;
+  if ((st = sph_iad(c)) != SPH_OK) return st;
+  if ((st = sph_momentum_energy(c, dt_out)) != SPH_OK) return st;
+  return sph_advance(c);
+}
+
+static sph_status copy_state(sph_ctx* c, const sph_particles* host, bool up) {
+  const sph_particles& P = c->P;
+  const int64_t n = up ? host->n : P.n;
+  if (up && (n < 0 || n > c->cap || n > P.capacity))
+    return fail(c, SPH_ERR_CAPACITY, "upload: n exceeds capacity");
+  double* const dev[13] = {P.x, P.y, P.z, P.vx, P.vy, P.vz, P.h, P.m, P.u, P.vhx, P.vhy, P.vhz, P.du_prev};
+  double* const hst[13] = {host->x, host->y, host->z, host->vx, host->vy, host->vz, host->h,
+                           host->m, host->u, host->vhx, host->vhy, host->vhz, host->du_prev};
+  auto kind = up ? cudaMemcpyHostToDevice : cudaMemcpyDeviceToHost;
+  for (int k = 0; k < 13; ++k) {
+    if (!hst[k]) continue;
+    CK(cudaMemcpyAsync(up ? (void*)dev[k] : (void*)hst[k], up ? (const void*)hst[k] : (const void*)dev[k],
+                       sizeof(double) * n, kind, c->stream));
+  }
+  if (host->id)
+    CK(cudaMemcpyAsync(up ? (void*)P.id : (void*)host->id, up ? (const void*)host->id : (const void*)P.id,
+                       sizeof(int64_t) * n, kind, c->stream));
+  return SPH_OK;
+}
+
+sph_status sph_upload(sph_ctx* c, const sph_particles* host) {
+  if (!c || !host) return SPH_ERR_CONFIG;
+  if (c->status != SPH_OK) return c->status;
+  if (!c->attached) return fail(c, SPH_ERR_STATE, "no particles attached");
+  sph_status st = copy_state(c, host, true);
+  if (st != SPH_OK) return st;
+  c->P.n = host->n;
+  c->stage = 0;
+  return SPH_OK;
+}
+
+sph_status sph_download(sph_ctx* c, sph_particles* host) {
+  if (!c || !host) return SPH_ERR_CONFIG;
+  if (c->status != SPH_OK) return c->status;
+  if (!c->attached) return fail(c, SPH_ERR_STATE, "no particles attached");
+  sph_status st = copy_state(c, host, false);
+  if (st != SPH_OK) return st;
+  host->n = c->P.n;
+  CK(cudaStreamSynchronize(c->stream));
+  return SPH_OK;
+}
+
+sph_status sph_diagnostics(sph_ctx* c, sph_diag* out) {
+  if (!c || !out) return SPH_ERR_CONFIG;
+  if (c->status != SPH_OK) return c->status;
+  memset(out, 0, sizeof(*out));
+  double d[8] = {0};
+  if (c->attached && c->P.n) {
+    launch_diag(c);
+    CKL();
+    CK(cudaMemcpyAsync(d, c->s.diag, sizeof(d), cudaMemcpyDeviceToHost, c->stream));
+  }
+  unsigned long long cnt[kCounters];
+  double dts[DT_SLOTS];
+  CK(cudaMemcpyAsync(cnt, c->s.cnt, sizeof(cnt), cudaMemcpyDeviceToHost, c->stream));
+  CK(cudaMemcpyAsync(dts, c->s.dts, sizeof(dts), cudaMemcpyDeviceToHost, c->stream));
+  CK(cudaStreamSynchronize(c->stream));
+  out->n_owned = c->P.n;
+  out->n_halo = 0;
+  out->nbr_total = (int64_t)d[7];
+  out->omega_clamped = (int64_t)cnt[CNT_OMEGA];
+  out->iad_singular = (int64_t)cnt[CNT_IAD_SINGULAR];
+  out->coincident_pairs = (int64_t)cnt[CNT_COINCIDENT];
+  out->u_floored = (int64_t)cnt[CNT_U_FLOOR];
+  out->h_clamped = (int64_t)cnt[CNT_H_CLAMP];
+  out->steps = c->steps;
+  out->dt = dts[DT_CUR];
+  out->dt_prev = dts[DT_COMMITTED];
+  out->time = dts[DT_TIME];
+  for (int k = 0; k < 3; ++k) {
+    out->momentum[k] = d[k];
+    out->ang_momentum[k] = d[3 + k];
+    out->grid[k] = c->grid.nc[k];
+  }
+  out->energy = d[6];
+  if (cnt[CNT_NONFINITE]) return fail(c, SPH_ERR_NUMERIC, "non-finite dt encountered");
+  return SPH_OK;
+}
+
+sph_status sph_set_profiling(sph_ctx* c, int on) {
+  if (!c) return SPH_ERR_CONFIG;
+  c->prof = on != 0;
+  return SPH_OK;
+}
+
+sph_status sph_phase_times(sph_ctx* c, double* ms_out, int64_t* launches_out, int reset) {
+  if (!c) return SPH_ERR_CONFIG;
+  drain_profile(c);
+  for (int k = 0; k < SPH_PH_COUNT; ++k) {
+    if (ms_out) ms_out[k] = c->phase_ms[k];
+    if (launches_out) launches_out[k] = c->phase_launches[k];
+    if (reset) {
+      c->phase_ms[k] = 0.0;
+      c->phase_launches[k] = 0;
+    }
+  }
+  return SPH_OK;
+}
+
+sph_status sph_destroy(sph_ctx* c) {
+  if (!c) return SPH_OK;
+  drain_profile(c);
+  cudaStreamSynchronize(c->stream);
+  Scratch& s = c->s;
+  void* ptrs[] = {s.keys, s.keys_alt, s.idx, s.idx_alt, s.hist, s.scan_tmp, s.gather, s.gather_id,
+                  s.cell_start, s.cell_end, s.nbr, s.ncount, s.nbr_maxcount, s.wB, s.ih2, s.vol,
+                  s.rinv, s.X, s.red, s.bbox, s.dts, s.cnt, s.diag};
+  for (void* p : ptrs)
+    if (p) cudaFree(p);
+  delete c;
+  return SPH_OK;
+}
+
+}  // extern "C"

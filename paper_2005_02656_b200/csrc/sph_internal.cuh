@@ -1,0 +1,143 @@
+// sph_internal.cuh -- shared definitions of the CUDA path (sm_100a).
+//
+// Layout in HBM: every per-particle quantity is its own fp64
+// array (SoA) in Morton-cell order; neighbour lists are uint32 rows of fixed
+// stride `maxn` (row-major: the warp that owns a target reads its row with
+// coalesced 128-byte loads); the search grid is a dense table of cell ranges
+// [cell_start, cell_end) into the sorted order.
+#pragma once
+
+#include <cuda_runtime.h>
+
+#include <cstdint>
+#include <cstdio>
+#include <string>
+#include <vector>
+
+#include "../../include/sph.h"
+
+namespace sphb {
+
+constexpr int kPolyTerms = 13;   // Maclaurin terms of sinc(pi sqrt(t) / 2) in t = v^2
+constexpr int kCounters = 8;     // device event counters (see enum below)
+enum { CNT_OMEGA = 0, CNT_IAD_SINGULAR, CNT_COINCIDENT, CNT_U_FLOOR, CNT_H_CLAMP, CNT_NONFINITE };
+
+// Search grid (a3).  Identical formula on every rank (derived from the global bbox).
+struct Grid {
+  double lo[3];     // origin of cell 0 per dim
+  double inv[3];    // cells per unit length (nc / extent); 0 when nc == 1 and extent == 0
+  double L[3];      // period of periodic dims (box_hi - box_lo)
+  int nc[3];        // cells per dim
+  int periodic[3];
+  int cbits;        // Morton bits per dim
+  int idbits;       // id bits below the Morton code in the sort key
+  int64_t ncell;
+};
+
+// Physics constants by value (kernel parameter space = constant bank).
+struct Phys {
+  double B;                 // B_n of Eq. 6
+  double poly[kPolyTerms];  // P(t) = sum_k poly[k] t^k = sinc(pi sqrt(t) / 2)
+  double dpoly[kPolyTerms]; // P'(t)
+  int n;                    // integer kernel exponent
+  int eos, omega_mode;
+  double alpha, c0, rho0, gamma, courant, dt_growth, n_target, h_min, h_max, u_floor;
+  double L[3];
+  int periodic[3];
+  double box_lo[3], box_hi[3];
+};
+
+// Device-side scalars of the integrator: written by kernels, read by kernels.
+enum { DT_RAW_BITS = 0, DT_CUR = 1, DT_PREV = 2, DT_COMMITTED = 3, DT_TIME = 4, DT_SLOTS = 8 };
+
+struct Scratch {
+  // sort
+  uint64_t* keys = nullptr;
+  uint64_t* keys_alt = nullptr;
+  uint32_t* idx = nullptr;
+  uint32_t* idx_alt = nullptr;
+  uint32_t* hist = nullptr;      // 256 * nblk
+  uint32_t* scan_tmp = nullptr;  // block sums for the scan
+  double* gather = nullptr;      // 13 * cap doubles (permutation staging)
+  int64_t* gather_id = nullptr;  // cap
+  // cells
+  uint32_t* cell_start = nullptr;
+  uint32_t* cell_end = nullptr;
+  int64_t max_cells = 0;
+  // neighbours
+  uint32_t* nbr = nullptr;       // cap * maxn
+  uint32_t* ncount = nullptr;    // cap
+  unsigned int* nbr_maxcount = nullptr;  // device scalar
+  // per-particle auxiliaries written by density, read by iad / momentum
+  double* wB = nullptr;    // B / h^3
+  double* ih2 = nullptr;   // 1 / h^2
+  double* vol = nullptr;   // m / rho
+  double* rinv = nullptr;  // 1 / rho
+  double* X = nullptr;     // P / (Omega rho^2)   (reading R1)
+  // reductions
+  double* red = nullptr;   // block partials
+  double* bbox = nullptr;  // 8 doubles (device)
+  double* dts = nullptr;   // DT_SLOTS
+  unsigned long long* cnt = nullptr;  // kCounters
+  double* diag = nullptr;  // 8
+};
+
+struct PhaseEv {
+  int ph;
+  cudaEvent_t a, b;
+};
+
+}  // namespace sphb
+
+struct sph_ctx {
+  sph_params prm;
+  cudaStream_t stream = nullptr;
+  int64_t cap = 0;
+  int maxn = 512;
+  sph_particles P{};
+  bool attached = false;
+  int stage = 0;            // 0 none, 1 neighbours, 2 density, 3 iad, 4 momentum
+  bool first = true;        // next advance is the integrator's first step
+  int64_t steps = 0;
+  sphb::Grid grid{};
+  sphb::Phys phys{};
+  sphb::Scratch s;
+  int nblk_red = 0;
+  int num_sms = 148;
+  int64_t nbr_total = 0;
+  int64_t nbr_max = 0;
+  sph_status status = SPH_OK;
+  std::string err;
+  // profiling
+  bool prof = false;
+  std::vector<sphb::PhaseEv> pending;
+  double phase_ms[SPH_PH_COUNT] = {0};
+  int64_t phase_launches[SPH_PH_COUNT] = {0};
+  int64_t launches = 0;
+};
+
+namespace sphb {
+
+// ---- launchers (each returns the number of kernels it launched) ----
+int launch_bbox(sph_ctx* c);
+int launch_keys(sph_ctx* c);
+int launch_sort(sph_ctx* c, int nbits, const uint32_t** perm_out);
+int launch_permute(sph_ctx* c, const uint32_t* perm);
+int launch_cells(sph_ctx* c);
+int launch_neighbors(sph_ctx* c);
+int launch_density(sph_ctx* c);
+int launch_iad(sph_ctx* c);
+int launch_momentum(sph_ctx* c);
+int launch_dt_finalize(sph_ctx* c);
+int launch_update(sph_ctx* c);
+int launch_diag(sph_ctx* c);
+
+inline int grid_blocks(const sph_ctx* c, int64_t work_items, int threads, int per_sm) {
+  int64_t b = (work_items + threads - 1) / threads;
+  int64_t mx = (int64_t)c->num_sms * per_sm;
+  if (b > mx) b = mx;
+  if (b < 1) b = 1;
+  return (int)b;
+}
+
+}  // namespace sphb

@@ -1,0 +1,79 @@
+"""CPU checks of the boundary: the library builds for sm_100a, loads, and exports
+every entry point include/sph.h declares; the CUDA path and the oracle share no
+code and never import each other (no CPU fallback on the product path)."""
+import ctypes
+import os
+import re
+import subprocess
+
+import pytest
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+
+
+def declared_symbols():
+    src = open(os.path.join(ROOT, "include", "sph.h")).read()
+    return sorted(set(re.findall(r"^\s*(?:sph_status|int|const char\*)\s+(sph_[a-z_]+)\s*\(", src,
+                                 re.M)))
+
+
+@pytest.fixture(scope="module")
+def libpath():
+    from paper_2005_02656_b200 import _build
+    return _build.build()
+
+
+def test_header_declares_north_star_calls():
+    syms = declared_symbols()
+    for s in ("sph_init", "sph_find_neighbors", "sph_density", "sph_iad", "sph_momentum_energy",
+              "sph_step"):
+        assert s in syms
+
+
+def test_library_exports_every_declared_symbol(libpath):
+    out = subprocess.run(["nm", "-D", "--defined-only", libpath], capture_output=True, text=True,
+                         check=True).stdout
+    exported = set(re.findall(r" T (sph_\w+)", out))
+    missing = [s for s in declared_symbols() if s not in exported]
+    assert not missing, missing
+
+
+def test_library_loads_and_reports_abi(libpath):
+    from paper_2005_02656_b200 import sph
+    L = sph.lib()
+    assert L.sph_abi_version() == sph.ABI_VERSION
+    for s in declared_symbols():
+        assert hasattr(L, s)
+
+
+def test_init_rejects_bad_params_without_gpu(libpath):
+    """Validation happens before any device call: a bad exponent / ABI is SPH_ERR_CONFIG."""
+    from paper_2005_02656_b200 import inputs, sph
+    d = inputs.square_patch(4, 4)
+    p = sph.make_params(d, n=6.5)
+    ctx = ctypes.c_void_p()
+    assert sph.lib().sph_init(ctypes.byref(p), 64, ctypes.byref(ctx)) == 2
+    p = sph.make_params(d)
+    p.abi_version = 99
+    assert sph.lib().sph_init(ctypes.byref(p), 64, ctypes.byref(ctx)) == 2
+    assert not ctx.value
+
+
+def test_sass_is_sm100a(libpath):
+    out = subprocess.run(["cuobjdump", "--list-elf", libpath], capture_output=True, text=True).stdout
+    assert "sm_100a" in out
+
+
+def test_no_shared_code_between_oracle_and_cuda_path():
+    pkg = os.path.join(ROOT, "paper_2005_02656_b200")
+    for dirpath, _, files in os.walk(pkg):
+        for f in files:
+            if f.endswith((".py", ".cu", ".cuh", ".h")):
+                s = open(os.path.join(dirpath, f)).read()
+                assert not re.search(r"^\s*(import|from)\s+oracle\b", s, re.M), f
+                assert "sph_oracle" not in s, f
+    for f in os.listdir(os.path.join(ROOT, "oracle")):
+        if f.endswith((".py", ".c", ".h")):
+            s = open(os.path.join(ROOT, "oracle", f)).read()
+            assert not re.search(r"^\s*(import|from)\s+paper_2005_02656_b200", s, re.M), f
+            assert not re.search(r'#include\s+["<].*(sph\.h|csrc)', s), f

@@ -1,0 +1,209 @@
+"""GPU <-> oracle parity through the C ABI (-m gpu).  Every comparison feeds the
+SAME generated input to both sides; tolerances in tests/parity_util.py."""
+import ctypes
+
+import numpy as np
+import pytest
+
+from paper_2005_02656_b200 import inputs as I
+from tests import parity_util as U
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.fixture(scope="module")
+def S():
+    import torch
+    if not torch.cuda.is_available():
+        pytest.skip("no GPU")
+    from paper_2005_02656_b200 import _build, sph
+    _build.build()
+    return sph
+
+
+@pytest.fixture(scope="module")
+def O(oracle_mod):
+    return oracle_mod
+
+
+def per_call_parity(S, O, d, method=1, **kw):
+    """find -> density -> iad -> momentum -> advance, each compared with the oracle
+    on the GPU's own (sorted) state."""
+    sim = S.Simulation(d, **kw)
+    sim.find_neighbors()
+    st = U.with_meta(sim.state(), d)
+    # the permutation keeps every particle: same ids, same fields
+    assert np.array_equal(np.sort(st["id"]), np.sort(d["id"]))
+    off_g, ids_g = sim.get_neighbors()
+    o, off, nbr, dn, C, me = U.oracle_pipeline(O, st, method)
+    U.assert_neighbors_equal(off_g, ids_g, off, st["id"][nbr])
+    sim.density()
+    U.check_density(sim.dev.numpy(("rho", "omega", "p", "c")), dn, d)
+    sim.iad()
+    U.check_iad(sim.dev.numpy(("c11", "c12", "c13", "c22", "c23", "c33")), C)
+    dt = sim.momentum_energy(want_dt=True)
+    g = sim.dev.numpy(("ax", "ay", "az", "du", "vsig"))
+    U.check_momentum(g, me)
+    dt_o = o.timestep(st["h"], me["vsig"], 0.0, True)
+    assert abs(dt - dt_o) <= 1e-12 * dt_o
+    # elementwise update from identical inputs (GPU's a, du, dt)
+    ref = {k: st[k].copy() for k in ("x", "y", "z", "vx", "vy", "vz", "u", "h")}
+    for k in ("vhx", "vhy", "vhz", "du_prev"):
+        ref[k] = np.zeros_like(st["x"])
+    o.update(ref, g, dt, dt, True)
+    o.update_h(ref["h"], off)
+    sim.advance()
+    after = sim.dev.numpy()
+    amag = np.sqrt(g["ax"] ** 2 + g["ay"] ** 2 + g["az"] ** 2)
+    vmag = np.sqrt(st["vx"] ** 2 + st["vy"] ** 2 + st["vz"] ** 2)
+    for k in ("x", "y", "z", "vx", "vy", "vz", "vhx", "vhy", "vhz", "u", "h", "du_prev"):
+        if k in ("x", "y", "z"):
+            scale = np.abs(ref[k]) + dt * (vmag + dt * amag)
+        elif k in ("u", "du_prev"):
+            scale = np.abs(ref[k]) + np.abs(st["u"]) + dt * np.abs(g["du"])
+        elif k == "h":
+            scale = np.abs(ref[k])
+        else:
+            scale = np.abs(ref[k]) + vmag + dt * amag
+        U._viol(f"update {k}", after[k] - ref[k], 1e-14 * scale + 1e-300)
+    return sim, o
+
+
+def test_config1_square_patch_per_call(S, O):
+    per_call_parity(S, O, I.square_patch(20))
+
+
+def test_jittered_shuffled_patch(S, O):
+    d = I.shuffled(I.jitter(I.square_patch(14, 10)))
+    per_call_parity(S, O, d)
+
+
+def test_random_cloud_variable_h_periodic_xz(S, O):
+    d = I.random_cloud(3000, box=9.0, h0=0.8, hspread=0.2, periodic=(1, 0, 1))
+    per_call_parity(S, O, d)
+
+
+def test_evrard_shaped_variable_h(S, O):
+    per_call_parity(S, O, I.evrard(36))
+
+
+def test_pressure_ics_and_half_cells(S, O):
+    d = I.square_patch(16, 12, pressure_ics=True)
+    per_call_parity(S, O, d, cell_factor=0.5)
+
+
+def test_brute_force_small_and_ragged(S, O):
+    # ragged sizes: not multiples of a warp / tile
+    for n in (1, 2, 33, 257):
+        d = I.random_cloud(n, box=3.0, h0=0.9, periodic=(0, 0, 1), seed=n)
+        sim = S.Simulation(d)
+        sim.find_neighbors()
+        st = U.with_meta(sim.state(), d)
+        off_g, ids_g = sim.get_neighbors()
+        o = O.Oracle(O.Params.from_inputs(st))
+        off, nbr = o.neighbors(st, 0)
+        U.assert_neighbors_equal(off_g, ids_g, off, st["id"][nbr])
+        sim.density()
+        sim.iad()
+        sim.momentum_energy(want_dt=True)
+        sim.advance()
+
+
+def test_shuffle_invariance_bit_exact(S, O):
+    """Canonical (Morton cell, id) order: any input order gives bit-identical results."""
+    d = I.jitter(I.square_patch(12, 12))
+    outs = []
+    for dd in (d, I.shuffled(d, seed=1), I.shuffled(d, seed=2)):
+        sim = S.Simulation(dd)
+        dt = sim.step(want_dt=True)
+        outs.append((dt, sim.state()))
+    for dt, st in outs[1:]:
+        assert dt == outs[0][0]
+        for k in ("id", "x", "y", "z", "vx", "vy", "vz", "u", "h", "rho", "ax", "du"):
+            assert np.array_equal(st[k], outs[0][1][k]), k
+
+
+def test_edge_cases_and_errors(S, O):
+    import torch
+    # empty
+    d = I.random_cloud(4, box=3.0)
+    d0 = I.subset(d, np.arange(0))
+    sim = S.Simulation(d0, capacity=16)
+    sim.step()
+    # out-of-order call -> SPH_ERR_STATE (sticky)
+    sim2 = S.Simulation(d)
+    with pytest.raises(S.SphError) as e:
+        sim2.iad()
+    assert e.value.status == 6
+    # neighbour-row overflow -> SPH_ERR_CAPACITY, never silent truncation
+    sim3 = S.Simulation(I.square_patch(10, 10), max_neighbors=64)
+    with pytest.raises(S.SphError) as e:
+        sim3.find_neighbors()
+    assert e.value.status == 3
+    # coincident pair: counted, skipped in momentum
+    d = I.random_cloud(50, box=3.0, h0=0.9)
+    d["x"][1], d["y"][1], d["z"][1] = d["x"][0], d["y"][0], d["z"][0]
+    sim4 = S.Simulation(d)
+    sim4.step()
+    assert sim4.diagnostics()["coincident_pairs"] == 2
+    torch.cuda.synchronize()
+
+
+def test_shadowed_multistep_config1(S, O):
+    """20 steps; before each step the oracle is re-synced from the GPU state (T2)."""
+    d = I.square_patch(20)
+    sim = S.Simulation(d)
+    dt_prev, first = 0.0, True
+    for step in range(20):
+        st = U.with_meta(sim.state(), d)
+        st["dt_prev"], st["first"] = dt_prev, first
+        o = O.Oracle(O.Params.from_inputs(st))
+        r = o.step(st)
+        dt = sim.step(want_dt=True)
+        assert abs(dt - r["dt"]) <= 1e-12 * r["dt"], (step, dt, r["dt"])
+        after = sim.state()
+        pos = np.argsort(after["id"])
+        ref = np.argsort(st["id"])
+        g = {k: after[k][pos] for k in after}
+        rs = {k: r["state"][k][ref] for k in ("x", "y", "z", "vx", "vy", "vz", "u", "h")}
+        for k in ("x", "y", "z"):
+            assert np.max(np.abs(g[k] - rs[k])) <= 1e-12 * 100.0, (step, k)
+        for k in ("vx", "vy", "vz"):
+            vs = np.abs(rs["vx"]) + np.abs(rs["vy"]) + 1.0
+            assert np.all(np.abs(g[k] - rs[k]) <= 1e-9 * vs), (step, k)
+        assert np.max(np.abs(g["h"] - rs["h"]) / rs["h"]) <= 1e-14
+        dt_prev, first = dt, False
+    diag = sim.diagnostics()
+    assert diag["steps"] == 20 and diag["omega_clamped"] == 0 and diag["iad_singular"] == 0
+
+
+def test_conservation_on_gpu(S, O):
+    """Uniform h: sum m a and the energy rate vanish to round-off on the GPU outputs."""
+    d = I.jitter(I.square_patch(16, 16))
+    d["vx"] = d["vx"] - 2.0 * d["x"]
+    sim = S.Simulation(d)
+    sim.find_neighbors()
+    sim.density()
+    sim.iad()
+    sim.momentum_energy()
+    st = U.with_meta(sim.state(), d)
+    o, off, nbr, dn, C, me = U.oracle_pipeline(O, st)
+    m = st["m"]
+    for k, ax in enumerate(("ax", "ay", "az")):
+        assert abs(np.sum(m * st[ax])) <= 1e-12 * np.sum(m * me["scale_a"][k])
+    e = np.sum(m * (st["du"] + st["vx"] * st["ax"] + st["vy"] * st["ay"] + st["vz"] * st["az"]))
+    sc = np.sum(m * (me["scale_du"] + np.abs(st["vx"]) * me["scale_a"][0] +
+                     np.abs(st["vy"]) * me["scale_a"][1] + np.abs(st["vz"]) * me["scale_a"][2]))
+    assert abs(e) <= 1e-12 * sc
+
+
+def test_upload_download_roundtrip(S, O):
+    d = I.square_patch(10, 10)
+    sim = S.Simulation(d)
+    host = S.HostParticles(d)
+    sim.upload(host)
+    sim.step()
+    sim.download(host)
+    st = sim.state()
+    for k in ("x", "vx", "h", "u", "id"):
+        assert np.array_equal(host.t[k][:host.n].numpy(), st[k])
