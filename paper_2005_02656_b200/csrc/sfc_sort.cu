@@ -359,21 +359,58 @@ __device__ __forceinline__ int64_t key_cell(const Grid& g, uint64_t key) {
 }
 
 __global__ void k_cells(const uint64_t* __restrict__ keys, int64_t n, Grid g,
-                        uint32_t* __restrict__ cstart, uint32_t* __restrict__ cend) {
+                        uint32_t* __restrict__ cstart, uint32_t* __restrict__ cend,
+                        uint32_t* __restrict__ flag) {
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
        i += (int64_t)gridDim.x * blockDim.x) {
     int64_t c = key_cell(g, keys[i]);
-    if (i == 0 || key_cell(g, keys[i - 1]) != c) cstart[c] = (uint32_t)i;
+    const bool head = i == 0 || key_cell(g, keys[i - 1]) != c;
+    if (head) cstart[c] = (uint32_t)i;
     if (i == n - 1 || key_cell(g, keys[i + 1]) != c) cend[c] = (uint32_t)(i + 1);
+    flag[i] = head ? 1u : 0u;
+  }
+}
+
+// non-empty cells in Morton order (deterministic: rank = exclusive scan of heads)
+__global__ void k_cell_list(const uint64_t* __restrict__ keys, int64_t n, Grid g,
+                            const uint32_t* __restrict__ flag, const uint32_t* __restrict__ rank,
+                            uint32_t* __restrict__ list, uint32_t* __restrict__ nlist) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    if (flag[i]) list[rank[i]] = (uint32_t)key_cell(g, keys[i]);
+    if (i == n - 1) *nlist = rank[i] + flag[i];
+  }
+}
+
+// max h per non-empty cell (one warp per cell): sets the cell's stencil radius
+__global__ void k_cell_hmax(const uint32_t* __restrict__ list, const uint32_t* __restrict__ nlist,
+                            const uint32_t* __restrict__ cstart, const uint32_t* __restrict__ cend,
+                            const double* __restrict__ h, unsigned long long* __restrict__ chmax) {
+  const int lane = threadIdx.x & 31;
+  const uint32_t nl = *nlist;
+  for (uint32_t w = (blockIdx.x * blockDim.x + threadIdx.x) >> 5; w < nl;
+       w += (gridDim.x * blockDim.x) >> 5) {
+    const uint32_t c = list[w];
+    double m = 0.0;
+    for (uint32_t i = cstart[c] + lane; i < cend[c]; i += 32) m = fmax(m, h[i]);
+    m = warp_max(m);
+    if (lane == 0) chmax[c] = (unsigned long long)__double_as_longlong(m);
   }
 }
 
 int launch_cells(sph_ctx* c) {
+  const int64_t n = c->P.n;
   cudaMemsetAsync(c->s.cell_start, 0, sizeof(uint32_t) * c->grid.ncell, c->stream);
   cudaMemsetAsync(c->s.cell_end, 0, sizeof(uint32_t) * c->grid.ncell, c->stream);
-  k_cells<<<grid_blocks(c, c->P.n, 256, 8), 256, 0, c->stream>>>(c->s.keys, c->P.n, c->grid,
-                                                                c->s.cell_start, c->s.cell_end);
-  return 1;
+  const int nb = grid_blocks(c, n, 256, 8);
+  k_cells<<<nb, 256, 0, c->stream>>>(c->s.keys, n, c->grid, c->s.cell_start, c->s.cell_end,
+                                     c->s.cell_flag);
+  int k = 1 + scan_excl(c, c->s.cell_flag, c->s.cell_rank, n);
+  k_cell_list<<<nb, 256, 0, c->stream>>>(c->s.keys, n, c->grid, c->s.cell_flag, c->s.cell_rank,
+                                         c->s.cell_list, c->s.ncell_list);
+  k_cell_hmax<<<grid_blocks(c, n, 256, 8), 256, 0, c->stream>>>(
+      c->s.cell_list, c->s.ncell_list, c->s.cell_start, c->s.cell_end, c->P.h, c->s.cell_hmax);
+  return k + 2;
 }
 
 }  // namespace sphb

@@ -6,7 +6,7 @@
 #include <cstring>
 #include <string>
 
-#include "sph_internal.cuh"
+#include "stencil.cuh"
 
 using namespace sphb;
 
@@ -148,7 +148,11 @@ sph_status choose_grid(sph_ctx* c, const double* bb) {
       ncell *= nc;
     }
     g.ncell = ncell;
-    if (ncell <= c->s.max_cells) break;
+    // the largest stencil (cell holding h_max) must fit kKMax slots
+    int64_t K = 1;
+    for (int d = 0; d < 3; ++d)
+      K *= std::min<int64_t>(2 * stencil_radius(g, d, reach_of(bb[6])) + 1, g.nc[d]);
+    if (ncell <= c->s.max_cells && K <= kKMax) break;
     edge *= 1.25;
   }
   if (g.ncell > c->s.max_cells) return fail(c, SPH_ERR_CAPACITY, "search grid too large");
@@ -246,11 +250,18 @@ sph_status sph_init(const sph_params* prm, int64_t capacity, sph_ctx** out) {
   AL(s.idx, cap);
   AL(s.idx_alt, cap);
   AL(s.hist, 256 * nblk_rs);
-  AL(s.scan_tmp, (256 * nblk_rs) / 8192 + 64);
+  AL(s.scan_tmp, (256 * nblk_rs + cap) / 8192 + 1024);
   AL(s.gather, 13 * cap);
   AL(s.gather_id, cap);
   AL(s.cell_start, s.max_cells);
   AL(s.cell_end, s.max_cells);
+  AL(s.cell_hmax, s.max_cells);
+  AL(s.cell_flag, cap);
+  AL(s.cell_rank, cap);
+  AL(s.cell_list, cap);
+  AL(s.ncell_list, 1);
+  AL(s.mX, cap);
+  AL(s.ct, 6 * cap);
   AL(s.nbr, cap * (int64_t)c->maxn);
   AL(s.ncount, cap);
   AL(s.nbr_maxcount, 1);
@@ -384,15 +395,37 @@ sph_status sph_get_neighbors(sph_ctx* c, int64_t* offsets, int64_t* ids, int64_t
   for (int64_t i = 0; i < n; ++i) offsets[i + 1] = offsets[i] + cnt[i];
   if (offsets[n] > cap) return SPH_ERR_CAPACITY;  // not sticky: caller retries with room
   if (!ids) return SPH_OK;
+  // rows hold packed (stencil slot, local) entries: decode with the cell tables
+  const Grid& g = c->grid;
+  std::vector<uint64_t> keys(n);
+  std::vector<uint32_t> cs(g.ncell), ce(g.ncell);
+  std::vector<unsigned long long> chm(g.ncell);
+  CK(cudaMemcpy(keys.data(), c->s.keys, sizeof(uint64_t) * n, cudaMemcpyDeviceToHost));
+  CK(cudaMemcpy(cs.data(), c->s.cell_start, sizeof(uint32_t) * g.ncell, cudaMemcpyDeviceToHost));
+  CK(cudaMemcpy(ce.data(), c->s.cell_end, sizeof(uint32_t) * g.ncell, cudaMemcpyDeviceToHost));
+  CK(cudaMemcpy(chm.data(), c->s.cell_hmax, sizeof(unsigned long long) * g.ncell,
+                cudaMemcpyDeviceToHost));
   const int64_t chunk = 1 << 14;
   std::vector<uint32_t> rows((size_t)chunk * c->maxn);
   for (int64_t r0 = 0; r0 < n; r0 += chunk) {
     int64_t nr = std::min(chunk, n - r0);
     CK(cudaMemcpy(rows.data(), c->s.nbr + (size_t)r0 * c->maxn, sizeof(uint32_t) * nr * c->maxn,
                   cudaMemcpyDeviceToHost));
-    for (int64_t i = 0; i < nr; ++i)
-      for (uint32_t k = 0; k < cnt[r0 + i]; ++k)
-        ids[offsets[r0 + i] + k] = id[rows[(size_t)i * c->maxn + k]];
+    for (int64_t i = 0; i < nr; ++i) {
+      const int64_t cell = key_cell_hd(g, keys[r0 + i]);
+      int c3[3];
+      cell_coords(g, cell, c3);
+      double hm;
+      memcpy(&hm, &chm[cell], sizeof(double));
+      Stencil st;
+      make_stencil(g, c3, reach_of(hm), st);
+      for (uint32_t k = 0; k < cnt[r0 + i]; ++k) {
+        const uint32_t e = rows[(size_t)i * c->maxn + k];
+        int sh[3];
+        const int64_t sc = slot_cell(g, st, (int)(e >> kLocalBits), sh);
+        ids[offsets[r0 + i] + k] = id[cs[sc] + (e & kLocalMask)];
+      }
+    }
   }
   return SPH_OK;
 }
@@ -578,8 +611,9 @@ sph_status sph_destroy(sph_ctx* c) {
   cudaStreamSynchronize(c->stream);
   Scratch& s = c->s;
   void* ptrs[] = {s.keys, s.keys_alt, s.idx, s.idx_alt, s.hist, s.scan_tmp, s.gather, s.gather_id,
-                  s.cell_start, s.cell_end, s.nbr, s.ncount, s.nbr_maxcount, s.wB, s.ih2, s.vol,
-                  s.rinv, s.X, s.red, s.bbox, s.dts, s.cnt, s.diag};
+                  s.cell_start, s.cell_end, s.cell_hmax, s.cell_flag, s.cell_rank, s.cell_list,
+                  s.ncell_list, s.nbr, s.ncount, s.nbr_maxcount, s.wB, s.ih2, s.vol, s.rinv, s.X,
+                  s.mX, s.ct, s.red, s.bbox, s.dts, s.cnt, s.diag};
   for (void* p : ptrs)
     if (p) cudaFree(p);
   delete c;

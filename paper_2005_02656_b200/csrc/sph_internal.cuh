@@ -63,6 +63,11 @@ struct Scratch {
   // cells
   uint32_t* cell_start = nullptr;
   uint32_t* cell_end = nullptr;
+  unsigned long long* cell_hmax = nullptr;  // bit pattern of max h in the cell (h > 0)
+  uint32_t* cell_flag = nullptr;            // cap: 1 at the first particle of a cell
+  uint32_t* cell_rank = nullptr;            // cap: exclusive scan of cell_flag
+  uint32_t* cell_list = nullptr;            // non-empty cells in Morton order
+  uint32_t* ncell_list = nullptr;           // device scalar
   int64_t max_cells = 0;
   // neighbours
   uint32_t* nbr = nullptr;       // cap * maxn
@@ -74,6 +79,8 @@ struct Scratch {
   double* vol = nullptr;   // m / rho
   double* rinv = nullptr;  // 1 / rho
   double* X = nullptr;     // P / (Omega rho^2)   (reading R1)
+  double* mX = nullptr;    // m P / (Omega rho^2)
+  double* ct = nullptr;    // 6 x cap: (B/h^3) C, written by IAD, staged by momentum
   // reductions
   double* red = nullptr;   // block partials
   double* bbox = nullptr;  // 8 doubles (device)

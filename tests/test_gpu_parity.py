@@ -160,11 +160,15 @@ def test_shadowed_multistep_config1(S, O):
         o = O.Oracle(O.Params.from_inputs(st))
         r = o.step(st)
         dt = sim.step(want_dt=True)
-        assert abs(dt - r["dt"]) <= 1e-12 * r["dt"], (step, dt, r["dt"])
         after = sim.state()
         pos = np.argsort(after["id"])
         ref = np.argsort(st["id"])
         g = {k: after[k][pos] for k in after}
+        # rates of this step (outputs stay in the step's sorted order, map by id)
+        U.check_density(g, {k: v[ref] for k, v in r["dens"].items()}, d)
+        acc = {k: (v[:, ref] if k == "scale_a" else v[ref]) for k, v in r["acc"].items()}
+        U.check_momentum(g, acc)
+        assert abs(dt - r["dt"]) <= 1e-12 * r["dt"], (step, dt, r["dt"])
         rs = {k: r["state"][k][ref] for k in ("x", "y", "z", "vx", "vy", "vz", "u", "h")}
         for k in ("x", "y", "z"):
             assert np.max(np.abs(g[k] - rs[k])) <= 1e-12 * 100.0, (step, k)
@@ -175,6 +179,17 @@ def test_shadowed_multistep_config1(S, O):
         dt_prev, first = dt, False
     diag = sim.diagnostics()
     assert diag["steps"] == 20 and diag["omega_clamped"] == 0 and diag["iad_singular"] == 0
+
+
+def test_per_call_parity_after_gpu_evolution(S, O):
+    """Per-call parity on a state the GPU itself evolved (non-rigid flow, grown h at the
+    free surface, AV active)."""
+    d = I.square_patch(20)
+    sim = S.Simulation(d)
+    for _ in range(3):
+        sim.step()
+    st = U.with_meta(sim.state(), d)
+    per_call_parity(S, O, st)
 
 
 def test_conservation_on_gpu(S, O):
