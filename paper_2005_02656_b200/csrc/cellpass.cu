@@ -1,32 +1,45 @@
 // cellpass.cu -- a5 neighbour search, a6 density + Omega + EOS, a8 IAD and
 // a10-a11 momentum + energy + AV + dt, each as ONE CTA PER SEARCH CELL.
 //
-// Why: the per-target gathers of the warp-per-target kernels are latency bound
-// (ncu, profiles/r1_ncu_v1_1m.md: long-scoreboard stalls, 16 warps/SM).  Here a
-// CTA owns a cell of ~72 targets, stages the source particles of the cell's
-// stencil into shared memory with coalesced loads (each cell is a contiguous
-// range of the Morton order), and lets one warp per target walk the target's
-// neighbour row with lanes striding over entries.  Every source particle is
-// read from L2/HBM once per target CELL instead of once per pair.
+// A CTA owns a search cell (~72 targets at the paper's 300 neighbours), stages
+// the source particles of the cell's stencil into shared memory with coalesced
+// loads (each cell is a contiguous range of the Morton order; periodic images
+// are shifted at staging time, so no pair needs a minimum image), and one warp
+// per target walks the target's neighbour row, lanes striding over entries.
+// Every source particle is read from L2/HBM once per target CELL instead of once
+// per pair (profiles/r1_ncu_summary.md has the measurements behind this).
 //
-// Neighbour rows hold packed entries (slot << 20 | local) -> the shared-memory
-// index of a neighbour is slot_off[slot] + local: no search, no global gather.
+// Neighbour rows hold packed entries (slot << 20 | local): the shared-memory
+// index of a neighbour is slot_off[slot] + local -- no search, no global gather.
+// Row chunks are prefetched one chunk ahead, across target boundaries.
 //
 // The search tests r^2 < (2 h_a)^2 first in fp32 on cell-relative coordinates
-// with an error band derived below; candidates inside the band are decided by
+// inside an error band derived in DESIGN.md §6; candidates inside the band get
 // the exact fp64 test in the oracle's association, so lists stay bit-exact.
 #include "stencil.cuh"
 
 namespace sphb {
 
-constexpr int kCT = 256;            // threads per CTA
-constexpr int kNW = kCT / 32;       // warps per CTA
-constexpr int kTgtMax = 256;        // targets per sub-block (per-target state in smem)
-constexpr int kMaxUnits = 160;      // staged (slot, local range) pieces per group
-constexpr int kSearchCap = 2048;    // staged candidates per group (float4 = 32 KB)
-constexpr int kDensCap = 2048;      // staged particles per group, 4 fp64 fields (64 KB)
-constexpr int kMomCap = 576;        // staged particles per group, 17 fp64 fields (78 KB)
+constexpr int kCT = 256;          // threads per CTA
+constexpr int kNW = kCT / 32;     // warps per CTA
+constexpr int kTgt = 128;         // targets per sub-block (per-target state in smem)
+constexpr int kSlots = 512;       // slot tables (R <= 3 in every dim: 343 slots)
+constexpr int kMaxUnits = 128;    // staged (slot, local range) pieces per group
+constexpr int kSearchCap = 2048;  // staged candidates per group (float4)
+constexpr int kDensCap = 2048;    // staged particles per group, 4 fp64 fields
+constexpr int kMomCap = 512;      // staged particles per group, 17 fp64 fields
 constexpr int kMomFields = 17;
+constexpr uint32_t kSent = 0xffffffffu;
+
+static_assert(kSlots <= kKMax, "slot table");
+
+__constant__ double c_poly[kPolyTerms];   // sinc(pi sqrt(t)/2) = sum c_poly[k] t^k
+__constant__ double c_dpoly[kPolyTerms];  // derivative in t
+
+void set_poly_constants(const double* poly, const double* dpoly) {
+  cudaMemcpyToSymbol(c_poly, poly, sizeof(double) * kPolyTerms);
+  cudaMemcpyToSymbol(c_dpoly, dpoly, sizeof(double) * kPolyTerms);
+}
 
 struct GroupSm {
   int nu, total, k, l;
@@ -39,24 +52,16 @@ struct GroupSm {
 };
 
 struct CellSm {
-  uint32_t t_start[kKMax];
-  uint32_t t_cnt[kKMax];
-  int slot_off[kKMax];
-  signed char t_sh[kKMax][3];
+  uint32_t t_start[kSlots];
+  uint32_t t_cnt[kSlots];
+  int slot_off[kSlots];
+  signed char t_sh[kSlots][3];
   GroupSm G;
   Stencil st;
   int c3[3];
   uint32_t sc, ec;
   int kself;
 };
-
-__device__ __forceinline__ double min_img(double d, int periodic, double L) {
-  if (periodic) {
-    if (d > 0.5 * L) d -= L;
-    else if (d < -0.5 * L) d += L;
-  }
-  return d;
-}
 
 __device__ __forceinline__ double wsum(double v) {
 #pragma unroll
@@ -69,30 +74,44 @@ __device__ __forceinline__ double wmax(double v) {
   return v;
 }
 
-__device__ __forceinline__ double sinc_poly(const Phys& ph, double t) {
-  double p = ph.poly[kPolyTerms - 1];
+__device__ __forceinline__ double sinc_poly(double t) {
+  double p = c_poly[kPolyTerms - 1];
 #pragma unroll
-  for (int k = kPolyTerms - 2; k >= 0; --k) p = fma(p, t, ph.poly[k]);
+  for (int k = kPolyTerms - 2; k >= 0; --k) p = fma(p, t, c_poly[k]);
   return p;
 }
-__device__ __forceinline__ double sinc_dpoly(const Phys& ph, double t) {
-  double p = ph.dpoly[kPolyTerms - 2];
+__device__ __forceinline__ double sinc_dpoly(double t) {
+  double p = c_dpoly[kPolyTerms - 2];
 #pragma unroll
-  for (int k = kPolyTerms - 3; k >= 0; --k) p = fma(p, t, ph.dpoly[k]);
+  for (int k = kPolyTerms - 3; k >= 0; --k) p = fma(p, t, c_dpoly[k]);
   return p;
 }
-__device__ __forceinline__ double ipow(double s, int n) {  // "inline x*x*x..."
-  if (n == 6) {
+// "inline x*x*x*x..."; N > 0 fixes the exponent at compile time
+template <int N>
+__device__ __forceinline__ double ipow(double s, int n) {
+  if constexpr (N == 6) {
     double s2 = s * s;
     double s4 = s2 * s2;
     return s4 * s2;
+  } else if constexpr (N > 0) {
+    double r = s;
+#pragma unroll
+    for (int k = 1; k < N; ++k) r *= s;
+    return r;
+  } else {
+    double r = 1.0;
+    for (int k = 0; k < n; ++k) r *= s;
+    return r;
   }
-  double r = 1.0;
-  for (int k = 0; k < n; ++k) r *= s;
-  return r;
 }
 
-// CTA prologue for cell c: stencil + per-slot (start, count, shift) tables.
+__device__ __forceinline__ double min_img(double d, double L) {
+  if (d > 0.5 * L) d -= L;
+  else if (d < -0.5 * L) d += L;
+  return d;
+}
+
+// CTA prologue for cell c: stencil + per-slot (start, count, periodic shift) tables.
 __device__ void cell_setup(const Grid& g, uint32_t c, const uint32_t* __restrict__ cstart,
                            const uint32_t* __restrict__ cend,
                            const unsigned long long* __restrict__ chmax, CellSm& S) {
@@ -149,10 +168,60 @@ __device__ void build_group(CellSm& S, int cap) {
   G.total = total;
   G.k = k;
   G.l = l;
-  G.pend = k >= K ? 0xffffffffu : (((uint32_t)k << kLocalBits) | (uint32_t)l);
+  G.pend = k >= K ? kSent : (((uint32_t)k << kLocalBits) | (uint32_t)l);
+}
+
+__device__ __forceinline__ void shifts_of(const Grid& g, const CellSm& S, int slot, double sh[3]) {
+  sh[0] = S.t_sh[slot][0] * g.L[0];
+  sh[1] = S.t_sh[slot][1] * g.L[1];
+  sh[2] = S.t_sh[slot][2] * g.L[2];
+}
+
+// Warp-level walk over the entries of target rows that fall in the current
+// group [.., pend).  Row chunks are prefetched one chunk ahead; the first chunk
+// of the warp's next target is issued before the current target's work.
+template <class Body, class Finish>
+__device__ __forceinline__ void walk_targets(uint32_t t0, uint32_t t1, const uint32_t* __restrict__ nbr,
+                                             int maxn, const uint32_t* s_n, uint32_t* s_cur,
+                                             uint32_t pend, const int* slot_off, Body&& body,
+                                             Finish&& finish) {
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  uint32_t t = t0 + warp;
+  uint32_t ef = kSent;
+  if (t < t1) {
+    const uint32_t c0 = s_cur[t - t0];
+    ef = c0 + lane < s_n[t - t0] ? nbr[(size_t)t * maxn + c0 + lane] : kSent;
+  }
+  for (; t < t1; t += kNW) {
+    const uint32_t i = t - t0;
+    const uint32_t n = s_n[i];
+    const uint32_t* row = nbr + (size_t)t * maxn;
+    uint32_t cur = s_cur[i];
+    uint32_t e = ef;
+    // prefetch the next target's first chunk
+    const uint32_t tn = t + kNW;
+    if (tn < t1) {
+      const uint32_t cn = s_cur[tn - t0];
+      ef = cn + lane < s_n[tn - t0] ? nbr[(size_t)tn * maxn + cn + lane] : kSent;
+    }
+    body.begin(i);
+    for (;;) {
+      const bool in = e < pend;
+      const unsigned b = __ballot_sync(0xffffffffu, in);
+      const int m = __popc(b);
+      uint32_t enext = kSent;
+      if (m == 32 && cur + 32 + lane < n) enext = row[cur + 32 + lane];
+      if (in) body(slot_off[e >> kLocalBits] + (int)(e & kLocalMask));
+      cur += m;
+      if (m < 32) break;
+      e = enext;
+    }
+    finish(i, cur);
+  }
 }
 
 // ------------------------------------------------------------------ a5 search
+template <bool W2>
 __global__ void __launch_bounds__(kCT) k_search(const double* __restrict__ x,
                                                 const double* __restrict__ y,
                                                 const double* __restrict__ z,
@@ -165,9 +234,9 @@ __global__ void __launch_bounds__(kCT) k_search(const double* __restrict__ x,
                                                 uint32_t* __restrict__ nbr,
                                                 uint32_t* __restrict__ ncount, int maxn,
                                                 unsigned int* __restrict__ maxcount) {
-  extern __shared__ float4 cand[];  // kSearchCap staged candidates
+  extern __shared__ float4 cand[];  // kSearchCap + 32 padding
   __shared__ CellSm S;
-  __shared__ uint32_t tcount[kTgtMax];
+  __shared__ uint32_t tcount[kTgt];
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const unsigned lt = (1u << lane) - 1u;
   const uint32_t ncl = *nclist;
@@ -175,17 +244,18 @@ __global__ void __launch_bounds__(kCT) k_search(const double* __restrict__ x,
     cell_setup(g, clist[ci], cstart, cend, chmax, S);
     const Stencil st = S.st;
     double org[3], M = 0.0;
+#pragma unroll
     for (int d = 0; d < 3; ++d) {
-      double edge = g.inv[d] > 0.0 ? 1.0 / g.inv[d] : 0.0;
+      const double edge = g.inv[d] > 0.0 ? 1.0 / g.inv[d] : 0.0;
       org[d] = g.lo[d] + S.c3[d] * edge;
-      // bound on |staged coordinate - org| (cells of the stencil +1 cell of slack)
-      double Md = st.wrap[d] == 2 ? g.L[d]
-                                  : (double)(max(S.c3[d] - st.lo[d], st.lo[d] + st.cnt[d] - S.c3[d]) + 1) * edge;
+      // bound on |staged coordinate - org| (stencil cells + 1 cell of slack)
+      const double Md = st.wrap[d] == 2
+                            ? g.L[d]
+                            : (double)(max(S.c3[d] - st.lo[d], st.lo[d] + st.cnt[d] - S.c3[d]) + 1) * edge;
       M = fmax(M, Md);
     }
-    const float L32[3] = {(float)g.L[0], (float)g.L[1], (float)g.L[2]};
-    for (uint32_t t0 = S.sc; t0 < S.ec; t0 += kTgtMax) {
-      const uint32_t t1 = min(S.ec, t0 + kTgtMax);
+    for (uint32_t t0 = S.sc; t0 < S.ec; t0 += kTgt) {
+      const uint32_t t1 = min(S.ec, t0 + kTgt);
       for (uint32_t t = t0 + threadIdx.x; t < t1; t += blockDim.x) tcount[t - t0] = 0;
       if (threadIdx.x == 0) {
         S.G.k = 0;
@@ -200,26 +270,29 @@ __global__ void __launch_bounds__(kCT) k_search(const double* __restrict__ x,
         for (int u = warp; u < nu; u += kNW) {
           const int slot = S.G.u_slot[u], base = S.G.u_base[u], len = S.G.u_len[u], l0 = S.G.u_l0[u];
           const uint32_t g0 = S.G.u_g[u];
-          const double sx = S.t_sh[slot][0] * g.L[0], sy = S.t_sh[slot][1] * g.L[1],
-                       sz = S.t_sh[slot][2] * g.L[2];
+          double sh[3];
+          shifts_of(g, S, slot, sh);
           for (int i = lane; i < len; i += 32) {
             const uint32_t j = g0 + i;
             float4 v;
-            v.x = (float)((x[j] + sx) - org[0]);
-            v.y = (float)((y[j] + sy) - org[1]);
-            v.z = (float)((z[j] + sz) - org[2]);
+            v.x = (float)((x[j] + sh[0]) - org[0]);
+            v.y = (float)((y[j] + sh[1]) - org[1]);
+            v.z = (float)((z[j] + sh[2]) - org[2]);
             v.w = __uint_as_float(((uint32_t)slot << kLocalBits) | (uint32_t)(l0 + i));
             cand[base + i] = v;
           }
         }
+        // pad to a multiple of 32 with far-away sentinels (never hit, never ambiguous)
+        const int padded = (total + 31) & ~31;
+        for (int q = total + threadIdx.x; q < padded; q += blockDim.x)
+          cand[q] = make_float4(INFINITY, INFINITY, INFINITY, __uint_as_float(kSent));
         __syncthreads();
         for (uint32_t t = t0 + warp; t < t1; t += kNW) {
-          const double xa = x[t], ya = y[t], za = z[t];
-          const double tha = 2.0 * h[t];
+          const double xa = x[t], ya = y[t], za = z[t], ha = h[t];
+          const double tha = 2.0 * ha;
           const double lim = __dmul_rn(tha, tha);
-          // fp32 error band: |r2_32 - r2| <= delta * lim with
-          // delta = 2^-20 (2 + 2 M/h + 2^-20 (M/h)^2), M >= |coordinates|.
-          const double mh = M / h[t];
+          // fp32 error band: |r2_32 - r2| <= delta lim, delta = 2^-20 (2 + 2 M/h + 2^-20 (M/h)^2)
+          const double mh = M / ha;
           const double delta = 0x1p-20 * (2.0 + 2.0 * mh + 0x1p-20 * mh * mh);
           float lo32 = -1.0f, hi32 = INFINITY;
           if (delta < 0.25) {
@@ -230,36 +303,35 @@ __global__ void __launch_bounds__(kCT) k_search(const double* __restrict__ x,
           const uint32_t self_pk = ((uint32_t)S.kself << kLocalBits) | (t - S.sc);
           uint32_t count = tcount[t - t0];
           uint32_t* row = nbr + (size_t)t * maxn;
-          for (int q0 = 0; q0 < total; q0 += 32) {
-            const int q = q0 + lane;
-            bool hit = false;
-            uint32_t pk = 0;
-            if (q < total) {
-              const float4 cd = cand[q];
-              float dx = cd.x - ax, dy = cd.y - ay, dz = cd.z - az;
-              if (st.wrap[0] == 2) dx = dx > 0.5f * L32[0] ? dx - L32[0] : (dx < -0.5f * L32[0] ? dx + L32[0] : dx);
-              if (st.wrap[1] == 2) dy = dy > 0.5f * L32[1] ? dy - L32[1] : (dy < -0.5f * L32[1] ? dy + L32[1] : dy);
-              if (st.wrap[2] == 2) dz = dz > 0.5f * L32[2] ? dz - L32[2] : (dz < -0.5f * L32[2] ? dz + L32[2] : dz);
-              const float r2 = fmaf(dz, dz, fmaf(dy, dy, dx * dx));
-              pk = __float_as_uint(cd.w);
-              if (r2 < lo32) {
-                hit = pk != self_pk;
-              } else if (r2 < hi32) {  // inside the band: the exact fp64 test (oracle's association)
+          for (int q0 = 0; q0 < padded; q0 += 32) {
+            const float4 cd = cand[q0 + lane];
+            float dx = cd.x - ax, dy = cd.y - ay, dz = cd.z - az;
+            if constexpr (W2) {
+              const float L0 = (float)g.L[0], L1 = (float)g.L[1], L2 = (float)g.L[2];
+              if (st.wrap[0] == 2) dx = dx > 0.5f * L0 ? dx - L0 : (dx < -0.5f * L0 ? dx + L0 : dx);
+              if (st.wrap[1] == 2) dy = dy > 0.5f * L1 ? dy - L1 : (dy < -0.5f * L1 ? dy + L1 : dy);
+              if (st.wrap[2] == 2) dz = dz > 0.5f * L2 ? dz - L2 : (dz < -0.5f * L2 ? dz + L2 : dz);
+            }
+            const float r2 = fmaf(dz, dz, fmaf(dy, dy, dx * dx));
+            const uint32_t pk = __float_as_uint(cd.w);
+            bool hit = (r2 < lo32) & (pk != self_pk);
+            const bool amb = (r2 >= lo32) & (r2 < hi32);
+            if (__any_sync(0xffffffffu, amb)) {  // rare: exact fp64 test in the oracle's association
+              if (amb) {
                 const uint32_t j = S.t_start[pk >> kLocalBits] + (pk & kLocalMask);
                 if (j != t) {
-                  double ex = min_img(__dsub_rn(x[j], xa), g.periodic[0], g.L[0]);
-                  double ey = min_img(__dsub_rn(y[j], ya), g.periodic[1], g.L[1]);
-                  double ez = min_img(__dsub_rn(z[j], za), g.periodic[2], g.L[2]);
-                  double r2e = __dadd_rn(__dadd_rn(__dmul_rn(ex, ex), __dmul_rn(ey, ey)), __dmul_rn(ez, ez));
+                  double ex = __dsub_rn(x[j], xa), ey = __dsub_rn(y[j], ya), ez = __dsub_rn(z[j], za);
+                  if (g.periodic[0]) ex = min_img(ex, g.L[0]);
+                  if (g.periodic[1]) ey = min_img(ey, g.L[1]);
+                  if (g.periodic[2]) ez = min_img(ez, g.L[2]);
+                  const double r2e = __dadd_rn(__dadd_rn(__dmul_rn(ex, ex), __dmul_rn(ey, ey)), __dmul_rn(ez, ez));
                   hit = r2e < lim;
                 }
               }
             }
             const unsigned b = __ballot_sync(0xffffffffu, hit);
-            if (hit) {
-              const uint32_t p = count + __popc(b & lt);
-              if (p < (uint32_t)maxn) row[p] = pk;
-            }
+            const uint32_t p = count + __popc(b & lt);
+            if (hit && p < (uint32_t)maxn) row[p] = pk;
             count += __popc(b);
           }
           if (lane == 0) tcount[t - t0] = count;
@@ -276,27 +348,55 @@ __global__ void __launch_bounds__(kCT) k_search(const double* __restrict__ x,
   }
 }
 
-// Walk target t's row from its cursor over the entries of the current group;
-// calls body(smem index) for each entry owned by this lane.
-template <class Body>
-__device__ __forceinline__ uint32_t walk_group(const uint32_t* __restrict__ row, uint32_t cur,
-                                               uint32_t n, uint32_t pend, const int* slot_off,
-                                               Body&& body) {
-  const int lane = threadIdx.x & 31;
-  while (cur < n) {
-    const uint32_t p = cur + lane;
-    const uint32_t e = p < n ? row[p] : 0xffffffffu;
-    const bool in = e < pend;
-    const unsigned b = __ballot_sync(0xffffffffu, in);
-    if (in) body(slot_off[e >> kLocalBits] + (int)(e & kLocalMask));
-    const int m = __popc(b);
-    cur += m;
-    if (m < 32) break;
+// stage [x y z] (shifted) + one extra field of the current group into SoA smem
+__device__ __forceinline__ void stage4(const Grid& g, const CellSm& S, const double* __restrict__ x,
+                                       const double* __restrict__ y, const double* __restrict__ z,
+                                       const double* __restrict__ f, double* sx, double* sy, double* sz,
+                                       double* sf) {
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  for (int uu = warp; uu < S.G.nu; uu += kNW) {
+    const int base = S.G.u_base[uu], len = S.G.u_len[uu];
+    const uint32_t g0 = S.G.u_g[uu];
+    double sh[3];
+    shifts_of(g, S, S.G.u_slot[uu], sh);
+    for (int i = lane; i < len; i += 32) {
+      sx[base + i] = x[g0 + i] + sh[0];
+      sy[base + i] = y[g0 + i] + sh[1];
+      sz[base + i] = z[g0 + i] + sh[2];
+      sf[base + i] = f[g0 + i];
+    }
   }
-  return cur;
+}
+
+// minimum image only for periodic dims where the stencil spans every cell
+template <bool W2>
+__device__ __forceinline__ void delta3(const Stencil& st, const Grid& g, double& dx, double& dy,
+                                       double& dz) {
+  if constexpr (W2) {
+    if (st.wrap[0] == 2) dx = min_img(dx, g.L[0]);
+    if (st.wrap[1] == 2) dy = min_img(dy, g.L[1]);
+    if (st.wrap[2] == 2) dz = min_img(dz, g.L[2]);
+  }
 }
 
 // ------------------------------------------------------------------ a6 density + Omega + EOS
+struct DensBody {
+  const double *sx, *sy, *sz, *sm;
+  const double *tx, *ty, *tz, *tih2;
+  const Stencil* st;
+  const Grid* g;
+  double xa, ya, za, ih2a, sr, sd;
+  __device__ __forceinline__ void begin(uint32_t i) {
+    xa = tx[i];
+    ya = ty[i];
+    za = tz[i];
+    ih2a = tih2[i];
+    sr = 0.0;
+    sd = 0.0;
+  }
+};
+
+template <int N, bool W2>
 __global__ void __launch_bounds__(kCT) k_density_c(
     const double* __restrict__ x, const double* __restrict__ y, const double* __restrict__ z,
     const double* __restrict__ h, const double* __restrict__ m, const double* __restrict__ u,
@@ -314,18 +414,27 @@ __global__ void __launch_bounds__(kCT) k_density_c(
   double* sz = sy + kDensCap;
   double* sm = sz + kDensCap;
   __shared__ CellSm S;
-  __shared__ uint32_t cur[kTgtMax];
-  __shared__ double acc[kTgtMax][2];
-  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  __shared__ uint32_t s_n[kTgt], s_cur[kTgt];
+  __shared__ double tx[kTgt], ty[kTgt], tz[kTgt], tih2[kTgt], acc0[kTgt], acc1[kTgt];
+  const int lane = threadIdx.x & 31;
   const uint32_t ncl = *nclist;
+  const int n = N > 0 ? N : ph.n;
   for (uint32_t ci = blockIdx.x; ci < ncl; ci += gridDim.x) {
     cell_setup(g, clist[ci], cstart, cend, chmax, S);
-    for (uint32_t t0 = S.sc; t0 < S.ec; t0 += kTgtMax) {
-      const uint32_t t1 = min(S.ec, t0 + kTgtMax);
+    const Stencil st = S.st;
+    for (uint32_t t0 = S.sc; t0 < S.ec; t0 += kTgt) {
+      const uint32_t t1 = min(S.ec, t0 + kTgt);
       for (uint32_t t = t0 + threadIdx.x; t < t1; t += blockDim.x) {
-        cur[t - t0] = 0;
-        acc[t - t0][0] = 0.0;
-        acc[t - t0][1] = 0.0;
+        const uint32_t i = t - t0;
+        s_n[i] = ncount[t];
+        s_cur[i] = 0;
+        tx[i] = x[t];
+        ty[i] = y[t];
+        tz[i] = z[t];
+        const double ih = 1.0 / h[t];
+        tih2[i] = ih * ih;
+        acc0[i] = 0.0;
+        acc1[i] = 0.0;
       }
       if (threadIdx.x == 0) {
         S.G.k = 0;
@@ -335,55 +444,45 @@ __global__ void __launch_bounds__(kCT) k_density_c(
       for (;;) {
         if (threadIdx.x == 0) build_group(S, kDensCap);
         __syncthreads();
-        const int nu = S.G.nu;
-        if (nu == 0) break;
-        for (int uu = warp; uu < nu; uu += kNW) {
-          const int base = S.G.u_base[uu], len = S.G.u_len[uu];
-          const uint32_t g0 = S.G.u_g[uu];
-          for (int i = lane; i < len; i += 32) {
-            sx[base + i] = x[g0 + i];
-            sy[base + i] = y[g0 + i];
-            sz[base + i] = z[g0 + i];
-            sm[base + i] = m[g0 + i];
-          }
-        }
+        if (S.G.nu == 0) break;
+        stage4(g, S, x, y, z, m, sx, sy, sz, sm);
         __syncthreads();
-        const uint32_t pend = S.G.pend;
-        for (uint32_t t = t0 + warp; t < t1; t += kNW) {
-          const double xa = x[t], ya = y[t], za = z[t];
-          const double ih = 1.0 / h[t];
-          const double ih2a = ih * ih;
-          double sr = 0.0, sd = 0.0;
-          const uint32_t c2 = walk_group(nbr + (size_t)t * maxn, cur[t - t0], ncount[t], pend, S.slot_off,
-                                         [&](int q) {
-            const double dx = min_img(sx[q] - xa, ph.periodic[0], ph.L[0]);
-            const double dy = min_img(sy[q] - ya, ph.periodic[1], ph.L[1]);
-            const double dz = min_img(sz[q] - za, ph.periodic[2], ph.L[2]);
+        struct B : DensBody {
+          int n;
+          __device__ __forceinline__ void operator()(int q) {
+            double dx = sx[q] - xa, dy = sy[q] - ya, dz = sz[q] - za;
+            delta3<W2>(*st, *g, dx, dy, dz);
             const double tt = (dx * dx + dy * dy + dz * dz) * ih2a;
-            const double P = sinc_poly(ph, tt);
-            const double Pn1 = ipow(P, ph.n - 1);
-            const double dP = sinc_dpoly(ph, tt);
+            const double P = sinc_poly(tt);
+            const double Pn1 = ipow<N - 1 < 0 ? 0 : N - 1>(P, n - 1);
+            const double dP = sinc_dpoly(tt);
             const double mj = sm[q];
-            sr += mj * (Pn1 * P);
-            sd += mj * (Pn1 * (3.0 * P + 2.0 * ph.n * tt * dP));  // 3 S + v S'(v)
-          });
-          sr = wsum(sr);
-          sd = wsum(sd);
-          if (lane == 0) {
-            cur[t - t0] = c2;
-            acc[t - t0][0] += sr;
-            acc[t - t0][1] += sd;
+            sr = fma(mj, Pn1 * P, sr);
+            sd = fma(mj, Pn1 * (3.0 * P + (2.0 * n) * tt * dP), sd);  // 3 S + v S'(v)
           }
-        }
+        } body;
+        body.sx = sx; body.sy = sy; body.sz = sz; body.sm = sm;
+        body.tx = tx; body.ty = ty; body.tz = tz; body.tih2 = tih2;
+        body.st = &st; body.g = &g; body.n = n;
+        walk_targets(t0, t1, nbr, maxn, s_n, s_cur, S.G.pend, S.slot_off, body,
+                     [&](uint32_t i, uint32_t c2) {
+                       const double a = wsum(body.sr), b = wsum(body.sd);
+                       if (lane == 0) {
+                         s_cur[i] = c2;
+                         acc0[i] += a;
+                         acc1[i] += b;
+                       }
+                     });
         __syncthreads();
       }
       for (uint32_t t = t0 + threadIdx.x; t < t1; t += blockDim.x) {
+        const uint32_t i = t - t0;
         const double ha = h[t], ma = m[t];
         const double ih = 1.0 / ha;
         const double ih2a = ih * ih;
-        const double wBa = ph.B * ih * ih2a;                         // B / h^3
-        const double r = wBa * (ma + acc[t - t0][0]);                // Eq. 1 incl. self (R11)
-        const double dsum = -wBa * ih * (3.0 * ma + acc[t - t0][1]);  // sum m dW/dh
+        const double wBa = ph.B * ih * ih2a;               // B / h^3
+        const double r = wBa * (ma + acc0[i]);             // Eq. 1 incl. self (R11)
+        const double dsum = -wBa * ih * (3.0 * ma + acc1[i]);  // sum m dW/dh
         double om = ph.omega_mode ? 1.0 : 1.0 + ha / (3.0 * r) * dsum;  // R8
         if (om < 0.1) {
           om = 0.1;
@@ -415,6 +514,7 @@ __global__ void __launch_bounds__(kCT) k_density_c(
 }
 
 // ------------------------------------------------------------------ a8 IAD
+template <int N, bool W2>
 __global__ void __launch_bounds__(kCT) k_iad_c(
     const double* __restrict__ x, const double* __restrict__ y, const double* __restrict__ z,
     Grid g, const uint32_t* __restrict__ cstart, const uint32_t* __restrict__ cend,
@@ -431,17 +531,26 @@ __global__ void __launch_bounds__(kCT) k_iad_c(
   double* sz = sy + kDensCap;
   double* sv = sz + kDensCap;
   __shared__ CellSm S;
-  __shared__ uint32_t cur[kTgtMax];
-  __shared__ double acc[kTgtMax][6];
-  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  __shared__ uint32_t s_n[kTgt], s_cur[kTgt];
+  __shared__ double tx[kTgt], ty[kTgt], tz[kTgt], tih2[kTgt];
+  __shared__ double acc[6][kTgt];
+  const int lane = threadIdx.x & 31;
   const uint32_t ncl = *nclist;
+  const int n = N > 0 ? N : ph.n;
   for (uint32_t ci = blockIdx.x; ci < ncl; ci += gridDim.x) {
     cell_setup(g, clist[ci], cstart, cend, chmax, S);
-    for (uint32_t t0 = S.sc; t0 < S.ec; t0 += kTgtMax) {
-      const uint32_t t1 = min(S.ec, t0 + kTgtMax);
+    const Stencil st = S.st;
+    for (uint32_t t0 = S.sc; t0 < S.ec; t0 += kTgt) {
+      const uint32_t t1 = min(S.ec, t0 + kTgt);
       for (uint32_t t = t0 + threadIdx.x; t < t1; t += blockDim.x) {
-        cur[t - t0] = 0;
-        for (int k = 0; k < 6; ++k) acc[t - t0][k] = 0.0;
+        const uint32_t i = t - t0;
+        s_n[i] = ncount[t];
+        s_cur[i] = 0;
+        tx[i] = x[t];
+        ty[i] = y[t];
+        tz[i] = z[t];
+        tih2[i] = ih2[t];
+        for (int k = 0; k < 6; ++k) acc[k][i] = 0.0;
       }
       if (threadIdx.x == 0) {
         S.G.k = 0;
@@ -451,53 +560,56 @@ __global__ void __launch_bounds__(kCT) k_iad_c(
       for (;;) {
         if (threadIdx.x == 0) build_group(S, kDensCap);
         __syncthreads();
-        const int nu = S.G.nu;
-        if (nu == 0) break;
-        for (int uu = warp; uu < nu; uu += kNW) {
-          const int base = S.G.u_base[uu], len = S.G.u_len[uu];
-          const uint32_t g0 = S.G.u_g[uu];
-          for (int i = lane; i < len; i += 32) {
-            sx[base + i] = x[g0 + i];
-            sy[base + i] = y[g0 + i];
-            sz[base + i] = z[g0 + i];
-            sv[base + i] = vol[g0 + i];
-          }
-        }
+        if (S.G.nu == 0) break;
+        stage4(g, S, x, y, z, vol, sx, sy, sz, sv);
         __syncthreads();
-        const uint32_t pend = S.G.pend;
-        for (uint32_t t = t0 + warp; t < t1; t += kNW) {
-          const double xa = x[t], ya = y[t], za = z[t], ih2a = ih2[t];
-          double t11 = 0, t12 = 0, t13 = 0, t22 = 0, t23 = 0, t33 = 0;
-          const uint32_t c2 = walk_group(nbr + (size_t)t * maxn, cur[t - t0], ncount[t], pend, S.slot_off,
-                                         [&](int q) {
-            const double dx = min_img(sx[q] - xa, ph.periodic[0], ph.L[0]);
-            const double dy = min_img(sy[q] - ya, ph.periodic[1], ph.L[1]);
-            const double dz = min_img(sz[q] - za, ph.periodic[2], ph.L[2]);
-            const double tt = (dx * dx + dy * dy + dz * dz) * ih2a;
-            const double w = sv[q] * ipow(sinc_poly(ph, tt), ph.n);  // (m_b/rho_b) S
-            const double wx = w * dx, wy = w * dy;
-            t11 += wx * dx;
-            t12 += wx * dy;
-            t13 += wx * dz;
-            t22 += wy * dy;
-            t23 += wy * dz;
-            t33 += w * dz * dz;
-          });
-          t11 = wsum(t11); t12 = wsum(t12); t13 = wsum(t13);
-          t22 = wsum(t22); t23 = wsum(t23); t33 = wsum(t33);
-          if (lane == 0) {
-            cur[t - t0] = c2;
-            acc[t - t0][0] += t11; acc[t - t0][1] += t12; acc[t - t0][2] += t13;
-            acc[t - t0][3] += t22; acc[t - t0][4] += t23; acc[t - t0][5] += t33;
+        struct B {
+          const double *sx, *sy, *sz, *sv, *tx, *ty, *tz, *tih2;
+          const Stencil* st;
+          const Grid* g;
+          int n;
+          double xa, ya, za, ih2a, t11, t12, t13, t22, t23, t33;
+          __device__ __forceinline__ void begin(uint32_t i) {
+            xa = tx[i];
+            ya = ty[i];
+            za = tz[i];
+            ih2a = tih2[i];
+            t11 = t12 = t13 = t22 = t23 = t33 = 0.0;
           }
-        }
+          __device__ __forceinline__ void operator()(int q) {
+            double dx = sx[q] - xa, dy = sy[q] - ya, dz = sz[q] - za;
+            delta3<W2>(*st, *g, dx, dy, dz);
+            const double tt = (dx * dx + dy * dy + dz * dz) * ih2a;
+            const double w = sv[q] * ipow<N>(sinc_poly(tt), n);  // (m_b/rho_b) S
+            const double wx = w * dx, wy = w * dy;
+            t11 = fma(wx, dx, t11);
+            t12 = fma(wx, dy, t12);
+            t13 = fma(wx, dz, t13);
+            t22 = fma(wy, dy, t22);
+            t23 = fma(wy, dz, t23);
+            t33 = fma(w * dz, dz, t33);
+          }
+        } body;
+        body.sx = sx; body.sy = sy; body.sz = sz; body.sv = sv;
+        body.tx = tx; body.ty = ty; body.tz = tz; body.tih2 = tih2;
+        body.st = &st; body.g = &g; body.n = n;
+        walk_targets(t0, t1, nbr, maxn, s_n, s_cur, S.G.pend, S.slot_off, body,
+                     [&](uint32_t i, uint32_t c2) {
+                       const double a11 = wsum(body.t11), a12 = wsum(body.t12), a13 = wsum(body.t13);
+                       const double a22 = wsum(body.t22), a23 = wsum(body.t23), a33 = wsum(body.t33);
+                       if (lane == 0) {
+                         s_cur[i] = c2;
+                         acc[0][i] += a11; acc[1][i] += a12; acc[2][i] += a13;
+                         acc[3][i] += a22; acc[4][i] += a23; acc[5][i] += a33;
+                       }
+                     });
         __syncthreads();
       }
       for (uint32_t t = t0 + threadIdx.x; t < t1; t += blockDim.x) {
+        const uint32_t i = t - t0;
         const double s = wB[t];
-        const double* A = acc[t - t0];
-        const double a11 = A[0] * s, a12 = A[1] * s, a13 = A[2] * s, a22 = A[3] * s,
-                     a23 = A[4] * s, a33 = A[5] * s;
+        const double a11 = acc[0][i] * s, a12 = acc[1][i] * s, a13 = acc[2][i] * s,
+                     a22 = acc[3][i] * s, a23 = acc[4][i] * s, a33 = acc[5][i] * s;
         const double det = a11 * (a22 * a33 - a23 * a23) - a12 * (a12 * a33 - a23 * a13) +
                            a13 * (a12 * a23 - a22 * a13);
         const double id = 1.0 / det;
@@ -539,37 +651,61 @@ struct MomTgt {
 struct MomOut {
   double *ax, *ay, *az, *du, *vsig;
 };
+// staged field slots (SoA, kMomCap doubles each)
+enum { F_X, F_Y, F_Z, F_VX, F_VY, F_VZ, F_M, F_IH2, F_C, F_MX, F_MR, F_C11, F_C12, F_C13, F_C22, F_C23, F_C33 };
+// per-target smem fields
+enum { T_X, T_Y, T_Z, T_VX, T_VY, T_VZ, T_IH2, T_WB, T_RINV, T_XP, T_C, T_A11, T_A12, T_A13, T_A22, T_A23, T_A33, T_N };
 
+template <int N, bool W2>
 __global__ void __launch_bounds__(kCT, 2) k_momentum_c(
     MomSrc src, MomTgt tg, MomOut out, Grid g, const uint32_t* __restrict__ cstart,
     const uint32_t* __restrict__ cend, const unsigned long long* __restrict__ chmax,
     const uint32_t* __restrict__ clist, const uint32_t* __restrict__ nclist,
     const uint32_t* __restrict__ nbr, const uint32_t* __restrict__ ncount, int maxn, Phys ph,
     double* __restrict__ dts, unsigned long long* __restrict__ cnt) {
-  extern __shared__ double dsm[];
-  double* F[kMomFields];
-#pragma unroll
-  for (int k = 0; k < kMomFields; ++k) F[k] = dsm + k * kMomCap;
+  extern __shared__ double dsm[];  // kMomFields * kMomCap staged + T_N * kTgt target fields
+  double* const T = dsm + kMomFields * kMomCap;
   __shared__ CellSm S;
-  __shared__ uint32_t cur[kTgtMax];
-  __shared__ double acc[kTgtMax][5];
+  __shared__ uint32_t s_n[kTgt], s_cur[kTgt];
+  __shared__ double acc[5][kTgt];
   __shared__ double shdt[kNW];
   __shared__ unsigned long long shco;
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const uint32_t ncl = *nclist;
+  const int n = N > 0 ? N : ph.n;
   double dtmin = INFINITY;
   unsigned long long ncoinc = 0;
   for (uint32_t ci = blockIdx.x; ci < ncl; ci += gridDim.x) {
     cell_setup(g, clist[ci], cstart, cend, chmax, S);
-    for (uint32_t t0 = S.sc; t0 < S.ec; t0 += kTgtMax) {
-      const uint32_t t1 = min(S.ec, t0 + kTgtMax);
+    const Stencil st = S.st;
+    for (uint32_t t0 = S.sc; t0 < S.ec; t0 += kTgt) {
+      const uint32_t t1 = min(S.ec, t0 + kTgt);
       for (uint32_t t = t0 + threadIdx.x; t < t1; t += blockDim.x) {
-        cur[t - t0] = 0;
-        acc[t - t0][0] = 0.0;
-        acc[t - t0][1] = 0.0;
-        acc[t - t0][2] = 0.0;
-        acc[t - t0][3] = 0.0;
-        acc[t - t0][4] = -1.0;
+        const uint32_t i = t - t0;
+        s_n[i] = ncount[t];
+        s_cur[i] = 0;
+        T[T_X * kTgt + i] = src.x[t];
+        T[T_Y * kTgt + i] = src.y[t];
+        T[T_Z * kTgt + i] = src.z[t];
+        T[T_VX * kTgt + i] = src.vx[t];
+        T[T_VY * kTgt + i] = src.vy[t];
+        T[T_VZ * kTgt + i] = src.vz[t];
+        T[T_IH2 * kTgt + i] = src.ih2[t];
+        T[T_WB * kTgt + i] = tg.wB[t];
+        T[T_RINV * kTgt + i] = tg.rinv[t];
+        T[T_XP * kTgt + i] = tg.X[t];
+        T[T_C * kTgt + i] = src.c[t];
+        T[T_A11 * kTgt + i] = tg.c11[t];
+        T[T_A12 * kTgt + i] = tg.c12[t];
+        T[T_A13 * kTgt + i] = tg.c13[t];
+        T[T_A22 * kTgt + i] = tg.c22[t];
+        T[T_A23 * kTgt + i] = tg.c23[t];
+        T[T_A33 * kTgt + i] = tg.c33[t];
+        acc[0][i] = 0.0;
+        acc[1][i] = 0.0;
+        acc[2][i] = 0.0;
+        acc[3][i] = 0.0;
+        acc[4][i] = -1.0;
       }
       if (threadIdx.x == 0) {
         S.G.k = 0;
@@ -579,71 +715,84 @@ __global__ void __launch_bounds__(kCT, 2) k_momentum_c(
       for (;;) {
         if (threadIdx.x == 0) build_group(S, kMomCap);
         __syncthreads();
-        const int nu = S.G.nu;
-        if (nu == 0) break;
-        for (int uu = warp; uu < nu; uu += kNW) {
+        if (S.G.nu == 0) break;
+        for (int uu = warp; uu < S.G.nu; uu += kNW) {
           const int base = S.G.u_base[uu], len = S.G.u_len[uu];
           const uint32_t g0 = S.G.u_g[uu];
+          double sh[3];
+          shifts_of(g, S, S.G.u_slot[uu], sh);
           for (int i = lane; i < len; i += 32) {
             const uint32_t j = g0 + i;
-            const int q = base + i;
-            F[0][q] = src.x[j];
-            F[1][q] = src.y[j];
-            F[2][q] = src.z[j];
-            F[3][q] = src.vx[j];
-            F[4][q] = src.vy[j];
-            F[5][q] = src.vz[j];
-            F[6][q] = src.m[j];
-            F[7][q] = src.ih2[j];
-            F[8][q] = src.c[j];
-            F[9][q] = src.mX[j];
-            F[10][q] = src.mr[j];
+            double* q = dsm + base + i;
+            q[F_X * kMomCap] = src.x[j] + sh[0];
+            q[F_Y * kMomCap] = src.y[j] + sh[1];
+            q[F_Z * kMomCap] = src.z[j] + sh[2];
+            q[F_VX * kMomCap] = src.vx[j];
+            q[F_VY * kMomCap] = src.vy[j];
+            q[F_VZ * kMomCap] = src.vz[j];
+            q[F_M * kMomCap] = src.m[j];
+            q[F_IH2 * kMomCap] = src.ih2[j];
+            q[F_C * kMomCap] = src.c[j];
+            q[F_MX * kMomCap] = src.mX[j];
+            q[F_MR * kMomCap] = src.mr[j];
 #pragma unroll
-            for (int k = 0; k < 6; ++k) F[11 + k][q] = src.ct[k * src.ct_stride + j];
+            for (int k = 0; k < 6; ++k) q[(F_C11 + k) * kMomCap] = src.ct[k * src.ct_stride + j];
           }
         }
         __syncthreads();
-        const uint32_t pend = S.G.pend;
-        for (uint32_t t = t0 + warp; t < t1; t += kNW) {
-          const double xa = src.x[t], ya = src.y[t], za = src.z[t];
-          const double vxa = src.vx[t], vya = src.vy[t], vza = src.vz[t];
-          const double ih2a = src.ih2[t], wBa = tg.wB[t], rinva = tg.rinv[t], Xa = tg.X[t],
-                       ca = src.c[t];
-          const double a11 = tg.c11[t], a12 = tg.c12[t], a13 = tg.c13[t], a22 = tg.c22[t],
-                       a23 = tg.c23[t], a33 = tg.c33[t];
-          double fx = 0.0, fy = 0.0, fz = 0.0, fu = 0.0, vs = -1.0;
-          const uint32_t c2 = walk_group(nbr + (size_t)t * maxn, cur[t - t0], ncount[t], pend, S.slot_off,
-                                         [&](int q) {
-            const double dx = min_img(F[0][q] - xa, ph.periodic[0], ph.L[0]);  // Delta_ab = x_b - x_a
-            const double dy = min_img(F[1][q] - ya, ph.periodic[1], ph.L[1]);
-            const double dz = min_img(F[2][q] - za, ph.periodic[2], ph.L[2]);
+        struct B {
+          const double* F;
+          const double* T;
+          const Stencil* st;
+          const Grid* g;
+          double alpha;
+          int n;
+          unsigned long long* ncoinc;
+          double xa, ya, za, vxa, vya, vza, ih2a, wBa, rinva, Xa, ca, a11, a12, a13, a22, a23, a33;
+          double fx, fy, fz, fu, vs;
+          __device__ __forceinline__ void begin(uint32_t i) {
+            xa = T[T_X * kTgt + i]; ya = T[T_Y * kTgt + i]; za = T[T_Z * kTgt + i];
+            vxa = T[T_VX * kTgt + i]; vya = T[T_VY * kTgt + i]; vza = T[T_VZ * kTgt + i];
+            ih2a = T[T_IH2 * kTgt + i]; wBa = T[T_WB * kTgt + i]; rinva = T[T_RINV * kTgt + i];
+            Xa = T[T_XP * kTgt + i]; ca = T[T_C * kTgt + i];
+            a11 = T[T_A11 * kTgt + i]; a12 = T[T_A12 * kTgt + i]; a13 = T[T_A13 * kTgt + i];
+            a22 = T[T_A22 * kTgt + i]; a23 = T[T_A23 * kTgt + i]; a33 = T[T_A33 * kTgt + i];
+            fx = fy = fz = fu = 0.0;
+            vs = -1.0;
+          }
+          __device__ __forceinline__ void operator()(int qi) {
+            const double* q = F + qi;
+            double dx = q[F_X * kMomCap] - xa, dy = q[F_Y * kMomCap] - ya, dz = q[F_Z * kMomCap] - za;
+            delta3<W2>(*st, *g, dx, dy, dz);  // Delta_ab = x_b - x_a
             const double r2 = dx * dx + dy * dy + dz * dz;
             if (r2 == 0.0) {  // coincident pair: skipped, counted
-              ++ncoinc;
+              ++*ncoinc;
               return;
             }
             const double ta = r2 * ih2a;
-            const double Sa = ipow(sinc_poly(ph, ta), ph.n);
+            const double Sa = ipow<N>(sinc_poly(ta), n);
             const double Wa = wBa * Sa;
-            const double tb = r2 * F[7][q];
-            double Sb = 0.0;  // b's support may not reach a (variable h)
-            if (tb < 4.0) Sb = (tb == ta) ? Sa : ipow(sinc_poly(ph, tb), ph.n);
+            const double tb = r2 * q[F_IH2 * kMomCap];
+            double Sb = Sa;  // equal h: W(r, h_b) shares the kernel value
+            if (tb != ta) Sb = tb < 4.0 ? ipow<N>(sinc_poly(tb), n) : 0.0;
             // R5: A_ab(h_a) = C_a Delta W_ab(h_a);  R4: A_ab(h_b) = C~_b Delta S_b
             const double Aax = (a11 * dx + a12 * dy + a13 * dz) * Wa;
             const double Aay = (a12 * dx + a22 * dy + a23 * dz) * Wa;
             const double Aaz = (a13 * dx + a23 * dy + a33 * dz) * Wa;
-            const double Abx = (F[11][q] * dx + F[12][q] * dy + F[13][q] * dz) * Sb;
-            const double Aby = (F[12][q] * dx + F[14][q] * dy + F[15][q] * dz) * Sb;
-            const double Abz = (F[13][q] * dx + F[15][q] * dy + F[16][q] * dz) * Sb;
-            const double mb = F[6][q], mXb = F[9][q], mrb = F[10][q], cb = F[8][q];
-            const double vabx = vxa - F[3][q], vaby = vya - F[4][q], vabz = vza - F[5][q];
+            const double b11 = q[F_C11 * kMomCap], b12 = q[F_C12 * kMomCap], b13 = q[F_C13 * kMomCap];
+            const double b22 = q[F_C22 * kMomCap], b23 = q[F_C23 * kMomCap], b33 = q[F_C33 * kMomCap];
+            const double Abx = (b11 * dx + b12 * dy + b13 * dz) * Sb;
+            const double Aby = (b12 * dx + b22 * dy + b23 * dz) * Sb;
+            const double Abz = (b13 * dx + b23 * dy + b33 * dz) * Sb;
+            const double mb = q[F_M * kMomCap], mXb = q[F_MX * kMomCap], mrb = q[F_MR * kMomCap];
+            const double cb = q[F_C * kMomCap];
+            const double vabx = vxa - q[F_VX * kMomCap], vaby = vya - q[F_VY * kMomCap],
+                         vabz = vza - q[F_VZ * kMomCap];
             const double vdotx = -(vabx * dx + vaby * dy + vabz * dz);  // v_ab . x_ab
-            double Pi = 0.0, w = 0.0;
-            if (vdotx < 0.0) {  // Eq. 5
-              w = vdotx * rsqrt(r2);
-              Pi = -0.5 * ph.alpha * (ca + cb - 3.0 * w) * w;
-            }
-            vs = fmax(vs, ca + cb - 3.0 * w);  // v_sig
+            // Eq. 5: w_ab = v_ab . x_ab / |x_ab|, Pi' only when approaching
+            const double w = vdotx < 0.0 ? vdotx * rsqrt(r2) : 0.0;
+            const double Pi = -0.5 * alpha * (ca + cb - 3.0 * w) * w;
+            vs = fmax(vs, ca + cb - 3.0 * w);  // v_sig; w == min(w, 0)
             // g = 1/2 m_b Pi' (A_a / rho_a + A_b / rho_b)   (Eq. 4 pair term)
             const double hp = 0.5 * Pi;
             const double mra = mb * rinva;
@@ -651,35 +800,38 @@ __global__ void __launch_bounds__(kCT, 2) k_momentum_c(
             const double gy = hp * (mra * Aay + mrb * Aby);
             const double gz = hp * (mra * Aaz + mrb * Abz);
             const double mXa = mb * Xa;
-            fx += -(mXa * Aax + mXb * Abx) - gx;  // Eq. 2 with R2
-            fy += -(mXa * Aay + mXb * Aby) - gy;
-            fz += -(mXa * Aaz + mXb * Abz) - gz;
+            fx -= fma(mXa, Aax, fma(mXb, Abx, gx));  // Eq. 2 with R2
+            fy -= fma(mXa, Aay, fma(mXb, Aby, gy));
+            fz -= fma(mXa, Aaz, fma(mXb, Abz, gz));
             fu += mXa * (vabx * Aax + vaby * Aay + vabz * Aaz) +
                   0.5 * (vabx * gx + vaby * gy + vabz * gz);  // Eq. 3 with R1, R3
-          });
-          fx = wsum(fx);
-          fy = wsum(fy);
-          fz = wsum(fz);
-          fu = wsum(fu);
-          vs = wmax(vs);
-          if (lane == 0) {
-            cur[t - t0] = c2;
-            acc[t - t0][0] += fx;
-            acc[t - t0][1] += fy;
-            acc[t - t0][2] += fz;
-            acc[t - t0][3] += fu;
-            acc[t - t0][4] = fmax(acc[t - t0][4], vs);
           }
-        }
+        } body;
+        body.F = dsm; body.T = T; body.st = &st; body.g = &g; body.alpha = ph.alpha; body.n = n;
+        body.ncoinc = &ncoinc;
+        walk_targets(t0, t1, nbr, maxn, s_n, s_cur, S.G.pend, S.slot_off, body,
+                     [&](uint32_t i, uint32_t c2) {
+                       const double a = wsum(body.fx), b = wsum(body.fy), c = wsum(body.fz);
+                       const double d = wsum(body.fu), e = wmax(body.vs);
+                       if (lane == 0) {
+                         s_cur[i] = c2;
+                         acc[0][i] += a;
+                         acc[1][i] += b;
+                         acc[2][i] += c;
+                         acc[3][i] += d;
+                         acc[4][i] = fmax(acc[4][i], e);
+                       }
+                     });
         __syncthreads();
       }
       for (uint32_t t = t0 + threadIdx.x; t < t1; t += blockDim.x) {
-        double vsig = acc[t - t0][4];
-        if (vsig < 0.0) vsig = 2.0 * src.c[t];  // no interacting neighbour
-        out.ax[t] = acc[t - t0][0];
-        out.ay[t] = acc[t - t0][1];
-        out.az[t] = acc[t - t0][2];
-        out.du[t] = acc[t - t0][3];
+        const uint32_t i = t - t0;
+        double vsig = acc[4][i];
+        if (vsig < 0.0) vsig = 2.0 * T[T_C * kTgt + i];  // no interacting neighbour
+        out.ax[t] = acc[0][i];
+        out.ay[t] = acc[1][i];
+        out.az[t] = acc[2][i];
+        out.du[t] = acc[3][i];
         out.vsig[t] = vsig;
         const double dta = ph.courant * tg.h[t] / vsig;  // R19
         if (!(dta > 0.0)) atomicAdd(&cnt[CNT_NONFINITE], 1ull);
@@ -689,7 +841,7 @@ __global__ void __launch_bounds__(kCT, 2) k_momentum_c(
     }
   }
   // block min dt -> one atomicMin per block (positive doubles order like uint64)
-  dtmin = wmax(-dtmin) * -1.0;
+  dtmin = -wmax(-dtmin);
   if (threadIdx.x == 0) shco = 0;
   __syncthreads();
   if (ncoinc) atomicAdd(&shco, ncoinc);
@@ -711,63 +863,82 @@ static int cell_grid(const sph_ctx* c, int per_sm) {
   return (int)(cells < mx ? (cells > 0 ? cells : 1) : mx);
 }
 
+static bool any_wrap2(const sph_ctx* c) {
+  // a periodic dim whose stencil spans every cell (tiny periodic extents): per-pair minimum image
+  const Grid& g = c->grid;
+  for (int d = 0; d < 3; ++d)
+    if (g.periodic[d] && 2 * stencil_radius(g, d, reach_of(c->hmax)) + 1 >= g.nc[d]) return true;
+  return false;
+}
+
+template <class K>
+static void set_smem(K kern, size_t bytes) {
+  cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes);
+}
+
 int launch_neighbors(sph_ctx* c) {
-  static bool attr = false;
-  const size_t smem = kSearchCap * sizeof(float4);
-  if (!attr) {
-    cudaFuncSetAttribute(k_search, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    attr = true;
-  }
-  k_search<<<cell_grid(c, 4), kCT, smem, c->stream>>>(
+  const size_t smem = (kSearchCap + 32) * sizeof(float4);
+  auto kern = any_wrap2(c) ? k_search<true> : k_search<false>;
+  set_smem(kern, smem);
+  kern<<<cell_grid(c, 4), kCT, smem, c->stream>>>(
       c->P.x, c->P.y, c->P.z, c->P.h, c->grid, c->s.cell_start, c->s.cell_end, c->s.cell_hmax,
       c->s.cell_list, c->s.ncell_list, c->s.nbr, c->s.ncount, c->maxn, c->s.nbr_maxcount);
   return 1;
 }
 
-int launch_density(sph_ctx* c) {
-  static bool attr = false;
+template <int N, bool W2>
+static void density_t(sph_ctx* c) {
   const size_t smem = 4 * kDensCap * sizeof(double);
-  if (!attr) {
-    cudaFuncSetAttribute(k_density_c, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    attr = true;
-  }
+  set_smem(k_density_c<N, W2>, smem);
   sph_particles& P = c->P;
-  k_density_c<<<cell_grid(c, 2), kCT, smem, c->stream>>>(
+  k_density_c<N, W2><<<cell_grid(c, 2), kCT, smem, c->stream>>>(
       P.x, P.y, P.z, P.h, P.m, P.u, c->grid, c->s.cell_start, c->s.cell_end, c->s.cell_hmax,
       c->s.cell_list, c->s.ncell_list, c->s.nbr, c->s.ncount, c->maxn, c->phys, P.rho, P.omega,
       P.p, P.c, c->s.wB, c->s.ih2, c->s.vol, c->s.rinv, c->s.X, c->s.mX, c->s.cnt);
+}
+
+int launch_density(sph_ctx* c) {
+  const bool w2 = any_wrap2(c);
+  if (c->phys.n == 6) w2 ? density_t<6, true>(c) : density_t<6, false>(c);
+  else w2 ? density_t<0, true>(c) : density_t<0, false>(c);
   return 1;
 }
 
-int launch_iad(sph_ctx* c) {
-  static bool attr = false;
+template <int N, bool W2>
+static void iad_t(sph_ctx* c) {
   const size_t smem = 4 * kDensCap * sizeof(double);
-  if (!attr) {
-    cudaFuncSetAttribute(k_iad_c, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    attr = true;
-  }
+  set_smem(k_iad_c<N, W2>, smem);
   sph_particles& P = c->P;
-  k_iad_c<<<cell_grid(c, 2), kCT, smem, c->stream>>>(
+  k_iad_c<N, W2><<<cell_grid(c, 2), kCT, smem, c->stream>>>(
       P.x, P.y, P.z, c->grid, c->s.cell_start, c->s.cell_end, c->s.cell_hmax, c->s.cell_list,
       c->s.ncell_list, c->s.nbr, c->s.ncount, c->maxn, c->phys, c->s.wB, c->s.ih2, c->s.vol,
       P.c11, P.c12, P.c13, P.c22, P.c23, P.c33, c->s.ct, c->cap, c->s.cnt);
+}
+
+int launch_iad(sph_ctx* c) {
+  const bool w2 = any_wrap2(c);
+  if (c->phys.n == 6) w2 ? iad_t<6, true>(c) : iad_t<6, false>(c);
+  else w2 ? iad_t<0, true>(c) : iad_t<0, false>(c);
   return 1;
 }
 
-int launch_momentum(sph_ctx* c) {
-  static bool attr = false;
-  const size_t smem = (size_t)kMomFields * kMomCap * sizeof(double);
-  if (!attr) {
-    cudaFuncSetAttribute(k_momentum_c, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    attr = true;
-  }
+template <int N, bool W2>
+static void momentum_t(sph_ctx* c) {
+  const size_t smem = ((size_t)kMomFields * kMomCap + (size_t)T_N * kTgt) * sizeof(double);
+  set_smem(k_momentum_c<N, W2>, smem);
   sph_particles& P = c->P;
   MomSrc src = {P.x, P.y, P.z, P.vx, P.vy, P.vz, P.m, c->s.ih2, P.c, c->s.mX, c->s.vol, c->s.ct, c->cap};
   MomTgt tg = {P.h, c->s.wB, c->s.rinv, c->s.X, P.c11, P.c12, P.c13, P.c22, P.c23, P.c33};
   MomOut out = {P.ax, P.ay, P.az, P.du, P.vsig};
-  k_momentum_c<<<cell_grid(c, 2), kCT, smem, c->stream>>>(
+  k_momentum_c<N, W2><<<cell_grid(c, 2), kCT, smem, c->stream>>>(
       src, tg, out, c->grid, c->s.cell_start, c->s.cell_end, c->s.cell_hmax, c->s.cell_list,
       c->s.ncell_list, c->s.nbr, c->s.ncount, c->maxn, c->phys, c->s.dts, c->s.cnt);
+}
+
+int launch_momentum(sph_ctx* c) {
+  const bool w2 = any_wrap2(c);
+  if (c->phys.n == 6) w2 ? momentum_t<6, true>(c) : momentum_t<6, false>(c);
+  else w2 ? momentum_t<0, true>(c) : momentum_t<0, false>(c);
   return 1;
 }
 

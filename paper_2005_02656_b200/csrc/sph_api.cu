@@ -124,6 +124,7 @@ sph_status choose_grid(sph_ctx* c, const double* bb) {
   const int64_t n = c->P.n;
   Grid& g = c->grid;
   const double hmean = bb[7] / (double)n;
+  c->hmax = bb[6];
   if (!(hmean > 0.0) || !std::isfinite(hmean) || !std::isfinite(bb[6]))
     return fail(c, SPH_ERR_NUMERIC, "non-finite or non-positive smoothing lengths");
   for (int d = 0; d < 3; ++d) {
@@ -215,6 +216,7 @@ sph_status sph_init(const sph_params* prm, int64_t capacity, sph_ctx** out) {
   ph.n = (int)nexp;
   ph.B = kernel_norm(ph.n);
   sinc_coeffs(ph.poly, ph.dpoly);
+  set_poly_constants(ph.poly, ph.dpoly);
   ph.eos = prm->eos;
   ph.omega_mode = prm->omega_mode;
   ph.alpha = prm->alpha_av;

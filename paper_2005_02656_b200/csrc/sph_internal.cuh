@@ -112,6 +112,7 @@ struct sph_ctx {
   int nblk_red = 0;
   int num_sms = 148;
   int64_t nbr_total = 0;
+  double hmax = 0.0;        // global max h of the current step (grid geometry)
   int64_t nbr_max = 0;
   sph_status status = SPH_OK;
   std::string err;
@@ -138,6 +139,7 @@ int launch_momentum(sph_ctx* c);
 int launch_dt_finalize(sph_ctx* c);
 int launch_update(sph_ctx* c);
 int launch_diag(sph_ctx* c);
+void set_poly_constants(const double* poly, const double* dpoly);
 
 inline int grid_blocks(const sph_ctx* c, int64_t work_items, int threads, int per_sm) {
   int64_t b = (work_items + threads - 1) / threads;
