@@ -27,7 +27,9 @@ constexpr int kSlots = 512;       // slot tables (R <= 3 in every dim: 343 slots
 constexpr int kMaxUnits = 128;    // staged (slot, local range) pieces per group
 constexpr int kSearchCap = 2048;  // staged candidates per group (float4)
 constexpr int kDensCap = 2048;    // staged particles per group, 4 fp64 fields
-constexpr int kMomCap = 512;      // staged particles per group, 17 fp64 fields
+constexpr int kMomCap = 1024;     // staged particles per group, 17 fp64 fields (1 CTA/SM)
+constexpr int kCTM = 512;         // momentum CTA: 16 warps, one CTA per SM
+constexpr int kNWM = kCTM / 32;
 constexpr int kMomFields = 17;
 constexpr uint32_t kSent = 0xffffffffu;
 
@@ -72,6 +74,27 @@ __device__ __forceinline__ double wmax(double v) {
 #pragma unroll
   for (int o = 16; o; o >>= 1) v = fmax(v, __shfl_xor_sync(0xffffffffu, v, o));
   return v;
+}
+
+// Sum NV (power of two) per-lane values over the warp by transpose-reduce: each
+// exchange step halves the values a lane keeps, so the cost is NV-1+log2(32/NV)
+// shuffles instead of NV*5.  On return v[0] of lane k*(32/NV) holds the sum of
+// value k (lanes in between hold the same sums).
+template <int NV>
+__device__ __forceinline__ void warp_multi_sum(double (&v)[NV]) {
+  const int lane = threadIdx.x & 31;
+#pragma unroll
+  for (int cnt = NV, off = 16; cnt > 1; cnt >>= 1, off >>= 1) {
+    const bool upper = (lane & off) != 0;
+#pragma unroll
+    for (int i = 0; i < cnt / 2; ++i) {
+      const double send = upper ? v[i] : v[i + cnt / 2];
+      const double keep = upper ? v[i + cnt / 2] : v[i];
+      v[i] = keep + __shfl_xor_sync(0xffffffffu, send, off);
+    }
+  }
+#pragma unroll
+  for (int off = 16 / NV; off > 0; off >>= 1) v[0] += __shfl_xor_sync(0xffffffffu, v[0], off);
 }
 
 __device__ __forceinline__ double sinc_poly(double t) {
@@ -180,7 +203,7 @@ __device__ __forceinline__ void shifts_of(const Grid& g, const CellSm& S, int sl
 // Warp-level walk over the entries of target rows that fall in the current
 // group [.., pend).  Row chunks are prefetched one chunk ahead; the first chunk
 // of the warp's next target is issued before the current target's work.
-template <class Body, class Finish>
+template <int NW, class Body, class Finish>
 __device__ __forceinline__ void walk_targets(uint32_t t0, uint32_t t1, const uint32_t* __restrict__ nbr,
                                              int maxn, const uint32_t* s_n, uint32_t* s_cur,
                                              uint32_t pend, const int* slot_off, Body&& body,
@@ -192,14 +215,14 @@ __device__ __forceinline__ void walk_targets(uint32_t t0, uint32_t t1, const uin
     const uint32_t c0 = s_cur[t - t0];
     ef = c0 + lane < s_n[t - t0] ? nbr[(size_t)t * maxn + c0 + lane] : kSent;
   }
-  for (; t < t1; t += kNW) {
+  for (; t < t1; t += NW) {
     const uint32_t i = t - t0;
     const uint32_t n = s_n[i];
     const uint32_t* row = nbr + (size_t)t * maxn;
     uint32_t cur = s_cur[i];
     uint32_t e = ef;
     // prefetch the next target's first chunk
-    const uint32_t tn = t + kNW;
+    const uint32_t tn = t + NW;
     if (tn < t1) {
       const uint32_t cn = s_cur[tn - t0];
       ef = cn + lane < s_n[tn - t0] ? nbr[(size_t)tn * maxn + cn + lane] : kSent;
@@ -287,54 +310,79 @@ __global__ void __launch_bounds__(kCT) k_search(const double* __restrict__ x,
         for (int q = total + threadIdx.x; q < padded; q += blockDim.x)
           cand[q] = make_float4(INFINITY, INFINITY, INFINITY, __uint_as_float(kSent));
         __syncthreads();
-        for (uint32_t t = t0 + warp; t < t1; t += kNW) {
-          const double xa = x[t], ya = y[t], za = z[t], ha = h[t];
-          const double tha = 2.0 * ha;
-          const double lim = __dmul_rn(tha, tha);
-          // fp32 error band: |r2_32 - r2| <= delta lim, delta = 2^-20 (2 + 2 M/h + 2^-20 (M/h)^2)
-          const double mh = M / ha;
-          const double delta = 0x1p-20 * (2.0 + 2.0 * mh + 0x1p-20 * mh * mh);
-          float lo32 = -1.0f, hi32 = INFINITY;
-          if (delta < 0.25) {
-            lo32 = (float)(lim * (1.0 - delta));
-            hi32 = (float)(lim * (1.0 + delta));
+        // two targets per warp share every staged-candidate load
+        for (uint32_t ta = t0 + 2 * warp; ta < t1; ta += 2 * kNW) {
+          const uint32_t tb = ta + 1 < t1 ? ta + 1 : ta;  // odd tail: duplicate, not stored
+          const bool has_b = ta + 1 < t1;
+          float lo32[2], hi32[2], px[2], py[2], pz[2];
+          double lim[2], pos[2][3];
+          uint32_t self_pk[2], count[2];
+          uint32_t* row[2];
+#pragma unroll
+          for (int s = 0; s < 2; ++s) {
+            const uint32_t t = s ? tb : ta;
+            pos[s][0] = x[t];
+            pos[s][1] = y[t];
+            pos[s][2] = z[t];
+            const double ha = h[t];
+            const double tha = 2.0 * ha;
+            lim[s] = __dmul_rn(tha, tha);
+            // fp32 error band: |r2_32 - r2| <= delta lim, delta = 2^-20 (2 + 2 M/h + 2^-20 (M/h)^2)
+            const double mh = M / ha;
+            const double delta = 0x1p-20 * (2.0 + 2.0 * mh + 0x1p-20 * mh * mh);
+            lo32[s] = -1.0f;
+            hi32[s] = INFINITY;
+            if (delta < 0.25) {
+              lo32[s] = (float)(lim[s] * (1.0 - delta));
+              hi32[s] = (float)(lim[s] * (1.0 + delta));
+            }
+            px[s] = (float)(pos[s][0] - org[0]);
+            py[s] = (float)(pos[s][1] - org[1]);
+            pz[s] = (float)(pos[s][2] - org[2]);
+            self_pk[s] = ((uint32_t)S.kself << kLocalBits) | (t - S.sc);
+            count[s] = tcount[t - t0];
+            row[s] = nbr + (size_t)t * maxn;
           }
-          const float ax = (float)(xa - org[0]), ay = (float)(ya - org[1]), az = (float)(za - org[2]);
-          const uint32_t self_pk = ((uint32_t)S.kself << kLocalBits) | (t - S.sc);
-          uint32_t count = tcount[t - t0];
-          uint32_t* row = nbr + (size_t)t * maxn;
           for (int q0 = 0; q0 < padded; q0 += 32) {
             const float4 cd = cand[q0 + lane];
-            float dx = cd.x - ax, dy = cd.y - ay, dz = cd.z - az;
-            if constexpr (W2) {
-              const float L0 = (float)g.L[0], L1 = (float)g.L[1], L2 = (float)g.L[2];
-              if (st.wrap[0] == 2) dx = dx > 0.5f * L0 ? dx - L0 : (dx < -0.5f * L0 ? dx + L0 : dx);
-              if (st.wrap[1] == 2) dy = dy > 0.5f * L1 ? dy - L1 : (dy < -0.5f * L1 ? dy + L1 : dy);
-              if (st.wrap[2] == 2) dz = dz > 0.5f * L2 ? dz - L2 : (dz < -0.5f * L2 ? dz + L2 : dz);
-            }
-            const float r2 = fmaf(dz, dz, fmaf(dy, dy, dx * dx));
             const uint32_t pk = __float_as_uint(cd.w);
-            bool hit = (r2 < lo32) & (pk != self_pk);
-            const bool amb = (r2 >= lo32) & (r2 < hi32);
-            if (__any_sync(0xffffffffu, amb)) {  // rare: exact fp64 test in the oracle's association
-              if (amb) {
-                const uint32_t j = S.t_start[pk >> kLocalBits] + (pk & kLocalMask);
-                if (j != t) {
-                  double ex = __dsub_rn(x[j], xa), ey = __dsub_rn(y[j], ya), ez = __dsub_rn(z[j], za);
-                  if (g.periodic[0]) ex = min_img(ex, g.L[0]);
-                  if (g.periodic[1]) ey = min_img(ey, g.L[1]);
-                  if (g.periodic[2]) ez = min_img(ez, g.L[2]);
-                  const double r2e = __dadd_rn(__dadd_rn(__dmul_rn(ex, ex), __dmul_rn(ey, ey)), __dmul_rn(ez, ez));
-                  hit = r2e < lim;
+#pragma unroll
+            for (int s = 0; s < 2; ++s) {
+              float dx = cd.x - px[s], dy = cd.y - py[s], dz = cd.z - pz[s];
+              if constexpr (W2) {
+                const float L0 = (float)g.L[0], L1 = (float)g.L[1], L2 = (float)g.L[2];
+                if (st.wrap[0] == 2) dx = dx > 0.5f * L0 ? dx - L0 : (dx < -0.5f * L0 ? dx + L0 : dx);
+                if (st.wrap[1] == 2) dy = dy > 0.5f * L1 ? dy - L1 : (dy < -0.5f * L1 ? dy + L1 : dy);
+                if (st.wrap[2] == 2) dz = dz > 0.5f * L2 ? dz - L2 : (dz < -0.5f * L2 ? dz + L2 : dz);
+              }
+              const float r2 = fmaf(dz, dz, fmaf(dy, dy, dx * dx));
+              bool hit = (r2 < lo32[s]) & (pk != self_pk[s]);
+              const bool amb = (r2 >= lo32[s]) & (r2 < hi32[s]);
+              if (__ballot_sync(0xffffffffu, amb)) {  // rare: exact fp64 test, oracle's association
+                if (amb) {
+                  const uint32_t j = S.t_start[pk >> kLocalBits] + (pk & kLocalMask);
+                  const uint32_t t = s ? tb : ta;
+                  if (j != t) {
+                    double ex = __dsub_rn(x[j], pos[s][0]), ey = __dsub_rn(y[j], pos[s][1]),
+                           ez = __dsub_rn(z[j], pos[s][2]);
+                    if (g.periodic[0]) ex = min_img(ex, g.L[0]);
+                    if (g.periodic[1]) ey = min_img(ey, g.L[1]);
+                    if (g.periodic[2]) ez = min_img(ez, g.L[2]);
+                    const double r2e = __dadd_rn(__dadd_rn(__dmul_rn(ex, ex), __dmul_rn(ey, ey)), __dmul_rn(ez, ez));
+                    hit = r2e < lim[s];
+                  }
                 }
               }
+              const unsigned b = __ballot_sync(0xffffffffu, hit);
+              const uint32_t p = count[s] + __popc(b & lt);
+              if (hit && p < (uint32_t)maxn) row[s][p] = pk;
+              count[s] += __popc(b);
             }
-            const unsigned b = __ballot_sync(0xffffffffu, hit);
-            const uint32_t p = count + __popc(b & lt);
-            if (hit && p < (uint32_t)maxn) row[p] = pk;
-            count += __popc(b);
           }
-          if (lane == 0) tcount[t - t0] = count;
+          if (lane == 0) {
+            tcount[ta - t0] = count[0];
+            if (has_b) tcount[tb - t0] = count[1];
+          }
         }
         __syncthreads();
       }
@@ -464,15 +512,16 @@ __global__ void __launch_bounds__(kCT) k_density_c(
         body.sx = sx; body.sy = sy; body.sz = sz; body.sm = sm;
         body.tx = tx; body.ty = ty; body.tz = tz; body.tih2 = tih2;
         body.st = &st; body.g = &g; body.n = n;
-        walk_targets(t0, t1, nbr, maxn, s_n, s_cur, S.G.pend, S.slot_off, body,
-                     [&](uint32_t i, uint32_t c2) {
-                       const double a = wsum(body.sr), b = wsum(body.sd);
-                       if (lane == 0) {
-                         s_cur[i] = c2;
-                         acc0[i] += a;
-                         acc1[i] += b;
-                       }
-                     });
+        walk_targets<kNW>(t0, t1, nbr, maxn, s_n, s_cur, S.G.pend, S.slot_off, body,
+                          [&](uint32_t i, uint32_t c2) {
+                            double v[2] = {body.sr, body.sd};
+                            warp_multi_sum<2>(v);
+                            if (lane == 0) {
+                              s_cur[i] = c2;
+                              acc0[i] += v[0];
+                            }
+                            if (lane == 16) acc1[i] += v[0];
+                          });
         __syncthreads();
       }
       for (uint32_t t = t0 + threadIdx.x; t < t1; t += blockDim.x) {
@@ -593,16 +642,14 @@ __global__ void __launch_bounds__(kCT) k_iad_c(
         body.sx = sx; body.sy = sy; body.sz = sz; body.sv = sv;
         body.tx = tx; body.ty = ty; body.tz = tz; body.tih2 = tih2;
         body.st = &st; body.g = &g; body.n = n;
-        walk_targets(t0, t1, nbr, maxn, s_n, s_cur, S.G.pend, S.slot_off, body,
-                     [&](uint32_t i, uint32_t c2) {
-                       const double a11 = wsum(body.t11), a12 = wsum(body.t12), a13 = wsum(body.t13);
-                       const double a22 = wsum(body.t22), a23 = wsum(body.t23), a33 = wsum(body.t33);
-                       if (lane == 0) {
-                         s_cur[i] = c2;
-                         acc[0][i] += a11; acc[1][i] += a12; acc[2][i] += a13;
-                         acc[3][i] += a22; acc[4][i] += a23; acc[5][i] += a33;
-                       }
-                     });
+        walk_targets<kNW>(t0, t1, nbr, maxn, s_n, s_cur, S.G.pend, S.slot_off, body,
+                          [&](uint32_t i, uint32_t c2) {
+                            double v[8] = {body.t11, body.t12, body.t13, body.t22,
+                                           body.t23, body.t33, 0.0, 0.0};
+                            warp_multi_sum<8>(v);
+                            if ((lane & 3) == 0 && lane < 24) acc[lane >> 2][i] += v[0];
+                            if (lane == 0) s_cur[i] = c2;
+                          });
         __syncthreads();
       }
       for (uint32_t t = t0 + threadIdx.x; t < t1; t += blockDim.x) {
@@ -657,7 +704,7 @@ enum { F_X, F_Y, F_Z, F_VX, F_VY, F_VZ, F_M, F_IH2, F_C, F_MX, F_MR, F_C11, F_C1
 enum { T_X, T_Y, T_Z, T_VX, T_VY, T_VZ, T_IH2, T_WB, T_RINV, T_XP, T_C, T_A11, T_A12, T_A13, T_A22, T_A23, T_A33, T_N };
 
 template <int N, bool W2>
-__global__ void __launch_bounds__(kCT, 2) k_momentum_c(
+__global__ void __launch_bounds__(kCTM, 1) k_momentum_c(
     MomSrc src, MomTgt tg, MomOut out, Grid g, const uint32_t* __restrict__ cstart,
     const uint32_t* __restrict__ cend, const unsigned long long* __restrict__ chmax,
     const uint32_t* __restrict__ clist, const uint32_t* __restrict__ nclist,
@@ -668,7 +715,7 @@ __global__ void __launch_bounds__(kCT, 2) k_momentum_c(
   __shared__ CellSm S;
   __shared__ uint32_t s_n[kTgt], s_cur[kTgt];
   __shared__ double acc[5][kTgt];
-  __shared__ double shdt[kNW];
+  __shared__ double shdt[kNWM];
   __shared__ unsigned long long shco;
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const uint32_t ncl = *nclist;
@@ -716,7 +763,7 @@ __global__ void __launch_bounds__(kCT, 2) k_momentum_c(
         if (threadIdx.x == 0) build_group(S, kMomCap);
         __syncthreads();
         if (S.G.nu == 0) break;
-        for (int uu = warp; uu < S.G.nu; uu += kNW) {
+        for (int uu = warp; uu < S.G.nu; uu += kNWM) {
           const int base = S.G.u_base[uu], len = S.G.u_len[uu];
           const uint32_t g0 = S.G.u_g[uu];
           double sh[3];
@@ -765,10 +812,10 @@ __global__ void __launch_bounds__(kCT, 2) k_momentum_c(
             double dx = q[F_X * kMomCap] - xa, dy = q[F_Y * kMomCap] - ya, dz = q[F_Z * kMomCap] - za;
             delta3<W2>(*st, *g, dx, dy, dz);  // Delta_ab = x_b - x_a
             const double r2 = dx * dx + dy * dy + dz * dz;
-            if (r2 == 0.0) {  // coincident pair: skipped, counted
-              ++*ncoinc;
-              return;
-            }
+            // coincident pair: Delta = 0 zeroes every term below; it is only
+            // kept out of v_sig and counted (no branch)
+            const bool coinc = r2 == 0.0;
+            *ncoinc += coinc;
             const double ta = r2 * ih2a;
             const double Sa = ipow<N>(sinc_poly(ta), n);
             const double Wa = wBa * Sa;
@@ -792,7 +839,8 @@ __global__ void __launch_bounds__(kCT, 2) k_momentum_c(
             // Eq. 5: w_ab = v_ab . x_ab / |x_ab|, Pi' only when approaching
             const double w = vdotx < 0.0 ? vdotx * rsqrt(r2) : 0.0;
             const double Pi = -0.5 * alpha * (ca + cb - 3.0 * w) * w;
-            vs = fmax(vs, ca + cb - 3.0 * w);  // v_sig; w == min(w, 0)
+            const double vsab = coinc ? -1.0 : ca + cb - 3.0 * w;  // v_sig; w == min(w, 0)
+            vs = vsab > vs ? vsab : vs;
             // g = 1/2 m_b Pi' (A_a / rho_a + A_b / rho_b)   (Eq. 4 pair term)
             const double hp = 0.5 * Pi;
             const double mra = mb * rinva;
@@ -809,19 +857,17 @@ __global__ void __launch_bounds__(kCT, 2) k_momentum_c(
         } body;
         body.F = dsm; body.T = T; body.st = &st; body.g = &g; body.alpha = ph.alpha; body.n = n;
         body.ncoinc = &ncoinc;
-        walk_targets(t0, t1, nbr, maxn, s_n, s_cur, S.G.pend, S.slot_off, body,
-                     [&](uint32_t i, uint32_t c2) {
-                       const double a = wsum(body.fx), b = wsum(body.fy), c = wsum(body.fz);
-                       const double d = wsum(body.fu), e = wmax(body.vs);
-                       if (lane == 0) {
-                         s_cur[i] = c2;
-                         acc[0][i] += a;
-                         acc[1][i] += b;
-                         acc[2][i] += c;
-                         acc[3][i] += d;
-                         acc[4][i] = fmax(acc[4][i], e);
-                       }
-                     });
+        walk_targets<kNWM>(t0, t1, nbr, maxn, s_n, s_cur, S.G.pend, S.slot_off, body,
+                           [&](uint32_t i, uint32_t c2) {
+                             double v[4] = {body.fx, body.fy, body.fz, body.fu};
+                             warp_multi_sum<4>(v);
+                             const double e = wmax(body.vs);
+                             if ((lane & 7) == 0) acc[lane >> 3][i] += v[0];
+                             if (lane == 0) {
+                               s_cur[i] = c2;
+                               acc[4][i] = fmax(acc[4][i], e);
+                             }
+                           });
         __syncthreads();
       }
       for (uint32_t t = t0 + threadIdx.x; t < t1; t += blockDim.x) {
@@ -849,7 +895,7 @@ __global__ void __launch_bounds__(kCT, 2) k_momentum_c(
   __syncthreads();
   if (threadIdx.x == 0) {
     double mn = shdt[0];
-    for (int q = 1; q < kNW; ++q) mn = fmin(mn, shdt[q]);
+    for (int q = 1; q < kNWM; ++q) mn = fmin(mn, shdt[q]);
     if (mn > 0.0)
       atomicMin((unsigned long long*)&dts[DT_RAW_BITS], (unsigned long long)__double_as_longlong(mn));
     if (shco) atomicAdd(&cnt[CNT_COINCIDENT], shco);
@@ -930,7 +976,7 @@ static void momentum_t(sph_ctx* c) {
   MomSrc src = {P.x, P.y, P.z, P.vx, P.vy, P.vz, P.m, c->s.ih2, P.c, c->s.mX, c->s.vol, c->s.ct, c->cap};
   MomTgt tg = {P.h, c->s.wB, c->s.rinv, c->s.X, P.c11, P.c12, P.c13, P.c22, P.c23, P.c33};
   MomOut out = {P.ax, P.ay, P.az, P.du, P.vsig};
-  k_momentum_c<N, W2><<<cell_grid(c, 2), kCT, smem, c->stream>>>(
+  k_momentum_c<N, W2><<<cell_grid(c, 1), kCTM, smem, c->stream>>>(
       src, tg, out, c->grid, c->s.cell_start, c->s.cell_end, c->s.cell_hmax, c->s.cell_list,
       c->s.ncell_list, c->s.nbr, c->s.ncount, c->maxn, c->phys, c->s.dts, c->s.cnt);
 }
