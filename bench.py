@@ -44,9 +44,10 @@ def workload(name: str, G: int, rank: int):
     if name == "weak":  # config 5: 292 x 292 x (292 G), slab per rank
         d = I.square_patch_weak(292, G, rank if G > 1 else None)
         desc = f"config5 weak-scaling square patch 292x292x{292 * G}, {292 ** 3} particles/GPU"
-    elif name == "patch27m":  # config 4 (strong scaling)
-        d = I.square_patch(300)
-        desc = "config4 square patch 300^3 = 27M particles"
+    elif name == "patch27m":  # config 4 (strong scaling): z-slab of the 300^3 patch per rank
+        zl = (rank * 300 // G, (rank + 1) * 300 // G) if G > 1 else None
+        d = I.square_patch(300, z_layers=zl)
+        desc = f"config4 square patch 300^3 = 27M particles over {G} GPU(s)"
     elif name == "patch1m":  # config 2
         d = I.square_patch(100)
         desc = "config2 square patch 100^3 = 1M particles"
@@ -204,19 +205,18 @@ def run_ours(args):
     import numpy as np
     import torch
 
+    from paper_2005_02656_b200 import dist as D
     from paper_2005_02656_b200 import sph
-    world, rank, local = dist_env()
-    if world > 1:
-        import torch.distributed as dist
-        torch.cuda.set_device(local)
-        dist.init_process_group("nccl", init_method="env://")
-    else:
-        torch.cuda.set_device(0)
+    world, rank, local = D.init("nccl")
+    uid = D.share_unique_id(rank, world)
     d, desc = workload(args.workload, max(world, 1), rank)
     n_local = d["x"].size
+    # room for halos + migrants (multi-GPU); a single GPU needs exactly n
+    cap = n_local if world == 1 else int(n_local * 1.25) + 4096
     stream = torch.cuda.Stream()
     with torch.cuda.stream(stream):
-        sim = sph.Simulation(d, stream=stream.cuda_stream)
+        sim = sph.Simulation(d, capacity=cap, stream=stream.cuda_stream, rank=rank, nranks=world,
+                             unique_id=uid)
         for _ in range(args.warmup):
             sim.step()
         torch.cuda.synchronize()
@@ -279,7 +279,7 @@ def run_ours(args):
     line = {
         "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": max(world, 1),
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms_step,
-        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+        "higher_is_better": True, "scaling": "strong" if args.workload == "patch27m" else "weak", "vs_baseline": None, "dtype": "f64",
         "data": "synthetic",
         "config": {"workload": workload_label(args), "description": desc,
                    "particles_per_gpu": n_local, "particles_total": n_total,

@@ -132,7 +132,11 @@ sph_status  sph_step(sph_ctx* ctx, double* dt_out);             /* a1-a13       
  * sph_upload also sets n.  Both are stream-ordered; sph_download synchronises. */
 sph_status  sph_upload(sph_ctx* ctx, const sph_particles* host);
 sph_status  sph_download(sph_ctx* ctx, sph_particles* host);
-/* Conserved sums and counters ("tracking total momentum and energy").  Synchronises. */
+/* Particles currently owned by this rank (== the attached arrays' valid prefix; it changes
+ * when particles migrate between ranks) and halo particles held during the current step. */
+sph_status  sph_local_count(const sph_ctx* ctx, int64_t* n_owned, int64_t* n_halo);
+/* Conserved sums and counters ("tracking total momentum and energy"), summed over all
+ * ranks when nranks > 1 (n_owned is then the global particle count).  Synchronises. */
 sph_status  sph_diagnostics(sph_ctx* ctx, sph_diag* out);
 /* Phase timing: on != 0 records CUDA events around every phase; ms_out[SPH_PH_COUNT]
  * receives the accumulated milliseconds and launch counts since the last reset. */
@@ -140,6 +144,16 @@ sph_status  sph_set_profiling(sph_ctx* ctx, int on);
 sph_status  sph_phase_times(sph_ctx* ctx, double* ms_out, int64_t* launches_out, int reset);
 const char* sph_error_string(const sph_ctx* ctx);
 sph_status  sph_destroy(sph_ctx* ctx);
+/* Multi-GPU bootstrap: write rank 0's 128-byte ncclUniqueId to out (host memory, size >= 128).
+ * The caller broadcasts it (e.g. torch.distributed) and passes it as params.nccl_unique_id
+ * to sph_init on every rank (one process per GPU).  SPH_ERR_CONFIG if built without NCCL. */
+sph_status  sph_nccl_unique_id(void* out, int size);
+/* Host-side decomposition helpers (no GPU needed; used by the library and by CPU tests).
+ * splitters: rank r owns key-prefix bins [split[r], split[r+1]) of a global histogram
+ * hist[nbins], split[G+1] at equal particle counts (the paper's global tree + bucket rule,
+ * P:194-197).  owner: the rank owning a bin. */
+int         sph_decomp_splitters(const int64_t* hist, int64_t nbins, int G, int64_t* split);
+int         sph_decomp_owner(const int64_t* split, int G, int64_t bin);
 /* Utility (not a step of the method): measured FP64 DFMA throughput of this GPU in
  * TFLOP/s (FMA = 2 flops), the roofline denominator of the FP64-bound pair passes.
  * Launches on `stream` (a cudaStream_t) and synchronises it. */

@@ -114,10 +114,13 @@ __global__ void k_keys(const double* __restrict__ x, const double* __restrict__ 
   }
 }
 
-int launch_keys(sph_ctx* c) {
-  int64_t n = c->P.n;
-  k_keys<<<grid_blocks(c, n, 256, 8), 256, 0, c->stream>>>(c->P.x, c->P.y, c->P.z, c->P.id, n,
-                                                          c->grid, c->s.keys, c->s.idx);
+int launch_keys(sph_ctx* c) { return launch_keys_range(c, 0, c->P.n); }
+
+int launch_keys_range(sph_ctx* c, int64_t i0, int64_t n) {
+  if (n <= 0) return 0;
+  k_keys<<<grid_blocks(c, n, 256, 8), 256, 0, c->stream>>>(c->P.x + i0, c->P.y + i0, c->P.z + i0,
+                                                          c->P.id + i0, n, c->grid, c->s.keys + i0,
+                                                          c->s.idx + i0);
   return 1;
 }
 
@@ -398,10 +401,37 @@ __global__ void k_cell_hmax(const uint32_t* __restrict__ list, const uint32_t* _
   }
 }
 
+// cell ranges of the halo segment [i0, i0 + n) (sorted; cells disjoint from owned ones)
+__global__ void k_cells_range(const uint64_t* __restrict__ keys, int64_t i0, int64_t n, Grid g,
+                              uint32_t* __restrict__ cstart, uint32_t* __restrict__ cend) {
+  for (int64_t k = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; k < n;
+       k += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t i = i0 + k;
+    const int64_t c = key_cell(g, keys[i]);
+    if (k == 0 || key_cell(g, keys[i - 1]) != c) cstart[c] = (uint32_t)i;
+    if (k == n - 1 || key_cell(g, keys[i + 1]) != c) cend[c] = (uint32_t)(i + 1);
+  }
+}
+
+int launch_cells_halo(sph_ctx* c, int64_t i0, int64_t n) {
+  if (n <= 0) return 0;
+  k_cells_range<<<grid_blocks(c, n, 256, 8), 256, 0, c->stream>>>(c->s.keys, i0, n, c->grid,
+                                                                 c->s.cell_start, c->s.cell_end);
+  return 1;
+}
+
+int scan_u32(sph_ctx* c, const uint32_t* in, uint32_t* out, int64_t n) {
+  return n > 0 ? scan_excl(c, in, out, n) : 0;
+}
+
 int launch_cells(sph_ctx* c) {
   const int64_t n = c->P.n;
   cudaMemsetAsync(c->s.cell_start, 0, sizeof(uint32_t) * c->grid.ncell, c->stream);
   cudaMemsetAsync(c->s.cell_end, 0, sizeof(uint32_t) * c->grid.ncell, c->stream);
+  if (n == 0) {  // a rank may own no particle
+    cudaMemsetAsync(c->s.ncell_list, 0, sizeof(uint32_t), c->stream);
+    return 0;
+  }
   const int nb = grid_blocks(c, n, 256, 8);
   k_cells<<<nb, 256, 0, c->stream>>>(c->s.keys, n, c->grid, c->s.cell_start, c->s.cell_end,
                                      c->s.cell_flag);

@@ -6,6 +6,7 @@
 #include <cstring>
 #include <string>
 
+#include "sph_dist.cuh"
 #include "stencil.cuh"
 
 using namespace sphb;
@@ -119,9 +120,8 @@ sph_status dalloc(sph_ctx* c, T** p, size_t count) {
   return SPH_OK;
 }
 
-sph_status choose_grid(sph_ctx* c, const double* bb) {
+sph_status choose_grid(sph_ctx* c, const double* bb, int64_t n) {
   const sph_params& q = c->prm;
-  const int64_t n = c->P.n;
   Grid& g = c->grid;
   const double hmean = bb[7] / (double)n;
   c->hmax = bb[6];
@@ -196,7 +196,8 @@ sph_status sph_init(const sph_params* prm, int64_t capacity, sph_ctx** out) {
   double nexp = prm->sinc_n;
   if (!(nexp >= 3.0 && nexp <= 9.0 && nexp == std::floor(nexp))) return SPH_ERR_CONFIG;
   if (capacity < 1 || capacity > 0xffffffffLL) return SPH_ERR_CONFIG;
-  if (prm->nranks != 1) return SPH_ERR_CONFIG;  // multi-rank context: see sph_dist.cu
+  if (prm->nranks < 1 || prm->rank < 0 || prm->rank >= prm->nranks) return SPH_ERR_CONFIG;
+  if (prm->nranks > 1 && !prm->nccl_unique_id) return SPH_ERR_CONFIG;
   for (int d = 0; d < 3; ++d)
     if (prm->periodic[d] && !(prm->box_hi[d] > prm->box_lo[d])) return SPH_ERR_CONFIG;
   if (prm->eos != SPH_EOS_LINEAR && prm->eos != SPH_EOS_IDEAL) return SPH_ERR_CONFIG;
@@ -294,6 +295,11 @@ sph_status sph_init(const sph_params* prm, int64_t capacity, sph_ctx** out) {
     *out = c;
     return SPH_ERR_CUDA;
   }
+  if (prm->nranks > 1 && !dist_init(c, prm)) {  // NCCL communicator + exchange buffers
+    fail(c, SPH_ERR_COMM, c->dist_err);
+    *out = c;
+    return SPH_ERR_COMM;
+  }
   *out = c;
   return SPH_OK;
 }
@@ -316,27 +322,8 @@ sph_status sph_attach(sph_ctx* c, const sph_particles* p) {
   return SPH_OK;
 }
 
-sph_status sph_find_neighbors(sph_ctx* c) {
-  if (!c) return SPH_ERR_CONFIG;
-  if (c->status != SPH_OK) return c->status;
-  if (!c->attached) return fail(c, SPH_ERR_STATE, "no particles attached");
-  const int64_t n = c->P.n;
-  c->stage = 0;
-  if (n == 0) {
-    c->nbr_total = c->nbr_max = 0;
-    c->stage = 1;
-    return SPH_OK;
-  }
-  double bb[16];
-  {
-    Phase ph(c, SPH_PH_BBOX);
-    int k = launch_bbox(c);
-    CKL();
-    ph.done(k);
-  }
-  CK(cudaMemcpyAsync(bb, c->s.bbox, 9 * sizeof(double), cudaMemcpyDeviceToHost, c->stream));
-  CK(cudaStreamSynchronize(c->stream));
-  if (choose_grid(c, bb) != SPH_OK) return c->status;
+static sph_status sort_owned(sph_ctx* c) {  // a1-a2 on [0, P.n): keys, radix sort, permutation
+  if (c->P.n == 0) return SPH_OK;
   const int nbits = 3 * c->grid.cbits + c->grid.idbits;
   {
     Phase ph(c, SPH_PH_KEYS);
@@ -357,14 +344,70 @@ sph_status sph_find_neighbors(sph_ctx* c) {
     CKL();
     ph.done(k);
   }
+  return SPH_OK;
+}
+
+sph_status sph_find_neighbors(sph_ctx* c) {
+  if (!c) return SPH_ERR_CONFIG;
+  if (c->status != SPH_OK) return c->status;
+  if (!c->attached) return fail(c, SPH_ERR_STATE, "no particles attached");
+  const bool multi = c->dist != nullptr;
+  c->stage = 0;
+  c->n_halo = 0;
+  if (!multi && c->P.n == 0) {
+    c->nbr_total = c->nbr_max = 0;
+    CK(cudaMemsetAsync(c->s.ncell_list, 0, sizeof(uint32_t), c->stream));
+    c->stage = 1;
+    return SPH_OK;
+  }
+  double bb[16];
+  {
+    Phase ph(c, SPH_PH_BBOX);
+    int k = launch_bbox(c);
+    CKL();
+    ph.done(k);
+  }
+  int64_t n_total = c->P.n;
+  if (multi) {  // global domain size + h statistics (P:194 allreduce)
+    if (!dist_global_bbox(c, bb)) return fail(c, SPH_ERR_COMM, c->dist_err);
+    n_total = dist_n_total(c);
+  } else {
+    CK(cudaMemcpyAsync(bb, c->s.bbox, 9 * sizeof(double), cudaMemcpyDeviceToHost, c->stream));
+    CK(cudaStreamSynchronize(c->stream));
+  }
+  if (n_total == 0) {
+    c->stage = 1;
+    return SPH_OK;
+  }
+  if (choose_grid(c, bb, n_total) != SPH_OK) return c->status;
+  if (sort_owned(c) != SPH_OK) return c->status;
+  if (multi) {  // a14: splitters from the global key histogram, migration
+    bool moved = false;
+    {
+      Phase ph(c, SPH_PH_HALO);
+      if (!dist_splitters(c) || !dist_migrate(c, &moved)) return fail(c, SPH_ERR_COMM, c->dist_err);
+      CKL();
+      ph.done(0);
+    }
+    if (moved && sort_owned(c) != SPH_OK) return c->status;
+  }
   {
     Phase ph(c, SPH_PH_CELLS);
     int k = launch_cells(c);
     CKL();
     ph.done(k);
   }
+  if (multi) {  // a4: halo identification + exchange #1
+    Phase ph(c, SPH_PH_HALO);
+    if (!dist_halo_plan_and_exchange1(c)) return fail(c, SPH_ERR_COMM, c->dist_err);
+    c->n_halo = dist_n_halo(c);
+    int k = launch_keys_range(c, c->P.n, c->n_halo);
+    k += launch_cells_halo(c, c->P.n, c->n_halo);
+    CKL();
+    ph.done(k);
+  }
   CK(cudaMemsetAsync(c->s.nbr_maxcount, 0, sizeof(unsigned int), c->stream));
-  {
+  if (c->P.n) {
     Phase ph(c, SPH_PH_NEIGHBORS);
     int k = launch_neighbors(c);
     CKL();
@@ -387,11 +430,12 @@ sph_status sph_get_neighbors(sph_ctx* c, int64_t* offsets, int64_t* ids, int64_t
   if (c->stage < 1) return fail(c, SPH_ERR_STATE, "sph_get_neighbors before sph_find_neighbors");
   const int64_t n = c->P.n;
   std::vector<uint32_t> cnt(n > 0 ? n : 1);
-  std::vector<int64_t> id(n > 0 ? n : 1);
+  const int64_t nl = n + c->n_halo;  // neighbours may be halo particles
+  std::vector<int64_t> id(nl > 0 ? nl : 1);
   CK(cudaStreamSynchronize(c->stream));
   if (n) {
     CK(cudaMemcpy(cnt.data(), c->s.ncount, sizeof(uint32_t) * n, cudaMemcpyDeviceToHost));
-    CK(cudaMemcpy(id.data(), c->P.id, sizeof(int64_t) * n, cudaMemcpyDeviceToHost));
+    CK(cudaMemcpy(id.data(), c->P.id, sizeof(int64_t) * nl, cudaMemcpyDeviceToHost));
   }
   offsets[0] = 0;
   for (int64_t i = 0; i < n; ++i) offsets[i + 1] = offsets[i] + cnt[i];
@@ -442,6 +486,11 @@ sph_status sph_density(sph_ctx* c) {
     CKL();
     ph.done(k);
   }
+  if (c->dist) {  // a7: halo exchange #2 (R21)
+    Phase ph(c, SPH_PH_HALO);
+    if (!dist_exchange2(c)) return fail(c, SPH_ERR_COMM, c->dist_err);
+    ph.done(0);
+  }
   c->stage = 2;
   return SPH_OK;
 }
@@ -456,6 +505,11 @@ sph_status sph_iad(sph_ctx* c) {
     CKL();
     ph.done(k);
   }
+  if (c->dist) {  // a9: halo exchange #3 (R21)
+    Phase ph(c, SPH_PH_HALO);
+    if (!dist_exchange3(c)) return fail(c, SPH_ERR_COMM, c->dist_err);
+    ph.done(0);
+  }
   c->stage = 3;
   return SPH_OK;
 }
@@ -467,6 +521,7 @@ sph_status sph_momentum_energy(sph_ctx* c, double* dt_out) {
   {
     Phase ph(c, SPH_PH_MOMENTUM);
     int k = c->P.n ? launch_momentum(c) : 0;
+    if (c->dist && !dist_allreduce_dt(c)) return fail(c, SPH_ERR_COMM, c->dist_err);  // a11
     k += launch_dt_finalize(c);
     CKL();
     ph.done(k);
@@ -558,15 +613,23 @@ sph_status sph_diagnostics(sph_ctx* c, sph_diag* out) {
   if (c->attached && c->P.n) {
     launch_diag(c);
     CKL();
-    CK(cudaMemcpyAsync(d, c->s.diag, sizeof(d), cudaMemcpyDeviceToHost, c->stream));
+  } else {
+    CK(cudaMemsetAsync(c->s.diag, 0, sizeof(d), c->stream));
   }
+  int64_t n_owned = c->P.n;
+  if (c->dist) {  // a15: optional global sums
+    if (!dist_allreduce_diag(c, c->s.diag, c->s.cnt)) return fail(c, SPH_ERR_COMM, c->dist_err);
+    n_owned = dist_n_total(c);
+  }
+  CK(cudaMemcpyAsync(d, c->s.diag, sizeof(d), cudaMemcpyDeviceToHost, c->stream));
   unsigned long long cnt[kCounters];
   double dts[DT_SLOTS];
-  CK(cudaMemcpyAsync(cnt, c->s.cnt, sizeof(cnt), cudaMemcpyDeviceToHost, c->stream));
+  CK(cudaMemcpyAsync(cnt, c->dist ? dist_counters(c) : c->s.cnt, sizeof(cnt), cudaMemcpyDeviceToHost,
+                     c->stream));
   CK(cudaMemcpyAsync(dts, c->s.dts, sizeof(dts), cudaMemcpyDeviceToHost, c->stream));
   CK(cudaStreamSynchronize(c->stream));
-  out->n_owned = c->P.n;
-  out->n_halo = 0;
+  out->n_owned = n_owned;
+  out->n_halo = c->n_halo;
   out->nbr_total = (int64_t)d[7];
   out->omega_clamped = (int64_t)cnt[CNT_OMEGA];
   out->iad_singular = (int64_t)cnt[CNT_IAD_SINGULAR];
@@ -584,6 +647,13 @@ sph_status sph_diagnostics(sph_ctx* c, sph_diag* out) {
   }
   out->energy = d[6];
   if (cnt[CNT_NONFINITE]) return fail(c, SPH_ERR_NUMERIC, "non-finite dt encountered");
+  return SPH_OK;
+}
+
+sph_status sph_local_count(const sph_ctx* c, int64_t* n_owned, int64_t* n_halo) {
+  if (!c) return SPH_ERR_CONFIG;
+  if (n_owned) *n_owned = c->P.n;
+  if (n_halo) *n_halo = c->n_halo;
   return SPH_OK;
 }
 
@@ -611,6 +681,7 @@ sph_status sph_destroy(sph_ctx* c) {
   if (!c) return SPH_OK;
   drain_profile(c);
   cudaStreamSynchronize(c->stream);
+  dist_destroy(c);
   Scratch& s = c->s;
   void* ptrs[] = {s.keys, s.keys_alt, s.idx, s.idx_alt, s.hist, s.scan_tmp, s.gather, s.gather_id,
                   s.cell_start, s.cell_end, s.cell_hmax, s.cell_flag, s.cell_rank, s.cell_list,

@@ -1,0 +1,552 @@
+// sph_dist.cu -- multi-GPU SFC domain decomposition (§4.3-4.4, P:191-222;
+// SURVEY §8(e)): global bbox/h allreduce, key-prefix histogram allreduce ->
+// splitters at equal counts (the paper's global top tree), migration of
+// particles that left the rank's key range, halo identification, and the
+// three halo exchanges per step (reading R21) over NCCL send/recv.
+//
+// Local layout on every rank during a step: [owned, sorted by key | halo, sorted
+// by key].  Every search cell belongs to exactly one rank and halos are whole
+// cells, so a target's stencil slots and the within-cell order are the same as
+// on one GPU: per-particle results are bit-identical for any rank count.
+#include <algorithm>
+#include <numeric>
+#include <string>
+#include <vector>
+
+#include "stencil.cuh"
+#include "sph_dist.cuh"
+
+namespace sphb {
+
+// ------------------------------------------------------------------ host logic (testable on CPU)
+// Splitters: rank r owns key-prefix bins [split[r], split[r+1]); split[r] is the
+// first bin whose inclusive prefix count exceeds floor(r * total / G).
+void compute_splitters(const int64_t* hist, int64_t nbins, int G, int64_t* split) {
+  int64_t total = 0;
+  for (int64_t b = 0; b < nbins; ++b) total += hist[b];
+  split[0] = 0;
+  int64_t acc = 0, b = 0;
+  for (int r = 1; r < G; ++r) {
+    const int64_t target = (int64_t)((__int128)total * r / G);
+    while (b < nbins && acc + hist[b] <= target) acc += hist[b++];
+    split[r] = b;
+  }
+  split[G] = nbins;
+  for (int r = 1; r <= G; ++r) split[r] = std::max(split[r], split[r - 1]);
+}
+
+int owner_of_bin(const int64_t* split, int G, int64_t bin) {
+  int lo = 0, hi = G;  // largest r with split[r] <= bin
+  while (hi - lo > 1) {
+    int mid = (lo + hi) / 2;
+    if (split[mid] <= bin) lo = mid;
+    else hi = mid;
+  }
+  return lo;
+}
+
+#ifdef SPH_WITH_NCCL
+
+#define NCK(call)                                                                           \
+  do {                                                                                      \
+    ncclResult_t r_ = (call);                                                               \
+    if (r_ != ncclSuccess) {                                                                \
+      c->dist_err = std::string(#call) + ": " + ncclGetErrorString(r_);                     \
+      return false;                                                                         \
+    }                                                                                       \
+  } while (0)
+#define CUK(call)                                                                           \
+  do {                                                                                      \
+    cudaError_t e_ = (call);                                                                \
+    if (e_ != cudaSuccess) {                                                                \
+      c->dist_err = std::string(#call) + ": " + cudaGetErrorString(e_);                     \
+      return false;                                                                         \
+    }                                                                                       \
+  } while (0)
+
+// ------------------------------------------------------------------ kernels
+__device__ __forceinline__ uint64_t spread3d(uint64_t v) {
+  v &= 0x1fffffull;
+  v = (v | (v << 32)) & 0x1f00000000ffffull;
+  v = (v | (v << 16)) & 0x1f0000ff0000ffull;
+  v = (v | (v << 8)) & 0x100f00f00f00f00full;
+  v = (v | (v << 4)) & 0x10c30c30c30c30c3ull;
+  v = (v | (v << 2)) & 0x1249249249249249ull;
+  return v;
+}
+
+__device__ __forceinline__ int64_t key_bin(const Grid& g, uint64_t key, int shift) {
+  const uint64_t m = g.idbits >= 64 ? 0 : key >> g.idbits;
+  return (int64_t)(m >> shift);
+}
+
+__global__ void k_bin_hist(const uint64_t* __restrict__ keys, int64_t n, Grid g, int shift,
+                           unsigned long long* __restrict__ hist) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
+       i += (int64_t)gridDim.x * blockDim.x)
+    atomicAdd(&hist[key_bin(g, keys[i], shift)], 1ull);
+}
+
+// off[r] = first sorted index whose bin >= split[r] (r = 0..G)
+__global__ void k_block_offsets(const uint64_t* __restrict__ keys, int64_t n, Grid g, int shift,
+                                const int64_t* __restrict__ split, int G,
+                                int64_t* __restrict__ off) {
+  const int r = threadIdx.x;
+  if (r > G) return;
+  int64_t lo = 0, hi = n;
+  while (lo < hi) {
+    const int64_t mid = (lo + hi) / 2;
+    if (key_bin(g, keys[mid], shift) < split[r]) lo = mid + 1;
+    else hi = mid;
+  }
+  off[r] = r == G ? n : lo;
+}
+
+__device__ __forceinline__ int owner_dev(const int64_t* split, int G, int64_t bin) {
+  int lo = 0, hi = G;
+  while (hi - lo > 1) {
+    const int mid = (lo + hi) >> 1;
+    if (split[mid] <= bin) lo = mid;
+    else hi = mid;
+  }
+  return lo;
+}
+
+// per owned non-empty cell: bit r set if rank r owns a cell within the halo box
+__global__ void k_halo_mask(const uint32_t* __restrict__ clist, const uint32_t* __restrict__ ncl,
+                            Grid g, int Rx, int Ry, int Rz, const int64_t* __restrict__ split, int G,
+                            int rank, int shift, unsigned long long* __restrict__ mask) {
+  const uint32_t nl = *ncl;
+  for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < nl; i += gridDim.x * blockDim.x) {
+    int c3[3];
+    cell_coords(g, clist[i], c3);
+    const int R[3] = {Rx, Ry, Rz};
+    int lo[3], cnt[3];
+    for (int d = 0; d < 3; ++d) {
+      if (2 * R[d] + 1 >= g.nc[d]) {
+        lo[d] = 0;
+        cnt[d] = g.nc[d];
+      } else if (g.periodic[d]) {
+        lo[d] = c3[d] - R[d];
+        cnt[d] = 2 * R[d] + 1;
+      } else {
+        const int l = max(0, c3[d] - R[d]), u = min(g.nc[d] - 1, c3[d] + R[d]);
+        lo[d] = l;
+        cnt[d] = u - l + 1;
+      }
+    }
+    unsigned long long m = 0;
+    for (int iz = 0; iz < cnt[2]; ++iz)
+      for (int iy = 0; iy < cnt[1]; ++iy)
+        for (int ix = 0; ix < cnt[0]; ++ix) {
+          int q[3] = {lo[0] + ix, lo[1] + iy, lo[2] + iz};
+          for (int d = 0; d < 3; ++d) q[d] = q[d] < 0 ? q[d] + g.nc[d] : (q[d] >= g.nc[d] ? q[d] - g.nc[d] : q[d]);
+          const uint64_t mort = spread3d(q[0]) | (spread3d(q[1]) << 1) | (spread3d(q[2]) << 2);
+          const int o = owner_dev(split, G, (int64_t)(mort >> shift));
+          if (o != rank) m |= 1ull << o;
+        }
+    mask[i] = m;
+  }
+}
+
+// particles each owned cell sends to peer r (0 when the bit is clear)
+__global__ void k_peer_counts(const uint32_t* __restrict__ clist, const uint32_t* __restrict__ ncl,
+                              const uint32_t* __restrict__ cstart, const uint32_t* __restrict__ cend,
+                              const unsigned long long* __restrict__ mask, int r,
+                              uint32_t* __restrict__ cnt) {
+  const uint32_t nl = *ncl;
+  for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < nl; i += gridDim.x * blockDim.x) {
+    const uint32_t c = clist[i];
+    cnt[i] = (mask[i] >> r) & 1ull ? cend[c] - cstart[c] : 0u;
+  }
+}
+
+__global__ void k_fill_send(const uint32_t* __restrict__ clist, const uint32_t* __restrict__ ncl,
+                            const uint32_t* __restrict__ cstart, const uint32_t* __restrict__ cend,
+                            const unsigned long long* __restrict__ mask, int r,
+                            const uint32_t* __restrict__ off, uint32_t* __restrict__ out) {
+  const uint32_t nl = *ncl;
+  const int lane = threadIdx.x & 31;
+  for (uint32_t i = (blockIdx.x * blockDim.x + threadIdx.x) >> 5; i < nl;
+       i += (gridDim.x * blockDim.x) >> 5) {
+    if (!((mask[i] >> r) & 1ull)) continue;
+    const uint32_t c = clist[i], s = cstart[c], e = cend[c], o = off[i];
+    for (uint32_t k = lane; k < e - s; k += 32) out[o + k] = s + k;
+  }
+}
+
+__global__ void k_total(const uint32_t* __restrict__ cnt, const uint32_t* __restrict__ off,
+                        const uint32_t* __restrict__ ncl, int64_t* __restrict__ tot) {
+  const uint32_t nl = *ncl;
+  *tot = nl ? (int64_t)off[nl - 1] + cnt[nl - 1] : 0;
+}
+
+struct FieldSet {
+  uint64_t* f[16];
+  int nf;
+};
+
+// sendbuf layout per peer: nf blocks of cnt_r elements
+__global__ void k_pack(FieldSet fs, const uint32_t* __restrict__ idx, int64_t n, int64_t base,
+                       uint64_t* __restrict__ buf) {
+  for (int64_t k = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; k < n;
+       k += (int64_t)gridDim.x * blockDim.x) {
+    const uint32_t j = idx[k];
+    for (int f = 0; f < fs.nf; ++f) buf[base * fs.nf + f * n + k] = fs.f[f][j];
+  }
+}
+__global__ void k_pack_range(FieldSet fs, int64_t src0, int64_t n, int64_t base,
+                             uint64_t* __restrict__ buf) {
+  for (int64_t k = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; k < n;
+       k += (int64_t)gridDim.x * blockDim.x)
+    for (int f = 0; f < fs.nf; ++f) buf[base * fs.nf + f * n + k] = fs.f[f][src0 + k];
+}
+__global__ void k_unpack(FieldSet fs, const uint64_t* __restrict__ buf, int64_t n, int64_t base,
+                         int64_t dst0) {
+  for (int64_t k = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; k < n;
+       k += (int64_t)gridDim.x * blockDim.x)
+    for (int f = 0; f < fs.nf; ++f) fs.f[f][dst0 + k] = buf[base * fs.nf + f * n + k];
+}
+// move [src0, src0+n) -> [0, n) through a staging buffer (ranges may overlap)
+__global__ void k_copy_out(FieldSet fs, int64_t src0, int64_t n, uint64_t* __restrict__ tmp) {
+  for (int64_t k = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; k < n;
+       k += (int64_t)gridDim.x * blockDim.x)
+    for (int f = 0; f < fs.nf; ++f) tmp[f * n + k] = fs.f[f][src0 + k];
+}
+__global__ void k_copy_in(FieldSet fs, int64_t n, const uint64_t* __restrict__ tmp) {
+  for (int64_t k = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; k < n;
+       k += (int64_t)gridDim.x * blockDim.x)
+    for (int f = 0; f < fs.nf; ++f) fs.f[f][k] = tmp[f * n + k];
+}
+
+__global__ void k_bbox_pack(const double* __restrict__ bb, int64_t n, double* __restrict__ mx,
+                            double* __restrict__ sm) {
+  // MAX of {-min x,y,z, max x,y,z, max h, max id}; SUM of {sum h, n}
+  mx[0] = -bb[0]; mx[1] = -bb[1]; mx[2] = -bb[2];
+  mx[3] = bb[3]; mx[4] = bb[4]; mx[5] = bb[5];
+  mx[6] = bb[6]; mx[7] = bb[8];
+  sm[0] = n ? bb[7] : 0.0;
+  sm[1] = (double)n;
+}
+
+// ------------------------------------------------------------------ orchestration
+static FieldSet state_fields(sph_ctx* c, bool with_hist) {
+  sph_particles& P = c->P;
+  FieldSet fs{};
+  uint64_t** f = fs.f;
+  int k = 0;
+  for (double* p : {P.x, P.y, P.z, P.vx, P.vy, P.vz, P.h, P.m, P.u}) f[k++] = (uint64_t*)p;
+  if (with_hist)
+    for (double* p : {P.vhx, P.vhy, P.vhz, P.du_prev}) f[k++] = (uint64_t*)p;
+  f[k++] = (uint64_t*)P.id;
+  fs.nf = k;
+  return fs;
+}
+
+static bool exchange(sph_ctx* c, const FieldSet& fs, bool halo_mode) {
+  // halo_mode: send the send_idx lists, receive after the owned particles.
+  Dist& D = *c->dist;
+  const int G = D.G, me = D.rank;
+  const int F = fs.nf;
+  int64_t sbase = 0, rbase = 0;
+  for (int r = 0; r < G; ++r) {
+    if (D.scnt[r] && r != me) {
+      if (halo_mode) {
+        k_pack<<<grid_blocks(c, D.scnt[r], 256, 4), 256, 0, c->stream>>>(fs, D.send_idx + D.soff[r],
+                                                                         D.scnt[r], sbase, D.sendbuf);
+      } else {
+        k_pack_range<<<grid_blocks(c, D.scnt[r], 256, 4), 256, 0, c->stream>>>(fs, D.soff[r], D.scnt[r],
+                                                                               sbase, D.sendbuf);
+      }
+      c->launches++;
+    }
+    if (r != me) sbase += D.scnt[r];
+  }
+  CUK(cudaGetLastError());
+  NCK(ncclGroupStart());
+  sbase = 0;
+  for (int r = 0; r < G; ++r) {
+    if (r == me) continue;
+    if (D.scnt[r])
+      NCK(ncclSend(D.sendbuf + sbase * F, (size_t)D.scnt[r] * F, ncclUint64, r, D.comm, c->stream));
+    if (D.rcnt[r])
+      NCK(ncclRecv(D.recvbuf + rbase * F, (size_t)D.rcnt[r] * F, ncclUint64, r, D.comm, c->stream));
+    sbase += D.scnt[r];
+    rbase += D.rcnt[r];
+  }
+  NCK(ncclGroupEnd());
+  return true;
+}
+
+static bool unpack_all(sph_ctx* c, const FieldSet& fs, int64_t dst0) {
+  Dist& D = *c->dist;
+  int64_t rbase = 0;
+  for (int r = 0; r < D.G; ++r) {
+    if (r == D.rank) continue;
+    if (D.rcnt[r]) {
+      k_unpack<<<grid_blocks(c, D.rcnt[r], 256, 4), 256, 0, c->stream>>>(fs, D.recvbuf, D.rcnt[r], rbase,
+                                                                        dst0 + rbase);
+      c->launches++;
+    }
+    rbase += D.rcnt[r];
+  }
+  CUK(cudaGetLastError());
+  return true;
+}
+
+// all-gather the per-peer send counts, derive receive counts
+static bool swap_counts(sph_ctx* c) {
+  Dist& D = *c->dist;
+  const int G = D.G;
+  CUK(cudaMemcpyAsync(D.cnt_d, D.scnt.data(), sizeof(int64_t) * G, cudaMemcpyHostToDevice, c->stream));
+  NCK(ncclAllGather(D.cnt_d, D.cnt_all_d, G, ncclInt64, D.comm, c->stream));
+  std::vector<int64_t> all((size_t)G * G);
+  CUK(cudaMemcpyAsync(all.data(), D.cnt_all_d, sizeof(int64_t) * G * G, cudaMemcpyDeviceToHost, c->stream));
+  CUK(cudaStreamSynchronize(c->stream));
+  for (int s = 0; s < G; ++s) D.rcnt[s] = s == D.rank ? 0 : all[(size_t)s * G + D.rank];
+  D.moved_total = 0;
+  for (int s = 0; s < G; ++s)
+    for (int r = 0; r < G; ++r)
+      if (r != s) D.moved_total += all[(size_t)s * G + r];
+  return true;
+}
+
+bool dist_global_bbox(sph_ctx* c, double* bb_out) {
+  Dist& D = *c->dist;
+  k_bbox_pack<<<1, 1, 0, c->stream>>>(c->s.bbox, c->P.n, D.red_d, D.red_d + 8);
+  NCK(ncclGroupStart());
+  NCK(ncclAllReduce(D.red_d, D.red_d, 8, ncclFloat64, ncclMax, D.comm, c->stream));
+  NCK(ncclAllReduce(D.red_d + 8, D.red_d + 8, 2, ncclFloat64, ncclSum, D.comm, c->stream));
+  NCK(ncclGroupEnd());
+  double v[10];
+  CUK(cudaMemcpyAsync(v, D.red_d, sizeof(v), cudaMemcpyDeviceToHost, c->stream));
+  CUK(cudaStreamSynchronize(c->stream));
+  bb_out[0] = -v[0]; bb_out[1] = -v[1]; bb_out[2] = -v[2];
+  bb_out[3] = v[3]; bb_out[4] = v[4]; bb_out[5] = v[5];
+  bb_out[6] = v[6]; bb_out[7] = v[8]; bb_out[8] = v[7];
+  D.n_total = (int64_t)v[9];
+  return true;
+}
+
+// splitters from the global key-prefix histogram; ranges of the sorted owned array
+bool dist_splitters(sph_ctx* c) {
+  Dist& D = *c->dist;
+  const Grid& g = c->grid;
+  const int mbits = 3 * g.cbits;
+  D.shift = mbits > kBinBits ? mbits - kBinBits : 0;
+  D.nbins = (int64_t)1 << (mbits - D.shift);
+  CUK(cudaMemsetAsync(D.hist_d, 0, sizeof(unsigned long long) * D.nbins, c->stream));
+  if (c->P.n) {
+    k_bin_hist<<<grid_blocks(c, c->P.n, 256, 8), 256, 0, c->stream>>>(c->s.keys, c->P.n, g, D.shift, D.hist_d);
+    c->launches++;
+  }
+  NCK(ncclAllReduce(D.hist_d, D.hist_d, D.nbins, ncclUint64, ncclSum, D.comm, c->stream));
+  std::vector<int64_t> hist(D.nbins);
+  CUK(cudaMemcpyAsync(hist.data(), D.hist_d, sizeof(int64_t) * D.nbins, cudaMemcpyDeviceToHost, c->stream));
+  CUK(cudaStreamSynchronize(c->stream));
+  compute_splitters(hist.data(), D.nbins, D.G, D.split.data());
+  CUK(cudaMemcpyAsync(D.split_d, D.split.data(), sizeof(int64_t) * (D.G + 1), cudaMemcpyHostToDevice, c->stream));
+  return true;
+}
+
+// after the local sort: ship particles outside this rank's key range to their owners
+bool dist_migrate(sph_ctx* c, bool* moved) {
+  Dist& D = *c->dist;
+  const int G = D.G;
+  std::vector<int64_t> off(G + 1);
+  k_block_offsets<<<1, 64, 0, c->stream>>>(c->s.keys, c->P.n, c->grid, D.shift, D.split_d, G, D.off_d);
+  c->launches++;
+  CUK(cudaMemcpyAsync(off.data(), D.off_d, sizeof(int64_t) * (G + 1), cudaMemcpyDeviceToHost, c->stream));
+  CUK(cudaStreamSynchronize(c->stream));
+  for (int r = 0; r < G; ++r) {
+    D.soff[r] = off[r];
+    D.scnt[r] = r == D.rank ? 0 : off[r + 1] - off[r];
+  }
+  if (!swap_counts(c)) return false;
+  *moved = D.moved_total > 0;
+  if (!*moved) return true;
+  int64_t nrecv = 0, nsend = 0;
+  for (int r = 0; r < G; ++r) {
+    nrecv += D.rcnt[r];
+    nsend += D.scnt[r];
+  }
+  const int64_t kept = off[D.rank + 1] - off[D.rank];
+  if (kept + nrecv > c->cap || nsend > D.xcap || nrecv > D.xcap) {
+    c->dist_err = "migration exceeds capacity";
+    return false;
+  }
+  FieldSet fs = state_fields(c, true);
+  if (!exchange(c, fs, false)) return false;
+  // kept block -> front (through the send buffer tail is unsafe: use the permutation scratch)
+  uint64_t* tmp = (uint64_t*)c->s.gather;
+  k_copy_out<<<grid_blocks(c, kept, 256, 8), 256, 0, c->stream>>>(fs, off[D.rank], kept, tmp);
+  k_copy_in<<<grid_blocks(c, kept, 256, 8), 256, 0, c->stream>>>(fs, kept, tmp);
+  c->launches += 2;
+  if (!unpack_all(c, fs, kept)) return false;
+  c->P.n = kept + nrecv;
+  return true;
+}
+
+// halo plan (who needs which of my cells) + exchange #1 (x, v, h, m, u, id)
+bool dist_halo_plan_and_exchange1(sph_ctx* c) {
+  Dist& D = *c->dist;
+  const Grid& g = c->grid;
+  const int G = D.G;
+  const double reach = reach_of(c->hmax);
+  const int Rx = stencil_radius(g, 0, reach), Ry = stencil_radius(g, 1, reach), Rz = stencil_radius(g, 2, reach);
+  const int64_t n = c->P.n;
+  const int nbc = grid_blocks(c, n, 256, 8);
+  k_halo_mask<<<nbc, 256, 0, c->stream>>>(c->s.cell_list, c->s.ncell_list, g, Rx, Ry, Rz, D.split_d, G,
+                                          D.rank, D.shift, D.mask_d);
+  c->launches++;
+  int64_t total = 0;
+  for (int r = 0; r < G; ++r) {
+    D.soff[r] = total;
+    D.scnt[r] = 0;
+    if (r == D.rank) continue;
+    k_peer_counts<<<nbc, 256, 0, c->stream>>>(c->s.cell_list, c->s.ncell_list, c->s.cell_start, c->s.cell_end,
+                                              D.mask_d, r, D.pcnt_d);
+    scan_u32(c, D.pcnt_d, D.poff_d, n);
+    k_total<<<1, 1, 0, c->stream>>>(D.pcnt_d, D.poff_d, c->s.ncell_list, D.tot_d + r);
+    c->launches += 5;
+    int64_t t = 0;
+    CUK(cudaMemcpyAsync(&t, D.tot_d + r, sizeof(int64_t), cudaMemcpyDeviceToHost, c->stream));
+    CUK(cudaStreamSynchronize(c->stream));
+    if (total + t > D.xcap) {
+      c->dist_err = "halo send list exceeds capacity";
+      return false;
+    }
+    k_fill_send<<<nbc, 256, 0, c->stream>>>(c->s.cell_list, c->s.ncell_list, c->s.cell_start, c->s.cell_end,
+                                            D.mask_d, r, D.poff_d, D.send_idx + total);
+    c->launches++;
+    D.scnt[r] = t;
+    total += t;
+  }
+  if (!swap_counts(c)) return false;
+  D.n_halo = 0;
+  for (int r = 0; r < G; ++r) D.n_halo += D.rcnt[r];
+  if (n + D.n_halo > c->cap || D.n_halo > D.xcap) {
+    c->dist_err = "halo exceeds capacity";
+    return false;
+  }
+  FieldSet fs = state_fields(c, false);
+  if (!exchange(c, fs, true)) return false;
+  return unpack_all(c, fs, n);
+}
+
+bool dist_exchange2(sph_ctx* c) {  // after density: quantities IAD / momentum read at sources
+  FieldSet fs{};
+  fs.f[0] = (uint64_t*)c->s.vol;
+  fs.f[1] = (uint64_t*)c->s.ih2;
+  fs.f[2] = (uint64_t*)c->P.c;
+  fs.f[3] = (uint64_t*)c->s.mX;
+  fs.nf = 4;
+  return exchange(c, fs, true) && unpack_all(c, fs, c->P.n);
+}
+
+bool dist_exchange3(sph_ctx* c) {  // after IAD: C~ = (B/h^3) C of the sources
+  FieldSet fs{};
+  for (int k = 0; k < 6; ++k) fs.f[k] = (uint64_t*)(c->s.ct + (size_t)k * c->cap);
+  fs.nf = 6;
+  return exchange(c, fs, true) && unpack_all(c, fs, c->P.n);
+}
+
+bool dist_allreduce_dt(sph_ctx* c) {
+  Dist& D = *c->dist;
+  NCK(ncclAllReduce(c->s.dts + DT_RAW_BITS, c->s.dts + DT_RAW_BITS, 1, ncclUint64, ncclMin, D.comm, c->stream));
+  return true;
+}
+
+bool dist_allreduce_diag(sph_ctx* c, double* d_dev, unsigned long long* cnt_dev) {
+  Dist& D = *c->dist;
+  NCK(ncclGroupStart());
+  NCK(ncclAllReduce(d_dev, d_dev, 8, ncclFloat64, ncclSum, D.comm, c->stream));
+  NCK(ncclAllReduce(cnt_dev, D.cntred_d, kCounters, ncclUint64, ncclSum, D.comm, c->stream));
+  NCK(ncclGroupEnd());
+  return true;
+}
+
+bool dist_init(sph_ctx* c, const sph_params* prm) {
+  Dist* D = new Dist();
+  c->dist = D;
+  D->G = prm->nranks;
+  D->rank = prm->rank;
+  D->split.assign(D->G + 1, 0);
+  D->soff.assign(D->G, 0);
+  D->scnt.assign(D->G, 0);
+  D->rcnt.assign(D->G, 0);
+  ncclUniqueId id;
+  memcpy(&id, prm->nccl_unique_id, sizeof(id));
+  NCK(ncclCommInitRank(&D->comm, D->G, id, D->rank));
+  D->xcap = c->cap;
+  const int64_t cap = c->cap;
+  CUK(cudaMalloc(&D->hist_d, sizeof(unsigned long long) << kBinBits));
+  CUK(cudaMalloc(&D->split_d, sizeof(int64_t) * (D->G + 1)));
+  CUK(cudaMalloc(&D->off_d, sizeof(int64_t) * (D->G + 1)));
+  CUK(cudaMalloc(&D->cnt_d, sizeof(int64_t) * D->G));
+  CUK(cudaMalloc(&D->cnt_all_d, sizeof(int64_t) * D->G * D->G));
+  CUK(cudaMalloc(&D->tot_d, sizeof(int64_t) * D->G));
+  CUK(cudaMalloc(&D->red_d, sizeof(double) * 16));
+  CUK(cudaMalloc(&D->cntred_d, sizeof(unsigned long long) * kCounters));
+  CUK(cudaMalloc(&D->mask_d, sizeof(unsigned long long) * cap));
+  CUK(cudaMalloc(&D->pcnt_d, sizeof(uint32_t) * cap));
+  CUK(cudaMalloc(&D->poff_d, sizeof(uint32_t) * cap));
+  CUK(cudaMalloc(&D->send_idx, sizeof(uint32_t) * D->xcap));
+  CUK(cudaMalloc(&D->sendbuf, sizeof(uint64_t) * 14 * D->xcap));
+  CUK(cudaMalloc(&D->recvbuf, sizeof(uint64_t) * 14 * D->xcap));
+  return true;
+}
+
+void dist_destroy(sph_ctx* c) {
+  Dist* D = c->dist;
+  if (!D) return;
+  if (D->comm) ncclCommDestroy(D->comm);
+  void* ptrs[] = {D->hist_d, D->split_d, D->off_d, D->cnt_d, D->cnt_all_d, D->tot_d, D->red_d,
+                  D->mask_d, D->pcnt_d, D->poff_d, D->send_idx, D->sendbuf, D->recvbuf, D->cntred_d};
+  for (void* p : ptrs)
+    if (p) cudaFree(p);
+  delete D;
+  c->dist = nullptr;
+}
+
+#else  // !SPH_WITH_NCCL
+bool dist_init(sph_ctx* c, const sph_params*) {
+  c->dist_err = "built without NCCL";
+  return false;
+}
+void dist_destroy(sph_ctx*) {}
+bool dist_global_bbox(sph_ctx*, double*) { return false; }
+bool dist_splitters(sph_ctx*) { return false; }
+bool dist_migrate(sph_ctx*, bool*) { return false; }
+bool dist_halo_plan_and_exchange1(sph_ctx*) { return false; }
+bool dist_exchange2(sph_ctx*) { return false; }
+bool dist_exchange3(sph_ctx*) { return false; }
+bool dist_allreduce_dt(sph_ctx*) { return false; }
+bool dist_allreduce_diag(sph_ctx*, double*, unsigned long long*) { return false; }
+#endif
+
+}  // namespace sphb
+
+extern "C" sph_status sph_nccl_unique_id(void* out, int size) {
+#ifdef SPH_WITH_NCCL
+  if (!out || size < (int)sizeof(ncclUniqueId)) return SPH_ERR_CONFIG;
+  ncclUniqueId id;
+  if (ncclGetUniqueId(&id) != ncclSuccess) return SPH_ERR_COMM;
+  memcpy(out, &id, sizeof(id));
+  return SPH_OK;
+#else
+  (void)out;
+  (void)size;
+  return SPH_ERR_CONFIG;
+#endif
+}
+
+// host-side decomposition helpers, exported for CPU tests (no GPU needed)
+extern "C" int sph_decomp_splitters(const int64_t* hist, int64_t nbins, int G, int64_t* split) {
+  if (!hist || !split || G < 1 || nbins < 1) return SPH_ERR_CONFIG;
+  sphb::compute_splitters(hist, nbins, G, split);
+  return SPH_OK;
+}
+extern "C" int sph_decomp_owner(const int64_t* split, int G, int64_t bin) {
+  return sphb::owner_of_bin(split, G, bin);
+}

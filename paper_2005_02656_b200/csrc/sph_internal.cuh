@@ -94,6 +94,8 @@ struct PhaseEv {
   cudaEvent_t a, b;
 };
 
+struct Dist;  // multi-GPU state (sph_dist.cuh)
+
 }  // namespace sphb
 
 struct sph_ctx {
@@ -122,6 +124,10 @@ struct sph_ctx {
   double phase_ms[SPH_PH_COUNT] = {0};
   int64_t phase_launches[SPH_PH_COUNT] = {0};
   int64_t launches = 0;
+  // multi-GPU (nranks > 1): owned particles are [0, P.n), halos [P.n, P.n + n_halo)
+  sphb::Dist* dist = nullptr;
+  int64_t n_halo = 0;
+  std::string dist_err;
 };
 
 namespace sphb {
@@ -129,6 +135,9 @@ namespace sphb {
 // ---- launchers (each returns the number of kernels it launched) ----
 int launch_bbox(sph_ctx* c);
 int launch_keys(sph_ctx* c);
+int launch_keys_range(sph_ctx* c, int64_t i0, int64_t n);
+int launch_cells_halo(sph_ctx* c, int64_t i0, int64_t n);
+int scan_u32(sph_ctx* c, const uint32_t* in, uint32_t* out, int64_t n);
 int launch_sort(sph_ctx* c, int nbits, const uint32_t** perm_out);
 int launch_permute(sph_ctx* c, const uint32_t* perm);
 int launch_cells(sph_ctx* c);

@@ -28,6 +28,31 @@ OUT_FIELDS = ("rho", "omega", "p", "c", "c11", "c12", "c13", "c22", "c23", "c33"
 ALL_FIELDS = STATE_FIELDS + OUT_FIELDS
 
 
+def nccl_unique_id() -> bytes:
+    """Rank 0's 128-byte NCCL id (sph_nccl_unique_id); broadcast it to all ranks."""
+    buf = C.create_string_buffer(128)
+    st = lib().sph_nccl_unique_id(buf, 128)
+    if st != 0:
+        raise SphError(st, "sph_nccl_unique_id failed (built without NCCL?)")
+    return buf.raw
+
+
+def decomp_splitters(hist: np.ndarray, G: int) -> np.ndarray:
+    """split[G+1]: rank r owns key-prefix bins [split[r], split[r+1]) (host helper of the C ABI)."""
+    h = np.ascontiguousarray(hist, dtype=np.int64)
+    out = np.zeros(G + 1, dtype=np.int64)
+    st = lib().sph_decomp_splitters(h.ctypes.data_as(C.POINTER(C.c_int64)), h.size, G,
+                                    out.ctypes.data_as(C.POINTER(C.c_int64)))
+    if st != 0:
+        raise SphError(st, "sph_decomp_splitters")
+    return out
+
+
+def decomp_owner(split: np.ndarray, b: int) -> int:
+    s = np.ascontiguousarray(split, dtype=np.int64)
+    return lib().sph_decomp_owner(s.ctypes.data_as(C.POINTER(C.c_int64)), s.size - 1, int(b))
+
+
 def measure_fp64_peak(stream=None) -> float:
     """Measured FP64 DFMA TFLOP/s of the current GPU (roofline denominator)."""
     import torch
@@ -114,6 +139,15 @@ def lib():
         L.sph_set_profiling.argtypes = [vp, C.c_int]
         L.sph_phase_times.argtypes = [vp, _P, C.POINTER(C.c_int64), C.c_int]
         L.sph_measure_fp64_peak.argtypes = [vp, _P]
+        L.sph_local_count.argtypes = [vp, C.POINTER(C.c_int64), C.POINTER(C.c_int64)]
+        L.sph_local_count.restype = C.c_int
+        L.sph_nccl_unique_id.argtypes = [vp, C.c_int]
+        L.sph_nccl_unique_id.restype = C.c_int
+        L.sph_decomp_splitters.argtypes = [C.POINTER(C.c_int64), C.c_int64, C.c_int,
+                                           C.POINTER(C.c_int64)]
+        L.sph_decomp_splitters.restype = C.c_int
+        L.sph_decomp_owner.argtypes = [C.POINTER(C.c_int64), C.c_int, C.c_int64]
+        L.sph_decomp_owner.restype = C.c_int
         for f in ("sph_init", "sph_attach", "sph_find_neighbors", "sph_get_neighbors", "sph_density",
                   "sph_iad", "sph_momentum_energy", "sph_advance", "sph_step", "sph_upload",
                   "sph_download", "sph_diagnostics", "sph_set_profiling", "sph_phase_times",
@@ -215,12 +249,16 @@ class HostParticles:
 class Simulation:
     """One context of libsph bound to a DeviceParticles set."""
 
-    def __init__(self, d: dict, capacity: int | None = None, device="cuda", stream=None, **kw):
+    def __init__(self, d: dict, capacity: int | None = None, device="cuda", stream=None,
+                 unique_id: bytes | None = None, **kw):
         import torch
         self.dev = DeviceParticles(d, capacity, device)
         if stream is None:
             stream = torch.cuda.current_stream().cuda_stream
         self.params = make_params(d, stream=stream, **kw)
+        if self.params.nranks > 1:  # NCCL communicator from rank 0's id (dist.py)
+            self._uid = C.create_string_buffer(unique_id, 128)
+            self.params.nccl_unique_id = C.cast(self._uid, C.c_void_p)
         self._ctx = C.c_void_p()
         st = lib().sph_init(C.byref(self.params), self.dev.capacity, C.byref(self._ctx))
         if st != 0:
@@ -250,9 +288,17 @@ class Simulation:
     def n(self) -> int:
         return self.dev.n
 
+    def _sync_n(self):
+        no, nh = C.c_int64(0), C.c_int64(0)
+        self._check(lib().sph_local_count(self._ctx, C.byref(no), C.byref(nh)))
+        self.dev.n = no.value
+        self.n_halo = nh.value
+
     # -- the method
     def find_neighbors(self):
-        self._check(lib().sph_find_neighbors(self._ctx))
+        st = lib().sph_find_neighbors(self._ctx)
+        self._sync_n()
+        self._check(st)
 
     def get_neighbors(self):
         n = self.dev.n
@@ -282,7 +328,10 @@ class Simulation:
 
     def step(self, want_dt: bool = False):
         dt = C.c_double(0.0)
-        self._check(lib().sph_step(self._ctx, C.byref(dt) if want_dt else None))
+        st = lib().sph_step(self._ctx, C.byref(dt) if want_dt else None)
+        if self.params.nranks > 1:
+            self._sync_n()
+        self._check(st)
         return dt.value if want_dt else None
 
     def upload(self, host: HostParticles):
