@@ -266,7 +266,7 @@ def run_ours(args):
         return
     ms_step = ms / args.steps
     value = n_total * args.steps / (ms * 1e-3)
-    pairs = diag["nbr_total"]
+    pairs = diag["nbr_total"] / max(world, 1)  # diagnostics sum over ranks; per-rank average
     mom_ms = phase_ms["momentum"] / args.steps
     mom_flops = FLOPS_PER_PAIR["momentum"] * pairs
     achieved = mom_flops / (mom_ms * 1e-3) / 1e12
@@ -283,7 +283,7 @@ def run_ours(args):
         "data": "synthetic",
         "config": {"workload": workload_label(args), "description": desc,
                    "particles_per_gpu": n_local, "particles_total": n_total,
-                   "neighbors_mean": pairs / max(1, diag["n_owned"]),
+                   "neighbors_mean": diag["nbr_total"] / max(1, diag["n_owned"]),
                    "l2": "no flush: every SoA field array >= 200 MB > 126 MB L2",
                    "parallelism": f"sfc{max(world, 1)}" if world > 1 else "1 GPU"},
         "roofline": {"kernel": "k_momentum", "bound": "alu", "achieved": achieved,
