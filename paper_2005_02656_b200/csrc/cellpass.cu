@@ -29,6 +29,8 @@ constexpr int kSearchCap = 2048;  // staged candidates per group (float4)
 constexpr int kDensCap = 2048;    // staged particles per group, 4 fp64 fields
 constexpr int kMomCap = 1024;     // staged particles per group, 17 fp64 fields (1 CTA/SM)
 constexpr int kCTM = 512;         // momentum CTA: 16 warps, one CTA per SM
+constexpr int kCTD = 512;         // density / IAD CTA: 16 warps, two CTAs per SM
+constexpr int kNWD = kCTD / 32;
 constexpr int kNWM = kCTM / 32;
 constexpr int kMomFields = 17;
 constexpr uint32_t kSent = 0xffffffffu;
@@ -243,6 +245,32 @@ __device__ __forceinline__ void walk_targets(uint32_t t0, uint32_t t1, const uin
   }
 }
 
+struct TgtW {  // per-warp search target data (exact-test fp64 + fp32 band)
+  double pos[3];
+  double lim;
+  float f[5];
+};
+
+__device__ __forceinline__ bool exact_hit(const Grid& g, const double* __restrict__ x,
+                                          const double* __restrict__ y, const double* __restrict__ z,
+                                          uint32_t j, uint32_t t, const double* pos, double lim) {
+  // r^2 in the oracle's association, no FMA, minimum image (Eq. 6; R10)
+  if (j == t) return false;
+  double ex = __dsub_rn(x[j], pos[0]), ey = __dsub_rn(y[j], pos[1]), ez = __dsub_rn(z[j], pos[2]);
+  if (g.periodic[0]) ex = min_img(ex, g.L[0]);
+  if (g.periodic[1]) ey = min_img(ey, g.L[1]);
+  if (g.periodic[2]) ez = min_img(ez, g.L[2]);
+  return __dadd_rn(__dadd_rn(__dmul_rn(ex, ex), __dmul_rn(ey, ey)), __dmul_rn(ez, ez)) < lim;
+}
+
+__device__ __forceinline__ void wrap32(const Stencil& st, const Grid& g, float& dx, float& dy,
+                                       float& dz) {
+  const float L0 = (float)g.L[0], L1 = (float)g.L[1], L2 = (float)g.L[2];
+  if (st.wrap[0] == 2) dx = dx > 0.5f * L0 ? dx - L0 : (dx < -0.5f * L0 ? dx + L0 : dx);
+  if (st.wrap[1] == 2) dy = dy > 0.5f * L1 ? dy - L1 : (dy < -0.5f * L1 ? dy + L1 : dy);
+  if (st.wrap[2] == 2) dz = dz > 0.5f * L2 ? dz - L2 : (dz < -0.5f * L2 ? dz + L2 : dz);
+}
+
 // ------------------------------------------------------------------ a5 search
 template <bool W2>
 __global__ void __launch_bounds__(kCT) k_search(const double* __restrict__ x,
@@ -260,6 +288,7 @@ __global__ void __launch_bounds__(kCT) k_search(const double* __restrict__ x,
   extern __shared__ float4 cand[];  // kSearchCap + 32 padding
   __shared__ CellSm S;
   __shared__ uint32_t tcount[kTgt];
+  __shared__ TgtW TW[kNW][2];
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const unsigned lt = (1u << lane) - 1u;
   const uint32_t ncl = *nclist;
@@ -310,79 +339,77 @@ __global__ void __launch_bounds__(kCT) k_search(const double* __restrict__ x,
         for (int q = total + threadIdx.x; q < padded; q += blockDim.x)
           cand[q] = make_float4(INFINITY, INFINITY, INFINITY, __uint_as_float(kSent));
         __syncthreads();
-        // two targets per warp share every staged-candidate load
+        // two targets per warp share every staged-candidate load (fp32 test data in
+        // registers; the fp64 data of the rare exact test in shared memory)
         for (uint32_t ta = t0 + 2 * warp; ta < t1; ta += 2 * kNW) {
-          const uint32_t tb = ta + 1 < t1 ? ta + 1 : ta;  // odd tail: duplicate, not stored
           const bool has_b = ta + 1 < t1;
-          float lo32[2], hi32[2], px[2], py[2], pz[2];
-          double lim[2], pos[2][3];
-          uint32_t self_pk[2], count[2];
-          uint32_t* row[2];
-#pragma unroll
-          for (int s = 0; s < 2; ++s) {
-            const uint32_t t = s ? tb : ta;
-            pos[s][0] = x[t];
-            pos[s][1] = y[t];
-            pos[s][2] = z[t];
-            const double ha = h[t];
-            const double tha = 2.0 * ha;
-            lim[s] = __dmul_rn(tha, tha);
+          const uint32_t tb = has_b ? ta + 1 : ta;  // odd tail: duplicate, identical writes
+          if (lane < 2) {
+            const uint32_t t = lane ? tb : ta;
+            const double ha = h[t], tha = 2.0 * ha;
+            const double lim = __dmul_rn(tha, tha);
             // fp32 error band: |r2_32 - r2| <= delta lim, delta = 2^-20 (2 + 2 M/h + 2^-20 (M/h)^2)
             const double mh = M / ha;
             const double delta = 0x1p-20 * (2.0 + 2.0 * mh + 0x1p-20 * mh * mh);
-            lo32[s] = -1.0f;
-            hi32[s] = INFINITY;
+            float lo = -1.0f, hi = INFINITY;
             if (delta < 0.25) {
-              lo32[s] = (float)(lim[s] * (1.0 - delta));
-              hi32[s] = (float)(lim[s] * (1.0 + delta));
+              lo = (float)(lim * (1.0 - delta));
+              hi = (float)(lim * (1.0 + delta));
             }
-            px[s] = (float)(pos[s][0] - org[0]);
-            py[s] = (float)(pos[s][1] - org[1]);
-            pz[s] = (float)(pos[s][2] - org[2]);
-            self_pk[s] = ((uint32_t)S.kself << kLocalBits) | (t - S.sc);
-            count[s] = tcount[t - t0];
-            row[s] = nbr + (size_t)t * maxn;
+            const double px = x[t], py = y[t], pz = z[t];
+            TW[warp][lane].pos[0] = px;
+            TW[warp][lane].pos[1] = py;
+            TW[warp][lane].pos[2] = pz;
+            TW[warp][lane].lim = lim;
+            TW[warp][lane].f[0] = (float)(px - org[0]);
+            TW[warp][lane].f[1] = (float)(py - org[1]);
+            TW[warp][lane].f[2] = (float)(pz - org[2]);
+            TW[warp][lane].f[3] = lo;
+            TW[warp][lane].f[4] = hi;
           }
+          __syncwarp();
+          const float ax0 = TW[warp][0].f[0], ay0 = TW[warp][0].f[1], az0 = TW[warp][0].f[2];
+          const float lo0 = TW[warp][0].f[3], hi0 = TW[warp][0].f[4];
+          const float ax1 = TW[warp][1].f[0], ay1 = TW[warp][1].f[1], az1 = TW[warp][1].f[2];
+          const float lo1 = TW[warp][1].f[3], hi1 = TW[warp][1].f[4];
+          const uint32_t self0 = ((uint32_t)S.kself << kLocalBits) | (ta - S.sc);
+          const uint32_t self1 = ((uint32_t)S.kself << kLocalBits) | (tb - S.sc);
+          uint32_t cnt0 = tcount[ta - t0], cnt1 = tcount[tb - t0];
+          uint32_t* const row0 = nbr + (size_t)ta * maxn;
+          uint32_t* const row1 = nbr + (size_t)tb * maxn;
           for (int q0 = 0; q0 < padded; q0 += 32) {
             const float4 cd = cand[q0 + lane];
             const uint32_t pk = __float_as_uint(cd.w);
-#pragma unroll
-            for (int s = 0; s < 2; ++s) {
-              float dx = cd.x - px[s], dy = cd.y - py[s], dz = cd.z - pz[s];
-              if constexpr (W2) {
-                const float L0 = (float)g.L[0], L1 = (float)g.L[1], L2 = (float)g.L[2];
-                if (st.wrap[0] == 2) dx = dx > 0.5f * L0 ? dx - L0 : (dx < -0.5f * L0 ? dx + L0 : dx);
-                if (st.wrap[1] == 2) dy = dy > 0.5f * L1 ? dy - L1 : (dy < -0.5f * L1 ? dy + L1 : dy);
-                if (st.wrap[2] == 2) dz = dz > 0.5f * L2 ? dz - L2 : (dz < -0.5f * L2 ? dz + L2 : dz);
-              }
-              const float r2 = fmaf(dz, dz, fmaf(dy, dy, dx * dx));
-              bool hit = (r2 < lo32[s]) & (pk != self_pk[s]);
-              const bool amb = (r2 >= lo32[s]) & (r2 < hi32[s]);
-              if (__ballot_sync(0xffffffffu, amb)) {  // rare: exact fp64 test, oracle's association
-                if (amb) {
-                  const uint32_t j = S.t_start[pk >> kLocalBits] + (pk & kLocalMask);
-                  const uint32_t t = s ? tb : ta;
-                  if (j != t) {
-                    double ex = __dsub_rn(x[j], pos[s][0]), ey = __dsub_rn(y[j], pos[s][1]),
-                           ez = __dsub_rn(z[j], pos[s][2]);
-                    if (g.periodic[0]) ex = min_img(ex, g.L[0]);
-                    if (g.periodic[1]) ey = min_img(ey, g.L[1]);
-                    if (g.periodic[2]) ez = min_img(ez, g.L[2]);
-                    const double r2e = __dadd_rn(__dadd_rn(__dmul_rn(ex, ex), __dmul_rn(ey, ey)), __dmul_rn(ez, ez));
-                    hit = r2e < lim[s];
-                  }
-                }
-              }
-              const unsigned b = __ballot_sync(0xffffffffu, hit);
-              const uint32_t p = count[s] + __popc(b & lt);
-              if (hit && p < (uint32_t)maxn) row[s][p] = pk;
-              count[s] += __popc(b);
+            float dx0 = cd.x - ax0, dy0 = cd.y - ay0, dz0 = cd.z - az0;
+            float dx1 = cd.x - ax1, dy1 = cd.y - ay1, dz1 = cd.z - az1;
+            if constexpr (W2) {
+              wrap32(st, g, dx0, dy0, dz0);
+              wrap32(st, g, dx1, dy1, dz1);
             }
+            const float r0 = fmaf(dz0, dz0, fmaf(dy0, dy0, dx0 * dx0));
+            const float r1 = fmaf(dz1, dz1, fmaf(dy1, dy1, dx1 * dx1));
+            bool hit0 = (r0 < lo0) & (pk != self0);
+            bool hit1 = (r1 < lo1) & (pk != self1);
+            const bool amb0 = (r0 >= lo0) & (r0 < hi0);
+            const bool amb1 = (r1 >= lo1) & (r1 < hi1);
+            if (__ballot_sync(0xffffffffu, amb0 | amb1)) {  // rare: exact fp64 test
+              const uint32_t j = S.t_start[pk >> kLocalBits] + (pk & kLocalMask);
+              if (amb0) hit0 = exact_hit(g, x, y, z, j, ta, TW[warp][0].pos, TW[warp][0].lim);
+              if (amb1) hit1 = exact_hit(g, x, y, z, j, tb, TW[warp][1].pos, TW[warp][1].lim);
+            }
+            const unsigned b0 = __ballot_sync(0xffffffffu, hit0);
+            const unsigned b1 = __ballot_sync(0xffffffffu, hit1);
+            const uint32_t p0 = cnt0 + __popc(b0 & lt), p1 = cnt1 + __popc(b1 & lt);
+            if (hit0 & (p0 < (uint32_t)maxn)) row0[p0] = pk;
+            if (hit1 & (p1 < (uint32_t)maxn)) row1[p1] = pk;
+            cnt0 += __popc(b0);
+            cnt1 += __popc(b1);
           }
           if (lane == 0) {
-            tcount[ta - t0] = count[0];
-            if (has_b) tcount[tb - t0] = count[1];
+            tcount[ta - t0] = cnt0;
+            if (has_b) tcount[tb - t0] = cnt1;
           }
+          __syncwarp();
         }
         __syncthreads();
       }
@@ -402,7 +429,7 @@ __device__ __forceinline__ void stage4(const Grid& g, const CellSm& S, const dou
                                        const double* __restrict__ f, double* sx, double* sy, double* sz,
                                        double* sf) {
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  for (int uu = warp; uu < S.G.nu; uu += kNW) {
+  for (int uu = warp; uu < S.G.nu; uu += (int)(blockDim.x >> 5)) {
     const int base = S.G.u_base[uu], len = S.G.u_len[uu];
     const uint32_t g0 = S.G.u_g[uu];
     double sh[3];
@@ -445,7 +472,7 @@ struct DensBody {
 };
 
 template <int N, bool W2>
-__global__ void __launch_bounds__(kCT) k_density_c(
+__global__ void __launch_bounds__(kCTD, 2) k_density_c(
     const double* __restrict__ x, const double* __restrict__ y, const double* __restrict__ z,
     const double* __restrict__ h, const double* __restrict__ m, const double* __restrict__ u,
     Grid g, const uint32_t* __restrict__ cstart, const uint32_t* __restrict__ cend,
@@ -512,7 +539,7 @@ __global__ void __launch_bounds__(kCT) k_density_c(
         body.sx = sx; body.sy = sy; body.sz = sz; body.sm = sm;
         body.tx = tx; body.ty = ty; body.tz = tz; body.tih2 = tih2;
         body.st = &st; body.g = &g; body.n = n;
-        walk_targets<kNW>(t0, t1, nbr, maxn, s_n, s_cur, S.G.pend, S.slot_off, body,
+        walk_targets<kNWD>(t0, t1, nbr, maxn, s_n, s_cur, S.G.pend, S.slot_off, body,
                           [&](uint32_t i, uint32_t c2) {
                             double v[2] = {body.sr, body.sd};
                             warp_multi_sum<2>(v);
@@ -564,7 +591,7 @@ __global__ void __launch_bounds__(kCT) k_density_c(
 
 // ------------------------------------------------------------------ a8 IAD
 template <int N, bool W2>
-__global__ void __launch_bounds__(kCT) k_iad_c(
+__global__ void __launch_bounds__(kCTD, 2) k_iad_c(
     const double* __restrict__ x, const double* __restrict__ y, const double* __restrict__ z,
     Grid g, const uint32_t* __restrict__ cstart, const uint32_t* __restrict__ cend,
     const unsigned long long* __restrict__ chmax, const uint32_t* __restrict__ clist,
@@ -642,7 +669,7 @@ __global__ void __launch_bounds__(kCT) k_iad_c(
         body.sx = sx; body.sy = sy; body.sz = sz; body.sv = sv;
         body.tx = tx; body.ty = ty; body.tz = tz; body.tih2 = tih2;
         body.st = &st; body.g = &g; body.n = n;
-        walk_targets<kNW>(t0, t1, nbr, maxn, s_n, s_cur, S.G.pend, S.slot_off, body,
+        walk_targets<kNWD>(t0, t1, nbr, maxn, s_n, s_cur, S.G.pend, S.slot_off, body,
                           [&](uint32_t i, uint32_t c2) {
                             double v[8] = {body.t11, body.t12, body.t13, body.t22,
                                            body.t23, body.t33, 0.0, 0.0};
@@ -937,7 +964,7 @@ static void density_t(sph_ctx* c) {
   const size_t smem = 4 * kDensCap * sizeof(double);
   set_smem(k_density_c<N, W2>, smem);
   sph_particles& P = c->P;
-  k_density_c<N, W2><<<cell_grid(c, 2), kCT, smem, c->stream>>>(
+  k_density_c<N, W2><<<cell_grid(c, 2), kCTD, smem, c->stream>>>(
       P.x, P.y, P.z, P.h, P.m, P.u, c->grid, c->s.cell_start, c->s.cell_end, c->s.cell_hmax,
       c->s.cell_list, c->s.ncell_list, c->s.nbr, c->s.ncount, c->maxn, c->phys, P.rho, P.omega,
       P.p, P.c, c->s.wB, c->s.ih2, c->s.vol, c->s.rinv, c->s.X, c->s.mX, c->s.cnt);
@@ -955,7 +982,7 @@ static void iad_t(sph_ctx* c) {
   const size_t smem = 4 * kDensCap * sizeof(double);
   set_smem(k_iad_c<N, W2>, smem);
   sph_particles& P = c->P;
-  k_iad_c<N, W2><<<cell_grid(c, 2), kCT, smem, c->stream>>>(
+  k_iad_c<N, W2><<<cell_grid(c, 2), kCTD, smem, c->stream>>>(
       P.x, P.y, P.z, c->grid, c->s.cell_start, c->s.cell_end, c->s.cell_hmax, c->s.cell_list,
       c->s.ncell_list, c->s.nbr, c->s.ncount, c->maxn, c->phys, c->s.wB, c->s.ih2, c->s.vol,
       P.c11, P.c12, P.c13, P.c22, P.c23, P.c33, c->s.ct, c->cap, c->s.cnt);
