@@ -27,7 +27,7 @@ constexpr int kSlots = 512;       // slot tables (R <= 3 in every dim: 343 slots
 constexpr int kMaxUnits = 128;    // staged (slot, local range) pieces per group
 constexpr int kSearchCap = 2048;  // staged candidates per group (float4)
 constexpr int kDensCap = 2048;    // staged particles per group, 4 fp64 fields
-constexpr int kMomCap = 1024;     // staged particles per group, 17 fp64 fields (1 CTA/SM)
+constexpr int kMomCap = 1088;     // staged particles per group, 17 fp64 fields (1 CTA/SM; a 27-cell stencil in 2 groups)
 constexpr int kCTM = 512;         // momentum CTA: 16 warps, one CTA per SM
 constexpr int kCTD = 512;         // density / IAD CTA: 16 warps, two CTAs per SM
 constexpr int kNWD = kCTD / 32;
@@ -48,6 +48,7 @@ void set_poly_constants(const double* poly, const double* dpoly) {
 struct GroupSm {
   int nu, total, k, l;
   uint32_t pend;
+  uint32_t next;  // dynamic target counter of the group (walk_targets)
   int u_slot[kMaxUnits];
   uint32_t u_g[kMaxUnits];
   int u_base[kMaxUnits];
@@ -99,7 +100,7 @@ __device__ __forceinline__ void warp_multi_sum(double (&v)[NV]) {
   for (int off = 16 / NV; off > 0; off >>= 1) v[0] += __shfl_xor_sync(0xffffffffu, v[0], off);
 }
 
-__device__ __forceinline__ double sinc_poly(double t) {
+__device__ __forceinline__ double sinc_poly(double t) {  // Horner
   double p = c_poly[kPolyTerms - 1];
 #pragma unroll
   for (int k = kPolyTerms - 2; k >= 0; --k) p = fma(p, t, c_poly[k]);
@@ -110,6 +111,17 @@ __device__ __forceinline__ double sinc_dpoly(double t) {
 #pragma unroll
   for (int k = kPolyTerms - 3; k >= 0; --k) p = fma(p, t, c_dpoly[k]);
   return p;
+}
+// Estrin form (dependency depth ~5 instead of 12) for the momentum pass, where four
+// warps per SMSP cannot hide the DFMA latency of a Horner chain (ncu "wait").
+static_assert(kPolyTerms == 13, "Estrin scheme below is written for degree 12");
+__device__ __forceinline__ double sinc_poly_e(double t) {
+  const double* c = c_poly;
+  const double t2 = t * t, t4 = t2 * t2, t8 = t4 * t4;
+  const double q0 = fma(fma(c[3], t, c[2]), t2, fma(c[1], t, c[0]));
+  const double q1 = fma(fma(c[7], t, c[6]), t2, fma(c[5], t, c[4]));
+  const double q2 = fma(fma(c[11], t, c[10]), t2, fma(c[9], t, c[8]));
+  return fma(fma(c[12], t4, q2), t8, fma(q1, t4, q0));
 }
 // "inline x*x*x*x..."; N > 0 fixes the exponent at compile time
 template <int N>
@@ -194,6 +206,7 @@ __device__ void build_group(CellSm& S, int cap) {
   G.k = k;
   G.l = l;
   G.pend = k >= K ? kSent : (((uint32_t)k << kLocalBits) | (uint32_t)l);
+  G.next = 0;
 }
 
 __device__ __forceinline__ void shifts_of(const Grid& g, const CellSm& S, int slot, double sh[3]) {
@@ -203,28 +216,34 @@ __device__ __forceinline__ void shifts_of(const Grid& g, const CellSm& S, int sl
 }
 
 // Warp-level walk over the entries of target rows that fall in the current
-// group [.., pend).  Row chunks are prefetched one chunk ahead; the first chunk
-// of the warp's next target is issued before the current target's work.
+// group [.., pend).  Targets are handed out dynamically (shared counter, reset by
+// build_group) so warps reach the group barrier together; row chunks are
+// prefetched one chunk ahead, and the first chunk of the warp's next target is
+// issued before the current target's work.
 template <int NW, class Body, class Finish>
 __device__ __forceinline__ void walk_targets(uint32_t t0, uint32_t t1, const uint32_t* __restrict__ nbr,
                                              int maxn, const uint32_t* s_n, uint32_t* s_cur,
-                                             uint32_t pend, const int* slot_off, Body&& body,
-                                             Finish&& finish) {
-  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  uint32_t t = t0 + warp;
+                                             uint32_t pend, const int* slot_off, uint32_t* s_next,
+                                             Body&& body, Finish&& finish) {
+  const int lane = threadIdx.x & 31;
+  uint32_t t = 0;
+  if (lane == 0) t = t0 + atomicAdd(s_next, 1u);
+  t = __shfl_sync(0xffffffffu, t, 0);
   uint32_t ef = kSent;
   if (t < t1) {
     const uint32_t c0 = s_cur[t - t0];
     ef = c0 + lane < s_n[t - t0] ? nbr[(size_t)t * maxn + c0 + lane] : kSent;
   }
-  for (; t < t1; t += NW) {
+  while (t < t1) {
     const uint32_t i = t - t0;
     const uint32_t n = s_n[i];
     const uint32_t* row = nbr + (size_t)t * maxn;
     uint32_t cur = s_cur[i];
     uint32_t e = ef;
-    // prefetch the next target's first chunk
-    const uint32_t tn = t + NW;
+    // claim + prefetch the next target's first chunk
+    uint32_t tn = 0;
+    if (lane == 0) tn = t0 + atomicAdd(s_next, 1u);
+    tn = __shfl_sync(0xffffffffu, tn, 0);
     if (tn < t1) {
       const uint32_t cn = s_cur[tn - t0];
       ef = cn + lane < s_n[tn - t0] ? nbr[(size_t)tn * maxn + cn + lane] : kSent;
@@ -242,6 +261,7 @@ __device__ __forceinline__ void walk_targets(uint32_t t0, uint32_t t1, const uin
       e = enext;
     }
     finish(i, cur);
+    t = tn;
   }
 }
 
@@ -423,11 +443,12 @@ __global__ void __launch_bounds__(kCT) k_search(const double* __restrict__ x,
   }
 }
 
-// stage [x y z] (shifted) + one extra field of the current group into SoA smem
-__device__ __forceinline__ void stage4(const Grid& g, const CellSm& S, const double* __restrict__ x,
-                                       const double* __restrict__ y, const double* __restrict__ z,
-                                       const double* __restrict__ f, double* sx, double* sy, double* sz,
-                                       double* sf) {
+// stage (x, y) and (z, f) of the current group as double2 pairs: one 16-byte LDS
+// per pair of fields, bank conflicts only within 8-lane quarters (ncu: the
+// 8-byte SoA layout cost ~3x the ideal shared-memory wavefronts)
+__device__ __forceinline__ void stage2x2(const Grid& g, const CellSm& S, const double* __restrict__ x,
+                                         const double* __restrict__ y, const double* __restrict__ z,
+                                         const double* __restrict__ f, double2* s01, double2* s23) {
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   for (int uu = warp; uu < S.G.nu; uu += (int)(blockDim.x >> 5)) {
     const int base = S.G.u_base[uu], len = S.G.u_len[uu];
@@ -435,10 +456,8 @@ __device__ __forceinline__ void stage4(const Grid& g, const CellSm& S, const dou
     double sh[3];
     shifts_of(g, S, S.G.u_slot[uu], sh);
     for (int i = lane; i < len; i += 32) {
-      sx[base + i] = x[g0 + i] + sh[0];
-      sy[base + i] = y[g0 + i] + sh[1];
-      sz[base + i] = z[g0 + i] + sh[2];
-      sf[base + i] = f[g0 + i];
+      s01[base + i] = make_double2(x[g0 + i] + sh[0], y[g0 + i] + sh[1]);
+      s23[base + i] = make_double2(z[g0 + i] + sh[2], f[g0 + i]);
     }
   }
 }
@@ -456,7 +475,7 @@ __device__ __forceinline__ void delta3(const Stencil& st, const Grid& g, double&
 
 // ------------------------------------------------------------------ a6 density + Omega + EOS
 struct DensBody {
-  const double *sx, *sy, *sz, *sm;
+  const double2 *s01, *s23;
   const double *tx, *ty, *tz, *tih2;
   const Stencil* st;
   const Grid* g;
@@ -484,10 +503,8 @@ __global__ void __launch_bounds__(kCTD, 2) k_density_c(
     double* __restrict__ rinv, double* __restrict__ X, double* __restrict__ mX,
     unsigned long long* __restrict__ cnt) {
   extern __shared__ double dsm[];
-  double* sx = dsm;
-  double* sy = sx + kDensCap;
-  double* sz = sy + kDensCap;
-  double* sm = sz + kDensCap;
+  double2* s01 = reinterpret_cast<double2*>(dsm);
+  double2* s23 = s01 + kDensCap;
   __shared__ CellSm S;
   __shared__ uint32_t s_n[kTgt], s_cur[kTgt];
   __shared__ double tx[kTgt], ty[kTgt], tz[kTgt], tih2[kTgt], acc0[kTgt], acc1[kTgt];
@@ -520,26 +537,27 @@ __global__ void __launch_bounds__(kCTD, 2) k_density_c(
         if (threadIdx.x == 0) build_group(S, kDensCap);
         __syncthreads();
         if (S.G.nu == 0) break;
-        stage4(g, S, x, y, z, m, sx, sy, sz, sm);
+        stage2x2(g, S, x, y, z, m, s01, s23);
         __syncthreads();
         struct B : DensBody {
           int n;
           __device__ __forceinline__ void operator()(int q) {
-            double dx = sx[q] - xa, dy = sy[q] - ya, dz = sz[q] - za;
+            const double2 p01 = s01[q], p23 = s23[q];
+            double dx = p01.x - xa, dy = p01.y - ya, dz = p23.x - za;
             delta3<W2>(*st, *g, dx, dy, dz);
             const double tt = (dx * dx + dy * dy + dz * dz) * ih2a;
             const double P = sinc_poly(tt);
             const double Pn1 = ipow<N - 1 < 0 ? 0 : N - 1>(P, n - 1);
             const double dP = sinc_dpoly(tt);
-            const double mj = sm[q];
+            const double mj = p23.y;
             sr = fma(mj, Pn1 * P, sr);
             sd = fma(mj, Pn1 * (3.0 * P + (2.0 * n) * tt * dP), sd);  // 3 S + v S'(v)
           }
         } body;
-        body.sx = sx; body.sy = sy; body.sz = sz; body.sm = sm;
+        body.s01 = s01; body.s23 = s23;
         body.tx = tx; body.ty = ty; body.tz = tz; body.tih2 = tih2;
         body.st = &st; body.g = &g; body.n = n;
-        walk_targets<kNWD>(t0, t1, nbr, maxn, s_n, s_cur, S.G.pend, S.slot_off, body,
+        walk_targets<kNWD>(t0, t1, nbr, maxn, s_n, s_cur, S.G.pend, S.slot_off, &S.G.next, body,
                           [&](uint32_t i, uint32_t c2) {
                             double v[2] = {body.sr, body.sd};
                             warp_multi_sum<2>(v);
@@ -602,10 +620,8 @@ __global__ void __launch_bounds__(kCTD, 2) k_iad_c(
     double* __restrict__ c23, double* __restrict__ c33, double* __restrict__ ct,
     int64_t ct_stride, unsigned long long* __restrict__ cnt) {
   extern __shared__ double dsm[];
-  double* sx = dsm;
-  double* sy = sx + kDensCap;
-  double* sz = sy + kDensCap;
-  double* sv = sz + kDensCap;
+  double2* s01 = reinterpret_cast<double2*>(dsm);
+  double2* s23 = s01 + kDensCap;
   __shared__ CellSm S;
   __shared__ uint32_t s_n[kTgt], s_cur[kTgt];
   __shared__ double tx[kTgt], ty[kTgt], tz[kTgt], tih2[kTgt];
@@ -637,10 +653,11 @@ __global__ void __launch_bounds__(kCTD, 2) k_iad_c(
         if (threadIdx.x == 0) build_group(S, kDensCap);
         __syncthreads();
         if (S.G.nu == 0) break;
-        stage4(g, S, x, y, z, vol, sx, sy, sz, sv);
+        stage2x2(g, S, x, y, z, vol, s01, s23);
         __syncthreads();
         struct B {
-          const double *sx, *sy, *sz, *sv, *tx, *ty, *tz, *tih2;
+          const double2 *s01, *s23;
+          const double *tx, *ty, *tz, *tih2;
           const Stencil* st;
           const Grid* g;
           int n;
@@ -653,10 +670,11 @@ __global__ void __launch_bounds__(kCTD, 2) k_iad_c(
             t11 = t12 = t13 = t22 = t23 = t33 = 0.0;
           }
           __device__ __forceinline__ void operator()(int q) {
-            double dx = sx[q] - xa, dy = sy[q] - ya, dz = sz[q] - za;
+            const double2 p01 = s01[q], p23 = s23[q];
+            double dx = p01.x - xa, dy = p01.y - ya, dz = p23.x - za;
             delta3<W2>(*st, *g, dx, dy, dz);
             const double tt = (dx * dx + dy * dy + dz * dz) * ih2a;
-            const double w = sv[q] * ipow<N>(sinc_poly(tt), n);  // (m_b/rho_b) S
+            const double w = p23.y * ipow<N>(sinc_poly(tt), n);  // (m_b/rho_b) S
             const double wx = w * dx, wy = w * dy;
             t11 = fma(wx, dx, t11);
             t12 = fma(wx, dy, t12);
@@ -666,10 +684,10 @@ __global__ void __launch_bounds__(kCTD, 2) k_iad_c(
             t33 = fma(w * dz, dz, t33);
           }
         } body;
-        body.sx = sx; body.sy = sy; body.sz = sz; body.sv = sv;
+        body.s01 = s01; body.s23 = s23;
         body.tx = tx; body.ty = ty; body.tz = tz; body.tih2 = tih2;
         body.st = &st; body.g = &g; body.n = n;
-        walk_targets<kNWD>(t0, t1, nbr, maxn, s_n, s_cur, S.G.pend, S.slot_off, body,
+        walk_targets<kNWD>(t0, t1, nbr, maxn, s_n, s_cur, S.G.pend, S.slot_off, &S.G.next, body,
                           [&](uint32_t i, uint32_t c2) {
                             double v[8] = {body.t11, body.t12, body.t13, body.t22,
                                            body.t23, body.t33, 0.0, 0.0};
@@ -726,7 +744,10 @@ struct MomOut {
   double *ax, *ay, *az, *du, *vsig;
 };
 // staged field slots (SoA, kMomCap doubles each)
-enum { F_X, F_Y, F_Z, F_VX, F_VY, F_VZ, F_M, F_IH2, F_C, F_MX, F_MR, F_C11, F_C12, F_C13, F_C22, F_C23, F_C33 };
+// staged source fields as double2 pairs (kMomPairs arrays of kMomCap):
+//   0 (x, y)  1 (z, vx)  2 (vy, vz)  3 (m, 1/h^2)  4 (c, m X)  5 (m/rho, C~11)
+//   6 (C~12, C~13)  7 (C~22, C~23)  8 (C~33, -)
+constexpr int kMomPairs = 9;
 // per-target smem fields
 enum { T_X, T_Y, T_Z, T_VX, T_VY, T_VZ, T_IH2, T_WB, T_RINV, T_XP, T_C, T_A11, T_A12, T_A13, T_A22, T_A23, T_A33, T_N };
 
@@ -737,8 +758,9 @@ __global__ void __launch_bounds__(kCTM, 1) k_momentum_c(
     const uint32_t* __restrict__ clist, const uint32_t* __restrict__ nclist,
     const uint32_t* __restrict__ nbr, const uint32_t* __restrict__ ncount, int maxn, Phys ph,
     double* __restrict__ dts, unsigned long long* __restrict__ cnt) {
-  extern __shared__ double dsm[];  // kMomFields * kMomCap staged + T_N * kTgt target fields
-  double* const T = dsm + kMomFields * kMomCap;
+  extern __shared__ double dsm[];  // kMomPairs * kMomCap double2 staged + T_N * kTgt target fields
+  double2* const F2 = reinterpret_cast<double2*>(dsm);
+  double* const T = dsm + 2 * kMomPairs * kMomCap;
   __shared__ CellSm S;
   __shared__ uint32_t s_n[kTgt], s_cur[kTgt];
   __shared__ double acc[5][kTgt];
@@ -797,25 +819,22 @@ __global__ void __launch_bounds__(kCTM, 1) k_momentum_c(
           shifts_of(g, S, S.G.u_slot[uu], sh);
           for (int i = lane; i < len; i += 32) {
             const uint32_t j = g0 + i;
-            double* q = dsm + base + i;
-            q[F_X * kMomCap] = src.x[j] + sh[0];
-            q[F_Y * kMomCap] = src.y[j] + sh[1];
-            q[F_Z * kMomCap] = src.z[j] + sh[2];
-            q[F_VX * kMomCap] = src.vx[j];
-            q[F_VY * kMomCap] = src.vy[j];
-            q[F_VZ * kMomCap] = src.vz[j];
-            q[F_M * kMomCap] = src.m[j];
-            q[F_IH2 * kMomCap] = src.ih2[j];
-            q[F_C * kMomCap] = src.c[j];
-            q[F_MX * kMomCap] = src.mX[j];
-            q[F_MR * kMomCap] = src.mr[j];
-#pragma unroll
-            for (int k = 0; k < 6; ++k) q[(F_C11 + k) * kMomCap] = src.ct[k * src.ct_stride + j];
+            double2* q = F2 + base + i;
+            const int64_t cs = src.ct_stride;
+            q[0 * kMomCap] = make_double2(src.x[j] + sh[0], src.y[j] + sh[1]);
+            q[1 * kMomCap] = make_double2(src.z[j] + sh[2], src.vx[j]);
+            q[2 * kMomCap] = make_double2(src.vy[j], src.vz[j]);
+            q[3 * kMomCap] = make_double2(src.m[j], src.ih2[j]);
+            q[4 * kMomCap] = make_double2(src.c[j], src.mX[j]);
+            q[5 * kMomCap] = make_double2(src.mr[j], src.ct[j]);
+            q[6 * kMomCap] = make_double2(src.ct[cs + j], src.ct[2 * cs + j]);
+            q[7 * kMomCap] = make_double2(src.ct[3 * cs + j], src.ct[4 * cs + j]);
+            q[8 * kMomCap] = make_double2(src.ct[5 * cs + j], 0.0);
           }
         }
         __syncthreads();
         struct B {
-          const double* F;
+          const double2* F2;
           const double* T;
           const Stencil* st;
           const Grid* g;
@@ -835,8 +854,9 @@ __global__ void __launch_bounds__(kCTM, 1) k_momentum_c(
             vs = -1.0;
           }
           __device__ __forceinline__ void operator()(int qi) {
-            const double* q = F + qi;
-            double dx = q[F_X * kMomCap] - xa, dy = q[F_Y * kMomCap] - ya, dz = q[F_Z * kMomCap] - za;
+            const double2* q = F2 + qi;
+            const double2 p0 = q[0], p1 = q[kMomCap], p3 = q[3 * kMomCap];
+            double dx = p0.x - xa, dy = p0.y - ya, dz = p1.x - za;
             delta3<W2>(*st, *g, dx, dy, dz);  // Delta_ab = x_b - x_a
             const double r2 = dx * dx + dy * dy + dz * dz;
             // coincident pair: Delta = 0 zeroes every term below; it is only
@@ -844,47 +864,45 @@ __global__ void __launch_bounds__(kCTM, 1) k_momentum_c(
             const bool coinc = r2 == 0.0;
             *ncoinc += coinc;
             const double ta = r2 * ih2a;
-            const double Sa = ipow<N>(sinc_poly(ta), n);
+            const double Sa = ipow<N>(sinc_poly_e(ta), n);
             const double Wa = wBa * Sa;
-            const double tb = r2 * q[F_IH2 * kMomCap];
+            const double tb = r2 * p3.y;
             double Sb = Sa;  // equal h: W(r, h_b) shares the kernel value
-            if (tb != ta) Sb = tb < 4.0 ? ipow<N>(sinc_poly(tb), n) : 0.0;
-            // R5: A_ab(h_a) = C_a Delta W_ab(h_a);  R4: A_ab(h_b) = C~_b Delta S_b
-            const double Aax = (a11 * dx + a12 * dy + a13 * dz) * Wa;
-            const double Aay = (a12 * dx + a22 * dy + a23 * dz) * Wa;
-            const double Aaz = (a13 * dx + a23 * dy + a33 * dz) * Wa;
-            const double b11 = q[F_C11 * kMomCap], b12 = q[F_C12 * kMomCap], b13 = q[F_C13 * kMomCap];
-            const double b22 = q[F_C22 * kMomCap], b23 = q[F_C23 * kMomCap], b33 = q[F_C33 * kMomCap];
-            const double Abx = (b11 * dx + b12 * dy + b13 * dz) * Sb;
-            const double Aby = (b12 * dx + b22 * dy + b23 * dz) * Sb;
-            const double Abz = (b13 * dx + b23 * dy + b33 * dz) * Sb;
-            const double mb = q[F_M * kMomCap], mXb = q[F_MX * kMomCap], mrb = q[F_MR * kMomCap];
-            const double cb = q[F_C * kMomCap];
-            const double vabx = vxa - q[F_VX * kMomCap], vaby = vya - q[F_VY * kMomCap],
-                         vabz = vza - q[F_VZ * kMomCap];
+            if (tb != ta) Sb = tb < 4.0 ? ipow<N>(sinc_poly_e(tb), n) : 0.0;
+            // R5: A_ab(h_a) = C_a Delta W_ab(h_a) = Wa u;  R4: A_ab(h_b) = C~_b Delta S_b = Sb w
+            const double ux = a11 * dx + a12 * dy + a13 * dz;
+            const double uy = a12 * dx + a22 * dy + a23 * dz;
+            const double uz = a13 * dx + a23 * dy + a33 * dz;
+            const double2 p5 = q[5 * kMomCap], p6 = q[6 * kMomCap], p7 = q[7 * kMomCap], p8 = q[8 * kMomCap];
+            const double b11 = p5.y, b12 = p6.x, b13 = p6.y, b22 = p7.x, b23 = p7.y, b33 = p8.x;
+            const double wx = b11 * dx + b12 * dy + b13 * dz;
+            const double wy = b12 * dx + b22 * dy + b23 * dz;
+            const double wz = b13 * dx + b23 * dy + b33 * dz;
+            const double2 p2 = q[2 * kMomCap], p4 = q[4 * kMomCap];
+            const double mb = p3.x, mXb = p4.y, mrb = p5.x, cb = p4.x;
+            const double vabx = vxa - p1.y, vaby = vya - p2.x, vabz = vza - p2.y;
             const double vdotx = -(vabx * dx + vaby * dy + vabz * dz);  // v_ab . x_ab
             // Eq. 5: w_ab = v_ab . x_ab / |x_ab|, Pi' only when approaching
             const double w = vdotx < 0.0 ? vdotx * rsqrt(r2) : 0.0;
-            const double Pi = -0.5 * alpha * (ca + cb - 3.0 * w) * w;
-            const double vsab = coinc ? -1.0 : ca + cb - 3.0 * w;  // v_sig; w == min(w, 0)
-            vs = vsab > vs ? vsab : vs;
-            // g = 1/2 m_b Pi' (A_a / rho_a + A_b / rho_b)   (Eq. 4 pair term)
-            const double hp = 0.5 * Pi;
-            const double mra = mb * rinva;
-            const double gx = hp * (mra * Aax + mrb * Abx);
-            const double gy = hp * (mra * Aay + mrb * Aby);
-            const double gz = hp * (mra * Aaz + mrb * Abz);
-            const double mXa = mb * Xa;
-            fx -= fma(mXa, Aax, fma(mXb, Abx, gx));  // Eq. 2 with R2
-            fy -= fma(mXa, Aay, fma(mXb, Aby, gy));
-            fz -= fma(mXa, Aaz, fma(mXb, Abz, gz));
-            fu += mXa * (vabx * Aax + vaby * Aay + vabz * Aaz) +
-                  0.5 * (vabx * gx + vaby * gy + vabz * gz);  // Eq. 3 with R1, R3
+            const double vsab = ca + cb - 3.0 * w;  // v_sig; w == min(w, 0)
+            const double hp = -0.25 * alpha * vsab * w;  // Pi'/2, Eq. 5
+            vs = (!coinc && vsab > vs) ? vsab : vs;
+            // Eq. 2 with R2 and Eq. 4: a += -m_b (X_a A_a + X_b A_b) - g,
+            //   g = (Pi'/2) (m_b/rho_a A_a + m_b/rho_b A_b), folded onto u and w
+            const double ka = mb * fma(hp, rinva, Xa) * Wa;
+            const double kb = fma(hp, mrb, mXb) * Sb;
+            fx -= fma(ka, ux, kb * wx);
+            fy -= fma(ka, uy, kb * wy);
+            fz -= fma(ka, uz, kb * wz);
+            // Eq. 3 with R1, R3: du += m_b X_a v_ab.A_a + (1/2) v_ab.g
+            const double vu = vabx * ux + vaby * uy + vabz * uz;
+            const double vw = vabx * wx + vaby * wy + vabz * wz;
+            fu += mb * fma(0.5 * hp, rinva, Xa) * Wa * vu + 0.5 * hp * mrb * Sb * vw;
           }
         } body;
-        body.F = dsm; body.T = T; body.st = &st; body.g = &g; body.alpha = ph.alpha; body.n = n;
+        body.F2 = F2; body.T = T; body.st = &st; body.g = &g; body.alpha = ph.alpha; body.n = n;
         body.ncoinc = &ncoinc;
-        walk_targets<kNWM>(t0, t1, nbr, maxn, s_n, s_cur, S.G.pend, S.slot_off, body,
+        walk_targets<kNWM>(t0, t1, nbr, maxn, s_n, s_cur, S.G.pend, S.slot_off, &S.G.next, body,
                            [&](uint32_t i, uint32_t c2) {
                              double v[4] = {body.fx, body.fy, body.fz, body.fu};
                              warp_multi_sum<4>(v);
@@ -997,7 +1015,7 @@ int launch_iad(sph_ctx* c) {
 
 template <int N, bool W2>
 static void momentum_t(sph_ctx* c) {
-  const size_t smem = ((size_t)kMomFields * kMomCap + (size_t)T_N * kTgt) * sizeof(double);
+  const size_t smem = ((size_t)2 * kMomPairs * kMomCap + (size_t)T_N * kTgt) * sizeof(double);
   set_smem(k_momentum_c<N, W2>, smem);
   sph_particles& P = c->P;
   MomSrc src = {P.x, P.y, P.z, P.vx, P.vy, P.vz, P.m, c->s.ih2, P.c, c->s.mX, c->s.vol, c->s.ct, c->cap};
