@@ -293,7 +293,7 @@ __device__ __forceinline__ void wrap32(const Stencil& st, const Grid& g, float& 
 
 // ------------------------------------------------------------------ a5 search
 template <bool W2>
-__global__ void __launch_bounds__(kCT) k_search(const double* __restrict__ x,
+__global__ void __launch_bounds__(kCT, 2) k_search(const double* __restrict__ x,
                                                 const double* __restrict__ y,
                                                 const double* __restrict__ z,
                                                 const double* __restrict__ h, Grid g,
@@ -305,7 +305,7 @@ __global__ void __launch_bounds__(kCT) k_search(const double* __restrict__ x,
                                                 uint32_t* __restrict__ nbr,
                                                 uint32_t* __restrict__ ncount, int maxn,
                                                 unsigned int* __restrict__ maxcount) {
-  extern __shared__ float4 cand[];  // kSearchCap + 32 padding
+  extern __shared__ float4 cand[];  // kSearchCap + 64 padding
   __shared__ CellSm S;
   __shared__ uint32_t tcount[kTgt];
   __shared__ TgtW TW[kNW][2];
@@ -355,7 +355,7 @@ __global__ void __launch_bounds__(kCT) k_search(const double* __restrict__ x,
           }
         }
         // pad to a multiple of 32 with far-away sentinels (never hit, never ambiguous)
-        const int padded = (total + 31) & ~31;
+        const int padded = (total + 63) & ~63;  // the scan takes two tiles per iteration
         for (int q = total + threadIdx.x; q < padded; q += blockDim.x)
           cand[q] = make_float4(INFINITY, INFINITY, INFINITY, __uint_as_float(kSent));
         __syncthreads();
@@ -395,10 +395,12 @@ __global__ void __launch_bounds__(kCT) k_search(const double* __restrict__ x,
           const uint32_t self0 = ((uint32_t)S.kself << kLocalBits) | (ta - S.sc);
           const uint32_t self1 = ((uint32_t)S.kself << kLocalBits) | (tb - S.sc);
           uint32_t cnt0 = tcount[ta - t0], cnt1 = tcount[tb - t0];
-          uint32_t* const row0 = nbr + (size_t)ta * maxn;
-          uint32_t* const row1 = nbr + (size_t)tb * maxn;
-          for (int q0 = 0; q0 < padded; q0 += 32) {
-            const float4 cd = cand[q0 + lane];
+          uint32_t* row0 = nbr + (size_t)ta * maxn;
+          uint32_t* row1 = nbr + (size_t)tb * maxn;
+          // keep the row bases in registers (else ptxas re-derives nbr + t*maxn + p in 64-bit per store)
+          asm volatile("" : "+l"(row0), "+l"(row1));
+          // one staged candidate against both targets: fp32 band test, exact fp64 when inside it
+          auto test = [&](const float4 cd, bool& hit0, bool& hit1) {
             const uint32_t pk = __float_as_uint(cd.w);
             float dx0 = cd.x - ax0, dy0 = cd.y - ay0, dz0 = cd.z - az0;
             float dx1 = cd.x - ax1, dy1 = cd.y - ay1, dz1 = cd.z - az1;
@@ -408,8 +410,8 @@ __global__ void __launch_bounds__(kCT) k_search(const double* __restrict__ x,
             }
             const float r0 = fmaf(dz0, dz0, fmaf(dy0, dy0, dx0 * dx0));
             const float r1 = fmaf(dz1, dz1, fmaf(dy1, dy1, dx1 * dx1));
-            bool hit0 = (r0 < lo0) & (pk != self0);
-            bool hit1 = (r1 < lo1) & (pk != self1);
+            hit0 = (r0 < lo0) & (pk != self0);
+            hit1 = (r1 < lo1) & (pk != self1);
             const bool amb0 = (r0 >= lo0) & (r0 < hi0);
             const bool amb1 = (r1 >= lo1) & (r1 < hi1);
             if (__ballot_sync(0xffffffffu, amb0 | amb1)) {  // rare: exact fp64 test
@@ -417,13 +419,24 @@ __global__ void __launch_bounds__(kCT) k_search(const double* __restrict__ x,
               if (amb0) hit0 = exact_hit(g, x, y, z, j, ta, TW[warp][0].pos, TW[warp][0].lim);
               if (amb1) hit1 = exact_hit(g, x, y, z, j, tb, TW[warp][1].pos, TW[warp][1].lim);
             }
-            const unsigned b0 = __ballot_sync(0xffffffffu, hit0);
-            const unsigned b1 = __ballot_sync(0xffffffffu, hit1);
-            const uint32_t p0 = cnt0 + __popc(b0 & lt), p1 = cnt1 + __popc(b1 & lt);
-            if (hit0 & (p0 < (uint32_t)maxn)) row0[p0] = pk;
-            if (hit1 & (p1 < (uint32_t)maxn)) row1[p1] = pk;
-            cnt0 += __popc(b0);
-            cnt1 += __popc(b1);
+          };
+          // two tiles per iteration (padded to 64): four independent test chains in flight
+          for (int q0 = 0; q0 < padded; q0 += 64) {
+            const float4 cA = cand[q0 + lane], cB = cand[q0 + 32 + lane];
+            bool hA0, hA1, hB0, hB1;
+            test(cA, hA0, hA1);
+            test(cB, hB0, hB1);
+            const unsigned bA0 = __ballot_sync(0xffffffffu, hA0), bA1 = __ballot_sync(0xffffffffu, hA1);
+            const unsigned bB0 = __ballot_sync(0xffffffffu, hB0), bB1 = __ballot_sync(0xffffffffu, hB1);
+            const uint32_t pA0 = cnt0 + __popc(bA0 & lt), pA1 = cnt1 + __popc(bA1 & lt);
+            const uint32_t pB0 = cnt0 + __popc(bA0) + __popc(bB0 & lt);
+            const uint32_t pB1 = cnt1 + __popc(bA1) + __popc(bB1 & lt);
+            if (hA0 & (pA0 < (uint32_t)maxn)) row0[pA0] = __float_as_uint(cA.w);
+            if (hA1 & (pA1 < (uint32_t)maxn)) row1[pA1] = __float_as_uint(cA.w);
+            if (hB0 & (pB0 < (uint32_t)maxn)) row0[pB0] = __float_as_uint(cB.w);
+            if (hB1 & (pB1 < (uint32_t)maxn)) row1[pB1] = __float_as_uint(cB.w);
+            cnt0 += __popc(bA0) + __popc(bB0);
+            cnt1 += __popc(bA1) + __popc(bB1);
           }
           if (lane == 0) {
             tcount[ta - t0] = cnt0;
@@ -968,7 +981,7 @@ static void set_smem(K kern, size_t bytes) {
 }
 
 int launch_neighbors(sph_ctx* c) {
-  const size_t smem = (kSearchCap + 32) * sizeof(float4);
+  const size_t smem = (kSearchCap + 64) * sizeof(float4);
   auto kern = any_wrap2(c) ? k_search<true> : k_search<false>;
   set_smem(kern, smem);
   kern<<<cell_grid(c, 4), kCT, smem, c->stream>>>(
