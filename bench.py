@@ -276,6 +276,24 @@ def run_ours(args):
     except Exception:
         pass
     phases = {k: round(v / args.steps, 4) for k, v in phase_ms.items() if v}
+    # DRAM bytes per launch of the dominant kernel from the committed ncu --set full capture
+    # (profiles/r1_ncu_traffic.json; only for the workload it was captured on)
+    traffic = None
+    try:
+        tr = json.load(open(os.path.join(ROOT, "profiles", "r1_ncu_traffic.json")))
+        if args.workload == "weak" and world == 1:
+            k = tr["kernels"]["k_momentum_c"]
+            traffic = k["dram_read_bytes"] + k["dram_write_bytes"]
+    except Exception:
+        pass
+    # every FP64-bound pair pass against the same measured peak (algorithmic flops / event time)
+    pair_kernels = {}
+    for ph_name in ("density", "iad", "momentum"):
+        t = phase_ms.get(ph_name, 0.0) / args.steps
+        if t > 0:
+            a = FLOPS_PER_PAIR[ph_name] * pairs / (t * 1e-3) / 1e12
+            pair_kernels[ph_name] = {"ms": round(t, 3), "tflops": round(a, 3),
+                                     "frac": round(a / peak64, 4) if peak64 else None}
     line = {
         "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": max(world, 1),
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms_step,
@@ -289,9 +307,12 @@ def run_ours(args):
         "roofline": {"kernel": "k_momentum", "bound": "alu", "achieved": achieved,
                      "peak": peak64, "unit": "TFLOP/s",
                      "peak_source": "measured live: DFMA kernel (sph_measure_fp64_peak)",
-                     "frac": achieved / peak64 if peak64 else None, "traffic": None,
+                     "frac": achieved / peak64 if peak64 else None, "traffic": traffic,
+                     "traffic_source": "profiles/r1_ncu_traffic.json (dram__bytes_read+write, 1 launch)",
+                     "algorithmic_bytes": 4.0 * pairs + 136.0 * n_local,
                      "flops_per_pair": FLOPS_PER_PAIR["momentum"], "pairs_per_launch": pairs,
                      "avg_launch_ms": mom_ms},
+        "pair_kernels_fp64": pair_kernels,
         "phases_ms_per_step": phases,
         "gpu_launches": int(sum(phase_launch.values())),
         "e2e": {"value": n_total * e2e_steps / (e2e_ms * 1e-3), "unit": UNIT,
