@@ -212,7 +212,7 @@ def run_ours(args):
     d, desc = workload(args.workload, max(world, 1), rank)
     n_local = d["x"].size
     # room for halos + migrants (multi-GPU); a single GPU needs exactly n
-    cap = n_local if world == 1 else int(n_local * 1.25) + 4096
+    cap = n_local if world == 1 else int(n_local * 1.6) + 4096
     stream = torch.cuda.Stream()
     with torch.cuda.stream(stream):
         sim = sph.Simulation(d, capacity=cap, stream=stream.cuda_stream, rank=rank, nranks=world,

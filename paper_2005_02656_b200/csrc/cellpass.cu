@@ -100,6 +100,29 @@ __device__ __forceinline__ void warp_multi_sum(double (&v)[NV]) {
   for (int off = 16 / NV; off > 0; off >>= 1) v[0] += __shfl_xor_sync(0xffffffffu, v[0], off);
 }
 
+// transpose-reduce over each 16-lane half: value k of a half ends in its lane 4k (NV = 4)
+template <int NV>
+__device__ __forceinline__ void half_multi_sum(double (&v)[NV]) {
+  const int lane = threadIdx.x & 31;
+#pragma unroll
+  for (int cnt = NV, off = 8; cnt > 1; cnt >>= 1, off >>= 1) {
+    const bool upper = (lane & off) != 0;
+#pragma unroll
+    for (int i = 0; i < cnt / 2; ++i) {
+      const double send = upper ? v[i] : v[i + cnt / 2];
+      const double keep = upper ? v[i + cnt / 2] : v[i];
+      v[i] = keep + __shfl_xor_sync(0xffffffffu, send, off);
+    }
+  }
+#pragma unroll
+  for (int off = 8 / NV; off > 0; off >>= 1) v[0] += __shfl_xor_sync(0xffffffffu, v[0], off);
+}
+__device__ __forceinline__ double half_max(double v) {
+#pragma unroll
+  for (int o = 8; o; o >>= 1) v = fmax(v, __shfl_xor_sync(0xffffffffu, v, o));
+  return v;
+}
+
 __device__ __forceinline__ double sinc_poly(double t) {  // Horner
   double p = c_poly[kPolyTerms - 1];
 #pragma unroll
@@ -217,9 +240,14 @@ __device__ __forceinline__ void shifts_of(const Grid& g, const CellSm& S, int sl
 
 // Warp-level walk over the entries of target rows that fall in the current
 // group [.., pend).  Targets are handed out dynamically (shared counter, reset by
-// build_group) so warps reach the group barrier together; row chunks are
-// prefetched one chunk ahead, and the first chunk of the warp's next target is
-// issued before the current target's work.
+// build_group) so warps reach the group barrier together.  Row chunks (32
+// entries) stream through a 3-deep register ring (ncu: with one chunk of
+// prefetch the row load was the top stall), and the first three chunks of the
+// warp's next target are issued before the current target's work.
+__device__ __forceinline__ uint32_t row_chunk(const uint32_t* row, uint32_t pos, uint32_t n) {
+  return pos < n ? row[pos] : kSent;
+}
+
 template <int NW, class Body, class Finish>
 __device__ __forceinline__ void walk_targets(uint32_t t0, uint32_t t1, const uint32_t* __restrict__ nbr,
                                              int maxn, const uint32_t* s_n, uint32_t* s_cur,
@@ -229,38 +257,108 @@ __device__ __forceinline__ void walk_targets(uint32_t t0, uint32_t t1, const uin
   uint32_t t = 0;
   if (lane == 0) t = t0 + atomicAdd(s_next, 1u);
   t = __shfl_sync(0xffffffffu, t, 0);
-  uint32_t ef = kSent;
+  uint32_t f0 = kSent, f1 = kSent, f2 = kSent;
   if (t < t1) {
-    const uint32_t c0 = s_cur[t - t0];
-    ef = c0 + lane < s_n[t - t0] ? nbr[(size_t)t * maxn + c0 + lane] : kSent;
+    const uint32_t c0 = s_cur[t - t0] + lane, nn = s_n[t - t0];
+    const uint32_t* r = nbr + (size_t)t * maxn;
+    f0 = row_chunk(r, c0, nn);
+    f1 = row_chunk(r, c0 + 32, nn);
+    f2 = row_chunk(r, c0 + 64, nn);
   }
   while (t < t1) {
     const uint32_t i = t - t0;
     const uint32_t n = s_n[i];
     const uint32_t* row = nbr + (size_t)t * maxn;
     uint32_t cur = s_cur[i];
-    uint32_t e = ef;
-    // claim + prefetch the next target's first chunk
+    uint32_t e0 = f0, e1 = f1, e2 = f2;
+    // claim the next target and prefetch its first three chunks
     uint32_t tn = 0;
     if (lane == 0) tn = t0 + atomicAdd(s_next, 1u);
     tn = __shfl_sync(0xffffffffu, tn, 0);
     if (tn < t1) {
-      const uint32_t cn = s_cur[tn - t0];
-      ef = cn + lane < s_n[tn - t0] ? nbr[(size_t)tn * maxn + cn + lane] : kSent;
+      const uint32_t cn = s_cur[tn - t0] + lane, nn = s_n[tn - t0];
+      const uint32_t* r = nbr + (size_t)tn * maxn;
+      f0 = row_chunk(r, cn, nn);
+      f1 = row_chunk(r, cn + 32, nn);
+      f2 = row_chunk(r, cn + 64, nn);
     }
     body.begin(i);
     for (;;) {
-      const bool in = e < pend;
+      const bool in = e0 < pend;
       const unsigned b = __ballot_sync(0xffffffffu, in);
       const int m = __popc(b);
-      uint32_t enext = kSent;
-      if (m == 32 && cur + 32 + lane < n) enext = row[cur + 32 + lane];
-      if (in) body(slot_off[e >> kLocalBits] + (int)(e & kLocalMask));
+      const uint32_t e3 = m == 32 ? row_chunk(row, cur + 96 + lane, n) : kSent;
+      if (in) body(slot_off[e0 >> kLocalBits] + (int)(e0 & kLocalMask));
       cur += m;
       if (m < 32) break;
-      e = enext;
+      e0 = e1;
+      e1 = e2;
+      e2 = e3;
     }
     finish(i, cur);
+    t = tn;
+  }
+}
+
+// Same walk with 16 lanes per target (two targets per warp, one per half-warp):
+// the per-(target, group) setup and reduction is shared by two targets and the
+// unused lanes at the end of a segment drop from up to 31 to up to 15.  Both
+// halves step together; a half whose segment ended idles until the other is done.
+template <class Body, class Finish>
+__device__ __forceinline__ void walk_targets_half(uint32_t t0, uint32_t t1,
+                                                  const uint32_t* __restrict__ nbr, int maxn,
+                                                  const uint32_t* s_n, uint32_t* s_cur,
+                                                  uint32_t pend, const int* slot_off,
+                                                  uint32_t* s_next, Body&& body, Finish&& finish) {
+  const int lane = threadIdx.x & 31, l16 = lane & 15;
+  const unsigned hmask = (threadIdx.x & 16) ? 0xffff0000u : 0x0000ffffu;
+  auto claim = [&]() {
+    uint32_t v = 0;
+    if (l16 == 0) v = t0 + atomicAdd(s_next, 1u);
+    return __shfl_sync(0xffffffffu, v, lane & 16);
+  };
+  uint32_t t = claim();
+  uint32_t f0 = kSent, f1 = kSent, f2 = kSent;
+  if (t < t1) {
+    const uint32_t c0 = s_cur[t - t0] + l16, nn = s_n[t - t0];
+    const uint32_t* r = nbr + (size_t)t * maxn;
+    f0 = row_chunk(r, c0, nn);
+    f1 = row_chunk(r, c0 + 16, nn);
+    f2 = row_chunk(r, c0 + 32, nn);
+  }
+  while (__any_sync(0xffffffffu, t < t1)) {
+    const bool act = t < t1;
+    const uint32_t i = act ? t - t0 : 0;
+    const uint32_t n = act ? s_n[i] : 0;
+    const uint32_t* row = nbr + (size_t)(act ? t : 0) * maxn;
+    uint32_t cur = act ? s_cur[i] : 0;
+    uint32_t e0 = f0, e1 = f1, e2 = f2;
+    const uint32_t tn = claim();
+    f0 = f1 = f2 = kSent;
+    if (tn < t1) {
+      const uint32_t cn = s_cur[tn - t0] + l16, nn = s_n[tn - t0];
+      const uint32_t* r = nbr + (size_t)tn * maxn;
+      f0 = row_chunk(r, cn, nn);
+      f1 = row_chunk(r, cn + 16, nn);
+      f2 = row_chunk(r, cn + 32, nn);
+    }
+    if (act) body.begin(i);
+    bool live = act;
+    for (;;) {
+      const bool in = live && e0 < pend;
+      const unsigned b = __ballot_sync(0xffffffffu, in);
+      const int m = __popc(b & hmask);
+      const bool more = live && m == 16;
+      const uint32_t e3 = more ? row_chunk(row, cur + 48 + l16, n) : kSent;
+      if (in) body(slot_off[e0 >> kLocalBits] + (int)(e0 & kLocalMask));
+      cur += m;
+      live = more;
+      if (!__any_sync(0xffffffffu, live)) break;
+      e0 = e1;
+      e1 = e2;
+      e2 = e3;
+    }
+    finish(act, i, cur);
     t = tn;
   }
 }
@@ -915,17 +1013,20 @@ __global__ void __launch_bounds__(kCTM, 1) k_momentum_c(
         } body;
         body.F2 = F2; body.T = T; body.st = &st; body.g = &g; body.alpha = ph.alpha; body.n = n;
         body.ncoinc = &ncoinc;
-        walk_targets<kNWM>(t0, t1, nbr, maxn, s_n, s_cur, S.G.pend, S.slot_off, &S.G.next, body,
-                           [&](uint32_t i, uint32_t c2) {
-                             double v[4] = {body.fx, body.fy, body.fz, body.fu};
-                             warp_multi_sum<4>(v);
-                             const double e = wmax(body.vs);
-                             if ((lane & 7) == 0) acc[lane >> 3][i] += v[0];
-                             if (lane == 0) {
-                               s_cur[i] = c2;
-                               acc[4][i] = fmax(acc[4][i], e);
-                             }
-                           });
+        walk_targets_half(t0, t1, nbr, maxn, s_n, s_cur, S.G.pend, S.slot_off, &S.G.next, body,
+                          [&](bool act, uint32_t i, uint32_t c2) {
+                            double v[4] = {body.fx, body.fy, body.fz, body.fu};
+                            half_multi_sum<4>(v);
+                            const double e = half_max(body.vs);
+                            const int l16 = lane & 15;
+                            if (act) {
+                              if ((l16 & 3) == 0) acc[l16 >> 2][i] += v[0];
+                              if (l16 == 0) {
+                                s_cur[i] = c2;
+                                acc[4][i] = fmax(acc[4][i], e);
+                              }
+                            }
+                          });
         __syncthreads();
       }
       for (uint32_t t = t0 + threadIdx.x; t < t1; t += blockDim.x) {

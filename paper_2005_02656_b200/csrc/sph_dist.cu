@@ -295,19 +295,39 @@ static bool unpack_all(sph_ctx* c, const FieldSet& fs, int64_t dst0) {
 }
 
 // all-gather the per-peer send counts, derive receive counts
-static bool swap_counts(sph_ctx* c) {
+// All-gather every rank's row [send counts to each peer..., base count] and derive this
+// rank's receive counts.  `need(send_total, recv_total, base)` is then evaluated for EVERY
+// rank from the same matrix, so a capacity failure is a collective decision: all ranks
+// fail together instead of one rank leaving the others blocked in the next collective.
+template <class Need>
+static bool swap_counts(sph_ctx* c, int64_t base, Need&& need) {
   Dist& D = *c->dist;
-  const int G = D.G;
-  CUK(cudaMemcpyAsync(D.cnt_d, D.scnt.data(), sizeof(int64_t) * G, cudaMemcpyHostToDevice, c->stream));
-  NCK(ncclAllGather(D.cnt_d, D.cnt_all_d, G, ncclInt64, D.comm, c->stream));
-  std::vector<int64_t> all((size_t)G * G);
-  CUK(cudaMemcpyAsync(all.data(), D.cnt_all_d, sizeof(int64_t) * G * G, cudaMemcpyDeviceToHost, c->stream));
+  const int G = D.G, W = G + 1;
+  std::vector<int64_t> row(W);
+  for (int r = 0; r < G; ++r) row[r] = D.scnt[r];
+  row[G] = base;
+  CUK(cudaMemcpyAsync(D.cnt_d, row.data(), sizeof(int64_t) * W, cudaMemcpyHostToDevice, c->stream));
+  NCK(ncclAllGather(D.cnt_d, D.cnt_all_d, W, ncclInt64, D.comm, c->stream));
+  std::vector<int64_t> all((size_t)G * W);
+  CUK(cudaMemcpyAsync(all.data(), D.cnt_all_d, sizeof(int64_t) * G * W, cudaMemcpyDeviceToHost, c->stream));
   CUK(cudaStreamSynchronize(c->stream));
-  for (int s = 0; s < G; ++s) D.rcnt[s] = s == D.rank ? 0 : all[(size_t)s * G + D.rank];
+  for (int s = 0; s < G; ++s) D.rcnt[s] = s == D.rank ? 0 : all[(size_t)s * W + D.rank];
   D.moved_total = 0;
-  for (int s = 0; s < G; ++s)
-    for (int r = 0; r < G; ++r)
-      if (r != s) D.moved_total += all[(size_t)s * G + r];
+  for (int s = 0; s < G; ++s) {
+    int64_t sent = 0, recv = 0;
+    for (int r = 0; r < G; ++r) {
+      if (r == s) continue;
+      sent += all[(size_t)s * W + r];
+      recv += all[(size_t)r * W + s];
+    }
+    D.moved_total += sent;
+    if (!need(sent, recv, all[(size_t)s * W + G])) {
+      c->dist_err = "rank " + std::to_string(s) + " would exceed its particle capacity (sends " +
+                    std::to_string(sent) + ", receives " + std::to_string(recv) +
+                    "); raise the capacity passed to sph_init";
+      return false;
+    }
+  }
   return true;
 }
 
@@ -362,19 +382,16 @@ bool dist_migrate(sph_ctx* c, bool* moved) {
     D.soff[r] = off[r];
     D.scnt[r] = r == D.rank ? 0 : off[r + 1] - off[r];
   }
-  if (!swap_counts(c)) return false;
+  const int64_t cap = c->cap, xcap = D.xcap;
+  if (!swap_counts(c, c->P.n, [&](int64_t sent, int64_t recv, int64_t nb) {
+        return nb - sent + recv <= cap && sent <= xcap && recv <= xcap;
+      }))
+    return false;
   *moved = D.moved_total > 0;
   if (!*moved) return true;
-  int64_t nrecv = 0, nsend = 0;
-  for (int r = 0; r < G; ++r) {
-    nrecv += D.rcnt[r];
-    nsend += D.scnt[r];
-  }
+  int64_t nrecv = 0;
+  for (int r = 0; r < G; ++r) nrecv += D.rcnt[r];
   const int64_t kept = off[D.rank + 1] - off[D.rank];
-  if (kept + nrecv > c->cap || nsend > D.xcap || nrecv > D.xcap) {
-    c->dist_err = "migration exceeds capacity";
-    return false;
-  }
   FieldSet fs = state_fields(c, true);
   if (!exchange(c, fs, false)) return false;
   // kept block -> front (through the send buffer tail is unsafe: use the permutation scratch)
@@ -399,36 +416,42 @@ bool dist_halo_plan_and_exchange1(sph_ctx* c) {
   k_halo_mask<<<nbc, 256, 0, c->stream>>>(c->s.cell_list, c->s.ncell_list, g, Rx, Ry, Rz, D.split_d, G,
                                           D.rank, D.shift, D.mask_d);
   c->launches++;
-  int64_t total = 0;
+  // pass 1: per-peer totals only (nothing written yet), then a collective capacity check
+  std::vector<int64_t> tot(G, 0);
   for (int r = 0; r < G; ++r) {
-    D.soff[r] = total;
-    D.scnt[r] = 0;
     if (r == D.rank) continue;
     k_peer_counts<<<nbc, 256, 0, c->stream>>>(c->s.cell_list, c->s.ncell_list, c->s.cell_start, c->s.cell_end,
                                               D.mask_d, r, D.pcnt_d);
     scan_u32(c, D.pcnt_d, D.poff_d, n);
     k_total<<<1, 1, 0, c->stream>>>(D.pcnt_d, D.poff_d, c->s.ncell_list, D.tot_d + r);
     c->launches += 5;
-    int64_t t = 0;
-    CUK(cudaMemcpyAsync(&t, D.tot_d + r, sizeof(int64_t), cudaMemcpyDeviceToHost, c->stream));
-    CUK(cudaStreamSynchronize(c->stream));
-    if (total + t > D.xcap) {
-      c->dist_err = "halo send list exceeds capacity";
-      return false;
-    }
-    k_fill_send<<<nbc, 256, 0, c->stream>>>(c->s.cell_list, c->s.ncell_list, c->s.cell_start, c->s.cell_end,
-                                            D.mask_d, r, D.poff_d, D.send_idx + total);
-    c->launches++;
-    D.scnt[r] = t;
-    total += t;
   }
-  if (!swap_counts(c)) return false;
+  CUK(cudaMemsetAsync(D.tot_d + D.rank, 0, sizeof(int64_t), c->stream));
+  CUK(cudaMemcpyAsync(tot.data(), D.tot_d, sizeof(int64_t) * G, cudaMemcpyDeviceToHost, c->stream));
+  CUK(cudaStreamSynchronize(c->stream));
+  int64_t total = 0;
+  for (int r = 0; r < G; ++r) {
+    D.soff[r] = total;
+    D.scnt[r] = r == D.rank ? 0 : tot[r];
+    total += D.scnt[r];
+  }
+  const int64_t cap = c->cap, xcap = D.xcap;
+  if (!swap_counts(c, n, [&](int64_t sent, int64_t recv, int64_t nb) {
+        return sent <= xcap && recv <= xcap && nb + recv <= cap;
+      }))
+    return false;
+  // pass 2: fill the per-peer send lists (cells in Morton order -> key-sorted halos)
+  for (int r = 0; r < G; ++r) {
+    if (r == D.rank || D.scnt[r] == 0) continue;
+    k_peer_counts<<<nbc, 256, 0, c->stream>>>(c->s.cell_list, c->s.ncell_list, c->s.cell_start, c->s.cell_end,
+                                              D.mask_d, r, D.pcnt_d);
+    scan_u32(c, D.pcnt_d, D.poff_d, n);
+    k_fill_send<<<nbc, 256, 0, c->stream>>>(c->s.cell_list, c->s.ncell_list, c->s.cell_start, c->s.cell_end,
+                                            D.mask_d, r, D.poff_d, D.send_idx + D.soff[r]);
+    c->launches += 5;
+  }
   D.n_halo = 0;
   for (int r = 0; r < G; ++r) D.n_halo += D.rcnt[r];
-  if (n + D.n_halo > c->cap || D.n_halo > D.xcap) {
-    c->dist_err = "halo exceeds capacity";
-    return false;
-  }
   FieldSet fs = state_fields(c, false);
   if (!exchange(c, fs, true)) return false;
   return unpack_all(c, fs, n);
@@ -483,8 +506,8 @@ bool dist_init(sph_ctx* c, const sph_params* prm) {
   CUK(cudaMalloc(&D->hist_d, sizeof(unsigned long long) << kBinBits));
   CUK(cudaMalloc(&D->split_d, sizeof(int64_t) * (D->G + 1)));
   CUK(cudaMalloc(&D->off_d, sizeof(int64_t) * (D->G + 1)));
-  CUK(cudaMalloc(&D->cnt_d, sizeof(int64_t) * D->G));
-  CUK(cudaMalloc(&D->cnt_all_d, sizeof(int64_t) * D->G * D->G));
+  CUK(cudaMalloc(&D->cnt_d, sizeof(int64_t) * (D->G + 1)));
+  CUK(cudaMalloc(&D->cnt_all_d, sizeof(int64_t) * D->G * (D->G + 1)));
   CUK(cudaMalloc(&D->tot_d, sizeof(int64_t) * D->G));
   CUK(cudaMalloc(&D->red_d, sizeof(double) * 16));
   CUK(cudaMalloc(&D->cntred_d, sizeof(unsigned long long) * kCounters));

@@ -1,0 +1,84 @@
+"""Full-size parity (-m gpu): the BASELINE configs at their full sizes, in the launch
+configuration bench.py times, checked on sampled targets the oracle can compute one
+by one.
+
+A target's outputs depend only on particles within 6 h_max of it (momentum needs C_b
+and rho_b of its neighbours, C_b needs rho of their neighbours, rho of those their
+neighbours: 3 x 2h).  For each sample we cut that neighbourhood out of the GPU's
+sorted state (minimum image on periodic dims), run the oracle on the subset, and
+compare the sample's neighbour set (bit-exact), rho/Omega/P/c, C, a, du and v_sig
+(tolerances: tests/parity_util.py).  The global min-dt is checked against the
+minimum over all particles of courant h / v_sig of the GPU's own arrays.
+"""
+import numpy as np
+import pytest
+
+from paper_2005_02656_b200 import inputs as I
+from tests import parity_util as U
+
+pytestmark = pytest.mark.gpu
+
+CONFIGS = {
+    "weak_25M": lambda: I.square_patch_weak(292, 1),       # config 5 at N=1 (bench default)
+    "patch_1M": lambda: I.square_patch(100),                # config 2
+    "evrard_1M": lambda: I.evrard(124),                     # config 3
+}
+
+
+@pytest.fixture(scope="module")
+def S():
+    import torch
+    if not torch.cuda.is_available():
+        pytest.skip("no GPU")
+    from paper_2005_02656_b200 import _build, sph
+    _build.build()
+    return sph
+
+
+def _samples(st, k, rng):
+    n = st["x"].size
+    # spread over the sorted order + the particles nearest the domain corners / centre
+    pick = set(rng.choice(n, k, replace=False).tolist())
+    for sx in (-1, 1):  # the four xy corners (free-surface edge particles)
+        for sy in (-1, 1):
+            pick.add(int(np.argmax(sx * st["x"] + sy * st["y"])))
+    pick.add(int(np.argmin(st["x"] ** 2 + st["y"] ** 2 + st["z"] ** 2)))
+    return sorted(pick)
+
+
+@pytest.mark.parametrize("name", list(CONFIGS))
+def test_fullsize_sampled(S, oracle_mod, name):
+    O = oracle_mod
+    d = CONFIGS[name]()
+    sim = S.Simulation(d)
+    sim.find_neighbors()
+    off_g, ids_g = sim.get_neighbors()
+    sim.density()
+    sim.iad()
+    dt = sim.momentum_energy(want_dt=True)
+    st = U.with_meta(sim.state(), d)
+    # global min dt from the GPU's own arrays (checks the block-min + atomic reduction)
+    dt_np = np.min(0.3 * st["h"] / st["vsig"])
+    assert dt == dt_np
+    rng = np.random.default_rng(20050265)
+    hmax = st["h"].max()
+    lo, hi = np.asarray(d["box_lo"]), np.asarray(d["box_hi"])
+    for a in _samples(st, 12, rng):
+        D = np.stack([st["x"] - st["x"][a], st["y"] - st["y"][a], st["z"] - st["z"][a]])
+        for k in range(3):
+            if d["periodic"][k]:
+                L = hi[k] - lo[k]
+                D[k] = np.where(D[k] > L / 2, D[k] - L, np.where(D[k] < -L / 2, D[k] + L, D[k]))
+        sel = np.flatnonzero((D * D).sum(0) < (6.2 * hmax) ** 2)
+        sub = U.with_meta({k: st[k][sel] for k in st}, d)
+        ia = int(np.flatnonzero(sel == a)[0])
+        o, off, nbr, dn, C, me = U.oracle_pipeline(O, sub)
+        # neighbour set of the sample, bit-exact
+        mine = np.sort(ids_g[off_g[a]:off_g[a + 1]])
+        ref = np.sort(sub["id"][nbr[off[ia]:off[ia + 1]]])
+        np.testing.assert_array_equal(mine, ref, err_msg=f"{name}: neighbours of sample {a}")
+        one = lambda dd: {k: (v[:, ia:ia + 1] if k == "scale_a" else v[ia:ia + 1]) for k, v in dd.items()}
+        g = {k: st[k][a:a + 1] for k in st}
+        U.check_density(g, one(dn), d)
+        U.check_iad(g, one(C))
+        U.check_momentum(g, one(me))
