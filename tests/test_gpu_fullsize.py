@@ -70,7 +70,9 @@ def test_fullsize_sampled(S, oracle_mod, name):
                 L = hi[k] - lo[k]
                 D[k] = np.where(D[k] > L / 2, D[k] - L, np.where(D[k] < -L / 2, D[k] + L, D[k]))
         sel = np.flatnonzero((D * D).sum(0) < (6.2 * hmax) ** 2)
-        sub = U.with_meta({k: st[k][sel] for k in st}, d)
+        n = st["x"].size
+        sub = U.with_meta({k: v[sel] for k, v in st.items()
+                           if isinstance(v, np.ndarray) and v.shape == (n,)}, d)
         ia = int(np.flatnonzero(sel == a)[0])
         o, off, nbr, dn, C, me = U.oracle_pipeline(O, sub)
         # neighbour set of the sample, bit-exact
@@ -78,7 +80,7 @@ def test_fullsize_sampled(S, oracle_mod, name):
         ref = np.sort(sub["id"][nbr[off[ia]:off[ia + 1]]])
         np.testing.assert_array_equal(mine, ref, err_msg=f"{name}: neighbours of sample {a}")
         one = lambda dd: {k: (v[:, ia:ia + 1] if k == "scale_a" else v[ia:ia + 1]) for k, v in dd.items()}
-        g = {k: st[k][a:a + 1] for k in st}
+        g = {k: v[a:a + 1] for k, v in st.items() if isinstance(v, np.ndarray) and v.shape == (n,)}
         U.check_density(g, one(dn), d)
         U.check_iad(g, one(C))
         U.check_momentum(g, one(me))
