@@ -28,7 +28,7 @@ def main():
     ap.add_argument("--t-end", type=float, default=0.5)
     ap.add_argument("--pressure-ics", type=int, default=1)
     ap.add_argument("--max-steps", type=int, default=20000)
-    ap.add_argument("--out", default=os.path.join(ROOT, "profiles", "r1_validation.json"))
+    ap.add_argument("--out", default=os.path.join(ROOT, "gpurun_out", "validation.json"))
     a = ap.parse_args()
     torch.cuda.set_device(0)
     d = inputs.square_patch(a.n, pressure_ics=bool(a.pressure_ics))
@@ -43,8 +43,11 @@ def main():
         steps += 1
         if steps % 250 == 0 or t >= a.t_end:
             g = sim.diagnostics()
+            s = sim.state()
+            ke = 0.5 * float((s["m"] * (s["vx"] ** 2 + s["vy"] ** 2 + s["vz"] ** 2)).sum())
             hist.append({"step": steps, "t": t, "Lz": g["ang_momentum"][2], "E": g["energy"],
-                         "p": g["momentum"], "dt": dt})
+                         "KE": ke, "IE": g["energy"] - ke, "rho_min": float(s["rho"].min()),
+                         "rho_max": float(s["rho"].max()), "p": g["momentum"], "dt": dt})
             print(json.dumps(hist[-1]), flush=True)
     g = sim.diagnostics()
     Lz0, Lz = d0["ang_momentum"][2], g["ang_momentum"][2]
@@ -61,6 +64,7 @@ def main():
                                         "h_clamped")},
         "history": hist,
     }
+    os.makedirs(os.path.dirname(a.out), exist_ok=True)
     json.dump(res, open(a.out, "w"), indent=1)
     print(json.dumps({k: v for k, v in res.items() if k != "history"}), flush=True)
 
