@@ -29,8 +29,8 @@ def _nccl_paths():
             lib if glob.glob(os.path.join(lib, "libnccl.so*")) else None)
 
 
-def sources():
-    return sorted(glob.glob(os.path.join(CSRC, "*.cu")))
+def sources(csrc: str = CSRC):
+    return sorted(glob.glob(os.path.join(csrc, "*.cu")))
 
 
 def deps():
@@ -38,23 +38,28 @@ def deps():
         os.path.join(ROOT, "include", "sph.h")]
 
 
-def build(force: bool = False, verbose: bool = False) -> str:
+def build(force: bool = False, verbose: bool = False, csrc: str = CSRC, out: str = LIB) -> str:
     newest = max(os.path.getmtime(p) for p in deps())
-    if not force and os.path.exists(LIB) and os.path.getmtime(LIB) >= newest:
-        return LIB
+    if not force and os.path.exists(out) and os.path.getmtime(out) >= newest:
+        return out
     cmd = ["nvcc", *NVCC_FLAGS]
     inc, lib = _nccl_paths()
     if inc and lib:
         cmd += ["-DSPH_WITH_NCCL=1", f"-I{inc}", f"-L{lib}", "-l:libnccl.so.2",
                 f"-Xlinker", f"-rpath={lib}"]
-    tmp = LIB + f".tmp{os.getpid()}"
-    cmd += ["-o", tmp, *sources()]
+    tmp = out + f".tmp{os.getpid()}"
+    cmd += [f"-I{csrc}", "-o", tmp, *sources(csrc)]
     if verbose:
         print(" ".join(cmd))
     subprocess.check_call(cmd)
-    os.replace(tmp, LIB)
-    return LIB
+    os.replace(tmp, out)
+    return out
 
 
 if __name__ == "__main__":
-    print(build(force=True, verbose=True))
+    import argparse
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--csrc", default=CSRC, help="kernel source dir (variant builds)")
+    ap.add_argument("--out", default=LIB)
+    a = ap.parse_args()
+    print(build(force=True, verbose=True, csrc=os.path.abspath(a.csrc), out=os.path.abspath(a.out)))

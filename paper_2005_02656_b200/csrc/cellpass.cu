@@ -25,8 +25,10 @@ constexpr int kNW = kCT / 32;     // warps per CTA
 constexpr int kTgt = 128;         // targets per sub-block (per-target state in smem)
 constexpr int kSlots = 512;       // slot tables (R <= 3 in every dim: 343 slots)
 constexpr int kMaxUnits = 128;    // staged (slot, local range) pieces per group
-constexpr int kSearchCap = 2048;  // staged candidates per group (float4)
-constexpr int kDensCap = 2048;    // staged particles per group, 4 fp64 fields
+constexpr int kSearchCap = 3072;  // staged candidates per group (float4)
+constexpr int kSearchTiles = kSearchCap / 32 + 1;          // + the sentinel tile
+constexpr int kSearchWords = (kSearchCap / 32 + 31) / 32;  // tile bitmask words
+constexpr int kDensCap = 2560;    // staged particles per group, 4 fp64 fields
 constexpr int kMomCap = 1088;     // staged particles per group, 17 fp64 fields (1 CTA/SM; a 27-cell stencil in 2 groups)
 constexpr int kCTM = 512;         // momentum CTA: 16 warps, one CTA per SM
 constexpr int kCTD = 512;         // density / IAD CTA: 16 warps, two CTAs per SM
@@ -403,8 +405,9 @@ __global__ void __launch_bounds__(kCT, 2) k_search(const double* __restrict__ x,
                                                 uint32_t* __restrict__ nbr,
                                                 uint32_t* __restrict__ ncount, int maxn,
                                                 unsigned int* __restrict__ maxcount) {
-  extern __shared__ float4 cand[];  // kSearchCap + 64 padding
+  extern __shared__ float4 cand[];  // kSearchCap + 32 (tile round-up) + 32 (sentinel tile)
   __shared__ CellSm S;
+  __shared__ float4 tlo[kSearchTiles], thi[kSearchTiles];  // per staged tile: fp32 bounding box
   __shared__ uint32_t tcount[kTgt];
   __shared__ TgtW TW[kNW][2];
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
@@ -452,10 +455,33 @@ __global__ void __launch_bounds__(kCT, 2) k_search(const double* __restrict__ x,
             cand[base + i] = v;
           }
         }
-        // pad to a multiple of 32 with far-away sentinels (never hit, never ambiguous)
-        const int padded = (total + 63) & ~63;  // the scan takes two tiles per iteration
-        for (int q = total + threadIdx.x; q < padded; q += blockDim.x)
+        // pad to whole tiles with far-away sentinels (never hit, never ambiguous), plus
+        // one all-sentinel tile (index ntile) that partners an odd last tile
+        const int ntile = (total + 31) >> 5;
+        for (int q = total + threadIdx.x; q < 32 * ntile + 32; q += blockDim.x)
           cand[q] = make_float4(INFINITY, INFINITY, INFINITY, __uint_as_float(kSent));
+        __syncthreads();
+        // tile bounding boxes (staged candidates are Z-ordered within each cell, so a
+        // tile is a compact block)
+        for (int q = warp; q < ntile; q += kNW) {
+          const float4 v = cand[32 * q + lane];
+          const bool ok = __float_as_uint(v.w) != kSent;
+          float lx = ok ? v.x : INFINITY, ly = ok ? v.y : INFINITY, lz = ok ? v.z : INFINITY;
+          float hx = ok ? v.x : -INFINITY, hy = ok ? v.y : -INFINITY, hz = ok ? v.z : -INFINITY;
+#pragma unroll
+          for (int o = 16; o; o >>= 1) {
+            lx = fminf(lx, __shfl_xor_sync(0xffffffffu, lx, o));
+            ly = fminf(ly, __shfl_xor_sync(0xffffffffu, ly, o));
+            lz = fminf(lz, __shfl_xor_sync(0xffffffffu, lz, o));
+            hx = fmaxf(hx, __shfl_xor_sync(0xffffffffu, hx, o));
+            hy = fmaxf(hy, __shfl_xor_sync(0xffffffffu, hy, o));
+            hz = fmaxf(hz, __shfl_xor_sync(0xffffffffu, hz, o));
+          }
+          if (lane == 0) {
+            tlo[q] = make_float4(lx, ly, lz, 0.f);
+            thi[q] = make_float4(hx, hy, hz, 0.f);
+          }
+        }
         __syncthreads();
         // two targets per warp share every staged-candidate load (fp32 test data in
         // registers; the fp64 data of the rare exact test in shared memory)
@@ -518,9 +544,55 @@ __global__ void __launch_bounds__(kCT, 2) k_search(const double* __restrict__ x,
               if (amb1) hit1 = exact_hit(g, x, y, z, j, tb, TW[warp][1].pos, TW[warp][1].lim);
             }
           };
-          // two tiles per iteration (padded to 64): four independent test chains in flight
-          for (int q0 = 0; q0 < padded; q0 += 64) {
-            const float4 cA = cand[q0 + lane], cB = cand[q0 + 32 + lane];
+          // Tiles either target can reach.  Box distance in the prefilter's own fp32
+          // expression: rounding is monotone, so box d2 <= r2_32 of every member, and
+          // box d2 >= hi excludes hits and ambiguous candidates alike (lists stay exact).
+          uint32_t need[kSearchWords];
+#pragma unroll
+          for (int w = 0; w < kSearchWords; ++w) {
+            const int q = 32 * w + lane;
+            bool nd = false;
+            if (q < ntile) {
+              if constexpr (W2) {
+                nd = true;
+              } else {
+                const float4 L = tlo[q], H = thi[q];
+                const float bx0 = fmaxf(fmaxf(L.x - ax0, ax0 - H.x), 0.f);
+                const float by0 = fmaxf(fmaxf(L.y - ay0, ay0 - H.y), 0.f);
+                const float bz0 = fmaxf(fmaxf(L.z - az0, az0 - H.z), 0.f);
+                const float bx1 = fmaxf(fmaxf(L.x - ax1, ax1 - H.x), 0.f);
+                const float by1 = fmaxf(fmaxf(L.y - ay1, ay1 - H.y), 0.f);
+                const float bz1 = fmaxf(fmaxf(L.z - az1, az1 - H.z), 0.f);
+                nd = (fmaf(bz0, bz0, fmaf(by0, by0, bx0 * bx0)) < hi0) |
+                     (fmaf(bz1, bz1, fmaf(by1, by1, bx1 * bx1)) < hi1);
+              }
+            }
+            need[w] = __ballot_sync(0xffffffffu, nd);
+          }
+          static_assert(kSearchWords == 3, "tile mask held in three registers");
+          uint32_t n0 = need[0], n1 = need[1], n2 = need[2];
+          auto next_tile = [&]() -> int {  // lowest remaining needed tile (ascending: rows stay sorted)
+            int q;
+            if (n0) {
+              q = __ffs(n0) - 1;
+              n0 &= n0 - 1;
+            } else if (n1) {
+              q = 31 + __ffs(n1);
+              n1 &= n1 - 1;
+            } else if (n2) {
+              q = 63 + __ffs(n2);
+              n2 &= n2 - 1;
+            } else {
+              q = ntile;  // the sentinel tile
+            }
+            return q;
+          };
+          // two tiles per iteration: four independent test chains in flight
+          for (;;) {
+            const int qA = next_tile();
+            if (qA == ntile) break;
+            const int qB = next_tile();
+            const float4 cA = cand[32 * qA + lane], cB = cand[32 * qB + lane];
             bool hA0, hA1, hB0, hB1;
             test(cA, hA0, hA1);
             test(cB, hB0, hB1);
@@ -1082,7 +1154,7 @@ static void set_smem(K kern, size_t bytes) {
 }
 
 int launch_neighbors(sph_ctx* c) {
-  const size_t smem = (kSearchCap + 64) * sizeof(float4);
+  const size_t smem = (kSearchCap + 64) * sizeof(float4);  // + tile round-up + sentinel tile
   auto kern = any_wrap2(c) ? k_search<true> : k_search<false>;
   set_smem(kern, smem);
   kern<<<cell_grid(c, 4), kCT, smem, c->stream>>>(

@@ -106,8 +106,23 @@ __global__ void k_keys(const double* __restrict__ x, const double* __restrict__ 
                        Grid g, uint64_t* __restrict__ keys, uint32_t* __restrict__ idx) {
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
        i += (int64_t)gridDim.x * blockDim.x) {
-    uint64_t cx = cell_coord(g, 0, x[i]), cy = cell_coord(g, 1, y[i]), cz = cell_coord(g, 2, z[i]);
-    uint64_t morton = spread3(cx) | (spread3(cy) << 1) | (spread3(cz) << 2);
+    // cell Morton code (high bits), then the Morton code of the 2^sbits-per-dim
+    // sub-cell (so a cell's particles are Z-ordered: staged 32-particle tiles are
+    // compact blocks the search can cull), then the id (canonical tie-break, R25)
+    const double v3[3] = {x[i], y[i], z[i]};
+    uint64_t cc[3], sc[3];
+    const double sub = (double)(1 << g.sbits);
+#pragma unroll
+    for (int d = 0; d < 3; ++d) {
+      const double q = (v3[d] - g.lo[d]) * g.inv[d];
+      const int c = cell_coord(g, d, v3[d]);
+      int s = (int)floor((q - (double)c) * sub);
+      s = s < 0 ? 0 : (s > (1 << g.sbits) - 1 ? (1 << g.sbits) - 1 : s);
+      cc[d] = (uint64_t)c;
+      sc[d] = (uint64_t)s;
+    }
+    uint64_t morton = spread3(cc[0]) | (spread3(cc[1]) << 1) | (spread3(cc[2]) << 2);
+    morton = (morton << (3 * g.sbits)) | spread3(sc[0]) | (spread3(sc[1]) << 1) | (spread3(sc[2]) << 2);
     uint64_t idm = g.idbits >= 64 ? ~0ull : ((1ull << g.idbits) - 1);
     keys[i] = (g.idbits >= 64 ? 0 : (morton << g.idbits)) | ((uint64_t)id[i] & idm);
     idx[i] = (uint32_t)i;
@@ -356,7 +371,7 @@ __device__ __forceinline__ uint32_t compact3(uint64_t v) {  // inverse of spread
 }
 
 __device__ __forceinline__ int64_t key_cell(const Grid& g, uint64_t key) {
-  uint64_t m = g.idbits >= 64 ? 0 : key >> g.idbits;
+  uint64_t m = g.kshift >= 64 ? 0 : key >> g.kshift;
   int64_t cx = compact3(m), cy = compact3(m >> 1), cz = compact3(m >> 2);
   return cx + (int64_t)g.nc[0] * (cy + (int64_t)g.nc[1] * cz);
 }

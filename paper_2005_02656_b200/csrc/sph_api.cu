@@ -162,6 +162,8 @@ sph_status choose_grid(sph_ctx* c, const double* bb, int64_t n) {
   g.idbits = bits_for((uint64_t)bb[8]);
   if (3 * g.cbits + g.idbits > 64)
     return fail(c, SPH_ERR_CONFIG, "Morton key + id exceed 64 bits");
+  g.sbits = std::min(3, (64 - 3 * g.cbits - g.idbits) / 3);  // sub-cell order when bits remain
+  g.kshift = g.idbits + 3 * g.sbits;
   return SPH_OK;
 }
 
@@ -324,7 +326,7 @@ sph_status sph_attach(sph_ctx* c, const sph_particles* p) {
 
 static sph_status sort_owned(sph_ctx* c) {  // a1-a2 on [0, P.n): keys, radix sort, permutation
   if (c->P.n == 0) return SPH_OK;
-  const int nbits = 3 * c->grid.cbits + c->grid.idbits;
+  const int nbits = 3 * c->grid.cbits + c->grid.kshift;
   {
     Phase ph(c, SPH_PH_KEYS);
     int k = launch_keys(c);

@@ -76,7 +76,7 @@ __device__ __forceinline__ uint64_t spread3d(uint64_t v) {
 }
 
 __device__ __forceinline__ int64_t key_bin(const Grid& g, uint64_t key, int shift) {
-  const uint64_t m = g.idbits >= 64 ? 0 : key >> g.idbits;
+  const uint64_t m = g.kshift >= 64 ? 0 : key >> g.kshift;
   return (int64_t)(m >> shift);
 }
 

@@ -30,7 +30,9 @@ struct Grid {
   int nc[3];        // cells per dim
   int periodic[3];
   int cbits;        // Morton bits per dim
-  int idbits;       // id bits below the Morton code in the sort key
+  int idbits;       // id bits at the bottom of the sort key
+  int sbits;        // sub-cell Morton bits per dim between the cell code and the id
+  int kshift;       // idbits + 3 sbits: key >> kshift = Morton code of the cell
   int64_t ncell;
 };
 

@@ -92,9 +92,9 @@ __host__ __device__ __forceinline__ uint32_t compact3_hd(uint64_t v) {
   return (uint32_t)v;
 }
 
-// linear cell id of a sort key (Morton code of the cell above the id bits)
+// linear cell id of a sort key (Morton code of the cell above the sub-cell and id bits)
 __host__ __device__ __forceinline__ int64_t key_cell_hd(const Grid& g, uint64_t key) {
-  uint64_t m = g.idbits >= 64 ? 0 : key >> g.idbits;
+  uint64_t m = g.kshift >= 64 ? 0 : key >> g.kshift;
   int64_t cx = compact3_hd(m), cy = compact3_hd(m >> 1), cz = compact3_hd(m >> 2);
   return cx + (int64_t)g.nc[0] * (cy + (int64_t)g.nc[1] * cz);
 }

@@ -13,7 +13,8 @@ import os
 import numpy as np
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "libsph.so")
+# SPH_LIB selects another in-tree build of the same library (A/B runs of kernel variants)
+LIB_PATH = os.environ.get("SPH_LIB") or os.path.join(_HERE, "libsph.so")
 
 ABI_VERSION = 1
 EOS = {"linear": 0, "ideal": 1}
