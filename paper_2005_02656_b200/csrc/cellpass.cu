@@ -10,7 +10,7 @@
 // per pair (profiles/r1_ncu_summary.md has the measurements behind this).
 //
 // Neighbour rows hold packed entries (slot << 20 | local): the shared-memory
-// index of a neighbour is slot_off[slot] + local -- no search, no global gather.
+// index of a neighbour is cum[slot] + local - (group start) -- no search, no global gather.
 // Row chunks are prefetched one chunk ahead, across target boundaries.
 //
 // The search tests r^2 < (2 h_a)^2 first in fp32 on cell-relative coordinates
@@ -23,8 +23,7 @@ namespace sphb {
 constexpr int kCT = 256;          // threads per CTA
 constexpr int kNW = kCT / 32;     // warps per CTA
 constexpr int kTgt = 128;         // targets per sub-block (per-target state in smem)
-constexpr int kSlots = 512;       // slot tables (R <= 3 in every dim: 343 slots)
-constexpr int kMaxUnits = 128;    // staged (slot, local range) pieces per group
+constexpr int kSlots = kKMax;     // slot tables: every stencil the grid chooser admits
 constexpr int kSearchCap = 3072;  // staged candidates per group (float4)
 constexpr int kSearchTiles = kSearchCap / 32 + 1;          // + the sentinel tile
 constexpr int kSearchWords = (kSearchCap / 32 + 31) / 32;  // tile bitmask words
@@ -37,7 +36,7 @@ constexpr int kNWM = kCTM / 32;
 constexpr int kMomFields = 17;
 constexpr uint32_t kSent = 0xffffffffu;
 
-static_assert(kSlots <= kKMax, "slot table");
+static_assert(kSlots >= kKMax, "slot tables must hold the largest admitted stencil");
 
 __constant__ double c_poly[kPolyTerms];   // sinc(pi sqrt(t)/2) = sum c_poly[k] t^k
 __constant__ double c_dpoly[kPolyTerms];  // derivative in t
@@ -47,26 +46,20 @@ void set_poly_constants(const double* poly, const double* dpoly) {
   cudaMemcpyToSymbol(c_dpoly, dpoly, sizeof(double) * kPolyTerms);
 }
 
-struct GroupSm {
-  int nu, total, k, l;
-  uint32_t pend;
-  uint32_t next;  // dynamic target counter of the group (walk_targets)
-  int u_slot[kMaxUnits];
-  uint32_t u_g[kMaxUnits];
-  int u_base[kMaxUnits];
-  int u_len[kMaxUnits];
-  int u_l0[kMaxUnits];
-};
-
+// Per-cell stencil tables.  The stencil's particles form one flat sequence (slots
+// in order, each slot a contiguous cell range); cum[k] is the flat index of slot
+// k's first particle.  A staging group is the flat range [gb, ge): slot k's local
+// particle l sits at shared index cum[k] + l - gb, and a row entry (k << 20 | l)
+// belongs to the group iff it lies in [pack(gb), pack(ge)) -- row entries ascend in
+// flat order, so "entry < pend" selects a target's segment of the group.
 struct CellSm {
-  uint32_t t_start[kSlots];
-  uint32_t t_cnt[kSlots];
-  int slot_off[kSlots];
-  signed char t_sh[kSlots][3];
-  GroupSm G;
+  uint32_t t_start[kSlots];     // first sorted index of slot k's cell
+  uint32_t cum[kSlots + 1];     // exclusive prefix of the slot counts
+  signed char t_sh[kSlots][3];  // periodic image shift of slot k (in periods)
+  uint32_t next[2];             // dynamic target counters, by group parity
   Stencil st;
   int c3[3];
-  uint32_t sc, ec;
+  uint32_t sc, ec, total;
   int kself;
 };
 
@@ -173,65 +166,72 @@ __device__ __forceinline__ double min_img(double d, double L) {
   return d;
 }
 
-// CTA prologue for cell c: stencil + per-slot (start, count, periodic shift) tables.
+// CTA prologue for cell c (warp 0, one CTA barrier): stencil, per-slot tables and
+// their prefix (flat staging index of each slot).
 __device__ void cell_setup(const Grid& g, uint32_t c, const uint32_t* __restrict__ cstart,
                            const uint32_t* __restrict__ cend,
                            const unsigned long long* __restrict__ chmax, CellSm& S) {
-  if (threadIdx.x == 0) {
-    cell_coords(g, c, S.c3);
-    S.sc = cstart[c];
-    S.ec = cend[c];
-    make_stencil(g, S.c3, reach_of(__longlong_as_double((long long)chmax[c])), S.st);
-    S.kself = self_slot(S.st, S.c3);
-  }
-  __syncthreads();
-  for (int k = threadIdx.x; k < S.st.K; k += blockDim.x) {
-    int sh[3];
-    int64_t cell = slot_cell(g, S.st, k, sh);
-    uint32_t s0 = cstart[cell];
-    S.t_start[k] = s0;
-    S.t_cnt[k] = cend[cell] - s0;
-    S.t_sh[k][0] = (signed char)sh[0];
-    S.t_sh[k][1] = (signed char)sh[1];
-    S.t_sh[k][2] = (signed char)sh[2];
+  if (threadIdx.x < 32) {
+    const int lane = threadIdx.x;
+    if (lane == 0) {
+      cell_coords(g, c, S.c3);
+      S.sc = cstart[c];
+      S.ec = cend[c];
+      make_stencil(g, S.c3, reach_of(__longlong_as_double((long long)chmax[c])), S.st);
+      S.kself = self_slot(S.st, S.c3);
+    }
+    __syncwarp();
+    const int K = S.st.K;
+    uint32_t carry = 0;
+    for (int b = 0; b < K; b += 32) {
+      const int k = b + lane;
+      uint32_t cnt = 0;
+      if (k < K) {
+        int sh[3];
+        const int64_t cell = slot_cell(g, S.st, k, sh);
+        const uint32_t s0 = cstart[cell];
+        cnt = cend[cell] - s0;
+        S.t_start[k] = s0;
+        S.t_sh[k][0] = (signed char)sh[0];
+        S.t_sh[k][1] = (signed char)sh[1];
+        S.t_sh[k][2] = (signed char)sh[2];
+      }
+      uint32_t x = cnt;  // inclusive warp scan
+#pragma unroll
+      for (int o = 1; o < 32; o <<= 1) {
+        const uint32_t y = __shfl_up_sync(0xffffffffu, x, o);
+        if (lane >= o) x += y;
+      }
+      if (k < K) S.cum[k] = carry + x - cnt;
+      carry += __shfl_sync(0xffffffffu, x, 31);
+    }
+    if (lane == 0) {
+      S.cum[K] = carry;
+      S.total = carry;
+    }
   }
   __syncthreads();
 }
 
-// thread 0: next group of staged pieces from the (k, l) cursor, at most `cap` particles
-__device__ void build_group(CellSm& S, int cap) {
-  GroupSm& G = S.G;
-  int k = G.k, l = G.l, nu = 0, total = 0;
-  const int K = S.st.K;
-  while (k < K && nu < kMaxUnits && total < cap) {
-    int cnt = (int)S.t_cnt[k];
-    if (l >= cnt) {
-      ++k;
-      l = 0;
-      continue;
-    }
-    int take = min(cnt - l, cap - total);
-    G.u_slot[nu] = k;
-    G.u_g[nu] = S.t_start[k] + l;
-    G.u_base[nu] = total;
-    G.u_len[nu] = take;
-    G.u_l0[nu] = l;
-    S.slot_off[k] = total - l;
-    ++nu;
-    total += take;
-    l += take;
-    if (l >= cnt) {
-      ++k;
-      l = 0;
-    }
+// slot of flat index f: the largest k < K with cum[k] <= f (skips empty slots)
+__device__ __forceinline__ int slot_of(const CellSm& S, uint32_t f) {
+  int lo = 0, hi = S.st.K - 1;
+  while (lo < hi) {
+    const int mid = (lo + hi + 1) >> 1;
+    if (S.cum[mid] <= f) lo = mid;
+    else hi = mid - 1;
   }
-  while (k < K && S.t_cnt[k] == 0) ++k;  // tighten the end marker
-  G.nu = nu;
-  G.total = total;
-  G.k = k;
-  G.l = l;
-  G.pend = k >= K ? kSent : (((uint32_t)k << kLocalBits) | (uint32_t)l);
-  G.next = 0;
+  return lo;
+}
+// packed row entry of flat index ge (the first entry past the group), kSent at the end
+__device__ __forceinline__ uint32_t pend_of(const CellSm& S, uint32_t ge) {
+  if (ge >= S.total) return kSent;
+  const int k = slot_of(S, ge);
+  return ((uint32_t)k << kLocalBits) | (ge - S.cum[k]);
+}
+// shared-memory index of row entry e in the group starting at flat index gb
+__device__ __forceinline__ int qidx(const uint32_t* cum, uint32_t gb, uint32_t e) {
+  return (int)(cum[e >> kLocalBits] + (e & kLocalMask) - gb);
 }
 
 __device__ __forceinline__ void shifts_of(const Grid& g, const CellSm& S, int slot, double sh[3]) {
@@ -242,7 +242,7 @@ __device__ __forceinline__ void shifts_of(const Grid& g, const CellSm& S, int sl
 
 // Warp-level walk over the entries of target rows that fall in the current
 // group [.., pend).  Targets are handed out dynamically (shared counter, reset by
-// build_group) so warps reach the group barrier together.  Row chunks (32
+// the group loop) so warps reach the group barrier together.  Row chunks (32
 // entries) stream through a 3-deep register ring (ncu: with one chunk of
 // prefetch the row load was the top stall), and the first three chunks of the
 // warp's next target are issued before the current target's work.
@@ -253,8 +253,8 @@ __device__ __forceinline__ uint32_t row_chunk(const uint32_t* row, uint32_t pos,
 template <int NW, class Body, class Finish>
 __device__ __forceinline__ void walk_targets(uint32_t t0, uint32_t t1, const uint32_t* __restrict__ nbr,
                                              int maxn, const uint32_t* s_n, uint32_t* s_cur,
-                                             uint32_t pend, const int* slot_off, uint32_t* s_next,
-                                             Body&& body, Finish&& finish) {
+                                             uint32_t pend, const uint32_t* cum, uint32_t gb,
+                                             uint32_t* s_next, Body&& body, Finish&& finish) {
   const int lane = threadIdx.x & 31;
   uint32_t t = 0;
   if (lane == 0) t = t0 + atomicAdd(s_next, 1u);
@@ -290,7 +290,7 @@ __device__ __forceinline__ void walk_targets(uint32_t t0, uint32_t t1, const uin
       const unsigned b = __ballot_sync(0xffffffffu, in);
       const int m = __popc(b);
       const uint32_t e3 = m == 32 ? row_chunk(row, cur + 96 + lane, n) : kSent;
-      if (in) body(slot_off[e0 >> kLocalBits] + (int)(e0 & kLocalMask));
+      if (in) body(qidx(cum, gb, e0));
       cur += m;
       if (m < 32) break;
       e0 = e1;
@@ -310,7 +310,7 @@ template <class Body, class Finish>
 __device__ __forceinline__ void walk_targets_half(uint32_t t0, uint32_t t1,
                                                   const uint32_t* __restrict__ nbr, int maxn,
                                                   const uint32_t* s_n, uint32_t* s_cur,
-                                                  uint32_t pend, const int* slot_off,
+                                                  uint32_t pend, const uint32_t* cum, uint32_t gb,
                                                   uint32_t* s_next, Body&& body, Finish&& finish) {
   const int lane = threadIdx.x & 31, l16 = lane & 15;
   const unsigned hmask = (threadIdx.x & 16) ? 0xffff0000u : 0x0000ffffu;
@@ -352,7 +352,7 @@ __device__ __forceinline__ void walk_targets_half(uint32_t t0, uint32_t t1,
       const int m = __popc(b & hmask);
       const bool more = live && m == 16;
       const uint32_t e3 = more ? row_chunk(row, cur + 48 + l16, n) : kSent;
-      if (in) body(slot_off[e0 >> kLocalBits] + (int)(e0 & kLocalMask));
+      if (in) body(qidx(cum, gb, e0));
       cur += m;
       live = more;
       if (!__any_sync(0xffffffffu, live)) break;
@@ -430,30 +430,21 @@ __global__ void __launch_bounds__(kCT, 2) k_search(const double* __restrict__ x,
     for (uint32_t t0 = S.sc; t0 < S.ec; t0 += kTgt) {
       const uint32_t t1 = min(S.ec, t0 + kTgt);
       for (uint32_t t = t0 + threadIdx.x; t < t1; t += blockDim.x) tcount[t - t0] = 0;
-      if (threadIdx.x == 0) {
-        S.G.k = 0;
-        S.G.l = 0;
-      }
       __syncthreads();
-      for (;;) {
-        if (threadIdx.x == 0) build_group(S, kSearchCap);
-        __syncthreads();
-        const int nu = S.G.nu, total = S.G.total;
-        if (nu == 0) break;
-        for (int u = warp; u < nu; u += kNW) {
-          const int slot = S.G.u_slot[u], base = S.G.u_base[u], len = S.G.u_len[u], l0 = S.G.u_l0[u];
-          const uint32_t g0 = S.G.u_g[u];
+      for (uint32_t gb = 0; gb < S.total; gb += kSearchCap) {
+        const int total = (int)(min(S.total, gb + kSearchCap) - gb);
+        for (int q = threadIdx.x; q < total; q += blockDim.x) {  // flat staging, all threads
+          const uint32_t f = gb + q;
+          const int slot = slot_of(S, f);
+          const uint32_t l = f - S.cum[slot], j = S.t_start[slot] + l;
           double sh[3];
           shifts_of(g, S, slot, sh);
-          for (int i = lane; i < len; i += 32) {
-            const uint32_t j = g0 + i;
-            float4 v;
-            v.x = (float)((x[j] + sh[0]) - org[0]);
-            v.y = (float)((y[j] + sh[1]) - org[1]);
-            v.z = (float)((z[j] + sh[2]) - org[2]);
-            v.w = __uint_as_float(((uint32_t)slot << kLocalBits) | (uint32_t)(l0 + i));
-            cand[base + i] = v;
-          }
+          float4 v;
+          v.x = (float)((x[j] + sh[0]) - org[0]);
+          v.y = (float)((y[j] + sh[1]) - org[1]);
+          v.z = (float)((z[j] + sh[2]) - org[2]);
+          v.w = __uint_as_float(((uint32_t)slot << kLocalBits) | l);
+          cand[q] = v;
         }
         // pad to whole tiles with far-away sentinels (never hit, never ambiguous), plus
         // one all-sentinel tile (index ntile) that partners an odd last tile
@@ -629,19 +620,18 @@ __global__ void __launch_bounds__(kCT, 2) k_search(const double* __restrict__ x,
 // stage (x, y) and (z, f) of the current group as double2 pairs: one 16-byte LDS
 // per pair of fields, bank conflicts only within 8-lane quarters (ncu: the
 // 8-byte SoA layout cost ~3x the ideal shared-memory wavefronts)
-__device__ __forceinline__ void stage2x2(const Grid& g, const CellSm& S, const double* __restrict__ x,
-                                         const double* __restrict__ y, const double* __restrict__ z,
-                                         const double* __restrict__ f, double2* s01, double2* s23) {
-  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  for (int uu = warp; uu < S.G.nu; uu += (int)(blockDim.x >> 5)) {
-    const int base = S.G.u_base[uu], len = S.G.u_len[uu];
-    const uint32_t g0 = S.G.u_g[uu];
+__device__ __forceinline__ void stage2x2(const Grid& g, const CellSm& S, uint32_t gb, uint32_t ge,
+                                         const double* __restrict__ x, const double* __restrict__ y,
+                                         const double* __restrict__ z, const double* __restrict__ f,
+                                         double2* s01, double2* s23) {
+  for (uint32_t q = threadIdx.x; q < ge - gb; q += blockDim.x) {  // flat: every thread equal work
+    const uint32_t fi = gb + q;
+    const int k = slot_of(S, fi);
+    const uint32_t j = S.t_start[k] + (fi - S.cum[k]);
     double sh[3];
-    shifts_of(g, S, S.G.u_slot[uu], sh);
-    for (int i = lane; i < len; i += 32) {
-      s01[base + i] = make_double2(x[g0 + i] + sh[0], y[g0 + i] + sh[1]);
-      s23[base + i] = make_double2(z[g0 + i] + sh[2], f[g0 + i]);
-    }
+    shifts_of(g, S, k, sh);
+    s01[q] = make_double2(x[j] + sh[0], y[j] + sh[1]);
+    s23[q] = make_double2(z[j] + sh[2], f[j]);
   }
 }
 
@@ -711,16 +701,12 @@ __global__ void __launch_bounds__(kCTD, 2) k_density_c(
         acc0[i] = 0.0;
         acc1[i] = 0.0;
       }
-      if (threadIdx.x == 0) {
-        S.G.k = 0;
-        S.G.l = 0;
-      }
+      if (threadIdx.x == 0) S.next[0] = 0;
       __syncthreads();
-      for (;;) {
-        if (threadIdx.x == 0) build_group(S, kDensCap);
-        __syncthreads();
-        if (S.G.nu == 0) break;
-        stage2x2(g, S, x, y, z, m, s01, s23);
+      for (uint32_t gb = 0, gi = 0; gb < S.total; gb += kDensCap, ++gi) {
+        const uint32_t ge = min(S.total, gb + kDensCap), pend = pend_of(S, ge);
+        if (threadIdx.x == 0) S.next[(gi + 1) & 1] = 0;
+        stage2x2(g, S, gb, ge, x, y, z, m, s01, s23);
         __syncthreads();
         struct B : DensBody {
           int n;
@@ -740,7 +726,7 @@ __global__ void __launch_bounds__(kCTD, 2) k_density_c(
         body.s01 = s01; body.s23 = s23;
         body.tx = tx; body.ty = ty; body.tz = tz; body.tih2 = tih2;
         body.st = &st; body.g = &g; body.n = n;
-        walk_targets<kNWD>(t0, t1, nbr, maxn, s_n, s_cur, S.G.pend, S.slot_off, &S.G.next, body,
+        walk_targets<kNWD>(t0, t1, nbr, maxn, s_n, s_cur, pend, S.cum, gb, &S.next[gi & 1], body,
                           [&](uint32_t i, uint32_t c2) {
                             double v[2] = {body.sr, body.sd};
                             warp_multi_sum<2>(v);
@@ -827,16 +813,12 @@ __global__ void __launch_bounds__(kCTD, 2) k_iad_c(
         tih2[i] = ih2[t];
         for (int k = 0; k < 6; ++k) acc[k][i] = 0.0;
       }
-      if (threadIdx.x == 0) {
-        S.G.k = 0;
-        S.G.l = 0;
-      }
+      if (threadIdx.x == 0) S.next[0] = 0;
       __syncthreads();
-      for (;;) {
-        if (threadIdx.x == 0) build_group(S, kDensCap);
-        __syncthreads();
-        if (S.G.nu == 0) break;
-        stage2x2(g, S, x, y, z, vol, s01, s23);
+      for (uint32_t gb = 0, gi = 0; gb < S.total; gb += kDensCap, ++gi) {
+        const uint32_t ge = min(S.total, gb + kDensCap), pend = pend_of(S, ge);
+        if (threadIdx.x == 0) S.next[(gi + 1) & 1] = 0;
+        stage2x2(g, S, gb, ge, x, y, z, vol, s01, s23);
         __syncthreads();
         struct B {
           const double2 *s01, *s23;
@@ -870,7 +852,7 @@ __global__ void __launch_bounds__(kCTD, 2) k_iad_c(
         body.s01 = s01; body.s23 = s23;
         body.tx = tx; body.ty = ty; body.tz = tz; body.tih2 = tih2;
         body.st = &st; body.g = &g; body.n = n;
-        walk_targets<kNWD>(t0, t1, nbr, maxn, s_n, s_cur, S.G.pend, S.slot_off, &S.G.next, body,
+        walk_targets<kNWD>(t0, t1, nbr, maxn, s_n, s_cur, pend, S.cum, gb, &S.next[gi & 1], body,
                           [&](uint32_t i, uint32_t c2) {
                             double v[8] = {body.t11, body.t12, body.t13, body.t22,
                                            body.t23, body.t33, 0.0, 0.0};
@@ -986,23 +968,19 @@ __global__ void __launch_bounds__(kCTM, 1) k_momentum_c(
         acc[3][i] = 0.0;
         acc[4][i] = -1.0;
       }
-      if (threadIdx.x == 0) {
-        S.G.k = 0;
-        S.G.l = 0;
-      }
+      if (threadIdx.x == 0) S.next[0] = 0;
       __syncthreads();
-      for (;;) {
-        if (threadIdx.x == 0) build_group(S, kMomCap);
-        __syncthreads();
-        if (S.G.nu == 0) break;
-        for (int uu = warp; uu < S.G.nu; uu += kNWM) {
-          const int base = S.G.u_base[uu], len = S.G.u_len[uu];
-          const uint32_t g0 = S.G.u_g[uu];
-          double sh[3];
-          shifts_of(g, S, S.G.u_slot[uu], sh);
-          for (int i = lane; i < len; i += 32) {
-            const uint32_t j = g0 + i;
-            double2* q = F2 + base + i;
+      for (uint32_t gb = 0, gi = 0; gb < S.total; gb += kMomCap, ++gi) {
+        const uint32_t ge = min(S.total, gb + kMomCap), pend = pend_of(S, ge);
+        if (threadIdx.x == 0) S.next[(gi + 1) & 1] = 0;
+        for (uint32_t qq = threadIdx.x; qq < ge - gb; qq += blockDim.x) {  // flat staging
+          {
+            const uint32_t fi = gb + qq;
+            const int k = slot_of(S, fi);
+            const uint32_t j = S.t_start[k] + (fi - S.cum[k]);
+            double sh[3];
+            shifts_of(g, S, k, sh);
+            double2* q = F2 + qq;
             const int64_t cs = src.ct_stride;
             q[0 * kMomCap] = make_double2(src.x[j] + sh[0], src.y[j] + sh[1]);
             q[1 * kMomCap] = make_double2(src.z[j] + sh[2], src.vx[j]);
@@ -1085,7 +1063,7 @@ __global__ void __launch_bounds__(kCTM, 1) k_momentum_c(
         } body;
         body.F2 = F2; body.T = T; body.st = &st; body.g = &g; body.alpha = ph.alpha; body.n = n;
         body.ncoinc = &ncoinc;
-        walk_targets_half(t0, t1, nbr, maxn, s_n, s_cur, S.G.pend, S.slot_off, &S.G.next, body,
+        walk_targets_half(t0, t1, nbr, maxn, s_n, s_cur, pend, S.cum, gb, &S.next[gi & 1], body,
                           [&](bool act, uint32_t i, uint32_t c2) {
                             double v[4] = {body.fx, body.fy, body.fz, body.fu};
                             half_multi_sum<4>(v);
