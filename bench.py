@@ -216,7 +216,7 @@ def run_ours(args):
     stream = torch.cuda.Stream()
     with torch.cuda.stream(stream):
         sim = sph.Simulation(d, capacity=cap, stream=stream.cuda_stream, rank=rank, nranks=world,
-                             unique_id=uid)
+                             unique_id=uid, kernel_mode=sph.KERNEL_MODES[args.kernel_mode])
         for _ in range(args.warmup):
             sim.step()
         torch.cuda.synchronize()
@@ -301,6 +301,7 @@ def run_ours(args):
         "data": "synthetic",
         "config": {"workload": workload_label(args), "description": desc,
                    "particles_per_gpu": n_local, "particles_total": n_total,
+                   "kernel_mode": args.kernel_mode,
                    "neighbors_mean": diag["nbr_total"] / max(1, diag["n_owned"]),
                    "l2": "no flush: every SoA field array >= 200 MB > 126 MB L2",
                    "parallelism": f"sfc{max(world, 1)}" if world > 1 else "1 GPU"},
@@ -334,6 +335,8 @@ def main():
     ap.add_argument("--workload", default="weak", choices=["weak", "patch27m", "patch1m", "evrard"])
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--kernel-mode", default="poly", choices=["poly", "table", "sin"],
+                    help="kernel evaluation in the pair passes (sph.h SPH_KERNEL_*; A/B of P:248)")
     args = ap.parse_args()
     if args.impl == "reference":
         run_reference(args)

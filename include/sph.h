@@ -42,7 +42,7 @@
 extern "C" {
 #endif
 
-#define SPH_ABI_VERSION 1
+#define SPH_ABI_VERSION 2
 
 typedef struct sph_ctx sph_ctx;
 
@@ -57,6 +57,17 @@ typedef enum {
 } sph_status;
 
 enum { SPH_EOS_LINEAR = 0, SPH_EOS_IDEAL = 1 };
+
+/* How the kernel value S_n(v) = [sinc(pi v / 2)]^n of Eq. 6 is evaluated in the
+ * pair passes.  Every mode is exact to its own
+ * definition; the grad-h derivative term of Omega uses the exact polynomial in all
+ * modes (the oracle evaluates it directly in all modes, reading R12).             */
+enum {
+  SPH_KERNEL_POLY = 0,   /* default: 13-term Maclaurin polynomial of sinc in t = v^2 (no sqrt) */
+  SPH_KERNEL_TABLE = 1,  /* the paper's table: table_size samples of S_n on [0, 2] incl. both
+                            ends, index floor(v (K-1)/2), linear interpolation (R12)  */
+  SPH_KERNEL_SIN = 2     /* direct: sin(x)/x, x = pi v / 2, raised to n                      */
+};
 
 typedef struct {
   int    abi_version;     /* must equal SPH_ABI_VERSION                                  */
@@ -78,6 +89,8 @@ typedef struct {
   int    rank, nranks;    /* multi-GPU: this rank / number of ranks (1 for one GPU)       */
   const void* nccl_unique_id; /* 128-byte ncclUniqueId (rank 0's), NULL when nranks == 1  */
   void*  stream;          /* cudaStream_t                                                 */
+  int    kernel_mode;     /* SPH_KERNEL_* (0: polynomial)                                 */
+  int    table_size;      /* samples K of SPH_KERNEL_TABLE (0: 20,000 as in P:248); >= 2  */
 } sph_params;
 
 typedef struct {          /* caller-owned DEVICE buffers, each >= capacity elements       */

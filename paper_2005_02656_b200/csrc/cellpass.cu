@@ -33,7 +33,6 @@ constexpr int kCTM = 512;         // momentum CTA: 16 warps, one CTA per SM
 constexpr int kCTD = 512;         // density / IAD CTA: 16 warps, two CTAs per SM
 constexpr int kNWD = kCTD / 32;
 constexpr int kNWM = kCTM / 32;
-constexpr int kMomFields = 17;
 constexpr uint32_t kSent = 0xffffffffu;
 
 static_assert(kSlots >= kKMax, "slot tables must hold the largest admitted stencil");
@@ -157,6 +156,25 @@ __device__ __forceinline__ double ipow(double s, int n) {
     double r = 1.0;
     for (int k = 0; k < n; ++k) r *= s;
     return r;
+  }
+}
+
+// Kernel value S_n at t = v^2 = r^2/h^2 < 4 in the selected evaluation mode (sph.h
+// SPH_KERNEL_*): the polynomial (Horner, or Estrin when EST), the paper's table
+// (reading R12: floor index, linear interpolation in v), or sin(x)/x directly.
+template <int KM, int N, bool EST>
+__device__ __forceinline__ double kern_S(double t, int n, const double* __restrict__ tab, int K) {
+  if constexpr (KM == SPH_KERNEL_TABLE) {
+    const double q = sqrt(t) * (0.5 * (double)(K - 1));
+    int i = (int)q;  // floor (q >= 0)
+    i = i > K - 2 ? K - 2 : i;
+    const double a = __ldg(tab + i), b = __ldg(tab + i + 1);
+    return fma(b - a, q - (double)i, a);
+  } else if constexpr (KM == SPH_KERNEL_SIN) {
+    const double x = 1.5707963267948966 * sqrt(t);  // pi v / 2
+    return ipow<N>(x > 0.0 ? sin(x) / x : 1.0, n);
+  } else {
+    return ipow<N>(EST ? sinc_poly_e(t) : sinc_poly(t), n);
   }
 }
 
@@ -663,7 +681,7 @@ struct DensBody {
   }
 };
 
-template <int N, bool W2>
+template <int N, bool W2, int KM>
 __global__ void __launch_bounds__(kCTD, 2) k_density_c(
     const double* __restrict__ x, const double* __restrict__ y, const double* __restrict__ z,
     const double* __restrict__ h, const double* __restrict__ m, const double* __restrict__ u,
@@ -709,7 +727,8 @@ __global__ void __launch_bounds__(kCTD, 2) k_density_c(
         stage2x2(g, S, gb, ge, x, y, z, m, s01, s23);
         __syncthreads();
         struct B : DensBody {
-          int n;
+          int n, K;
+          const double* tab;
           __device__ __forceinline__ void operator()(int q) {
             const double2 p01 = s01[q], p23 = s23[q];
             double dx = p01.x - xa, dy = p01.y - ya, dz = p23.x - za;
@@ -719,13 +738,19 @@ __global__ void __launch_bounds__(kCTD, 2) k_density_c(
             const double Pn1 = ipow<N - 1 < 0 ? 0 : N - 1>(P, n - 1);
             const double dP = sinc_dpoly(tt);
             const double mj = p23.y;
-            sr = fma(mj, Pn1 * P, sr);
-            sd = fma(mj, Pn1 * (3.0 * P + (2.0 * n) * tt * dP), sd);  // 3 S + v S'(v)
+            if constexpr (KM == SPH_KERNEL_POLY) {
+              sr = fma(mj, Pn1 * P, sr);
+              sd = fma(mj, Pn1 * (3.0 * P + (2.0 * n) * tt * dP), sd);  // 3 S + v S'(v)
+            } else {  // S from the selected mode; v S'(v) from the exact polynomial (R12)
+              const double S_ = kern_S<KM, N, false>(tt, n, tab, K);
+              sr = fma(mj, S_, sr);
+              sd = fma(mj, fma(3.0, S_, Pn1 * (2.0 * n) * tt * dP), sd);
+            }
           }
         } body;
         body.s01 = s01; body.s23 = s23;
         body.tx = tx; body.ty = ty; body.tz = tz; body.tih2 = tih2;
-        body.st = &st; body.g = &g; body.n = n;
+        body.st = &st; body.g = &g; body.n = n; body.K = ph.tableK; body.tab = ph.table;
         walk_targets<kNWD>(t0, t1, nbr, maxn, s_n, s_cur, pend, S.cum, gb, &S.next[gi & 1], body,
                           [&](uint32_t i, uint32_t c2) {
                             double v[2] = {body.sr, body.sd};
@@ -777,7 +802,7 @@ __global__ void __launch_bounds__(kCTD, 2) k_density_c(
 }
 
 // ------------------------------------------------------------------ a8 IAD
-template <int N, bool W2>
+template <int N, bool W2, int KM>
 __global__ void __launch_bounds__(kCTD, 2) k_iad_c(
     const double* __restrict__ x, const double* __restrict__ y, const double* __restrict__ z,
     Grid g, const uint32_t* __restrict__ cstart, const uint32_t* __restrict__ cend,
@@ -825,7 +850,8 @@ __global__ void __launch_bounds__(kCTD, 2) k_iad_c(
           const double *tx, *ty, *tz, *tih2;
           const Stencil* st;
           const Grid* g;
-          int n;
+          int n, K;
+          const double* tab;
           double xa, ya, za, ih2a, t11, t12, t13, t22, t23, t33;
           __device__ __forceinline__ void begin(uint32_t i) {
             xa = tx[i];
@@ -839,7 +865,7 @@ __global__ void __launch_bounds__(kCTD, 2) k_iad_c(
             double dx = p01.x - xa, dy = p01.y - ya, dz = p23.x - za;
             delta3<W2>(*st, *g, dx, dy, dz);
             const double tt = (dx * dx + dy * dy + dz * dz) * ih2a;
-            const double w = p23.y * ipow<N>(sinc_poly(tt), n);  // (m_b/rho_b) S
+            const double w = p23.y * kern_S<KM, N, false>(tt, n, tab, K);  // (m_b/rho_b) S
             const double wx = w * dx, wy = w * dy;
             t11 = fma(wx, dx, t11);
             t12 = fma(wx, dy, t12);
@@ -851,7 +877,7 @@ __global__ void __launch_bounds__(kCTD, 2) k_iad_c(
         } body;
         body.s01 = s01; body.s23 = s23;
         body.tx = tx; body.ty = ty; body.tz = tz; body.tih2 = tih2;
-        body.st = &st; body.g = &g; body.n = n;
+        body.st = &st; body.g = &g; body.n = n; body.K = ph.tableK; body.tab = ph.table;
         walk_targets<kNWD>(t0, t1, nbr, maxn, s_n, s_cur, pend, S.cum, gb, &S.next[gi & 1], body,
                           [&](uint32_t i, uint32_t c2) {
                             double v[8] = {body.t11, body.t12, body.t13, body.t22,
@@ -916,7 +942,7 @@ constexpr int kMomPairs = 9;
 // per-target smem fields
 enum { T_X, T_Y, T_Z, T_VX, T_VY, T_VZ, T_IH2, T_WB, T_RINV, T_XP, T_C, T_A11, T_A12, T_A13, T_A22, T_A23, T_A33, T_N };
 
-template <int N, bool W2>
+template <int N, bool W2, int KM>
 __global__ void __launch_bounds__(kCTM, 1) k_momentum_c(
     MomSrc src, MomTgt tg, MomOut out, Grid g, const uint32_t* __restrict__ cstart,
     const uint32_t* __restrict__ cend, const unsigned long long* __restrict__ chmax,
@@ -1000,7 +1026,8 @@ __global__ void __launch_bounds__(kCTM, 1) k_momentum_c(
           const Stencil* st;
           const Grid* g;
           double alpha;
-          int n;
+          int n, K;
+          const double* tab;
           unsigned long long* ncoinc;
           double xa, ya, za, vxa, vya, vza, ih2a, wBa, rinva, Xa, ca, a11, a12, a13, a22, a23, a33;
           double fx, fy, fz, fu, vs;
@@ -1025,11 +1052,11 @@ __global__ void __launch_bounds__(kCTM, 1) k_momentum_c(
             const bool coinc = r2 == 0.0;
             *ncoinc += coinc;
             const double ta = r2 * ih2a;
-            const double Sa = ipow<N>(sinc_poly_e(ta), n);
+            const double Sa = kern_S<KM, N, true>(ta, n, tab, K);
             const double Wa = wBa * Sa;
             const double tb = r2 * p3.y;
             double Sb = Sa;  // equal h: W(r, h_b) shares the kernel value
-            if (tb != ta) Sb = tb < 4.0 ? ipow<N>(sinc_poly_e(tb), n) : 0.0;
+            if (tb != ta) Sb = tb < 4.0 ? kern_S<KM, N, true>(tb, n, tab, K) : 0.0;
             // R5: A_ab(h_a) = C_a Delta W_ab(h_a) = Wa u;  R4: A_ab(h_b) = C~_b Delta S_b = Sb w
             const double ux = a11 * dx + a12 * dy + a13 * dz;
             const double uy = a12 * dx + a22 * dy + a23 * dz;
@@ -1062,6 +1089,7 @@ __global__ void __launch_bounds__(kCTM, 1) k_momentum_c(
           }
         } body;
         body.F2 = F2; body.T = T; body.st = &st; body.g = &g; body.alpha = ph.alpha; body.n = n;
+        body.K = ph.tableK; body.tab = ph.table;
         body.ncoinc = &ncoinc;
         walk_targets_half(t0, t1, nbr, maxn, s_n, s_cur, pend, S.cum, gb, &S.next[gi & 1], body,
                           [&](bool act, uint32_t i, uint32_t c2) {
@@ -1141,59 +1169,73 @@ int launch_neighbors(sph_ctx* c) {
   return 1;
 }
 
-template <int N, bool W2>
+template <int N, bool W2, int KM>
 static void density_t(sph_ctx* c) {
   const size_t smem = 4 * kDensCap * sizeof(double);
-  set_smem(k_density_c<N, W2>, smem);
+  set_smem(k_density_c<N, W2, KM>, smem);
   sph_particles& P = c->P;
-  k_density_c<N, W2><<<cell_grid(c, 2), kCTD, smem, c->stream>>>(
+  k_density_c<N, W2, KM><<<cell_grid(c, 2), kCTD, smem, c->stream>>>(
       P.x, P.y, P.z, P.h, P.m, P.u, c->grid, c->s.cell_start, c->s.cell_end, c->s.cell_hmax,
       c->s.cell_list, c->s.ncell_list, c->s.nbr, c->s.ncount, c->maxn, c->phys, P.rho, P.omega,
       P.p, P.c, c->s.wB, c->s.ih2, c->s.vol, c->s.rinv, c->s.X, c->s.mX, c->s.cnt);
 }
 
+// kernel-mode x exponent x wrap dispatch of a pair pass
+#define SPH_DISPATCH(fn)                                                              \
+  do {                                                                                \
+    const bool w2 = any_wrap2(c);                                                     \
+    const bool n6 = c->phys.n == 6;                                                   \
+    switch (c->phys.kmode) {                                                          \
+      case SPH_KERNEL_TABLE:                                                          \
+        n6 ? (w2 ? fn<6, true, 1>(c) : fn<6, false, 1>(c))                            \
+           : (w2 ? fn<0, true, 1>(c) : fn<0, false, 1>(c));                           \
+        break;                                                                        \
+      case SPH_KERNEL_SIN:                                                            \
+        n6 ? (w2 ? fn<6, true, 2>(c) : fn<6, false, 2>(c))                            \
+           : (w2 ? fn<0, true, 2>(c) : fn<0, false, 2>(c));                           \
+        break;                                                                        \
+      default:                                                                        \
+        n6 ? (w2 ? fn<6, true, 0>(c) : fn<6, false, 0>(c))                            \
+           : (w2 ? fn<0, true, 0>(c) : fn<0, false, 0>(c));                           \
+    }                                                                                 \
+  } while (0)
+
 int launch_density(sph_ctx* c) {
-  const bool w2 = any_wrap2(c);
-  if (c->phys.n == 6) w2 ? density_t<6, true>(c) : density_t<6, false>(c);
-  else w2 ? density_t<0, true>(c) : density_t<0, false>(c);
+  SPH_DISPATCH(density_t);
   return 1;
 }
 
-template <int N, bool W2>
+template <int N, bool W2, int KM>
 static void iad_t(sph_ctx* c) {
   const size_t smem = 4 * kDensCap * sizeof(double);
-  set_smem(k_iad_c<N, W2>, smem);
+  set_smem(k_iad_c<N, W2, KM>, smem);
   sph_particles& P = c->P;
-  k_iad_c<N, W2><<<cell_grid(c, 2), kCTD, smem, c->stream>>>(
+  k_iad_c<N, W2, KM><<<cell_grid(c, 2), kCTD, smem, c->stream>>>(
       P.x, P.y, P.z, c->grid, c->s.cell_start, c->s.cell_end, c->s.cell_hmax, c->s.cell_list,
       c->s.ncell_list, c->s.nbr, c->s.ncount, c->maxn, c->phys, c->s.wB, c->s.ih2, c->s.vol,
       P.c11, P.c12, P.c13, P.c22, P.c23, P.c33, c->s.ct, c->cap, c->s.cnt);
 }
 
 int launch_iad(sph_ctx* c) {
-  const bool w2 = any_wrap2(c);
-  if (c->phys.n == 6) w2 ? iad_t<6, true>(c) : iad_t<6, false>(c);
-  else w2 ? iad_t<0, true>(c) : iad_t<0, false>(c);
+  SPH_DISPATCH(iad_t);
   return 1;
 }
 
-template <int N, bool W2>
+template <int N, bool W2, int KM>
 static void momentum_t(sph_ctx* c) {
   const size_t smem = ((size_t)2 * kMomPairs * kMomCap + (size_t)T_N * kTgt) * sizeof(double);
-  set_smem(k_momentum_c<N, W2>, smem);
+  set_smem(k_momentum_c<N, W2, KM>, smem);
   sph_particles& P = c->P;
   MomSrc src = {P.x, P.y, P.z, P.vx, P.vy, P.vz, P.m, c->s.ih2, P.c, c->s.mX, c->s.vol, c->s.ct, c->cap};
   MomTgt tg = {P.h, c->s.wB, c->s.rinv, c->s.X, P.c11, P.c12, P.c13, P.c22, P.c23, P.c33};
   MomOut out = {P.ax, P.ay, P.az, P.du, P.vsig};
-  k_momentum_c<N, W2><<<cell_grid(c, 1), kCTM, smem, c->stream>>>(
+  k_momentum_c<N, W2, KM><<<cell_grid(c, 1), kCTM, smem, c->stream>>>(
       src, tg, out, c->grid, c->s.cell_start, c->s.cell_end, c->s.cell_hmax, c->s.cell_list,
       c->s.ncell_list, c->s.nbr, c->s.ncount, c->maxn, c->phys, c->s.dts, c->s.cnt);
 }
 
 int launch_momentum(sph_ctx* c) {
-  const bool w2 = any_wrap2(c);
-  if (c->phys.n == 6) w2 ? momentum_t<6, true>(c) : momentum_t<6, false>(c);
-  else w2 ? momentum_t<0, true>(c) : momentum_t<0, false>(c);
+  SPH_DISPATCH(momentum_t);
   return 1;
 }
 

@@ -203,6 +203,9 @@ sph_status sph_init(const sph_params* prm, int64_t capacity, sph_ctx** out) {
   for (int d = 0; d < 3; ++d)
     if (prm->periodic[d] && !(prm->box_hi[d] > prm->box_lo[d])) return SPH_ERR_CONFIG;
   if (prm->eos != SPH_EOS_LINEAR && prm->eos != SPH_EOS_IDEAL) return SPH_ERR_CONFIG;
+  if (prm->kernel_mode < SPH_KERNEL_POLY || prm->kernel_mode > SPH_KERNEL_SIN) return SPH_ERR_CONFIG;
+  if (prm->kernel_mode == SPH_KERNEL_TABLE && prm->table_size != 0 && prm->table_size < 2)
+    return SPH_ERR_CONFIG;
 
   sph_ctx* c = new sph_ctx();
   c->prm = *prm;
@@ -220,6 +223,9 @@ sph_status sph_init(const sph_params* prm, int64_t capacity, sph_ctx** out) {
   ph.B = kernel_norm(ph.n);
   sinc_coeffs(ph.poly, ph.dpoly);
   set_poly_constants(ph.poly, ph.dpoly);
+  ph.kmode = prm->kernel_mode;
+  ph.tableK = prm->table_size > 0 ? prm->table_size : 20000;
+  ph.table = nullptr;
   ph.eos = prm->eos;
   ph.omega_mode = prm->omega_mode;
   ph.alpha = prm->alpha_av;
@@ -273,6 +279,19 @@ sph_status sph_init(const sph_params* prm, int64_t capacity, sph_ctx** out) {
   AL(s.wB, cap);
   AL(s.ih2, cap);
   AL(s.vol, cap);
+  if (ph.kmode == SPH_KERNEL_TABLE) {  // the paper's table: K samples on [0, 2] incl. ends
+    AL(s.ktable, ph.tableK);
+    std::vector<double> tab(ph.tableK);
+    for (int k = 0; k < ph.tableK; ++k) {
+      const long double v = 2.0L * (long double)k / (long double)(ph.tableK - 1);
+      tab[k] = v < 2.0L ? (double)sinc_pow_ld(v, ph.n) : 0.0;
+    }
+    if (cudaMemcpy(s.ktable, tab.data(), sizeof(double) * ph.tableK, cudaMemcpyHostToDevice) != cudaSuccess) {
+      *out = c;
+      return SPH_ERR_CUDA;
+    }
+    ph.table = s.ktable;
+  }
   AL(s.rinv, cap);
   AL(s.X, cap);
   AL(s.red, (int64_t)c->num_sms * 64 * 9);
@@ -688,7 +707,7 @@ sph_status sph_destroy(sph_ctx* c) {
   void* ptrs[] = {s.keys, s.keys_alt, s.idx, s.idx_alt, s.hist, s.scan_tmp, s.gather, s.gather_id,
                   s.cell_start, s.cell_end, s.cell_hmax, s.cell_flag, s.cell_rank, s.cell_list,
                   s.ncell_list, s.nbr, s.ncount, s.nbr_maxcount, s.wB, s.ih2, s.vol, s.rinv, s.X,
-                  s.mX, s.ct, s.red, s.bbox, s.dts, s.cnt, s.diag};
+                  s.mX, s.ct, s.red, s.bbox, s.dts, s.cnt, s.diag, s.ktable};
   for (void* p : ptrs)
     if (p) cudaFree(p);
   delete c;

@@ -42,6 +42,9 @@ struct Phys {
   double poly[kPolyTerms];  // P(t) = sum_k poly[k] t^k = sinc(pi sqrt(t) / 2)
   double dpoly[kPolyTerms]; // P'(t)
   int n;                    // integer kernel exponent
+  int kmode;                // SPH_KERNEL_* (sph.h)
+  int tableK;               // samples of the SPH_KERNEL_TABLE table
+  const double* table;      // device table T_k = S_n(2k/(K-1)) (SPH_KERNEL_TABLE), else null
   int eos, omega_mode;
   double alpha, c0, rho0, gamma, courant, dt_growth, n_target, h_min, h_max, u_floor;
   double L[3];
@@ -54,6 +57,7 @@ enum { DT_RAW_BITS = 0, DT_CUR = 1, DT_PREV = 2, DT_COMMITTED = 3, DT_TIME = 4, 
 
 struct Scratch {
   // sort
+  double* ktable = nullptr;      // SPH_KERNEL_TABLE samples
   uint64_t* keys = nullptr;
   uint64_t* keys_alt = nullptr;
   uint32_t* idx = nullptr;

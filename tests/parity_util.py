@@ -80,9 +80,10 @@ def check_momentum(g: dict, o: dict, idx=None):
     _viol("vsig", g["vsig"][sl] - o["vsig"], 1e-12 * np.abs(o["vsig"]))
 
 
-def oracle_pipeline(O, st: dict, method: int = 1):
-    """Oracle on a state dict (any order); returns neighbours + all outputs."""
-    o = O.Oracle(O.Params.from_inputs(st))
+def oracle_pipeline(O, st: dict, method: int = 1, **okw):
+    """Oracle on a state dict (any order); returns neighbours + all outputs.
+    okw: oracle Params overrides (e.g. table_K for the table kernel mode)."""
+    o = O.Oracle(O.Params.from_inputs(st, **okw))
     off, nbr = o.neighbors(st, method)
     dn = o.density(st, off, nbr)
     C = o.iad(st, dn["rho"], off, nbr)

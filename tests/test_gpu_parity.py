@@ -26,7 +26,7 @@ def O(oracle_mod):
     return oracle_mod
 
 
-def per_call_parity(S, O, d, method=1, **kw):
+def per_call_parity(S, O, d, method=1, oracle_kw=None, **kw):
     """find -> density -> iad -> momentum -> advance, each compared with the oracle
     on the GPU's own (sorted) state."""
     sim = S.Simulation(d, **kw)
@@ -35,7 +35,7 @@ def per_call_parity(S, O, d, method=1, **kw):
     # the permutation keeps every particle: same ids, same fields
     assert np.array_equal(np.sort(st["id"]), np.sort(d["id"]))
     off_g, ids_g = sim.get_neighbors()
-    o, off, nbr, dn, C, me = U.oracle_pipeline(O, st, method)
+    o, off, nbr, dn, C, me = U.oracle_pipeline(O, st, method, **(oracle_kw or {}))
     U.assert_neighbors_equal(off_g, ids_g, off, st["id"][nbr])
     sim.density()
     U.check_density(sim.dev.numpy(("rho", "omega", "p", "c")), dn, d)
@@ -81,6 +81,17 @@ def test_jittered_shuffled_patch(S, O):
 def test_random_cloud_variable_h_periodic_xz(S, O):
     d = I.random_cloud(3000, box=9.0, h0=0.8, hspread=0.2, periodic=(1, 0, 1))
     per_call_parity(S, O, d)
+
+
+@pytest.mark.parametrize("mode", ["table", "sin"])
+@pytest.mark.parametrize("case", ["jitter", "cloud"])
+def test_kernel_modes(S, O, mode, case):
+    """SPH_KERNEL_TABLE (the paper's 20,000-sample table) against the oracle's
+    table mode, SPH_KERNEL_SIN against the oracle's direct sin; variable h included."""
+    d = (I.shuffled(I.jitter(I.square_patch(14, 10))) if case == "jitter" else
+         I.random_cloud(3000, box=9.0, h0=0.8, hspread=0.2, periodic=(1, 0, 1)))
+    okw = {"table_K": 20000} if mode == "table" else {}
+    per_call_parity(S, O, d, oracle_kw=okw, kernel_mode=S.KERNEL_MODES[mode])
 
 
 def test_evrard_shaped_variable_h(S, O):
