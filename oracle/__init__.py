@@ -43,7 +43,7 @@ class _Params(C.Structure):
         ("omega_mode", C.c_int), ("courant", C.c_double), ("dt_growth", C.c_double),
         ("n_target", C.c_double), ("h_min", C.c_double), ("h_max", C.c_double),
         ("u_floor", C.c_double), ("box_lo", C.c_double * 3), ("box_hi", C.c_double * 3),
-        ("periodic", C.c_int * 3),
+        ("periodic", C.c_int * 3), ("symmetric", C.c_int),
     ]
 
 
@@ -125,6 +125,7 @@ class Params:
     box_lo: tuple = (0.0, 0.0, 0.0)
     box_hi: tuple = (1.0, 1.0, 1.0)
     periodic: tuple = (0, 0, 0)
+    symmetric: int = 0
 
     @classmethod
     def from_inputs(cls, d: dict, **kw) -> "Params":
@@ -155,6 +156,7 @@ class Params:
             s.box_lo[k] = self.box_lo[k]
             s.box_hi[k] = self.box_hi[k]
             s.periodic[k] = int(self.periodic[k])
+        s.symmetric = int(self.symmetric)
         return s
 
 

@@ -127,13 +127,16 @@ static double r2_of(const double d[3]) {
 }
 
 /* b is a neighbour of a iff b != a and r^2 < (2 h_a)^2: "v = |x_a - x_b| / h_a"
- * and compact support v <= 2 (Eq. 6), strict (R10).                  */
+ * and compact support v <= 2 (Eq. 6), strict (R10).  Symmetric mode:
+ * r^2 < (2 max(h_a, h_b))^2, so b in N(a) iff a in N(b); the kernel terms of the
+ * extra pairs (r >= 2 h_a) that carry W(r, h_a) vanish by compact support.     */
 static int is_neighbor(const orc_params* p, const double* x, const double* y, const double* z,
                        const double* h, int64_t a, int64_t b) {
   if (a == b) return 0;
   double d[3];
   delta_ab(p, x, y, z, a, b, d);
   double tha = 2.0 * h[a];
+  if (p->symmetric && h[b] > h[a]) tha = 2.0 * h[b];
   return r2_of(d) < tha * tha;
 }
 

@@ -39,6 +39,9 @@ typedef struct {
   double u_floor;      /* u clamp after update                                 */
   double box_lo[3], box_hi[3];
   int    periodic[3];  /* square patch: {0,0,1}                        */
+  int    symmetric;    /* 0: N(a) = {r < 2 h_a} (gather, R10); 1: r < 2 max(h_a, h_b)
+                          (pairwise-antisymmetric forces, exact
+                          conservation for variable h; closes reading R24)      */
 } orc_params;
 
 typedef struct {

@@ -39,8 +39,9 @@ def center_index(side):
     return k + side * (k + side * k)
 
 
-def brute_numpy(d):
-    """Independent O(N^2) neighbour sets: same r^2 association, min image on periodic dims."""
+def brute_numpy(d, symmetric=False):
+    """Independent O(N^2) neighbour sets: same r^2 association, min image on periodic dims
+    (symmetric: r < 2 max(h_a, h_b))."""
     X = np.stack([d["x"], d["y"], d["z"]])
     N = X.shape[1]
     lo, hi = np.asarray(d["box_lo"]), np.asarray(d["box_hi"])
@@ -52,7 +53,7 @@ def brute_numpy(d):
                 L = hi[k] - lo[k]
                 D[k] = np.where(D[k] > 0.5 * L, D[k] - L, np.where(D[k] < -0.5 * L, D[k] + L, D[k]))
         r2 = (D[0] * D[0] + D[1] * D[1]) + D[2] * D[2]
-        tha = 2.0 * d["h"][a]
+        tha = 2.0 * (np.maximum(d["h"][a], d["h"]) if symmetric else d["h"][a])
         ok = r2 < tha * tha
         ok[a] = False
         sets.append(np.flatnonzero(ok))
@@ -307,6 +308,65 @@ def test_iad_singular_fallback(O):
     C = o.iad(d, np.ones(3), off, nbr)
     assert o.counters.iad_singular == 3
     assert C["c12"][0] == 0.0 and C["c11"][0] == C["c22"][0] == C["c33"][0] > 0
+
+
+# ------------------------------------------------------------------ symmetric relation (8(f) NEXT-4)
+
+@pytest.mark.parametrize("periodic", [(1, 0, 1), (0, 0, 0)])
+def test_symmetric_neighbors_brute_force(O, periodic):
+    """r < 2 max(h_a, h_b): brute force, both search methods, a true symmetric relation
+    and a superset of the gather lists."""
+    d = I.random_cloud(1200, box=8.0, h0=0.9, hspread=0.3, periodic=periodic, seed=11)
+    ref = brute_numpy(d, symmetric=True)
+    gat = brute_numpy(d)
+    o = mk(O, d, symmetric=1)
+    for method in (0, 1):
+        off, nbr = o.neighbors(d, method)
+        for a in range(d["x"].size):
+            np.testing.assert_array_equal(nbr[off[a]:off[a + 1]], ref[a])
+    pairs = {(a, b) for a in range(len(ref)) for b in ref[a]}
+    assert all((b, a) in pairs for a, b in pairs)
+    assert sum(len(s) for s in ref) > sum(len(s) for s in gat)  # variable h adds pairs
+    assert all(set(g) <= set(s) for g, s in zip(gat, ref))
+
+
+def test_symmetric_density_iad_unchanged(O):
+    """Extra pairs (r >= 2 h_a) carry W(r, h_a) = 0 (compact support, Eq. 6): rho, Omega
+    and C are the gather values."""
+    d = I.random_cloud(1200, box=8.0, h0=0.9, hspread=0.3, periodic=(1, 0, 1), seed=12)
+    out = []
+    for sym in (0, 1):
+        o = mk(O, d, symmetric=sym)
+        off, nbr = o.neighbors(d, 1)
+        dn = o.density(d, off, nbr)
+        C = o.iad(d, dn["rho"], off, nbr)
+        out.append((dn, C))
+    for k in ("rho", "omega", "p"):
+        np.testing.assert_allclose(out[1][0][k], out[0][0][k], rtol=1e-14, atol=0)
+    for k in ("c11", "c12", "c13", "c22", "c23", "c33"):
+        sc = np.abs(out[0][1]["c11"]) + np.abs(out[0][1]["c22"]) + np.abs(out[0][1]["c33"])
+        assert np.max(np.abs(out[1][1][k] - out[0][1][k]) / sc) < 1e-13
+
+
+def test_symmetric_conservation_variable_h(O):
+    """Closes R24: with r < 2 max(h_a, h_b) every pair interacts both ways, so sum m a = 0
+    and sum m (du + v.a) = 0 to round-off for variable h.  The gather relation on the
+    same input does not conserve (the test is sensitive to the relation)."""
+    d = I.random_cloud(1500, box=8.0, h0=0.9, hspread=0.3, periodic=(0, 0, 1), seed=13)
+    d["vx"] = 0.3 * np.sin(d["y"])
+    d["vy"] = -0.2 * d["x"]
+    m = d["m"]
+    res = {}
+    for sym in (0, 1):
+        r = _rates(O, d, symmetric=sym)[-1]
+        mom = max(abs(np.sum(m * r[ax])) / np.sum(m * r["scale_a"][k])
+                  for k, ax in enumerate(("ax", "ay", "az")))
+        e = np.sum(m * (r["du"] + d["vx"] * r["ax"] + d["vy"] * r["ay"] + d["vz"] * r["az"]))
+        sc = np.sum(m * (r["scale_du"] + np.abs(d["vx"]) * r["scale_a"][0] +
+                         np.abs(d["vy"]) * r["scale_a"][1] + np.abs(d["vz"]) * r["scale_a"][2]))
+        res[sym] = (mom, abs(e) / sc)
+    assert res[1][0] < 1e-13 and res[1][1] < 1e-13
+    assert res[0][0] > 1e-6 or res[0][1] > 1e-6
 
 
 # ------------------------------------------------------------------ O7 momentum / energy
