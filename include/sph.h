@@ -42,7 +42,7 @@
 extern "C" {
 #endif
 
-#define SPH_ABI_VERSION 2
+#define SPH_ABI_VERSION 3
 
 typedef struct sph_ctx sph_ctx;
 
@@ -91,6 +91,9 @@ typedef struct {
   void*  stream;          /* cudaStream_t                                                 */
   int    kernel_mode;     /* SPH_KERNEL_* (0: polynomial)                                 */
   int    table_size;      /* samples K of SPH_KERNEL_TABLE (0: 20,000 as in P:248); >= 2  */
+  int    symmetric;       /* 0: N(a) = {b : r < 2 h_a} (gather, R10);                     */
+                          /* 1: r < 2 max(h_a, h_b) -- b in N(a) iff a in N(b), pair forces */
+                          /* antisymmetric, exact conservation for variable h (closes R24) */
 } sph_params;
 
 typedef struct {          /* caller-owned DEVICE buffers, each >= capacity elements       */

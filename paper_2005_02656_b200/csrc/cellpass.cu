@@ -195,7 +195,7 @@ __device__ void cell_setup(const Grid& g, uint32_t c, const uint32_t* __restrict
       cell_coords(g, c, S.c3);
       S.sc = cstart[c];
       S.ec = cend[c];
-      make_stencil(g, S.c3, reach_of(__longlong_as_double((long long)chmax[c])), S.st);
+      make_stencil(g, S.c3, cell_reach(g, __longlong_as_double((long long)chmax[c])), S.st);
       S.kself = self_slot(S.st, S.c3);
     }
     __syncwarp();
@@ -410,7 +410,20 @@ __device__ __forceinline__ void wrap32(const Stencil& st, const Grid& g, float& 
 }
 
 // ------------------------------------------------------------------ a5 search
-template <bool W2>
+// fp32 band [lo, hi) around lim = (2h)^2 for a staged-coordinate bound M (DESIGN.md
+// §6): r2_32 < lo implies r2 < lim, r2_32 >= hi implies r2 >= lim
+__device__ __forceinline__ float2 band32(double hh, double M) {
+  const double th = 2.0 * hh, lim = __dmul_rn(th, th);
+  const double mh = M / hh;
+  const double delta = 0x1p-20 * (2.0 + 2.0 * mh + 0x1p-20 * mh * mh);
+  if (!(delta < 0.25)) return make_float2(-1.0f, INFINITY);
+  return make_float2((float)(lim * (1.0 - delta)), (float)(lim * (1.0 + delta)));
+}
+
+// SYM: symmetric relation r < 2 max(h_a, h_b) -- each staged candidate carries its
+// own band (candidate side) next to the target's, and the exact test uses the larger
+// of the two limits (the oracle's (2 max h)^2)
+template <bool W2, bool SYM>
 __global__ void __launch_bounds__(kCT, 2) k_search(const double* __restrict__ x,
                                                 const double* __restrict__ y,
                                                 const double* __restrict__ z,
@@ -424,6 +437,7 @@ __global__ void __launch_bounds__(kCT, 2) k_search(const double* __restrict__ x,
                                                 uint32_t* __restrict__ ncount, int maxn,
                                                 unsigned int* __restrict__ maxcount) {
   extern __shared__ float4 cand[];  // kSearchCap + 32 (tile round-up) + 32 (sentinel tile)
+  float2* const candb = reinterpret_cast<float2*>(cand + kSearchCap + 64);  // SYM: per-candidate band
   __shared__ CellSm S;
   __shared__ float4 tlo[kSearchTiles], thi[kSearchTiles];  // per staged tile: fp32 bounding box
   __shared__ uint32_t tcount[kTgt];
@@ -463,12 +477,15 @@ __global__ void __launch_bounds__(kCT, 2) k_search(const double* __restrict__ x,
           v.z = (float)((z[j] + sh[2]) - org[2]);
           v.w = __uint_as_float(((uint32_t)slot << kLocalBits) | l);
           cand[q] = v;
+          if constexpr (SYM) candb[q] = band32(h[j], M);
         }
         // pad to whole tiles with far-away sentinels (never hit, never ambiguous), plus
         // one all-sentinel tile (index ntile) that partners an odd last tile
         const int ntile = (total + 31) >> 5;
-        for (int q = total + threadIdx.x; q < 32 * ntile + 32; q += blockDim.x)
+        for (int q = total + threadIdx.x; q < 32 * ntile + 32; q += blockDim.x) {
           cand[q] = make_float4(INFINITY, INFINITY, INFINITY, __uint_as_float(kSent));
+          if constexpr (SYM) candb[q] = make_float2(-1.0f, -1.0f);
+        }
         __syncthreads();
         // tile bounding boxes (staged candidates are Z-ordered within each cell, so a
         // tile is a compact block)
@@ -477,8 +494,11 @@ __global__ void __launch_bounds__(kCT, 2) k_search(const double* __restrict__ x,
           const bool ok = __float_as_uint(v.w) != kSent;
           float lx = ok ? v.x : INFINITY, ly = ok ? v.y : INFINITY, lz = ok ? v.z : INFINITY;
           float hx = ok ? v.x : -INFINITY, hy = ok ? v.y : -INFINITY, hz = ok ? v.z : -INFINITY;
+          float hb = -1.0f;  // SYM: largest candidate band of the tile
+          if constexpr (SYM) hb = ok ? candb[32 * q + lane].y : -1.0f;
 #pragma unroll
           for (int o = 16; o; o >>= 1) {
+            if constexpr (SYM) hb = fmaxf(hb, __shfl_xor_sync(0xffffffffu, hb, o));
             lx = fminf(lx, __shfl_xor_sync(0xffffffffu, lx, o));
             ly = fminf(ly, __shfl_xor_sync(0xffffffffu, ly, o));
             lz = fminf(lz, __shfl_xor_sync(0xffffffffu, lz, o));
@@ -488,7 +508,7 @@ __global__ void __launch_bounds__(kCT, 2) k_search(const double* __restrict__ x,
           }
           if (lane == 0) {
             tlo[q] = make_float4(lx, ly, lz, 0.f);
-            thi[q] = make_float4(hx, hy, hz, 0.f);
+            thi[q] = make_float4(hx, hy, hz, hb);
           }
         }
         __syncthreads();
@@ -502,13 +522,8 @@ __global__ void __launch_bounds__(kCT, 2) k_search(const double* __restrict__ x,
             const double ha = h[t], tha = 2.0 * ha;
             const double lim = __dmul_rn(tha, tha);
             // fp32 error band: |r2_32 - r2| <= delta lim, delta = 2^-20 (2 + 2 M/h + 2^-20 (M/h)^2)
-            const double mh = M / ha;
-            const double delta = 0x1p-20 * (2.0 + 2.0 * mh + 0x1p-20 * mh * mh);
-            float lo = -1.0f, hi = INFINITY;
-            if (delta < 0.25) {
-              lo = (float)(lim * (1.0 - delta));
-              hi = (float)(lim * (1.0 + delta));
-            }
+            const float2 bd = band32(ha, M);
+            const float lo = bd.x, hi = bd.y;
             const double px = x[t], py = y[t], pz = z[t];
             TW[warp][lane].pos[0] = px;
             TW[warp][lane].pos[1] = py;
@@ -533,7 +548,7 @@ __global__ void __launch_bounds__(kCT, 2) k_search(const double* __restrict__ x,
           // keep the row bases in registers (else ptxas re-derives nbr + t*maxn + p in 64-bit per store)
           asm volatile("" : "+l"(row0), "+l"(row1));
           // one staged candidate against both targets: fp32 band test, exact fp64 when inside it
-          auto test = [&](const float4 cd, bool& hit0, bool& hit1) {
+          auto test = [&](const float4 cd, const float2 cb, bool& hit0, bool& hit1) {
             const uint32_t pk = __float_as_uint(cd.w);
             float dx0 = cd.x - ax0, dy0 = cd.y - ay0, dz0 = cd.z - az0;
             float dx1 = cd.x - ax1, dy1 = cd.y - ay1, dz1 = cd.z - az1;
@@ -543,14 +558,27 @@ __global__ void __launch_bounds__(kCT, 2) k_search(const double* __restrict__ x,
             }
             const float r0 = fmaf(dz0, dz0, fmaf(dy0, dy0, dx0 * dx0));
             const float r1 = fmaf(dz1, dz1, fmaf(dy1, dy1, dx1 * dx1));
-            hit0 = (r0 < lo0) & (pk != self0);
-            hit1 = (r1 < lo1) & (pk != self1);
-            const bool amb0 = (r0 >= lo0) & (r0 < hi0);
-            const bool amb1 = (r1 >= lo1) & (r1 < hi1);
+            bool in0 = r0 < lo0, in1 = r1 < lo1;
+            bool amb0 = (r0 >= lo0) & (r0 < hi0), amb1 = (r1 >= lo1) & (r1 < hi1);
+            if constexpr (SYM) {  // either side's support
+              in0 |= r0 < cb.x;
+              in1 |= r1 < cb.x;
+              amb0 = !in0 & (amb0 | (r0 < cb.y));
+              amb1 = !in1 & (amb1 | (r1 < cb.y));
+            }
+            hit0 = in0 & (pk != self0);
+            hit1 = in1 & (pk != self1);
             if (__ballot_sync(0xffffffffu, amb0 | amb1)) {  // rare: exact fp64 test
               const uint32_t j = S.t_start[pk >> kLocalBits] + (pk & kLocalMask);
-              if (amb0) hit0 = exact_hit(g, x, y, z, j, ta, TW[warp][0].pos, TW[warp][0].lim);
-              if (amb1) hit1 = exact_hit(g, x, y, z, j, tb, TW[warp][1].pos, TW[warp][1].lim);
+              double limb = 0.0;
+              if constexpr (SYM) {
+                if (amb0 | amb1) {
+                  const double thb = 2.0 * h[j];
+                  limb = __dmul_rn(thb, thb);
+                }
+              }
+              if (amb0) hit0 = exact_hit(g, x, y, z, j, ta, TW[warp][0].pos, fmax(TW[warp][0].lim, limb));
+              if (amb1) hit1 = exact_hit(g, x, y, z, j, tb, TW[warp][1].pos, fmax(TW[warp][1].lim, limb));
             }
           };
           // Tiles either target can reach.  Box distance in the prefilter's own fp32
@@ -572,8 +600,9 @@ __global__ void __launch_bounds__(kCT, 2) k_search(const double* __restrict__ x,
                 const float bx1 = fmaxf(fmaxf(L.x - ax1, ax1 - H.x), 0.f);
                 const float by1 = fmaxf(fmaxf(L.y - ay1, ay1 - H.y), 0.f);
                 const float bz1 = fmaxf(fmaxf(L.z - az1, az1 - H.z), 0.f);
-                nd = (fmaf(bz0, bz0, fmaf(by0, by0, bx0 * bx0)) < hi0) |
-                     (fmaf(bz1, bz1, fmaf(by1, by1, bx1 * bx1)) < hi1);
+                const float hb = SYM ? H.w : -1.0f;
+                nd = (fmaf(bz0, bz0, fmaf(by0, by0, bx0 * bx0)) < fmaxf(hi0, hb)) |
+                     (fmaf(bz1, bz1, fmaf(by1, by1, bx1 * bx1)) < fmaxf(hi1, hb));
               }
             }
             need[w] = __ballot_sync(0xffffffffu, nd);
@@ -602,9 +631,14 @@ __global__ void __launch_bounds__(kCT, 2) k_search(const double* __restrict__ x,
             if (qA == ntile) break;
             const int qB = next_tile();
             const float4 cA = cand[32 * qA + lane], cB = cand[32 * qB + lane];
+            float2 bA = make_float2(-1.0f, -1.0f), bB = bA;
+            if constexpr (SYM) {
+              bA = candb[32 * qA + lane];
+              bB = candb[32 * qB + lane];
+            }
             bool hA0, hA1, hB0, hB1;
-            test(cA, hA0, hA1);
-            test(cB, hB0, hB1);
+            test(cA, bA, hA0, hA1);
+            test(cB, bB, hB0, hB1);
             const unsigned bA0 = __ballot_sync(0xffffffffu, hA0), bA1 = __ballot_sync(0xffffffffu, hA1);
             const unsigned bB0 = __ballot_sync(0xffffffffu, hB0), bB1 = __ballot_sync(0xffffffffu, hB1);
             const uint32_t pA0 = cnt0 + __popc(bA0 & lt), pA1 = cnt1 + __popc(bA1 & lt);
@@ -727,13 +761,14 @@ __global__ void __launch_bounds__(kCTD, 2) k_density_c(
         stage2x2(g, S, gb, ge, x, y, z, m, s01, s23);
         __syncthreads();
         struct B : DensBody {
-          int n, K;
+          int n, K, sym;
           const double* tab;
           __device__ __forceinline__ void operator()(int q) {
             const double2 p01 = s01[q], p23 = s23[q];
             double dx = p01.x - xa, dy = p01.y - ya, dz = p23.x - za;
             delta3<W2>(*st, *g, dx, dy, dz);
             const double tt = (dx * dx + dy * dy + dz * dz) * ih2a;
+            if (sym && !(tt < 4.0)) return;  // symmetric extra pair: W(r, h_a) = 0
             const double P = sinc_poly(tt);
             const double Pn1 = ipow<N - 1 < 0 ? 0 : N - 1>(P, n - 1);
             const double dP = sinc_dpoly(tt);
@@ -751,6 +786,7 @@ __global__ void __launch_bounds__(kCTD, 2) k_density_c(
         body.s01 = s01; body.s23 = s23;
         body.tx = tx; body.ty = ty; body.tz = tz; body.tih2 = tih2;
         body.st = &st; body.g = &g; body.n = n; body.K = ph.tableK; body.tab = ph.table;
+        body.sym = ph.sym;
         walk_targets<kNWD>(t0, t1, nbr, maxn, s_n, s_cur, pend, S.cum, gb, &S.next[gi & 1], body,
                           [&](uint32_t i, uint32_t c2) {
                             double v[2] = {body.sr, body.sd};
@@ -850,7 +886,7 @@ __global__ void __launch_bounds__(kCTD, 2) k_iad_c(
           const double *tx, *ty, *tz, *tih2;
           const Stencil* st;
           const Grid* g;
-          int n, K;
+          int n, K, sym;
           const double* tab;
           double xa, ya, za, ih2a, t11, t12, t13, t22, t23, t33;
           __device__ __forceinline__ void begin(uint32_t i) {
@@ -865,6 +901,7 @@ __global__ void __launch_bounds__(kCTD, 2) k_iad_c(
             double dx = p01.x - xa, dy = p01.y - ya, dz = p23.x - za;
             delta3<W2>(*st, *g, dx, dy, dz);
             const double tt = (dx * dx + dy * dy + dz * dz) * ih2a;
+            if (sym && !(tt < 4.0)) return;  // symmetric extra pair: W(r, h_a) = 0
             const double w = p23.y * kern_S<KM, N, false>(tt, n, tab, K);  // (m_b/rho_b) S
             const double wx = w * dx, wy = w * dy;
             t11 = fma(wx, dx, t11);
@@ -878,6 +915,7 @@ __global__ void __launch_bounds__(kCTD, 2) k_iad_c(
         body.s01 = s01; body.s23 = s23;
         body.tx = tx; body.ty = ty; body.tz = tz; body.tih2 = tih2;
         body.st = &st; body.g = &g; body.n = n; body.K = ph.tableK; body.tab = ph.table;
+        body.sym = ph.sym;
         walk_targets<kNWD>(t0, t1, nbr, maxn, s_n, s_cur, pend, S.cum, gb, &S.next[gi & 1], body,
                           [&](uint32_t i, uint32_t c2) {
                             double v[8] = {body.t11, body.t12, body.t13, body.t22,
@@ -1026,7 +1064,7 @@ __global__ void __launch_bounds__(kCTM, 1) k_momentum_c(
           const Stencil* st;
           const Grid* g;
           double alpha;
-          int n, K;
+          int n, K, sym;
           const double* tab;
           unsigned long long* ncoinc;
           double xa, ya, za, vxa, vya, vza, ih2a, wBa, rinva, Xa, ca, a11, a12, a13, a22, a23, a33;
@@ -1052,7 +1090,8 @@ __global__ void __launch_bounds__(kCTM, 1) k_momentum_c(
             const bool coinc = r2 == 0.0;
             *ncoinc += coinc;
             const double ta = r2 * ih2a;
-            const double Sa = kern_S<KM, N, true>(ta, n, tab, K);
+            // symmetric extra pair (r >= 2 h_a): W(r, h_a) = 0, only the h_b terms remain
+            const double Sa = (sym && !(ta < 4.0)) ? 0.0 : kern_S<KM, N, true>(ta, n, tab, K);
             const double Wa = wBa * Sa;
             const double tb = r2 * p3.y;
             double Sb = Sa;  // equal h: W(r, h_b) shares the kernel value
@@ -1089,7 +1128,7 @@ __global__ void __launch_bounds__(kCTM, 1) k_momentum_c(
           }
         } body;
         body.F2 = F2; body.T = T; body.st = &st; body.g = &g; body.alpha = ph.alpha; body.n = n;
-        body.K = ph.tableK; body.tab = ph.table;
+        body.K = ph.tableK; body.tab = ph.table; body.sym = ph.sym;
         body.ncoinc = &ncoinc;
         walk_targets_half(t0, t1, nbr, maxn, s_n, s_cur, pend, S.cum, gb, &S.next[gi & 1], body,
                           [&](bool act, uint32_t i, uint32_t c2) {
@@ -1160,8 +1199,11 @@ static void set_smem(K kern, size_t bytes) {
 }
 
 int launch_neighbors(sph_ctx* c) {
-  const size_t smem = (kSearchCap + 64) * sizeof(float4);  // + tile round-up + sentinel tile
-  auto kern = any_wrap2(c) ? k_search<true> : k_search<false>;
+  const bool sym = c->phys.sym != 0;
+  // + tile round-up + sentinel tile; symmetric: + the candidates' own bands
+  const size_t smem = (kSearchCap + 64) * sizeof(float4) + (sym ? (kSearchCap + 64) * sizeof(float2) : 0);
+  auto kern = any_wrap2(c) ? (sym ? k_search<true, true> : k_search<true, false>)
+                           : (sym ? k_search<false, true> : k_search<false, false>);
   set_smem(kern, smem);
   kern<<<cell_grid(c, 4), kCT, smem, c->stream>>>(
       c->P.x, c->P.y, c->P.z, c->P.h, c->grid, c->s.cell_start, c->s.cell_end, c->s.cell_hmax,

@@ -164,6 +164,7 @@ sph_status choose_grid(sph_ctx* c, const double* bb, int64_t n) {
     return fail(c, SPH_ERR_CONFIG, "Morton key + id exceed 64 bits");
   g.sbits = std::min(3, (64 - 3 * g.cbits - g.idbits) / 3);  // sub-cell order when bits remain
   g.kshift = g.idbits + 3 * g.sbits;
+  g.hsym = c->phys.sym ? bb[6] : 0.0;
   return SPH_OK;
 }
 
@@ -224,6 +225,7 @@ sph_status sph_init(const sph_params* prm, int64_t capacity, sph_ctx** out) {
   sinc_coeffs(ph.poly, ph.dpoly);
   set_poly_constants(ph.poly, ph.dpoly);
   ph.kmode = prm->kernel_mode;
+  ph.sym = prm->symmetric ? 1 : 0;
   ph.tableK = prm->table_size > 0 ? prm->table_size : 20000;
   ph.table = nullptr;
   ph.eos = prm->eos;
@@ -485,7 +487,7 @@ sph_status sph_get_neighbors(sph_ctx* c, int64_t* offsets, int64_t* ids, int64_t
       double hm;
       memcpy(&hm, &chm[cell], sizeof(double));
       Stencil st;
-      make_stencil(g, c3, reach_of(hm), st);
+      make_stencil(g, c3, cell_reach(g, hm), st);
       for (uint32_t k = 0; k < cnt[r0 + i]; ++k) {
         const uint32_t e = rows[(size_t)i * c->maxn + k];
         int sh[3];

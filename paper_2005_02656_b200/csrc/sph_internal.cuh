@@ -33,6 +33,7 @@ struct Grid {
   int idbits;       // id bits at the bottom of the sort key
   int sbits;        // sub-cell Morton bits per dim between the cell code and the id
   int kshift;       // idbits + 3 sbits: key >> kshift = Morton code of the cell
+  double hsym;      // symmetric relation: global h_max (every stencil reaches 2 max h); else 0
   int64_t ncell;
 };
 
@@ -43,6 +44,7 @@ struct Phys {
   double dpoly[kPolyTerms]; // P'(t)
   int n;                    // integer kernel exponent
   int kmode;                // SPH_KERNEL_* (sph.h)
+  int sym;                  // symmetric neighbour relation (sph_params.symmetric)
   int tableK;               // samples of the SPH_KERNEL_TABLE table
   const double* table;      // device table T_k = S_n(2k/(K-1)) (SPH_KERNEL_TABLE), else null
   int eos, omega_mode;

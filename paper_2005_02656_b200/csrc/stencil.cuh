@@ -102,5 +102,10 @@ __host__ __device__ __forceinline__ int64_t key_cell_hd(const Grid& g, uint64_t 
 __host__ __device__ __forceinline__ double reach_of(double hmax) {
   return 2.0 * hmax * (1.0 + 0x1p-20);
 }
+// stencil reach of a cell: 2 h_max of its own particles (gather), or of every
+// particle that may reach into it (symmetric relation: the global h_max)
+__host__ __device__ __forceinline__ double cell_reach(const Grid& g, double cell_hmax) {
+  return reach_of(cell_hmax > g.hsym ? cell_hmax : g.hsym);
+}
 
 }  // namespace sphb

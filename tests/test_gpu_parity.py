@@ -203,17 +203,33 @@ def test_per_call_parity_after_gpu_evolution(S, O):
     per_call_parity(S, O, st)
 
 
-def test_conservation_on_gpu(S, O):
-    """Uniform h: sum m a and the energy rate vanish to round-off on the GPU outputs."""
-    d = I.jitter(I.square_patch(16, 16))
+@pytest.mark.parametrize("case", ["evrard", "cloud"])
+def test_symmetric_relation(S, O, case):
+    """sph_params.symmetric: lists r < 2 max(h_a, h_b) bit-exact, every output within the
+    parity tolerances of the oracle's symmetric mode (variable h)."""
+    d = (I.evrard(36) if case == "evrard" else
+         I.random_cloud(3000, box=9.0, h0=0.8, hspread=0.3, periodic=(1, 0, 1)))
+    per_call_parity(S, O, d, oracle_kw={"symmetric": 1}, symmetric=1)
+
+
+@pytest.mark.parametrize("case", ["uniform", "variable_h_symmetric"])
+def test_conservation_on_gpu(S, O, case):
+    """sum m a and the energy rate vanish to round-off on the GPU outputs: uniform h with
+    the gather relation, variable h with the symmetric relation (R24 closed)."""
+    if case == "uniform":
+        d = I.jitter(I.square_patch(16, 16))
+        kw = {}
+    else:
+        d = I.random_cloud(3000, box=9.0, h0=0.8, hspread=0.3, periodic=(0, 0, 1), seed=5)
+        kw = {"symmetric": 1}
     d["vx"] = d["vx"] - 2.0 * d["x"]
-    sim = S.Simulation(d)
+    sim = S.Simulation(d, **kw)
     sim.find_neighbors()
     sim.density()
     sim.iad()
     sim.momentum_energy()
     st = U.with_meta(sim.state(), d)
-    o, off, nbr, dn, C, me = U.oracle_pipeline(O, st)
+    o, off, nbr, dn, C, me = U.oracle_pipeline(O, st, **kw)
     m = st["m"]
     for k, ax in enumerate(("ax", "ay", "az")):
         assert abs(np.sum(m * st[ax])) <= 1e-12 * np.sum(m * me["scale_a"][k])
