@@ -86,7 +86,7 @@ typedef struct {
   double cell_factor;     /* search-cell edge = cell_factor * 2 * mean(h) (0: 1.0)        */
   double box_lo[3], box_hi[3]; /* periodic dims: the period is box_hi - box_lo            */
   int    periodic[3];     /* square patch: {0,0,1}                               */
-  int    rank, nranks;    /* multi-GPU: this rank / number of ranks (1 for one GPU)       */
+  int    rank, nranks;    /* multi-GPU: this rank / number of ranks (1 for one GPU; <= 64) */
   const void* nccl_unique_id; /* 128-byte ncclUniqueId (rank 0's), NULL when nranks == 1  */
   void*  stream;          /* cudaStream_t                                                 */
   int    kernel_mode;     /* SPH_KERNEL_* (0: polynomial)                                 */

@@ -103,7 +103,8 @@ __device__ __forceinline__ uint64_t spread3(uint64_t v) {  // 21 bits -> every 3
 
 __global__ void k_keys(const double* __restrict__ x, const double* __restrict__ y,
                        const double* __restrict__ z, const int64_t* __restrict__ id, int64_t n,
-                       Grid g, uint64_t* __restrict__ keys, uint32_t* __restrict__ idx) {
+                       Grid g, uint64_t* __restrict__ keys, uint32_t* __restrict__ idx,
+                       int64_t i0) {  // idx[i] = i0 + i: absolute index for the sort
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
        i += (int64_t)gridDim.x * blockDim.x) {
     // cell Morton code (high bits), then the Morton code of the 2^sbits-per-dim
@@ -125,7 +126,7 @@ __global__ void k_keys(const double* __restrict__ x, const double* __restrict__ 
     morton = (morton << (3 * g.sbits)) | spread3(sc[0]) | (spread3(sc[1]) << 1) | (spread3(sc[2]) << 2);
     uint64_t idm = g.idbits >= 64 ? ~0ull : ((1ull << g.idbits) - 1);
     keys[i] = (g.idbits >= 64 ? 0 : (morton << g.idbits)) | ((uint64_t)id[i] & idm);
-    idx[i] = (uint32_t)i;
+    idx[i] = (uint32_t)(i0 + i);
   }
 }
 
@@ -135,7 +136,7 @@ int launch_keys_range(sph_ctx* c, int64_t i0, int64_t n) {
   if (n <= 0) return 0;
   k_keys<<<grid_blocks(c, n, 256, 8), 256, 0, c->stream>>>(c->P.x + i0, c->P.y + i0, c->P.z + i0,
                                                           c->P.id + i0, n, c->grid, c->s.keys + i0,
-                                                          c->s.idx + i0);
+                                                          c->s.idx + i0, i0);
   return 1;
 }
 

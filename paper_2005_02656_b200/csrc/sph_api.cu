@@ -162,7 +162,8 @@ sph_status choose_grid(sph_ctx* c, const double* bb, int64_t n) {
   g.idbits = bits_for((uint64_t)bb[8]);
   if (3 * g.cbits + g.idbits > 64)
     return fail(c, SPH_ERR_CONFIG, "Morton key + id exceed 64 bits");
-  g.sbits = std::min(3, (64 - 3 * g.cbits - g.idbits) / 3);  // sub-cell order when bits remain
+  // sub-cell order when bits remain; one bit stays free for the migration sentinel (multi-GPU)
+  g.sbits = std::max(0, std::min(3, (63 - 3 * g.cbits - g.idbits) / 3));
   g.kshift = g.idbits + 3 * g.sbits;
   g.hsym = c->phys.sym ? bb[6] : 0.0;
   return SPH_OK;
@@ -201,6 +202,7 @@ sph_status sph_init(const sph_params* prm, int64_t capacity, sph_ctx** out) {
   if (capacity < 1 || capacity > 0xffffffffLL) return SPH_ERR_CONFIG;
   if (prm->nranks < 1 || prm->rank < 0 || prm->rank >= prm->nranks) return SPH_ERR_CONFIG;
   if (prm->nranks > 1 && !prm->nccl_unique_id) return SPH_ERR_CONFIG;
+  if (prm->nranks > 64) return SPH_ERR_CONFIG;  // halo peer masks are 64-bit
   for (int d = 0; d < 3; ++d)
     if (prm->periodic[d] && !(prm->box_hi[d] > prm->box_lo[d])) return SPH_ERR_CONFIG;
   if (prm->eos != SPH_EOS_LINEAR && prm->eos != SPH_EOS_IDEAL) return SPH_ERR_CONFIG;
@@ -345,6 +347,47 @@ sph_status sph_attach(sph_ctx* c, const sph_particles* p) {
   return SPH_OK;
 }
 
+// Multi-GPU a1-a2 + a14 with ONE sort: keys of the owned set -> global key-prefix
+// histogram -> splitters -> owner of every particle from its key;
+// leavers are shipped to their owners, stayers close their holes, arrivals
+// are appended, and a single radix sort puts the new owned set in canonical
+// (cell, sub-cell, id) order.
+static sph_status sort_migrate(sph_ctx* c) {
+  const int nbits = 3 * c->grid.cbits + c->grid.kshift;
+  const int64_t n = c->P.n;
+  {
+    Phase ph(c, SPH_PH_KEYS);
+    int k = launch_keys(c);
+    CKL();
+    ph.done(k);
+  }
+  int64_t nleave = 0, nrecv = 0;
+  {
+    Phase ph(c, SPH_PH_HALO);
+    if (!dist_splitters(c) || !dist_migrate(c, &nleave, &nrecv)) return fail(c, SPH_ERR_COMM, c->dist_err);
+    c->P.n = n - nleave + nrecv;
+    // keys of the moved stayers and the arrivals (all keys: simpler than tracking holes)
+    int k = (nleave || nrecv) ? launch_keys(c) : 0;
+    CKL();
+    ph.done(k);
+  }
+  if (c->P.n == 0) return SPH_OK;
+  const uint32_t* perm = nullptr;
+  {
+    Phase ph(c, SPH_PH_SORT);
+    int k = launch_sort(c, nbits, &perm);
+    CKL();
+    ph.done(k);
+  }
+  {
+    Phase ph(c, SPH_PH_PERMUTE);
+    int k = launch_permute(c, perm);
+    CKL();
+    ph.done(k);
+  }
+  return SPH_OK;
+}
+
 static sph_status sort_owned(sph_ctx* c) {  // a1-a2 on [0, P.n): keys, radix sort, permutation
   if (c->P.n == 0) return SPH_OK;
   const int nbits = 3 * c->grid.cbits + c->grid.kshift;
@@ -403,16 +446,10 @@ sph_status sph_find_neighbors(sph_ctx* c) {
     return SPH_OK;
   }
   if (choose_grid(c, bb, n_total) != SPH_OK) return c->status;
-  if (sort_owned(c) != SPH_OK) return c->status;
-  if (multi) {  // a14: splitters from the global key histogram, migration
-    bool moved = false;
-    {
-      Phase ph(c, SPH_PH_HALO);
-      if (!dist_splitters(c) || !dist_migrate(c, &moved)) return fail(c, SPH_ERR_COMM, c->dist_err);
-      CKL();
-      ph.done(0);
-    }
-    if (moved && sort_owned(c) != SPH_OK) return c->status;
+  if (!multi) {
+    if (sort_owned(c) != SPH_OK) return c->status;
+  } else if (sort_migrate(c) != SPH_OK) {
+    return c->status;
   }
   {
     Phase ph(c, SPH_PH_CELLS);

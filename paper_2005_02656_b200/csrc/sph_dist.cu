@@ -87,21 +87,6 @@ __global__ void k_bin_hist(const uint64_t* __restrict__ keys, int64_t n, Grid g,
     atomicAdd(&hist[key_bin(g, keys[i], shift)], 1ull);
 }
 
-// off[r] = first sorted index whose bin >= split[r] (r = 0..G)
-__global__ void k_block_offsets(const uint64_t* __restrict__ keys, int64_t n, Grid g, int shift,
-                                const int64_t* __restrict__ split, int G,
-                                int64_t* __restrict__ off) {
-  const int r = threadIdx.x;
-  if (r > G) return;
-  int64_t lo = 0, hi = n;
-  while (lo < hi) {
-    const int64_t mid = (lo + hi) / 2;
-    if (key_bin(g, keys[mid], shift) < split[r]) lo = mid + 1;
-    else hi = mid;
-  }
-  off[r] = r == G ? n : lo;
-}
-
 __device__ __forceinline__ int owner_dev(const int64_t* split, int G, int64_t bin) {
   int lo = 0, hi = G;
   while (hi - lo > 1) {
@@ -110,6 +95,52 @@ __device__ __forceinline__ int owner_dev(const int64_t* split, int G, int64_t bi
     else hi = mid;
   }
   return lo;
+}
+
+struct FieldSet {
+  uint64_t* f[16];
+  int nf;
+};
+
+// a14: owner of every owned particle from its (unsorted) key; leavers per owner
+__global__ void k_owner_count(const uint64_t* __restrict__ keys, int64_t n, Grid g, int shift,
+                              const int64_t* __restrict__ split, int G, int me,
+                              uint32_t* __restrict__ dest, unsigned long long* __restrict__ cnt) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    const int o = owner_dev(split, G, key_bin(g, keys[i], shift));
+    dest[i] = (uint32_t)o;
+    if (o != me) atomicAdd(&cnt[o], 1ull);
+  }
+}
+// Leavers: per-owner send lists, and the compaction pairs -- leavers below n_keep
+// ("holes") and stayers at or above n_keep ("movers") are equally many; each mover
+// fills one hole.  Any order and pairing will do: the owned set is sorted next.
+__global__ void k_owner_fill(int64_t n, int64_t n_keep, const uint32_t* __restrict__ dest, int me,
+                             const int64_t* __restrict__ soff, unsigned long long* __restrict__ fill,
+                             uint32_t* __restrict__ send_idx, unsigned long long* __restrict__ hm,
+                             uint32_t* __restrict__ holes, uint32_t* __restrict__ movers) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    const uint32_t o = dest[i];
+    if ((int)o != me) {
+      const unsigned long long slot = atomicAdd(&fill[o], 1ull);
+      send_idx[soff[o] + (int64_t)slot] = (uint32_t)i;
+      if (i < n_keep) holes[atomicAdd(&hm[0], 1ull)] = (uint32_t)i;
+    } else if (i >= n_keep) {
+      movers[atomicAdd(&hm[1], 1ull)] = (uint32_t)i;
+    }
+  }
+}
+__global__ void k_fill_holes_dev(FieldSet fs, const uint32_t* __restrict__ holes,
+                                 const uint32_t* __restrict__ movers,
+                                 const unsigned long long* __restrict__ hm) {
+  const int64_t k = (int64_t)hm[0];  // == hm[1]
+  for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < k;
+       t += (int64_t)gridDim.x * blockDim.x) {
+    const uint32_t h = holes[t], m = movers[t];
+    for (int f = 0; f < fs.nf; ++f) fs.f[f][h] = fs.f[f][m];
+  }
 }
 
 // per owned non-empty cell: bit r set if rank r owns a cell within the halo box
@@ -149,6 +180,31 @@ __global__ void k_halo_mask(const uint32_t* __restrict__ clist, const uint32_t* 
   }
 }
 
+// per-peer halo totals in one pass (block-aggregated atomics; G <= 64)
+__global__ void k_peer_totals(const uint32_t* __restrict__ clist, const uint32_t* __restrict__ ncl,
+                              const uint32_t* __restrict__ cstart, const uint32_t* __restrict__ cend,
+                              const unsigned long long* __restrict__ mask, int G,
+                              unsigned long long* __restrict__ tot) {
+  __shared__ unsigned long long bt[64];
+  for (int r = threadIdx.x; r < G; r += blockDim.x) bt[r] = 0;
+  __syncthreads();
+  const uint32_t nl = *ncl;
+  for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < nl; i += gridDim.x * blockDim.x) {
+    unsigned long long m = mask[i];
+    if (!m) continue;
+    const uint32_t c = clist[i];
+    const unsigned long long cnt = cend[c] - cstart[c];
+    while (m) {
+      const int r = __ffsll((long long)m) - 1;
+      m &= m - 1;
+      atomicAdd(&bt[r], cnt);
+    }
+  }
+  __syncthreads();
+  for (int r = threadIdx.x; r < G; r += blockDim.x)
+    if (bt[r]) atomicAdd(&tot[r], bt[r]);
+}
+
 // particles each owned cell sends to peer r (0 when the bit is clear)
 __global__ void k_peer_counts(const uint32_t* __restrict__ clist, const uint32_t* __restrict__ ncl,
                               const uint32_t* __restrict__ cstart, const uint32_t* __restrict__ cend,
@@ -175,16 +231,7 @@ __global__ void k_fill_send(const uint32_t* __restrict__ clist, const uint32_t* 
   }
 }
 
-__global__ void k_total(const uint32_t* __restrict__ cnt, const uint32_t* __restrict__ off,
-                        const uint32_t* __restrict__ ncl, int64_t* __restrict__ tot) {
-  const uint32_t nl = *ncl;
-  *tot = nl ? (int64_t)off[nl - 1] + cnt[nl - 1] : 0;
-}
 
-struct FieldSet {
-  uint64_t* f[16];
-  int nf;
-};
 
 // sendbuf layout per peer: nf blocks of cnt_r elements
 __global__ void k_pack(FieldSet fs, const uint32_t* __restrict__ idx, int64_t n, int64_t base,
@@ -195,30 +242,12 @@ __global__ void k_pack(FieldSet fs, const uint32_t* __restrict__ idx, int64_t n,
     for (int f = 0; f < fs.nf; ++f) buf[base * fs.nf + f * n + k] = fs.f[f][j];
   }
 }
-__global__ void k_pack_range(FieldSet fs, int64_t src0, int64_t n, int64_t base,
-                             uint64_t* __restrict__ buf) {
-  for (int64_t k = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; k < n;
-       k += (int64_t)gridDim.x * blockDim.x)
-    for (int f = 0; f < fs.nf; ++f) buf[base * fs.nf + f * n + k] = fs.f[f][src0 + k];
-}
 __global__ void k_unpack(FieldSet fs, const uint64_t* __restrict__ buf, int64_t n, int64_t base,
                          int64_t dst0) {
   for (int64_t k = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; k < n;
        k += (int64_t)gridDim.x * blockDim.x)
     for (int f = 0; f < fs.nf; ++f) fs.f[f][dst0 + k] = buf[base * fs.nf + f * n + k];
 }
-// move [src0, src0+n) -> [0, n) through a staging buffer (ranges may overlap)
-__global__ void k_copy_out(FieldSet fs, int64_t src0, int64_t n, uint64_t* __restrict__ tmp) {
-  for (int64_t k = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; k < n;
-       k += (int64_t)gridDim.x * blockDim.x)
-    for (int f = 0; f < fs.nf; ++f) tmp[f * n + k] = fs.f[f][src0 + k];
-}
-__global__ void k_copy_in(FieldSet fs, int64_t n, const uint64_t* __restrict__ tmp) {
-  for (int64_t k = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; k < n;
-       k += (int64_t)gridDim.x * blockDim.x)
-    for (int f = 0; f < fs.nf; ++f) fs.f[f][k] = tmp[f * n + k];
-}
-
 __global__ void k_bbox_pack(const double* __restrict__ bb, int64_t n, double* __restrict__ mx,
                             double* __restrict__ sm) {
   // MAX of {-min x,y,z, max x,y,z, max h, max id}; SUM of {sum h, n}
@@ -243,21 +272,16 @@ static FieldSet state_fields(sph_ctx* c, bool with_hist) {
   return fs;
 }
 
-static bool exchange(sph_ctx* c, const FieldSet& fs, bool halo_mode) {
-  // halo_mode: send the send_idx lists, receive after the owned particles.
+static bool exchange(sph_ctx* c, const FieldSet& fs) {
+  // send the per-peer index lists (send_idx at soff), receive in rank order
   Dist& D = *c->dist;
   const int G = D.G, me = D.rank;
   const int F = fs.nf;
   int64_t sbase = 0, rbase = 0;
   for (int r = 0; r < G; ++r) {
     if (D.scnt[r] && r != me) {
-      if (halo_mode) {
-        k_pack<<<grid_blocks(c, D.scnt[r], 256, 4), 256, 0, c->stream>>>(fs, D.send_idx + D.soff[r],
-                                                                         D.scnt[r], sbase, D.sendbuf);
-      } else {
-        k_pack_range<<<grid_blocks(c, D.scnt[r], 256, 4), 256, 0, c->stream>>>(fs, D.soff[r], D.scnt[r],
-                                                                               sbase, D.sendbuf);
-      }
+      k_pack<<<grid_blocks(c, D.scnt[r], 256, 4), 256, 0, c->stream>>>(fs, D.send_idx + D.soff[r],
+                                                                       D.scnt[r], sbase, D.sendbuf);
       c->launches++;
     }
     if (r != me) sbase += D.scnt[r];
@@ -369,39 +393,61 @@ bool dist_splitters(sph_ctx* c) {
   return true;
 }
 
-// after the local sort: ship particles outside this rank's key range to their owners
-bool dist_migrate(sph_ctx* c, bool* moved) {
+// a14: ship particles outside this rank's key range to their owners.  Keys
+// of the owned set are current (unsorted).  After the leavers are packed, stayers
+// from the tail fill their holes and arrivals land behind: the new owned set is
+// [0, n - nleave + nrecv), unsorted -- sort_migrate sorts it once.
+bool dist_migrate(sph_ctx* c, int64_t* nleave, int64_t* nrecv) {
   Dist& D = *c->dist;
   const int G = D.G;
-  std::vector<int64_t> off(G + 1);
-  k_block_offsets<<<1, 64, 0, c->stream>>>(c->s.keys, c->P.n, c->grid, D.shift, D.split_d, G, D.off_d);
-  c->launches++;
-  CUK(cudaMemcpyAsync(off.data(), D.off_d, sizeof(int64_t) * (G + 1), cudaMemcpyDeviceToHost, c->stream));
+  const int64_t n = c->P.n;
+  *nleave = *nrecv = 0;
+  CUK(cudaMemsetAsync(D.tot_d, 0, sizeof(int64_t) * G, c->stream));
+  if (n) {
+    k_owner_count<<<grid_blocks(c, n, 256, 8), 256, 0, c->stream>>>(
+        c->s.keys, n, c->grid, D.shift, D.split_d, G, D.rank, D.pcnt_d, (unsigned long long*)D.tot_d);
+    c->launches++;
+  }
+  std::vector<int64_t> tot(G);
+  CUK(cudaMemcpyAsync(tot.data(), D.tot_d, sizeof(int64_t) * G, cudaMemcpyDeviceToHost, c->stream));
   CUK(cudaStreamSynchronize(c->stream));
+  int64_t off = 0;
   for (int r = 0; r < G; ++r) {
-    D.soff[r] = off[r];
-    D.scnt[r] = r == D.rank ? 0 : off[r + 1] - off[r];
+    D.soff[r] = off;
+    D.scnt[r] = r == D.rank ? 0 : tot[r];
+    off += D.scnt[r];
   }
   const int64_t cap = c->cap, xcap = D.xcap;
-  if (!swap_counts(c, c->P.n, [&](int64_t sent, int64_t recv, int64_t nb) {
+  if (!swap_counts(c, n, [&](int64_t sent, int64_t recv, int64_t nb) {
         return nb - sent + recv <= cap && sent <= xcap && recv <= xcap;
       }))
     return false;
-  *moved = D.moved_total > 0;
-  if (!*moved) return true;
-  int64_t nrecv = 0;
-  for (int r = 0; r < G; ++r) nrecv += D.rcnt[r];
-  const int64_t kept = off[D.rank + 1] - off[D.rank];
+  if (D.moved_total == 0) return true;
+  for (int r = 0; r < G; ++r) {
+    *nleave += D.scnt[r];
+    *nrecv += D.rcnt[r];
+  }
+  const int64_t n_keep = n - *nleave;
+  uint32_t* holes = c->s.cell_flag;   // scratch until launch_cells rebuilds the cell tables
+  uint32_t* movers = c->s.cell_rank;
+  if (*nleave) {
+    CUK(cudaMemcpyAsync(D.off_d, D.soff.data(), sizeof(int64_t) * G, cudaMemcpyHostToDevice, c->stream));
+    CUK(cudaMemsetAsync(D.cnt_d, 0, sizeof(int64_t) * (G + 1), c->stream));
+    CUK(cudaMemsetAsync(D.hm_d, 0, sizeof(unsigned long long) * 2, c->stream));
+    k_owner_fill<<<grid_blocks(c, n, 256, 8), 256, 0, c->stream>>>(
+        n, n_keep, D.pcnt_d, D.rank, D.off_d, (unsigned long long*)D.cnt_d, D.send_idx, D.hm_d, holes,
+        movers);
+    c->launches++;
+  }
   FieldSet fs = state_fields(c, true);
-  if (!exchange(c, fs, false)) return false;
-  // kept block -> front (through the send buffer tail is unsafe: use the permutation scratch)
-  uint64_t* tmp = (uint64_t*)c->s.gather;
-  k_copy_out<<<grid_blocks(c, kept, 256, 8), 256, 0, c->stream>>>(fs, off[D.rank], kept, tmp);
-  k_copy_in<<<grid_blocks(c, kept, 256, 8), 256, 0, c->stream>>>(fs, kept, tmp);
-  c->launches += 2;
-  if (!unpack_all(c, fs, kept)) return false;
-  c->P.n = kept + nrecv;
-  return true;
+  if (!exchange(c, fs)) return false;  // packs the leavers (stream order: before the moves)
+  if (*nleave) {
+    // holes below n_keep == stayers at or above n_keep (both equal nleave minus the
+    // leavers already at or above n_keep); the host does not need the count
+    k_fill_holes_dev<<<grid_blocks(c, *nleave, 256, 8), 256, 0, c->stream>>>(fs, holes, movers, D.hm_d);
+    c->launches++;
+  }
+  return unpack_all(c, fs, n_keep);
 }
 
 // halo plan (who needs which of my cells) + exchange #1 (x, v, h, m, u, id)
@@ -417,17 +463,14 @@ bool dist_halo_plan_and_exchange1(sph_ctx* c) {
                                           D.rank, D.shift, D.mask_d);
   c->launches++;
   // pass 1: per-peer totals only (nothing written yet), then a collective capacity check
+  CUK(cudaMemsetAsync(D.tot_d, 0, sizeof(int64_t) * G, c->stream));
+  k_peer_totals<<<nbc, 256, 0, c->stream>>>(c->s.cell_list, c->s.ncell_list, c->s.cell_start, c->s.cell_end,
+                                            D.mask_d, G, (unsigned long long*)D.tot_d);
+  c->launches++;
   std::vector<int64_t> tot(G, 0);
-  for (int r = 0; r < G; ++r) {
-    if (r == D.rank) continue;
-    k_peer_counts<<<nbc, 256, 0, c->stream>>>(c->s.cell_list, c->s.ncell_list, c->s.cell_start, c->s.cell_end,
-                                              D.mask_d, r, D.pcnt_d);
-    scan_u32(c, D.pcnt_d, D.poff_d, n);
-    k_total<<<1, 1, 0, c->stream>>>(D.pcnt_d, D.poff_d, c->s.ncell_list, D.tot_d + r);
-    c->launches += 5;
-  }
-  CUK(cudaMemsetAsync(D.tot_d + D.rank, 0, sizeof(int64_t), c->stream));
+  uint32_t ncl = 0;
   CUK(cudaMemcpyAsync(tot.data(), D.tot_d, sizeof(int64_t) * G, cudaMemcpyDeviceToHost, c->stream));
+  CUK(cudaMemcpyAsync(&ncl, c->s.ncell_list, sizeof(uint32_t), cudaMemcpyDeviceToHost, c->stream));
   CUK(cudaStreamSynchronize(c->stream));
   int64_t total = 0;
   for (int r = 0; r < G; ++r) {
@@ -441,19 +484,20 @@ bool dist_halo_plan_and_exchange1(sph_ctx* c) {
       }))
     return false;
   // pass 2: fill the per-peer send lists (cells in Morton order -> key-sorted halos)
+  const int nbl = grid_blocks(c, ncl, 256, 8);
   for (int r = 0; r < G; ++r) {
     if (r == D.rank || D.scnt[r] == 0) continue;
-    k_peer_counts<<<nbc, 256, 0, c->stream>>>(c->s.cell_list, c->s.ncell_list, c->s.cell_start, c->s.cell_end,
+    k_peer_counts<<<nbl, 256, 0, c->stream>>>(c->s.cell_list, c->s.ncell_list, c->s.cell_start, c->s.cell_end,
                                               D.mask_d, r, D.pcnt_d);
-    scan_u32(c, D.pcnt_d, D.poff_d, n);
-    k_fill_send<<<nbc, 256, 0, c->stream>>>(c->s.cell_list, c->s.ncell_list, c->s.cell_start, c->s.cell_end,
+    scan_u32(c, D.pcnt_d, D.poff_d, ncl);
+    k_fill_send<<<nbl, 256, 0, c->stream>>>(c->s.cell_list, c->s.ncell_list, c->s.cell_start, c->s.cell_end,
                                             D.mask_d, r, D.poff_d, D.send_idx + D.soff[r]);
-    c->launches += 5;
+    c->launches += 4;
   }
   D.n_halo = 0;
   for (int r = 0; r < G; ++r) D.n_halo += D.rcnt[r];
   FieldSet fs = state_fields(c, false);
-  if (!exchange(c, fs, true)) return false;
+  if (!exchange(c, fs)) return false;
   return unpack_all(c, fs, n);
 }
 
@@ -464,14 +508,14 @@ bool dist_exchange2(sph_ctx* c) {  // after density: quantities IAD / momentum r
   fs.f[2] = (uint64_t*)c->P.c;
   fs.f[3] = (uint64_t*)c->s.mX;
   fs.nf = 4;
-  return exchange(c, fs, true) && unpack_all(c, fs, c->P.n);
+  return exchange(c, fs) && unpack_all(c, fs, c->P.n);
 }
 
 bool dist_exchange3(sph_ctx* c) {  // after IAD: C~ = (B/h^3) C of the sources
   FieldSet fs{};
   for (int k = 0; k < 6; ++k) fs.f[k] = (uint64_t*)(c->s.ct + (size_t)k * c->cap);
   fs.nf = 6;
-  return exchange(c, fs, true) && unpack_all(c, fs, c->P.n);
+  return exchange(c, fs) && unpack_all(c, fs, c->P.n);
 }
 
 bool dist_allreduce_dt(sph_ctx* c) {
@@ -511,6 +555,7 @@ bool dist_init(sph_ctx* c, const sph_params* prm) {
   CUK(cudaMalloc(&D->tot_d, sizeof(int64_t) * D->G));
   CUK(cudaMalloc(&D->red_d, sizeof(double) * 16));
   CUK(cudaMalloc(&D->cntred_d, sizeof(unsigned long long) * kCounters));
+  CUK(cudaMalloc(&D->hm_d, sizeof(unsigned long long) * 2));
   CUK(cudaMalloc(&D->mask_d, sizeof(unsigned long long) * cap));
   CUK(cudaMalloc(&D->pcnt_d, sizeof(uint32_t) * cap));
   CUK(cudaMalloc(&D->poff_d, sizeof(uint32_t) * cap));
@@ -525,7 +570,8 @@ void dist_destroy(sph_ctx* c) {
   if (!D) return;
   if (D->comm) ncclCommDestroy(D->comm);
   void* ptrs[] = {D->hist_d, D->split_d, D->off_d, D->cnt_d, D->cnt_all_d, D->tot_d, D->red_d,
-                  D->mask_d, D->pcnt_d, D->poff_d, D->send_idx, D->sendbuf, D->recvbuf, D->cntred_d};
+                  D->mask_d, D->pcnt_d, D->poff_d, D->send_idx, D->sendbuf, D->recvbuf, D->cntred_d,
+                  D->hm_d};
   for (void* p : ptrs)
     if (p) cudaFree(p);
   delete D;
@@ -540,7 +586,7 @@ bool dist_init(sph_ctx* c, const sph_params*) {
 void dist_destroy(sph_ctx*) {}
 bool dist_global_bbox(sph_ctx*, double*) { return false; }
 bool dist_splitters(sph_ctx*) { return false; }
-bool dist_migrate(sph_ctx*, bool*) { return false; }
+bool dist_migrate(sph_ctx*, int64_t*, int64_t*) { return false; }
 bool dist_halo_plan_and_exchange1(sph_ctx*) { return false; }
 bool dist_exchange2(sph_ctx*) { return false; }
 bool dist_exchange3(sph_ctx*) { return false; }

@@ -32,6 +32,7 @@ struct Dist {
   uint32_t *pcnt_d = nullptr, *poff_d = nullptr, *send_idx = nullptr;
   uint64_t *sendbuf = nullptr, *recvbuf = nullptr;
   unsigned long long* cntred_d = nullptr;  // all-reduced event counters
+  unsigned long long* hm_d = nullptr;      // migration: hole / mover counters
 };
 
 void compute_splitters(const int64_t* hist, int64_t nbins, int G, int64_t* split);
@@ -44,7 +45,7 @@ inline unsigned long long* dist_counters(const sph_ctx* c) { return c->dist->cnt
 void dist_destroy(sph_ctx* c);
 bool dist_global_bbox(sph_ctx* c, double* bb_out);
 bool dist_splitters(sph_ctx* c);
-bool dist_migrate(sph_ctx* c, bool* moved);
+bool dist_migrate(sph_ctx* c, int64_t* nleave, int64_t* nrecv);
 bool dist_halo_plan_and_exchange1(sph_ctx* c);
 bool dist_exchange2(sph_ctx* c);
 bool dist_exchange3(sph_ctx* c);
