@@ -383,6 +383,71 @@ __device__ __forceinline__ void walk_targets_half(uint32_t t0, uint32_t t1,
   }
 }
 
+// Lean full-warp walk (density, IAD): the ring of three row chunks is consumed in
+// place -- each step refills the register it just used with the chunk three steps
+// ahead (a shifted ring makes every move wait for the latest load) -- through a
+// running row pointer, and the body runs on every lane with a validity flag instead
+// of a divergent branch (ncu: per-step bookkeeping was as large as the pair math).
+template <class Body, class Finish>
+__device__ __forceinline__ void walk_targets_fast(uint32_t t0, uint32_t t1,
+                                                  const uint32_t* __restrict__ nbr, int maxn,
+                                                  const uint32_t* s_n, const uint32_t* s_cur,
+                                                  uint32_t pend, const uint32_t* cum, uint32_t gb,
+                                                  uint32_t* s_next, Body&& body, Finish&& finish) {
+  const uint32_t lane = threadIdx.x & 31;
+  auto claim = [&]() {
+    uint32_t v = 0;
+    if (lane == 0) v = t0 + atomicAdd(s_next, 1u);
+    return __shfl_sync(0xffffffffu, v, 0);
+  };
+  uint32_t t = claim();
+  uint32_t f0 = kSent, f1 = kSent, f2 = kSent;
+  if (t < t1) {
+    const uint32_t c0 = s_cur[t - t0] + lane, nn = s_n[t - t0];
+    const uint32_t* r = nbr + (size_t)t * maxn;
+    f0 = row_chunk(r, c0, nn);
+    f1 = row_chunk(r, c0 + 32, nn);
+    f2 = row_chunk(r, c0 + 64, nn);
+  }
+  while (t < t1) {
+    const uint32_t i = t - t0, n = s_n[i];
+    uint32_t cur = s_cur[i];
+    const uint32_t lim = n - cur;  // valid positions: offset < lim from cur
+    const uint32_t* rp = nbr + (size_t)t * maxn + cur + lane + 96;
+    uint32_t off = lane + 96;
+    uint32_t e0 = f0, e1 = f1, e2 = f2;
+    const uint32_t tn = claim();
+    if (tn < t1) {  // the next target's first three chunks
+      const uint32_t cn = s_cur[tn - t0] + lane, nn = s_n[tn - t0];
+      const uint32_t* r = nbr + (size_t)tn * maxn;
+      f0 = row_chunk(r, cn, nn);
+      f1 = row_chunk(r, cn + 32, nn);
+      f2 = row_chunk(r, cn + 64, nn);
+    }
+    body.begin(i);
+#define SPH_FAST_STEP(R)                                                             \
+  {                                                                                  \
+    const uint32_t e = R;                                                            \
+    const bool in = e < pend;                                                        \
+    const int m = __popc(__ballot_sync(0xffffffffu, in));                            \
+    R = (m == 32 && off < lim) ? *rp : kSent;                                        \
+    rp += 32;                                                                        \
+    off += 32;                                                                       \
+    body(in ? (int)(cum[e >> kLocalBits] + (e & kLocalMask) - gb) : 0, in);          \
+    cur += m;                                                                        \
+    if (m < 32) break;                                                               \
+  }
+    for (;;) {
+      SPH_FAST_STEP(e0)
+      SPH_FAST_STEP(e1)
+      SPH_FAST_STEP(e2)
+    }
+#undef SPH_FAST_STEP
+    finish(i, cur);
+    t = tn;
+  }
+}
+
 struct TgtW {  // per-warp search target data (exact-test fp64 + fp32 band)
   double pos[3];
   double lim;
@@ -763,31 +828,36 @@ __global__ void __launch_bounds__(kCTD, 2) k_density_c(
         struct B : DensBody {
           int n, K, sym;
           const double* tab;
-          __device__ __forceinline__ void operator()(int q) {
+          // ok == false: padding lane of the walk; its terms are discarded by selects
+          // (not multiplied by 0: a far padding pair may overflow the polynomial)
+          __device__ __forceinline__ void operator()(int q, bool ok) {
             const double2 p01 = s01[q], p23 = s23[q];
             double dx = p01.x - xa, dy = p01.y - ya, dz = p23.x - za;
             delta3<W2>(*st, *g, dx, dy, dz);
             const double tt = (dx * dx + dy * dy + dz * dz) * ih2a;
-            if (sym && !(tt < 4.0)) return;  // symmetric extra pair: W(r, h_a) = 0
+            if (sym) ok = ok && tt < 4.0;  // symmetric extra pair: W(r, h_a) = 0
             const double P = sinc_poly(tt);
             const double Pn1 = ipow<N - 1 < 0 ? 0 : N - 1>(P, n - 1);
             const double dP = sinc_dpoly(tt);
             const double mj = p23.y;
+            double a, b;
             if constexpr (KM == SPH_KERNEL_POLY) {
-              sr = fma(mj, Pn1 * P, sr);
-              sd = fma(mj, Pn1 * (3.0 * P + (2.0 * n) * tt * dP), sd);  // 3 S + v S'(v)
+              a = Pn1 * P;
+              b = Pn1 * (3.0 * P + (2.0 * n) * tt * dP);  // 3 S + v S'(v)
             } else {  // S from the selected mode; v S'(v) from the exact polynomial (R12)
               const double S_ = kern_S<KM, N, false>(tt, n, tab, K);
-              sr = fma(mj, S_, sr);
-              sd = fma(mj, fma(3.0, S_, Pn1 * (2.0 * n) * tt * dP), sd);
+              a = S_;
+              b = fma(3.0, S_, Pn1 * (2.0 * n) * tt * dP);
             }
+            sr = fma(mj, ok ? a : 0.0, sr);
+            sd = fma(mj, ok ? b : 0.0, sd);
           }
         } body;
         body.s01 = s01; body.s23 = s23;
         body.tx = tx; body.ty = ty; body.tz = tz; body.tih2 = tih2;
         body.st = &st; body.g = &g; body.n = n; body.K = ph.tableK; body.tab = ph.table;
         body.sym = ph.sym;
-        walk_targets<kNWD>(t0, t1, nbr, maxn, s_n, s_cur, pend, S.cum, gb, &S.next[gi & 1], body,
+        walk_targets_fast(t0, t1, nbr, maxn, s_n, s_cur, pend, S.cum, gb, &S.next[gi & 1], body,
                           [&](uint32_t i, uint32_t c2) {
                             double v[2] = {body.sr, body.sd};
                             warp_multi_sum<2>(v);
@@ -896,13 +966,14 @@ __global__ void __launch_bounds__(kCTD, 2) k_iad_c(
             ih2a = tih2[i];
             t11 = t12 = t13 = t22 = t23 = t33 = 0.0;
           }
-          __device__ __forceinline__ void operator()(int q) {
+          __device__ __forceinline__ void operator()(int q, bool ok) {  // ok: see density
             const double2 p01 = s01[q], p23 = s23[q];
             double dx = p01.x - xa, dy = p01.y - ya, dz = p23.x - za;
             delta3<W2>(*st, *g, dx, dy, dz);
             const double tt = (dx * dx + dy * dy + dz * dz) * ih2a;
-            if (sym && !(tt < 4.0)) return;  // symmetric extra pair: W(r, h_a) = 0
-            const double w = p23.y * kern_S<KM, N, false>(tt, n, tab, K);  // (m_b/rho_b) S
+            if (sym) ok = ok && tt < 4.0;  // symmetric extra pair: W(r, h_a) = 0
+            const double S_ = kern_S<KM, N, false>(tt, n, tab, K);
+            const double w = p23.y * (ok ? S_ : 0.0);  // (m_b/rho_b) S
             const double wx = w * dx, wy = w * dy;
             t11 = fma(wx, dx, t11);
             t12 = fma(wx, dy, t12);
@@ -916,7 +987,7 @@ __global__ void __launch_bounds__(kCTD, 2) k_iad_c(
         body.tx = tx; body.ty = ty; body.tz = tz; body.tih2 = tih2;
         body.st = &st; body.g = &g; body.n = n; body.K = ph.tableK; body.tab = ph.table;
         body.sym = ph.sym;
-        walk_targets<kNWD>(t0, t1, nbr, maxn, s_n, s_cur, pend, S.cum, gb, &S.next[gi & 1], body,
+        walk_targets_fast(t0, t1, nbr, maxn, s_n, s_cur, pend, S.cum, gb, &S.next[gi & 1], body,
                           [&](uint32_t i, uint32_t c2) {
                             double v[8] = {body.t11, body.t12, body.t13, body.t22,
                                            body.t23, body.t33, 0.0, 0.0};
