@@ -506,7 +506,7 @@ __global__ void __launch_bounds__(kCT, 2) k_search(const double* __restrict__ x,
   __shared__ CellSm S;
   __shared__ float4 tlo[kSearchTiles], thi[kSearchTiles];  // per staged tile: fp32 bounding box
   __shared__ uint32_t tcount[kTgt];
-  __shared__ TgtW TW[kNW][2];
+  __shared__ TgtW TW[kTgt];  // per target of the block: computed once, in parallel
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const unsigned lt = (1u << lane) - 1u;
   const uint32_t ncl = *nclist;
@@ -526,7 +526,23 @@ __global__ void __launch_bounds__(kCT, 2) k_search(const double* __restrict__ x,
     }
     for (uint32_t t0 = S.sc; t0 < S.ec; t0 += kTgt) {
       const uint32_t t1 = min(S.ec, t0 + kTgt);
-      for (uint32_t t = t0 + threadIdx.x; t < t1; t += blockDim.x) tcount[t - t0] = 0;
+      for (uint32_t t = t0 + threadIdx.x; t < t1; t += blockDim.x) {
+        tcount[t - t0] = 0;
+        const double ha = h[t], tha = 2.0 * ha;
+        // fp32 error band: |r2_32 - r2| <= delta lim, delta = 2^-20 (2 + 2 M/h + 2^-20 (M/h)^2)
+        const float2 bd = band32(ha, M);
+        const double px = x[t], py = y[t], pz = z[t];
+        TgtW& w = TW[t - t0];
+        w.pos[0] = px;
+        w.pos[1] = py;
+        w.pos[2] = pz;
+        w.lim = __dmul_rn(tha, tha);
+        w.f[0] = (float)(px - org[0]);
+        w.f[1] = (float)(py - org[1]);
+        w.f[2] = (float)(pz - org[2]);
+        w.f[3] = bd.x;
+        w.f[4] = bd.y;
+      }
       __syncthreads();
       for (uint32_t gb = 0; gb < S.total; gb += kSearchCap) {
         const int total = (int)(min(S.total, gb + kSearchCap) - gb);
@@ -582,29 +598,10 @@ __global__ void __launch_bounds__(kCT, 2) k_search(const double* __restrict__ x,
         for (uint32_t ta = t0 + 2 * warp; ta < t1; ta += 2 * kNW) {
           const bool has_b = ta + 1 < t1;
           const uint32_t tb = has_b ? ta + 1 : ta;  // odd tail: duplicate, identical writes
-          if (lane < 2) {
-            const uint32_t t = lane ? tb : ta;
-            const double ha = h[t], tha = 2.0 * ha;
-            const double lim = __dmul_rn(tha, tha);
-            // fp32 error band: |r2_32 - r2| <= delta lim, delta = 2^-20 (2 + 2 M/h + 2^-20 (M/h)^2)
-            const float2 bd = band32(ha, M);
-            const float lo = bd.x, hi = bd.y;
-            const double px = x[t], py = y[t], pz = z[t];
-            TW[warp][lane].pos[0] = px;
-            TW[warp][lane].pos[1] = py;
-            TW[warp][lane].pos[2] = pz;
-            TW[warp][lane].lim = lim;
-            TW[warp][lane].f[0] = (float)(px - org[0]);
-            TW[warp][lane].f[1] = (float)(py - org[1]);
-            TW[warp][lane].f[2] = (float)(pz - org[2]);
-            TW[warp][lane].f[3] = lo;
-            TW[warp][lane].f[4] = hi;
-          }
-          __syncwarp();
-          const float ax0 = TW[warp][0].f[0], ay0 = TW[warp][0].f[1], az0 = TW[warp][0].f[2];
-          const float lo0 = TW[warp][0].f[3], hi0 = TW[warp][0].f[4];
-          const float ax1 = TW[warp][1].f[0], ay1 = TW[warp][1].f[1], az1 = TW[warp][1].f[2];
-          const float lo1 = TW[warp][1].f[3], hi1 = TW[warp][1].f[4];
+          const TgtW& TA = TW[ta - t0];
+          const TgtW& TB = TW[tb - t0];
+          const float ax0 = TA.f[0], ay0 = TA.f[1], az0 = TA.f[2], lo0 = TA.f[3], hi0 = TA.f[4];
+          const float ax1 = TB.f[0], ay1 = TB.f[1], az1 = TB.f[2], lo1 = TB.f[3], hi1 = TB.f[4];
           const uint32_t self0 = ((uint32_t)S.kself << kLocalBits) | (ta - S.sc);
           const uint32_t self1 = ((uint32_t)S.kself << kLocalBits) | (tb - S.sc);
           uint32_t cnt0 = tcount[ta - t0], cnt1 = tcount[tb - t0];
@@ -642,8 +639,8 @@ __global__ void __launch_bounds__(kCT, 2) k_search(const double* __restrict__ x,
                   limb = __dmul_rn(thb, thb);
                 }
               }
-              if (amb0) hit0 = exact_hit(g, x, y, z, j, ta, TW[warp][0].pos, fmax(TW[warp][0].lim, limb));
-              if (amb1) hit1 = exact_hit(g, x, y, z, j, tb, TW[warp][1].pos, fmax(TW[warp][1].lim, limb));
+              if (amb0) hit0 = exact_hit(g, x, y, z, j, ta, TA.pos, fmax(TA.lim, limb));
+              if (amb1) hit1 = exact_hit(g, x, y, z, j, tb, TB.pos, fmax(TB.lim, limb));
             }
           };
           // Tiles either target can reach.  Box distance in the prefilter's own fp32
