@@ -24,6 +24,7 @@ constexpr int kCT = 256;          // threads per CTA
 constexpr int kNW = kCT / 32;     // warps per CTA
 constexpr int kTgt = 128;         // targets per sub-block (per-target state in smem)
 constexpr int kSlots = kKMax;     // slot tables: every stencil the grid chooser admits
+constexpr int kCellChunk = 4;     // consecutive cells per claim (L2 reuse of shared stencils)
 constexpr int kSearchCap = 3072;  // staged candidates per group (float4)
 constexpr int kSearchTiles = kSearchCap / 32 + 1;          // + the sentinel tile
 constexpr int kSearchWords = (kSearchCap / 32 + 31) / 32;  // tile bitmask words
@@ -497,7 +498,7 @@ __global__ void __launch_bounds__(kCT, 2) k_search(const double* __restrict__ x,
                                                 const uint32_t* __restrict__ cend,
                                                 const unsigned long long* __restrict__ chmax,
                                                 const uint32_t* __restrict__ clist,
-                                                const uint32_t* __restrict__ nclist,
+                                                const uint32_t* __restrict__ nclist, uint32_t* __restrict__ work,
                                                 uint32_t* __restrict__ nbr,
                                                 uint32_t* __restrict__ ncount, int maxn,
                                                 unsigned int* __restrict__ maxcount) {
@@ -510,224 +511,235 @@ __global__ void __launch_bounds__(kCT, 2) k_search(const double* __restrict__ x,
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const unsigned lt = (1u << lane) - 1u;
   const uint32_t ncl = *nclist;
-  for (uint32_t ci = blockIdx.x; ci < ncl; ci += gridDim.x) {
-    cell_setup(g, clist[ci], cstart, cend, chmax, S);
-    const Stencil st = S.st;
-    double org[3], M = 0.0;
-#pragma unroll
-    for (int d = 0; d < 3; ++d) {
-      const double edge = g.inv[d] > 0.0 ? 1.0 / g.inv[d] : 0.0;
-      org[d] = g.lo[d] + S.c3[d] * edge;
-      // bound on |staged coordinate - org| (stencil cells + 1 cell of slack)
-      const double Md = st.wrap[d] == 2
-                            ? g.L[d]
-                            : (double)(max(S.c3[d] - st.lo[d], st.lo[d] + st.cnt[d] - S.c3[d]) + 1) * edge;
-      M = fmax(M, Md);
-    }
-    for (uint32_t t0 = S.sc; t0 < S.ec; t0 += kTgt) {
-      const uint32_t t1 = min(S.ec, t0 + kTgt);
-      for (uint32_t t = t0 + threadIdx.x; t < t1; t += blockDim.x) {
-        tcount[t - t0] = 0;
-        const double ha = h[t], tha = 2.0 * ha;
-        // fp32 error band: |r2_32 - r2| <= delta lim, delta = 2^-20 (2 + 2 M/h + 2^-20 (M/h)^2)
-        const float2 bd = band32(ha, M);
-        const double px = x[t], py = y[t], pz = z[t];
-        TgtW& w = TW[t - t0];
-        w.pos[0] = px;
-        w.pos[1] = py;
-        w.pos[2] = pz;
-        w.lim = __dmul_rn(tha, tha);
-        w.f[0] = (float)(px - org[0]);
-        w.f[1] = (float)(py - org[1]);
-        w.f[2] = (float)(pz - org[2]);
-        w.f[3] = bd.x;
-        w.f[4] = bd.y;
+  __shared__ uint32_t s_chunk;
+  // cells in chunks of kCellChunk consecutive (Morton-order) cells claimed from a
+  // counter: consecutive cells share most of their stencil, so a CTA's next staging
+  // finds its sources in L2 (a grid stride left the re-reads to HBM)
+  for (;;) {
+    if (threadIdx.x == 0) s_chunk = atomicAdd(work, (uint32_t)kCellChunk);
+    __syncthreads();
+    const uint32_t cfirst = s_chunk;
+    __syncthreads();
+    if (cfirst >= ncl) break;
+    for (uint32_t ci = cfirst; ci < min(ncl, cfirst + (uint32_t)kCellChunk); ++ci) {
+      cell_setup(g, clist[ci], cstart, cend, chmax, S);
+      const Stencil st = S.st;
+      double org[3], M = 0.0;
+  #pragma unroll
+      for (int d = 0; d < 3; ++d) {
+        const double edge = g.inv[d] > 0.0 ? 1.0 / g.inv[d] : 0.0;
+        org[d] = g.lo[d] + S.c3[d] * edge;
+        // bound on |staged coordinate - org| (stencil cells + 1 cell of slack)
+        const double Md = st.wrap[d] == 2
+                              ? g.L[d]
+                              : (double)(max(S.c3[d] - st.lo[d], st.lo[d] + st.cnt[d] - S.c3[d]) + 1) * edge;
+        M = fmax(M, Md);
       }
-      __syncthreads();
-      for (uint32_t gb = 0; gb < S.total; gb += kSearchCap) {
-        const int total = (int)(min(S.total, gb + kSearchCap) - gb);
-        for (int q = threadIdx.x; q < total; q += blockDim.x) {  // flat staging, all threads
-          const uint32_t f = gb + q;
-          const int slot = slot_of(S, f);
-          const uint32_t l = f - S.cum[slot], j = S.t_start[slot] + l;
-          double sh[3];
-          shifts_of(g, S, slot, sh);
-          float4 v;
-          v.x = (float)((x[j] + sh[0]) - org[0]);
-          v.y = (float)((y[j] + sh[1]) - org[1]);
-          v.z = (float)((z[j] + sh[2]) - org[2]);
-          v.w = __uint_as_float(((uint32_t)slot << kLocalBits) | l);
-          cand[q] = v;
-          if constexpr (SYM) candb[q] = band32(h[j], M);
-        }
-        // pad to whole tiles with far-away sentinels (never hit, never ambiguous), plus
-        // one all-sentinel tile (index ntile) that partners an odd last tile
-        const int ntile = (total + 31) >> 5;
-        for (int q = total + threadIdx.x; q < 32 * ntile + 32; q += blockDim.x) {
-          cand[q] = make_float4(INFINITY, INFINITY, INFINITY, __uint_as_float(kSent));
-          if constexpr (SYM) candb[q] = make_float2(-1.0f, -1.0f);
+      for (uint32_t t0 = S.sc; t0 < S.ec; t0 += kTgt) {
+        const uint32_t t1 = min(S.ec, t0 + kTgt);
+        for (uint32_t t = t0 + threadIdx.x; t < t1; t += blockDim.x) {
+          tcount[t - t0] = 0;
+          const double ha = h[t], tha = 2.0 * ha;
+          // fp32 error band: |r2_32 - r2| <= delta lim, delta = 2^-20 (2 + 2 M/h + 2^-20 (M/h)^2)
+          const float2 bd = band32(ha, M);
+          const double px = x[t], py = y[t], pz = z[t];
+          TgtW& w = TW[t - t0];
+          w.pos[0] = px;
+          w.pos[1] = py;
+          w.pos[2] = pz;
+          w.lim = __dmul_rn(tha, tha);
+          w.f[0] = (float)(px - org[0]);
+          w.f[1] = (float)(py - org[1]);
+          w.f[2] = (float)(pz - org[2]);
+          w.f[3] = bd.x;
+          w.f[4] = bd.y;
         }
         __syncthreads();
-        // tile bounding boxes (staged candidates are Z-ordered within each cell, so a
-        // tile is a compact block)
-        for (int q = warp; q < ntile; q += kNW) {
-          const float4 v = cand[32 * q + lane];
-          const bool ok = __float_as_uint(v.w) != kSent;
-          float lx = ok ? v.x : INFINITY, ly = ok ? v.y : INFINITY, lz = ok ? v.z : INFINITY;
-          float hx = ok ? v.x : -INFINITY, hy = ok ? v.y : -INFINITY, hz = ok ? v.z : -INFINITY;
-          float hb = -1.0f;  // SYM: largest candidate band of the tile
-          if constexpr (SYM) hb = ok ? candb[32 * q + lane].y : -1.0f;
-#pragma unroll
-          for (int o = 16; o; o >>= 1) {
-            if constexpr (SYM) hb = fmaxf(hb, __shfl_xor_sync(0xffffffffu, hb, o));
-            lx = fminf(lx, __shfl_xor_sync(0xffffffffu, lx, o));
-            ly = fminf(ly, __shfl_xor_sync(0xffffffffu, ly, o));
-            lz = fminf(lz, __shfl_xor_sync(0xffffffffu, lz, o));
-            hx = fmaxf(hx, __shfl_xor_sync(0xffffffffu, hx, o));
-            hy = fmaxf(hy, __shfl_xor_sync(0xffffffffu, hy, o));
-            hz = fmaxf(hz, __shfl_xor_sync(0xffffffffu, hz, o));
+        for (uint32_t gb = 0; gb < S.total; gb += kSearchCap) {
+          const int total = (int)(min(S.total, gb + kSearchCap) - gb);
+          for (int q = threadIdx.x; q < total; q += blockDim.x) {  // flat staging, all threads
+            const uint32_t f = gb + q;
+            const int slot = slot_of(S, f);
+            const uint32_t l = f - S.cum[slot], j = S.t_start[slot] + l;
+            double sh[3];
+            shifts_of(g, S, slot, sh);
+            float4 v;
+            v.x = (float)((x[j] + sh[0]) - org[0]);
+            v.y = (float)((y[j] + sh[1]) - org[1]);
+            v.z = (float)((z[j] + sh[2]) - org[2]);
+            v.w = __uint_as_float(((uint32_t)slot << kLocalBits) | l);
+            cand[q] = v;
+            if constexpr (SYM) candb[q] = band32(h[j], M);
           }
-          if (lane == 0) {
-            tlo[q] = make_float4(lx, ly, lz, 0.f);
-            thi[q] = make_float4(hx, hy, hz, hb);
+          // pad to whole tiles with far-away sentinels (never hit, never ambiguous), plus
+          // one all-sentinel tile (index ntile) that partners an odd last tile
+          const int ntile = (total + 31) >> 5;
+          for (int q = total + threadIdx.x; q < 32 * ntile + 32; q += blockDim.x) {
+            cand[q] = make_float4(INFINITY, INFINITY, INFINITY, __uint_as_float(kSent));
+            if constexpr (SYM) candb[q] = make_float2(-1.0f, -1.0f);
           }
-        }
-        __syncthreads();
-        // two targets per warp share every staged-candidate load (fp32 test data in
-        // registers; the fp64 data of the rare exact test in shared memory)
-        for (uint32_t ta = t0 + 2 * warp; ta < t1; ta += 2 * kNW) {
-          const bool has_b = ta + 1 < t1;
-          const uint32_t tb = has_b ? ta + 1 : ta;  // odd tail: duplicate, identical writes
-          const TgtW& TA = TW[ta - t0];
-          const TgtW& TB = TW[tb - t0];
-          const float ax0 = TA.f[0], ay0 = TA.f[1], az0 = TA.f[2], lo0 = TA.f[3], hi0 = TA.f[4];
-          const float ax1 = TB.f[0], ay1 = TB.f[1], az1 = TB.f[2], lo1 = TB.f[3], hi1 = TB.f[4];
-          const uint32_t self0 = ((uint32_t)S.kself << kLocalBits) | (ta - S.sc);
-          const uint32_t self1 = ((uint32_t)S.kself << kLocalBits) | (tb - S.sc);
-          uint32_t cnt0 = tcount[ta - t0], cnt1 = tcount[tb - t0];
-          uint32_t* row0 = nbr + (size_t)ta * maxn;
-          uint32_t* row1 = nbr + (size_t)tb * maxn;
-          // keep the row bases in registers (else ptxas re-derives nbr + t*maxn + p in 64-bit per store)
-          asm volatile("" : "+l"(row0), "+l"(row1));
-          // one staged candidate against both targets: fp32 band test, exact fp64 when inside it
-          auto test = [&](const float4 cd, const float2 cb, bool& hit0, bool& hit1) {
-            const uint32_t pk = __float_as_uint(cd.w);
-            float dx0 = cd.x - ax0, dy0 = cd.y - ay0, dz0 = cd.z - az0;
-            float dx1 = cd.x - ax1, dy1 = cd.y - ay1, dz1 = cd.z - az1;
-            if constexpr (W2) {
-              wrap32(st, g, dx0, dy0, dz0);
-              wrap32(st, g, dx1, dy1, dz1);
+          __syncthreads();
+          // tile bounding boxes (staged candidates are Z-ordered within each cell, so a
+          // tile is a compact block)
+          for (int q = warp; q < ntile; q += kNW) {
+            const float4 v = cand[32 * q + lane];
+            const bool ok = __float_as_uint(v.w) != kSent;
+            float lx = ok ? v.x : INFINITY, ly = ok ? v.y : INFINITY, lz = ok ? v.z : INFINITY;
+            float hx = ok ? v.x : -INFINITY, hy = ok ? v.y : -INFINITY, hz = ok ? v.z : -INFINITY;
+            float hb = -1.0f;  // SYM: largest candidate band of the tile
+            if constexpr (SYM) hb = ok ? candb[32 * q + lane].y : -1.0f;
+  #pragma unroll
+            for (int o = 16; o; o >>= 1) {
+              if constexpr (SYM) hb = fmaxf(hb, __shfl_xor_sync(0xffffffffu, hb, o));
+              lx = fminf(lx, __shfl_xor_sync(0xffffffffu, lx, o));
+              ly = fminf(ly, __shfl_xor_sync(0xffffffffu, ly, o));
+              lz = fminf(lz, __shfl_xor_sync(0xffffffffu, lz, o));
+              hx = fmaxf(hx, __shfl_xor_sync(0xffffffffu, hx, o));
+              hy = fmaxf(hy, __shfl_xor_sync(0xffffffffu, hy, o));
+              hz = fmaxf(hz, __shfl_xor_sync(0xffffffffu, hz, o));
             }
-            const float r0 = fmaf(dz0, dz0, fmaf(dy0, dy0, dx0 * dx0));
-            const float r1 = fmaf(dz1, dz1, fmaf(dy1, dy1, dx1 * dx1));
-            bool in0 = r0 < lo0, in1 = r1 < lo1;
-            bool amb0 = (r0 >= lo0) & (r0 < hi0), amb1 = (r1 >= lo1) & (r1 < hi1);
-            if constexpr (SYM) {  // either side's support
-              in0 |= r0 < cb.x;
-              in1 |= r1 < cb.x;
-              amb0 = !in0 & (amb0 | (r0 < cb.y));
-              amb1 = !in1 & (amb1 | (r1 < cb.y));
+            if (lane == 0) {
+              tlo[q] = make_float4(lx, ly, lz, 0.f);
+              thi[q] = make_float4(hx, hy, hz, hb);
             }
-            hit0 = in0 & (pk != self0);
-            hit1 = in1 & (pk != self1);
-            if (__ballot_sync(0xffffffffu, amb0 | amb1)) {  // rare: exact fp64 test
-              const uint32_t j = S.t_start[pk >> kLocalBits] + (pk & kLocalMask);
-              double limb = 0.0;
-              if constexpr (SYM) {
-                if (amb0 | amb1) {
-                  const double thb = 2.0 * h[j];
-                  limb = __dmul_rn(thb, thb);
+          }
+          __syncthreads();
+          // two targets per warp share every staged-candidate load (fp32 test data in
+          // registers; the fp64 data of the rare exact test in shared memory)
+          for (uint32_t ta = t0 + 2 * warp; ta < t1; ta += 2 * kNW) {
+            const bool has_b = ta + 1 < t1;
+            const uint32_t tb = has_b ? ta + 1 : ta;  // odd tail: duplicate, identical writes
+            const TgtW& TA = TW[ta - t0];
+            const TgtW& TB = TW[tb - t0];
+            const float ax0 = TA.f[0], ay0 = TA.f[1], az0 = TA.f[2], lo0 = TA.f[3], hi0 = TA.f[4];
+            const float ax1 = TB.f[0], ay1 = TB.f[1], az1 = TB.f[2], lo1 = TB.f[3], hi1 = TB.f[4];
+            const uint32_t self0 = ((uint32_t)S.kself << kLocalBits) | (ta - S.sc);
+            const uint32_t self1 = ((uint32_t)S.kself << kLocalBits) | (tb - S.sc);
+            uint32_t cnt0 = tcount[ta - t0], cnt1 = tcount[tb - t0];
+            uint32_t* row0 = nbr + (size_t)ta * maxn;
+            uint32_t* row1 = nbr + (size_t)tb * maxn;
+            // keep the row bases in registers (else ptxas re-derives nbr + t*maxn + p in 64-bit per store)
+            asm volatile("" : "+l"(row0), "+l"(row1));
+            // one staged candidate against both targets: fp32 band test, exact fp64 when inside it
+            auto test = [&](const float4 cd, const float2 cb, bool& hit0, bool& hit1) {
+              const uint32_t pk = __float_as_uint(cd.w);
+              float dx0 = cd.x - ax0, dy0 = cd.y - ay0, dz0 = cd.z - az0;
+              float dx1 = cd.x - ax1, dy1 = cd.y - ay1, dz1 = cd.z - az1;
+              if constexpr (W2) {
+                wrap32(st, g, dx0, dy0, dz0);
+                wrap32(st, g, dx1, dy1, dz1);
+              }
+              const float r0 = fmaf(dz0, dz0, fmaf(dy0, dy0, dx0 * dx0));
+              const float r1 = fmaf(dz1, dz1, fmaf(dy1, dy1, dx1 * dx1));
+              bool in0 = r0 < lo0, in1 = r1 < lo1;
+              bool amb0 = (r0 >= lo0) & (r0 < hi0), amb1 = (r1 >= lo1) & (r1 < hi1);
+              if constexpr (SYM) {  // either side's support
+                in0 |= r0 < cb.x;
+                in1 |= r1 < cb.x;
+                amb0 = !in0 & (amb0 | (r0 < cb.y));
+                amb1 = !in1 & (amb1 | (r1 < cb.y));
+              }
+              hit0 = in0 & (pk != self0);
+              hit1 = in1 & (pk != self1);
+              if (__ballot_sync(0xffffffffu, amb0 | amb1)) {  // rare: exact fp64 test
+                const uint32_t j = S.t_start[pk >> kLocalBits] + (pk & kLocalMask);
+                double limb = 0.0;
+                if constexpr (SYM) {
+                  if (amb0 | amb1) {
+                    const double thb = 2.0 * h[j];
+                    limb = __dmul_rn(thb, thb);
+                  }
+                }
+                if (amb0) hit0 = exact_hit(g, x, y, z, j, ta, TA.pos, fmax(TA.lim, limb));
+                if (amb1) hit1 = exact_hit(g, x, y, z, j, tb, TB.pos, fmax(TB.lim, limb));
+              }
+            };
+            // Tiles either target can reach.  Box distance in the prefilter's own fp32
+            // expression: rounding is monotone, so box d2 <= r2_32 of every member, and
+            // box d2 >= hi excludes hits and ambiguous candidates alike (lists stay exact).
+            uint32_t need[kSearchWords];
+  #pragma unroll
+            for (int w = 0; w < kSearchWords; ++w) {
+              const int q = 32 * w + lane;
+              bool nd = false;
+              if (q < ntile) {
+                if constexpr (W2) {
+                  nd = true;
+                } else {
+                  const float4 L = tlo[q], H = thi[q];
+                  const float bx0 = fmaxf(fmaxf(L.x - ax0, ax0 - H.x), 0.f);
+                  const float by0 = fmaxf(fmaxf(L.y - ay0, ay0 - H.y), 0.f);
+                  const float bz0 = fmaxf(fmaxf(L.z - az0, az0 - H.z), 0.f);
+                  const float bx1 = fmaxf(fmaxf(L.x - ax1, ax1 - H.x), 0.f);
+                  const float by1 = fmaxf(fmaxf(L.y - ay1, ay1 - H.y), 0.f);
+                  const float bz1 = fmaxf(fmaxf(L.z - az1, az1 - H.z), 0.f);
+                  const float hb = SYM ? H.w : -1.0f;
+                  nd = (fmaf(bz0, bz0, fmaf(by0, by0, bx0 * bx0)) < fmaxf(hi0, hb)) |
+                       (fmaf(bz1, bz1, fmaf(by1, by1, bx1 * bx1)) < fmaxf(hi1, hb));
                 }
               }
-              if (amb0) hit0 = exact_hit(g, x, y, z, j, ta, TA.pos, fmax(TA.lim, limb));
-              if (amb1) hit1 = exact_hit(g, x, y, z, j, tb, TB.pos, fmax(TB.lim, limb));
+              need[w] = __ballot_sync(0xffffffffu, nd);
             }
-          };
-          // Tiles either target can reach.  Box distance in the prefilter's own fp32
-          // expression: rounding is monotone, so box d2 <= r2_32 of every member, and
-          // box d2 >= hi excludes hits and ambiguous candidates alike (lists stay exact).
-          uint32_t need[kSearchWords];
-#pragma unroll
-          for (int w = 0; w < kSearchWords; ++w) {
-            const int q = 32 * w + lane;
-            bool nd = false;
-            if (q < ntile) {
-              if constexpr (W2) {
-                nd = true;
+            static_assert(kSearchWords == 3, "tile mask held in three registers");
+            uint32_t n0 = need[0], n1 = need[1], n2 = need[2];
+            auto next_tile = [&]() -> int {  // lowest remaining needed tile (ascending: rows stay sorted)
+              int q;
+              if (n0) {
+                q = __ffs(n0) - 1;
+                n0 &= n0 - 1;
+              } else if (n1) {
+                q = 31 + __ffs(n1);
+                n1 &= n1 - 1;
+              } else if (n2) {
+                q = 63 + __ffs(n2);
+                n2 &= n2 - 1;
               } else {
-                const float4 L = tlo[q], H = thi[q];
-                const float bx0 = fmaxf(fmaxf(L.x - ax0, ax0 - H.x), 0.f);
-                const float by0 = fmaxf(fmaxf(L.y - ay0, ay0 - H.y), 0.f);
-                const float bz0 = fmaxf(fmaxf(L.z - az0, az0 - H.z), 0.f);
-                const float bx1 = fmaxf(fmaxf(L.x - ax1, ax1 - H.x), 0.f);
-                const float by1 = fmaxf(fmaxf(L.y - ay1, ay1 - H.y), 0.f);
-                const float bz1 = fmaxf(fmaxf(L.z - az1, az1 - H.z), 0.f);
-                const float hb = SYM ? H.w : -1.0f;
-                nd = (fmaf(bz0, bz0, fmaf(by0, by0, bx0 * bx0)) < fmaxf(hi0, hb)) |
-                     (fmaf(bz1, bz1, fmaf(by1, by1, bx1 * bx1)) < fmaxf(hi1, hb));
+                q = ntile;  // the sentinel tile
               }
+              return q;
+            };
+            // two tiles per iteration: four independent test chains in flight
+            for (;;) {
+              const int qA = next_tile();
+              if (qA == ntile) break;
+              const int qB = next_tile();
+              const float4 cA = cand[32 * qA + lane], cB = cand[32 * qB + lane];
+              float2 bA = make_float2(-1.0f, -1.0f), bB = bA;
+              if constexpr (SYM) {
+                bA = candb[32 * qA + lane];
+                bB = candb[32 * qB + lane];
+              }
+              bool hA0, hA1, hB0, hB1;
+              test(cA, bA, hA0, hA1);
+              test(cB, bB, hB0, hB1);
+              const unsigned bA0 = __ballot_sync(0xffffffffu, hA0), bA1 = __ballot_sync(0xffffffffu, hA1);
+              const unsigned bB0 = __ballot_sync(0xffffffffu, hB0), bB1 = __ballot_sync(0xffffffffu, hB1);
+              const uint32_t pA0 = cnt0 + __popc(bA0 & lt), pA1 = cnt1 + __popc(bA1 & lt);
+              const uint32_t pB0 = cnt0 + __popc(bA0) + __popc(bB0 & lt);
+              const uint32_t pB1 = cnt1 + __popc(bA1) + __popc(bB1 & lt);
+              if (hA0 & (pA0 < (uint32_t)maxn)) row0[pA0] = __float_as_uint(cA.w);
+              if (hA1 & (pA1 < (uint32_t)maxn)) row1[pA1] = __float_as_uint(cA.w);
+              if (hB0 & (pB0 < (uint32_t)maxn)) row0[pB0] = __float_as_uint(cB.w);
+              if (hB1 & (pB1 < (uint32_t)maxn)) row1[pB1] = __float_as_uint(cB.w);
+              cnt0 += __popc(bA0) + __popc(bB0);
+              cnt1 += __popc(bA1) + __popc(bB1);
             }
-            need[w] = __ballot_sync(0xffffffffu, nd);
-          }
-          static_assert(kSearchWords == 3, "tile mask held in three registers");
-          uint32_t n0 = need[0], n1 = need[1], n2 = need[2];
-          auto next_tile = [&]() -> int {  // lowest remaining needed tile (ascending: rows stay sorted)
-            int q;
-            if (n0) {
-              q = __ffs(n0) - 1;
-              n0 &= n0 - 1;
-            } else if (n1) {
-              q = 31 + __ffs(n1);
-              n1 &= n1 - 1;
-            } else if (n2) {
-              q = 63 + __ffs(n2);
-              n2 &= n2 - 1;
-            } else {
-              q = ntile;  // the sentinel tile
+            if (lane == 0) {
+              tcount[ta - t0] = cnt0;
+              if (has_b) tcount[tb - t0] = cnt1;
             }
-            return q;
-          };
-          // two tiles per iteration: four independent test chains in flight
-          for (;;) {
-            const int qA = next_tile();
-            if (qA == ntile) break;
-            const int qB = next_tile();
-            const float4 cA = cand[32 * qA + lane], cB = cand[32 * qB + lane];
-            float2 bA = make_float2(-1.0f, -1.0f), bB = bA;
-            if constexpr (SYM) {
-              bA = candb[32 * qA + lane];
-              bB = candb[32 * qB + lane];
-            }
-            bool hA0, hA1, hB0, hB1;
-            test(cA, bA, hA0, hA1);
-            test(cB, bB, hB0, hB1);
-            const unsigned bA0 = __ballot_sync(0xffffffffu, hA0), bA1 = __ballot_sync(0xffffffffu, hA1);
-            const unsigned bB0 = __ballot_sync(0xffffffffu, hB0), bB1 = __ballot_sync(0xffffffffu, hB1);
-            const uint32_t pA0 = cnt0 + __popc(bA0 & lt), pA1 = cnt1 + __popc(bA1 & lt);
-            const uint32_t pB0 = cnt0 + __popc(bA0) + __popc(bB0 & lt);
-            const uint32_t pB1 = cnt1 + __popc(bA1) + __popc(bB1 & lt);
-            if (hA0 & (pA0 < (uint32_t)maxn)) row0[pA0] = __float_as_uint(cA.w);
-            if (hA1 & (pA1 < (uint32_t)maxn)) row1[pA1] = __float_as_uint(cA.w);
-            if (hB0 & (pB0 < (uint32_t)maxn)) row0[pB0] = __float_as_uint(cB.w);
-            if (hB1 & (pB1 < (uint32_t)maxn)) row1[pB1] = __float_as_uint(cB.w);
-            cnt0 += __popc(bA0) + __popc(bB0);
-            cnt1 += __popc(bA1) + __popc(bB1);
+            __syncwarp();
           }
-          if (lane == 0) {
-            tcount[ta - t0] = cnt0;
-            if (has_b) tcount[tb - t0] = cnt1;
-          }
-          __syncwarp();
+          __syncthreads();
+        }
+        for (uint32_t t = t0 + threadIdx.x; t < t1; t += blockDim.x) {
+          const uint32_t cn = tcount[t - t0];
+          ncount[t] = cn;
+          if (cn > (uint32_t)maxn) atomicMax(maxcount, cn);
         }
         __syncthreads();
       }
-      for (uint32_t t = t0 + threadIdx.x; t < t1; t += blockDim.x) {
-        const uint32_t cn = tcount[t - t0];
-        ncount[t] = cn;
-        if (cn > (uint32_t)maxn) atomicMax(maxcount, cn);
       }
-      __syncthreads();
-    }
   }
 }
 
@@ -783,7 +795,7 @@ __global__ void __launch_bounds__(kCTD, 2) k_density_c(
     const double* __restrict__ h, const double* __restrict__ m, const double* __restrict__ u,
     Grid g, const uint32_t* __restrict__ cstart, const uint32_t* __restrict__ cend,
     const unsigned long long* __restrict__ chmax, const uint32_t* __restrict__ clist,
-    const uint32_t* __restrict__ nclist, const uint32_t* __restrict__ nbr,
+    const uint32_t* __restrict__ nclist, uint32_t* __restrict__ work, const uint32_t* __restrict__ nbr,
     const uint32_t* __restrict__ ncount, int maxn, Phys ph, double* __restrict__ rho,
     double* __restrict__ omega, double* __restrict__ p, double* __restrict__ cs,
     double* __restrict__ wB, double* __restrict__ ih2, double* __restrict__ vol,
@@ -797,110 +809,121 @@ __global__ void __launch_bounds__(kCTD, 2) k_density_c(
   __shared__ double tx[kTgt], ty[kTgt], tz[kTgt], tih2[kTgt], acc0[kTgt], acc1[kTgt];
   const int lane = threadIdx.x & 31;
   const uint32_t ncl = *nclist;
+  __shared__ uint32_t s_chunk;
   const int n = N > 0 ? N : ph.n;
-  for (uint32_t ci = blockIdx.x; ci < ncl; ci += gridDim.x) {
-    cell_setup(g, clist[ci], cstart, cend, chmax, S);
-    const Stencil st = S.st;
-    for (uint32_t t0 = S.sc; t0 < S.ec; t0 += kTgt) {
-      const uint32_t t1 = min(S.ec, t0 + kTgt);
-      for (uint32_t t = t0 + threadIdx.x; t < t1; t += blockDim.x) {
-        const uint32_t i = t - t0;
-        s_n[i] = ncount[t];
-        s_cur[i] = 0;
-        tx[i] = x[t];
-        ty[i] = y[t];
-        tz[i] = z[t];
-        const double ih = 1.0 / h[t];
-        tih2[i] = ih * ih;
-        acc0[i] = 0.0;
-        acc1[i] = 0.0;
-      }
-      if (threadIdx.x == 0) S.next[0] = 0;
-      __syncthreads();
-      for (uint32_t gb = 0, gi = 0; gb < S.total; gb += kDensCap, ++gi) {
-        const uint32_t ge = min(S.total, gb + kDensCap), pend = pend_of(S, ge);
-        if (threadIdx.x == 0) S.next[(gi + 1) & 1] = 0;
-        stage2x2(g, S, gb, ge, x, y, z, m, s01, s23);
+  // cells in chunks of kCellChunk consecutive (Morton-order) cells claimed from a
+  // counter: consecutive cells share most of their stencil, so a CTA's next staging
+  // finds its sources in L2 (a grid stride left the re-reads to HBM)
+  for (;;) {
+    if (threadIdx.x == 0) s_chunk = atomicAdd(work, (uint32_t)kCellChunk);
+    __syncthreads();
+    const uint32_t cfirst = s_chunk;
+    __syncthreads();
+    if (cfirst >= ncl) break;
+    for (uint32_t ci = cfirst; ci < min(ncl, cfirst + (uint32_t)kCellChunk); ++ci) {
+      cell_setup(g, clist[ci], cstart, cend, chmax, S);
+      const Stencil st = S.st;
+      for (uint32_t t0 = S.sc; t0 < S.ec; t0 += kTgt) {
+        const uint32_t t1 = min(S.ec, t0 + kTgt);
+        for (uint32_t t = t0 + threadIdx.x; t < t1; t += blockDim.x) {
+          const uint32_t i = t - t0;
+          s_n[i] = ncount[t];
+          s_cur[i] = 0;
+          tx[i] = x[t];
+          ty[i] = y[t];
+          tz[i] = z[t];
+          const double ih = 1.0 / h[t];
+          tih2[i] = ih * ih;
+          acc0[i] = 0.0;
+          acc1[i] = 0.0;
+        }
+        if (threadIdx.x == 0) S.next[0] = 0;
         __syncthreads();
-        struct B : DensBody {
-          int n, K, sym;
-          const double* tab;
-          // ok == false: padding lane of the walk; its terms are discarded by selects
-          // (not multiplied by 0: a far padding pair may overflow the polynomial)
-          __device__ __forceinline__ void operator()(int q, bool ok) {
-            const double2 p01 = s01[q], p23 = s23[q];
-            double dx = p01.x - xa, dy = p01.y - ya, dz = p23.x - za;
-            delta3<W2>(*st, *g, dx, dy, dz);
-            const double tt = (dx * dx + dy * dy + dz * dz) * ih2a;
-            if (sym) ok = ok && tt < 4.0;  // symmetric extra pair: W(r, h_a) = 0
-            const double P = sinc_poly(tt);
-            const double Pn1 = ipow<N - 1 < 0 ? 0 : N - 1>(P, n - 1);
-            const double dP = sinc_dpoly(tt);
-            const double mj = p23.y;
-            double a, b;
-            if constexpr (KM == SPH_KERNEL_POLY) {
-              a = Pn1 * P;
-              b = Pn1 * (3.0 * P + (2.0 * n) * tt * dP);  // 3 S + v S'(v)
-            } else {  // S from the selected mode; v S'(v) from the exact polynomial (R12)
-              const double S_ = kern_S<KM, N, false>(tt, n, tab, K);
-              a = S_;
-              b = fma(3.0, S_, Pn1 * (2.0 * n) * tt * dP);
+        for (uint32_t gb = 0, gi = 0; gb < S.total; gb += kDensCap, ++gi) {
+          const uint32_t ge = min(S.total, gb + kDensCap), pend = pend_of(S, ge);
+          if (threadIdx.x == 0) S.next[(gi + 1) & 1] = 0;
+          stage2x2(g, S, gb, ge, x, y, z, m, s01, s23);
+          __syncthreads();
+          struct B : DensBody {
+            int n, K, sym;
+            const double* tab;
+            // ok == false: padding lane of the walk; its terms are discarded by selects
+            // (not multiplied by 0: a far padding pair may overflow the polynomial)
+            __device__ __forceinline__ void operator()(int q, bool ok) {
+              const double2 p01 = s01[q], p23 = s23[q];
+              double dx = p01.x - xa, dy = p01.y - ya, dz = p23.x - za;
+              delta3<W2>(*st, *g, dx, dy, dz);
+              const double tt = (dx * dx + dy * dy + dz * dz) * ih2a;
+              if (sym) ok = ok && tt < 4.0;  // symmetric extra pair: W(r, h_a) = 0
+              const double P = sinc_poly(tt);
+              const double Pn1 = ipow<N - 1 < 0 ? 0 : N - 1>(P, n - 1);
+              const double dP = sinc_dpoly(tt);
+              const double mj = p23.y;
+              double a, b;
+              if constexpr (KM == SPH_KERNEL_POLY) {
+                a = Pn1 * P;
+                b = Pn1 * (3.0 * P + (2.0 * n) * tt * dP);  // 3 S + v S'(v)
+              } else {  // S from the selected mode; v S'(v) from the exact polynomial (R12)
+                const double S_ = kern_S<KM, N, false>(tt, n, tab, K);
+                a = S_;
+                b = fma(3.0, S_, Pn1 * (2.0 * n) * tt * dP);
+              }
+              sr = fma(mj, ok ? a : 0.0, sr);
+              sd = fma(mj, ok ? b : 0.0, sd);
             }
-            sr = fma(mj, ok ? a : 0.0, sr);
-            sd = fma(mj, ok ? b : 0.0, sd);
+          } body;
+          body.s01 = s01; body.s23 = s23;
+          body.tx = tx; body.ty = ty; body.tz = tz; body.tih2 = tih2;
+          body.st = &st; body.g = &g; body.n = n; body.K = ph.tableK; body.tab = ph.table;
+          body.sym = ph.sym;
+          walk_targets_fast(t0, t1, nbr, maxn, s_n, s_cur, pend, S.cum, gb, &S.next[gi & 1], body,
+                            [&](uint32_t i, uint32_t c2) {
+                              double v[2] = {body.sr, body.sd};
+                              warp_multi_sum<2>(v);
+                              if (lane == 0) {
+                                s_cur[i] = c2;
+                                acc0[i] += v[0];
+                              }
+                              if (lane == 16) acc1[i] += v[0];
+                            });
+          __syncthreads();
+        }
+        for (uint32_t t = t0 + threadIdx.x; t < t1; t += blockDim.x) {
+          const uint32_t i = t - t0;
+          const double ha = h[t], ma = m[t];
+          const double ih = 1.0 / ha;
+          const double ih2a = ih * ih;
+          const double wBa = ph.B * ih * ih2a;               // B / h^3
+          const double r = wBa * (ma + acc0[i]);             // Eq. 1 incl. self (R11)
+          const double dsum = -wBa * ih * (3.0 * ma + acc1[i]);  // sum m dW/dh
+          double om = ph.omega_mode ? 1.0 : 1.0 + ha / (3.0 * r) * dsum;  // R8
+          if (om < 0.1) {
+            om = 0.1;
+            atomicAdd(&cnt[CNT_OMEGA], 1ull);
           }
-        } body;
-        body.s01 = s01; body.s23 = s23;
-        body.tx = tx; body.ty = ty; body.tz = tz; body.tih2 = tih2;
-        body.st = &st; body.g = &g; body.n = n; body.K = ph.tableK; body.tab = ph.table;
-        body.sym = ph.sym;
-        walk_targets_fast(t0, t1, nbr, maxn, s_n, s_cur, pend, S.cum, gb, &S.next[gi & 1], body,
-                          [&](uint32_t i, uint32_t c2) {
-                            double v[2] = {body.sr, body.sd};
-                            warp_multi_sum<2>(v);
-                            if (lane == 0) {
-                              s_cur[i] = c2;
-                              acc0[i] += v[0];
-                            }
-                            if (lane == 16) acc1[i] += v[0];
-                          });
+          double P_, c_;
+          if (ph.eos == SPH_EOS_LINEAR) {
+            P_ = ph.c0 * ph.c0 * (r - ph.rho0);
+            c_ = ph.c0;
+          } else {
+            P_ = (ph.gamma - 1.0) * r * u[t];
+            c_ = sqrt(ph.gamma * P_ / r);
+          }
+          const double Xt = P_ / (om * r * r);  // R1
+          rho[t] = r;
+          omega[t] = om;
+          p[t] = P_;
+          cs[t] = c_;
+          wB[t] = wBa;
+          ih2[t] = ih2a;
+          vol[t] = ma / r;
+          rinv[t] = 1.0 / r;
+          X[t] = Xt;
+          mX[t] = ma * Xt;
+        }
         __syncthreads();
       }
-      for (uint32_t t = t0 + threadIdx.x; t < t1; t += blockDim.x) {
-        const uint32_t i = t - t0;
-        const double ha = h[t], ma = m[t];
-        const double ih = 1.0 / ha;
-        const double ih2a = ih * ih;
-        const double wBa = ph.B * ih * ih2a;               // B / h^3
-        const double r = wBa * (ma + acc0[i]);             // Eq. 1 incl. self (R11)
-        const double dsum = -wBa * ih * (3.0 * ma + acc1[i]);  // sum m dW/dh
-        double om = ph.omega_mode ? 1.0 : 1.0 + ha / (3.0 * r) * dsum;  // R8
-        if (om < 0.1) {
-          om = 0.1;
-          atomicAdd(&cnt[CNT_OMEGA], 1ull);
-        }
-        double P_, c_;
-        if (ph.eos == SPH_EOS_LINEAR) {
-          P_ = ph.c0 * ph.c0 * (r - ph.rho0);
-          c_ = ph.c0;
-        } else {
-          P_ = (ph.gamma - 1.0) * r * u[t];
-          c_ = sqrt(ph.gamma * P_ / r);
-        }
-        const double Xt = P_ / (om * r * r);  // R1
-        rho[t] = r;
-        omega[t] = om;
-        p[t] = P_;
-        cs[t] = c_;
-        wB[t] = wBa;
-        ih2[t] = ih2a;
-        vol[t] = ma / r;
-        rinv[t] = 1.0 / r;
-        X[t] = Xt;
-        mX[t] = ma * Xt;
       }
-      __syncthreads();
-    }
   }
 }
 
@@ -910,7 +933,7 @@ __global__ void __launch_bounds__(kCTD, 2) k_iad_c(
     const double* __restrict__ x, const double* __restrict__ y, const double* __restrict__ z,
     Grid g, const uint32_t* __restrict__ cstart, const uint32_t* __restrict__ cend,
     const unsigned long long* __restrict__ chmax, const uint32_t* __restrict__ clist,
-    const uint32_t* __restrict__ nclist, const uint32_t* __restrict__ nbr,
+    const uint32_t* __restrict__ nclist, uint32_t* __restrict__ work, const uint32_t* __restrict__ nbr,
     const uint32_t* __restrict__ ncount, int maxn, Phys ph, const double* __restrict__ wB,
     const double* __restrict__ ih2, const double* __restrict__ vol, double* __restrict__ c11,
     double* __restrict__ c12, double* __restrict__ c13, double* __restrict__ c22,
@@ -925,106 +948,117 @@ __global__ void __launch_bounds__(kCTD, 2) k_iad_c(
   __shared__ double acc[6][kTgt];
   const int lane = threadIdx.x & 31;
   const uint32_t ncl = *nclist;
+  __shared__ uint32_t s_chunk;
   const int n = N > 0 ? N : ph.n;
-  for (uint32_t ci = blockIdx.x; ci < ncl; ci += gridDim.x) {
-    cell_setup(g, clist[ci], cstart, cend, chmax, S);
-    const Stencil st = S.st;
-    for (uint32_t t0 = S.sc; t0 < S.ec; t0 += kTgt) {
-      const uint32_t t1 = min(S.ec, t0 + kTgt);
-      for (uint32_t t = t0 + threadIdx.x; t < t1; t += blockDim.x) {
-        const uint32_t i = t - t0;
-        s_n[i] = ncount[t];
-        s_cur[i] = 0;
-        tx[i] = x[t];
-        ty[i] = y[t];
-        tz[i] = z[t];
-        tih2[i] = ih2[t];
-        for (int k = 0; k < 6; ++k) acc[k][i] = 0.0;
-      }
-      if (threadIdx.x == 0) S.next[0] = 0;
-      __syncthreads();
-      for (uint32_t gb = 0, gi = 0; gb < S.total; gb += kDensCap, ++gi) {
-        const uint32_t ge = min(S.total, gb + kDensCap), pend = pend_of(S, ge);
-        if (threadIdx.x == 0) S.next[(gi + 1) & 1] = 0;
-        stage2x2(g, S, gb, ge, x, y, z, vol, s01, s23);
-        __syncthreads();
-        struct B {
-          const double2 *s01, *s23;
-          const double *tx, *ty, *tz, *tih2;
-          const Stencil* st;
-          const Grid* g;
-          int n, K, sym;
-          const double* tab;
-          double xa, ya, za, ih2a, t11, t12, t13, t22, t23, t33;
-          __device__ __forceinline__ void begin(uint32_t i) {
-            xa = tx[i];
-            ya = ty[i];
-            za = tz[i];
-            ih2a = tih2[i];
-            t11 = t12 = t13 = t22 = t23 = t33 = 0.0;
-          }
-          __device__ __forceinline__ void operator()(int q, bool ok) {  // ok: see density
-            const double2 p01 = s01[q], p23 = s23[q];
-            double dx = p01.x - xa, dy = p01.y - ya, dz = p23.x - za;
-            delta3<W2>(*st, *g, dx, dy, dz);
-            const double tt = (dx * dx + dy * dy + dz * dz) * ih2a;
-            if (sym) ok = ok && tt < 4.0;  // symmetric extra pair: W(r, h_a) = 0
-            const double S_ = kern_S<KM, N, false>(tt, n, tab, K);
-            const double w = p23.y * (ok ? S_ : 0.0);  // (m_b/rho_b) S
-            const double wx = w * dx, wy = w * dy;
-            t11 = fma(wx, dx, t11);
-            t12 = fma(wx, dy, t12);
-            t13 = fma(wx, dz, t13);
-            t22 = fma(wy, dy, t22);
-            t23 = fma(wy, dz, t23);
-            t33 = fma(w * dz, dz, t33);
-          }
-        } body;
-        body.s01 = s01; body.s23 = s23;
-        body.tx = tx; body.ty = ty; body.tz = tz; body.tih2 = tih2;
-        body.st = &st; body.g = &g; body.n = n; body.K = ph.tableK; body.tab = ph.table;
-        body.sym = ph.sym;
-        walk_targets_fast(t0, t1, nbr, maxn, s_n, s_cur, pend, S.cum, gb, &S.next[gi & 1], body,
-                          [&](uint32_t i, uint32_t c2) {
-                            double v[8] = {body.t11, body.t12, body.t13, body.t22,
-                                           body.t23, body.t33, 0.0, 0.0};
-                            warp_multi_sum<8>(v);
-                            if ((lane & 3) == 0 && lane < 24) acc[lane >> 2][i] += v[0];
-                            if (lane == 0) s_cur[i] = c2;
-                          });
-        __syncthreads();
-      }
-      for (uint32_t t = t0 + threadIdx.x; t < t1; t += blockDim.x) {
-        const uint32_t i = t - t0;
-        const double s = wB[t];
-        const double a11 = acc[0][i] * s, a12 = acc[1][i] * s, a13 = acc[2][i] * s,
-                     a22 = acc[3][i] * s, a23 = acc[4][i] * s, a33 = acc[5][i] * s;
-        const double det = a11 * (a22 * a33 - a23 * a23) - a12 * (a12 * a33 - a23 * a13) +
-                           a13 * (a12 * a23 - a22 * a13);
-        const double id = 1.0 / det;
-        double i11 = (a22 * a33 - a23 * a23) * id;
-        double i12 = (a13 * a23 - a12 * a33) * id;
-        double i13 = (a12 * a23 - a13 * a22) * id;
-        double i22 = (a11 * a33 - a13 * a13) * id;
-        double i23 = (a12 * a13 - a11 * a23) * id;
-        double i33 = (a11 * a22 - a12 * a12) * id;
-        const double nt = sqrt(a11 * a11 + a22 * a22 + a33 * a33 + 2.0 * (a12 * a12 + a13 * a13 + a23 * a23));
-        const double ni = sqrt(i11 * i11 + i22 * i22 + i33 * i33 + 2.0 * (i12 * i12 + i13 * i13 + i23 * i23));
-        if (!(det > 0.0) || !(nt * ni <= 1e12)) {  // reading R29
-          const double tr = a11 + a22 + a33;
-          const double q = tr > 0.0 ? 3.0 / tr : 0.0;
-          i11 = q; i22 = q; i33 = q;
-          i12 = 0.0; i13 = 0.0; i23 = 0.0;
-          atomicAdd(&cnt[CNT_IAD_SINGULAR], 1ull);
+  // cells in chunks of kCellChunk consecutive (Morton-order) cells claimed from a
+  // counter: consecutive cells share most of their stencil, so a CTA's next staging
+  // finds its sources in L2 (a grid stride left the re-reads to HBM)
+  for (;;) {
+    if (threadIdx.x == 0) s_chunk = atomicAdd(work, (uint32_t)kCellChunk);
+    __syncthreads();
+    const uint32_t cfirst = s_chunk;
+    __syncthreads();
+    if (cfirst >= ncl) break;
+    for (uint32_t ci = cfirst; ci < min(ncl, cfirst + (uint32_t)kCellChunk); ++ci) {
+      cell_setup(g, clist[ci], cstart, cend, chmax, S);
+      const Stencil st = S.st;
+      for (uint32_t t0 = S.sc; t0 < S.ec; t0 += kTgt) {
+        const uint32_t t1 = min(S.ec, t0 + kTgt);
+        for (uint32_t t = t0 + threadIdx.x; t < t1; t += blockDim.x) {
+          const uint32_t i = t - t0;
+          s_n[i] = ncount[t];
+          s_cur[i] = 0;
+          tx[i] = x[t];
+          ty[i] = y[t];
+          tz[i] = z[t];
+          tih2[i] = ih2[t];
+          for (int k = 0; k < 6; ++k) acc[k][i] = 0.0;
         }
-        c11[t] = i11; c12[t] = i12; c13[t] = i13;
-        c22[t] = i22; c23[t] = i23; c33[t] = i33;
-        // C~ = (B/h^3) C, staged by the momentum pass (A_ab(h_b) = C~_b Delta S_b)
-        ct[0 * ct_stride + t] = s * i11; ct[1 * ct_stride + t] = s * i12; ct[2 * ct_stride + t] = s * i13;
-        ct[3 * ct_stride + t] = s * i22; ct[4 * ct_stride + t] = s * i23; ct[5 * ct_stride + t] = s * i33;
+        if (threadIdx.x == 0) S.next[0] = 0;
+        __syncthreads();
+        for (uint32_t gb = 0, gi = 0; gb < S.total; gb += kDensCap, ++gi) {
+          const uint32_t ge = min(S.total, gb + kDensCap), pend = pend_of(S, ge);
+          if (threadIdx.x == 0) S.next[(gi + 1) & 1] = 0;
+          stage2x2(g, S, gb, ge, x, y, z, vol, s01, s23);
+          __syncthreads();
+          struct B {
+            const double2 *s01, *s23;
+            const double *tx, *ty, *tz, *tih2;
+            const Stencil* st;
+            const Grid* g;
+            int n, K, sym;
+            const double* tab;
+            double xa, ya, za, ih2a, t11, t12, t13, t22, t23, t33;
+            __device__ __forceinline__ void begin(uint32_t i) {
+              xa = tx[i];
+              ya = ty[i];
+              za = tz[i];
+              ih2a = tih2[i];
+              t11 = t12 = t13 = t22 = t23 = t33 = 0.0;
+            }
+            __device__ __forceinline__ void operator()(int q, bool ok) {  // ok: see density
+              const double2 p01 = s01[q], p23 = s23[q];
+              double dx = p01.x - xa, dy = p01.y - ya, dz = p23.x - za;
+              delta3<W2>(*st, *g, dx, dy, dz);
+              const double tt = (dx * dx + dy * dy + dz * dz) * ih2a;
+              if (sym) ok = ok && tt < 4.0;  // symmetric extra pair: W(r, h_a) = 0
+              const double S_ = kern_S<KM, N, false>(tt, n, tab, K);
+              const double w = p23.y * (ok ? S_ : 0.0);  // (m_b/rho_b) S
+              const double wx = w * dx, wy = w * dy;
+              t11 = fma(wx, dx, t11);
+              t12 = fma(wx, dy, t12);
+              t13 = fma(wx, dz, t13);
+              t22 = fma(wy, dy, t22);
+              t23 = fma(wy, dz, t23);
+              t33 = fma(w * dz, dz, t33);
+            }
+          } body;
+          body.s01 = s01; body.s23 = s23;
+          body.tx = tx; body.ty = ty; body.tz = tz; body.tih2 = tih2;
+          body.st = &st; body.g = &g; body.n = n; body.K = ph.tableK; body.tab = ph.table;
+          body.sym = ph.sym;
+          walk_targets_fast(t0, t1, nbr, maxn, s_n, s_cur, pend, S.cum, gb, &S.next[gi & 1], body,
+                            [&](uint32_t i, uint32_t c2) {
+                              double v[8] = {body.t11, body.t12, body.t13, body.t22,
+                                             body.t23, body.t33, 0.0, 0.0};
+                              warp_multi_sum<8>(v);
+                              if ((lane & 3) == 0 && lane < 24) acc[lane >> 2][i] += v[0];
+                              if (lane == 0) s_cur[i] = c2;
+                            });
+          __syncthreads();
+        }
+        for (uint32_t t = t0 + threadIdx.x; t < t1; t += blockDim.x) {
+          const uint32_t i = t - t0;
+          const double s = wB[t];
+          const double a11 = acc[0][i] * s, a12 = acc[1][i] * s, a13 = acc[2][i] * s,
+                       a22 = acc[3][i] * s, a23 = acc[4][i] * s, a33 = acc[5][i] * s;
+          const double det = a11 * (a22 * a33 - a23 * a23) - a12 * (a12 * a33 - a23 * a13) +
+                             a13 * (a12 * a23 - a22 * a13);
+          const double id = 1.0 / det;
+          double i11 = (a22 * a33 - a23 * a23) * id;
+          double i12 = (a13 * a23 - a12 * a33) * id;
+          double i13 = (a12 * a23 - a13 * a22) * id;
+          double i22 = (a11 * a33 - a13 * a13) * id;
+          double i23 = (a12 * a13 - a11 * a23) * id;
+          double i33 = (a11 * a22 - a12 * a12) * id;
+          const double nt = sqrt(a11 * a11 + a22 * a22 + a33 * a33 + 2.0 * (a12 * a12 + a13 * a13 + a23 * a23));
+          const double ni = sqrt(i11 * i11 + i22 * i22 + i33 * i33 + 2.0 * (i12 * i12 + i13 * i13 + i23 * i23));
+          if (!(det > 0.0) || !(nt * ni <= 1e12)) {  // reading R29
+            const double tr = a11 + a22 + a33;
+            const double q = tr > 0.0 ? 3.0 / tr : 0.0;
+            i11 = q; i22 = q; i33 = q;
+            i12 = 0.0; i13 = 0.0; i23 = 0.0;
+            atomicAdd(&cnt[CNT_IAD_SINGULAR], 1ull);
+          }
+          c11[t] = i11; c12[t] = i12; c13[t] = i13;
+          c22[t] = i22; c23[t] = i23; c33[t] = i33;
+          // C~ = (B/h^3) C, staged by the momentum pass (A_ab(h_b) = C~_b Delta S_b)
+          ct[0 * ct_stride + t] = s * i11; ct[1 * ct_stride + t] = s * i12; ct[2 * ct_stride + t] = s * i13;
+          ct[3 * ct_stride + t] = s * i22; ct[4 * ct_stride + t] = s * i23; ct[5 * ct_stride + t] = s * i33;
+        }
+        __syncthreads();
       }
-      __syncthreads();
-    }
+      }
   }
 }
 
@@ -1052,7 +1086,7 @@ template <int N, bool W2, int KM>
 __global__ void __launch_bounds__(kCTM, 1) k_momentum_c(
     MomSrc src, MomTgt tg, MomOut out, Grid g, const uint32_t* __restrict__ cstart,
     const uint32_t* __restrict__ cend, const unsigned long long* __restrict__ chmax,
-    const uint32_t* __restrict__ clist, const uint32_t* __restrict__ nclist,
+    const uint32_t* __restrict__ clist, const uint32_t* __restrict__ nclist, uint32_t* __restrict__ work,
     const uint32_t* __restrict__ nbr, const uint32_t* __restrict__ ncount, int maxn, Phys ph,
     double* __restrict__ dts, unsigned long long* __restrict__ cnt) {
   extern __shared__ double dsm[];  // kMomPairs * kMomCap double2 staged + T_N * kTgt target fields
@@ -1065,170 +1099,181 @@ __global__ void __launch_bounds__(kCTM, 1) k_momentum_c(
   __shared__ unsigned long long shco;
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const uint32_t ncl = *nclist;
+  __shared__ uint32_t s_chunk;
   const int n = N > 0 ? N : ph.n;
   double dtmin = INFINITY;
   unsigned long long ncoinc = 0;
-  for (uint32_t ci = blockIdx.x; ci < ncl; ci += gridDim.x) {
-    cell_setup(g, clist[ci], cstart, cend, chmax, S);
-    const Stencil st = S.st;
-    for (uint32_t t0 = S.sc; t0 < S.ec; t0 += kTgt) {
-      const uint32_t t1 = min(S.ec, t0 + kTgt);
-      for (uint32_t t = t0 + threadIdx.x; t < t1; t += blockDim.x) {
-        const uint32_t i = t - t0;
-        s_n[i] = ncount[t];
-        s_cur[i] = 0;
-        T[T_X * kTgt + i] = src.x[t];
-        T[T_Y * kTgt + i] = src.y[t];
-        T[T_Z * kTgt + i] = src.z[t];
-        T[T_VX * kTgt + i] = src.vx[t];
-        T[T_VY * kTgt + i] = src.vy[t];
-        T[T_VZ * kTgt + i] = src.vz[t];
-        T[T_IH2 * kTgt + i] = src.ih2[t];
-        T[T_WB * kTgt + i] = tg.wB[t];
-        T[T_RINV * kTgt + i] = tg.rinv[t];
-        T[T_XP * kTgt + i] = tg.X[t];
-        T[T_C * kTgt + i] = src.c[t];
-        T[T_A11 * kTgt + i] = tg.c11[t];
-        T[T_A12 * kTgt + i] = tg.c12[t];
-        T[T_A13 * kTgt + i] = tg.c13[t];
-        T[T_A22 * kTgt + i] = tg.c22[t];
-        T[T_A23 * kTgt + i] = tg.c23[t];
-        T[T_A33 * kTgt + i] = tg.c33[t];
-        acc[0][i] = 0.0;
-        acc[1][i] = 0.0;
-        acc[2][i] = 0.0;
-        acc[3][i] = 0.0;
-        acc[4][i] = -1.0;
-      }
-      if (threadIdx.x == 0) S.next[0] = 0;
-      __syncthreads();
-      for (uint32_t gb = 0, gi = 0; gb < S.total; gb += kMomCap, ++gi) {
-        const uint32_t ge = min(S.total, gb + kMomCap), pend = pend_of(S, ge);
-        if (threadIdx.x == 0) S.next[(gi + 1) & 1] = 0;
-        for (uint32_t qq = threadIdx.x; qq < ge - gb; qq += blockDim.x) {  // flat staging
-          {
-            const uint32_t fi = gb + qq;
-            const int k = slot_of(S, fi);
-            const uint32_t j = S.t_start[k] + (fi - S.cum[k]);
-            double sh[3];
-            shifts_of(g, S, k, sh);
-            double2* q = F2 + qq;
-            const int64_t cs = src.ct_stride;
-            q[0 * kMomCap] = make_double2(src.x[j] + sh[0], src.y[j] + sh[1]);
-            q[1 * kMomCap] = make_double2(src.z[j] + sh[2], src.vx[j]);
-            q[2 * kMomCap] = make_double2(src.vy[j], src.vz[j]);
-            q[3 * kMomCap] = make_double2(src.m[j], src.ih2[j]);
-            q[4 * kMomCap] = make_double2(src.c[j], src.mX[j]);
-            q[5 * kMomCap] = make_double2(src.mr[j], src.ct[j]);
-            q[6 * kMomCap] = make_double2(src.ct[cs + j], src.ct[2 * cs + j]);
-            q[7 * kMomCap] = make_double2(src.ct[3 * cs + j], src.ct[4 * cs + j]);
-            q[8 * kMomCap] = make_double2(src.ct[5 * cs + j], 0.0);
+  // cells in chunks of kCellChunk consecutive (Morton-order) cells claimed from a
+  // counter: consecutive cells share most of their stencil, so a CTA's next staging
+  // finds its sources in L2 (a grid stride left the re-reads to HBM)
+  for (;;) {
+    if (threadIdx.x == 0) s_chunk = atomicAdd(work, (uint32_t)kCellChunk);
+    __syncthreads();
+    const uint32_t cfirst = s_chunk;
+    __syncthreads();
+    if (cfirst >= ncl) break;
+    for (uint32_t ci = cfirst; ci < min(ncl, cfirst + (uint32_t)kCellChunk); ++ci) {
+      cell_setup(g, clist[ci], cstart, cend, chmax, S);
+      const Stencil st = S.st;
+      for (uint32_t t0 = S.sc; t0 < S.ec; t0 += kTgt) {
+        const uint32_t t1 = min(S.ec, t0 + kTgt);
+        for (uint32_t t = t0 + threadIdx.x; t < t1; t += blockDim.x) {
+          const uint32_t i = t - t0;
+          s_n[i] = ncount[t];
+          s_cur[i] = 0;
+          T[T_X * kTgt + i] = src.x[t];
+          T[T_Y * kTgt + i] = src.y[t];
+          T[T_Z * kTgt + i] = src.z[t];
+          T[T_VX * kTgt + i] = src.vx[t];
+          T[T_VY * kTgt + i] = src.vy[t];
+          T[T_VZ * kTgt + i] = src.vz[t];
+          T[T_IH2 * kTgt + i] = src.ih2[t];
+          T[T_WB * kTgt + i] = tg.wB[t];
+          T[T_RINV * kTgt + i] = tg.rinv[t];
+          T[T_XP * kTgt + i] = tg.X[t];
+          T[T_C * kTgt + i] = src.c[t];
+          T[T_A11 * kTgt + i] = tg.c11[t];
+          T[T_A12 * kTgt + i] = tg.c12[t];
+          T[T_A13 * kTgt + i] = tg.c13[t];
+          T[T_A22 * kTgt + i] = tg.c22[t];
+          T[T_A23 * kTgt + i] = tg.c23[t];
+          T[T_A33 * kTgt + i] = tg.c33[t];
+          acc[0][i] = 0.0;
+          acc[1][i] = 0.0;
+          acc[2][i] = 0.0;
+          acc[3][i] = 0.0;
+          acc[4][i] = -1.0;
+        }
+        if (threadIdx.x == 0) S.next[0] = 0;
+        __syncthreads();
+        for (uint32_t gb = 0, gi = 0; gb < S.total; gb += kMomCap, ++gi) {
+          const uint32_t ge = min(S.total, gb + kMomCap), pend = pend_of(S, ge);
+          if (threadIdx.x == 0) S.next[(gi + 1) & 1] = 0;
+          for (uint32_t qq = threadIdx.x; qq < ge - gb; qq += blockDim.x) {  // flat staging
+            {
+              const uint32_t fi = gb + qq;
+              const int k = slot_of(S, fi);
+              const uint32_t j = S.t_start[k] + (fi - S.cum[k]);
+              double sh[3];
+              shifts_of(g, S, k, sh);
+              double2* q = F2 + qq;
+              const int64_t cs = src.ct_stride;
+              q[0 * kMomCap] = make_double2(src.x[j] + sh[0], src.y[j] + sh[1]);
+              q[1 * kMomCap] = make_double2(src.z[j] + sh[2], src.vx[j]);
+              q[2 * kMomCap] = make_double2(src.vy[j], src.vz[j]);
+              q[3 * kMomCap] = make_double2(src.m[j], src.ih2[j]);
+              q[4 * kMomCap] = make_double2(src.c[j], src.mX[j]);
+              q[5 * kMomCap] = make_double2(src.mr[j], src.ct[j]);
+              q[6 * kMomCap] = make_double2(src.ct[cs + j], src.ct[2 * cs + j]);
+              q[7 * kMomCap] = make_double2(src.ct[3 * cs + j], src.ct[4 * cs + j]);
+              q[8 * kMomCap] = make_double2(src.ct[5 * cs + j], 0.0);
+            }
           }
+          __syncthreads();
+          struct B {
+            const double2* F2;
+            const double* T;
+            const Stencil* st;
+            const Grid* g;
+            double alpha;
+            int n, K, sym;
+            const double* tab;
+            unsigned long long* ncoinc;
+            double xa, ya, za, vxa, vya, vza, ih2a, wBa, rinva, Xa, ca, a11, a12, a13, a22, a23, a33;
+            double fx, fy, fz, fu, vs;
+            __device__ __forceinline__ void begin(uint32_t i) {
+              xa = T[T_X * kTgt + i]; ya = T[T_Y * kTgt + i]; za = T[T_Z * kTgt + i];
+              vxa = T[T_VX * kTgt + i]; vya = T[T_VY * kTgt + i]; vza = T[T_VZ * kTgt + i];
+              ih2a = T[T_IH2 * kTgt + i]; wBa = T[T_WB * kTgt + i]; rinva = T[T_RINV * kTgt + i];
+              Xa = T[T_XP * kTgt + i]; ca = T[T_C * kTgt + i];
+              a11 = T[T_A11 * kTgt + i]; a12 = T[T_A12 * kTgt + i]; a13 = T[T_A13 * kTgt + i];
+              a22 = T[T_A22 * kTgt + i]; a23 = T[T_A23 * kTgt + i]; a33 = T[T_A33 * kTgt + i];
+              fx = fy = fz = fu = 0.0;
+              vs = -1.0;
+            }
+            __device__ __forceinline__ void operator()(int qi) {
+              const double2* q = F2 + qi;
+              const double2 p0 = q[0], p1 = q[kMomCap], p3 = q[3 * kMomCap];
+              double dx = p0.x - xa, dy = p0.y - ya, dz = p1.x - za;
+              delta3<W2>(*st, *g, dx, dy, dz);  // Delta_ab = x_b - x_a
+              const double r2 = dx * dx + dy * dy + dz * dz;
+              // coincident pair: Delta = 0 zeroes every term below; it is only
+              // kept out of v_sig and counted (no branch)
+              const bool coinc = r2 == 0.0;
+              *ncoinc += coinc;
+              const double ta = r2 * ih2a;
+              // symmetric extra pair (r >= 2 h_a): W(r, h_a) = 0, only the h_b terms remain
+              const double Sa = (sym && !(ta < 4.0)) ? 0.0 : kern_S<KM, N, true>(ta, n, tab, K);
+              const double Wa = wBa * Sa;
+              const double tb = r2 * p3.y;
+              double Sb = Sa;  // equal h: W(r, h_b) shares the kernel value
+              if (tb != ta) Sb = tb < 4.0 ? kern_S<KM, N, true>(tb, n, tab, K) : 0.0;
+              // R5: A_ab(h_a) = C_a Delta W_ab(h_a) = Wa u;  R4: A_ab(h_b) = C~_b Delta S_b = Sb w
+              const double ux = a11 * dx + a12 * dy + a13 * dz;
+              const double uy = a12 * dx + a22 * dy + a23 * dz;
+              const double uz = a13 * dx + a23 * dy + a33 * dz;
+              const double2 p5 = q[5 * kMomCap], p6 = q[6 * kMomCap], p7 = q[7 * kMomCap], p8 = q[8 * kMomCap];
+              const double b11 = p5.y, b12 = p6.x, b13 = p6.y, b22 = p7.x, b23 = p7.y, b33 = p8.x;
+              const double wx = b11 * dx + b12 * dy + b13 * dz;
+              const double wy = b12 * dx + b22 * dy + b23 * dz;
+              const double wz = b13 * dx + b23 * dy + b33 * dz;
+              const double2 p2 = q[2 * kMomCap], p4 = q[4 * kMomCap];
+              const double mb = p3.x, mXb = p4.y, mrb = p5.x, cb = p4.x;
+              const double vabx = vxa - p1.y, vaby = vya - p2.x, vabz = vza - p2.y;
+              const double vdotx = -(vabx * dx + vaby * dy + vabz * dz);  // v_ab . x_ab
+              // Eq. 5: w_ab = v_ab . x_ab / |x_ab|, Pi' only when approaching
+              const double w = vdotx < 0.0 ? vdotx * rsqrt(r2) : 0.0;
+              const double vsab = ca + cb - 3.0 * w;  // v_sig; w == min(w, 0)
+              const double hp = -0.25 * alpha * vsab * w;  // Pi'/2, Eq. 5
+              vs = (!coinc && vsab > vs) ? vsab : vs;
+              // Eq. 2 with R2 and Eq. 4: a += -m_b (X_a A_a + X_b A_b) - g,
+              //   g = (Pi'/2) (m_b/rho_a A_a + m_b/rho_b A_b), folded onto u and w
+              const double ka = mb * fma(hp, rinva, Xa) * Wa;
+              const double kb = fma(hp, mrb, mXb) * Sb;
+              fx -= fma(ka, ux, kb * wx);
+              fy -= fma(ka, uy, kb * wy);
+              fz -= fma(ka, uz, kb * wz);
+              // Eq. 3 with R1, R3: du += m_b X_a v_ab.A_a + (1/2) v_ab.g
+              const double vu = vabx * ux + vaby * uy + vabz * uz;
+              const double vw = vabx * wx + vaby * wy + vabz * wz;
+              fu += mb * fma(0.5 * hp, rinva, Xa) * Wa * vu + 0.5 * hp * mrb * Sb * vw;
+            }
+          } body;
+          body.F2 = F2; body.T = T; body.st = &st; body.g = &g; body.alpha = ph.alpha; body.n = n;
+          body.K = ph.tableK; body.tab = ph.table; body.sym = ph.sym;
+          body.ncoinc = &ncoinc;
+          walk_targets_half(t0, t1, nbr, maxn, s_n, s_cur, pend, S.cum, gb, &S.next[gi & 1], body,
+                            [&](bool act, uint32_t i, uint32_t c2) {
+                              double v[4] = {body.fx, body.fy, body.fz, body.fu};
+                              half_multi_sum<4>(v);
+                              const double e = half_max(body.vs);
+                              const int l16 = lane & 15;
+                              if (act) {
+                                if ((l16 & 3) == 0) acc[l16 >> 2][i] += v[0];
+                                if (l16 == 0) {
+                                  s_cur[i] = c2;
+                                  acc[4][i] = fmax(acc[4][i], e);
+                                }
+                              }
+                            });
+          __syncthreads();
+        }
+        for (uint32_t t = t0 + threadIdx.x; t < t1; t += blockDim.x) {
+          const uint32_t i = t - t0;
+          double vsig = acc[4][i];
+          if (vsig < 0.0) vsig = 2.0 * T[T_C * kTgt + i];  // no interacting neighbour
+          out.ax[t] = acc[0][i];
+          out.ay[t] = acc[1][i];
+          out.az[t] = acc[2][i];
+          out.du[t] = acc[3][i];
+          out.vsig[t] = vsig;
+          const double dta = ph.courant * tg.h[t] / vsig;  // R19
+          if (!(dta > 0.0)) atomicAdd(&cnt[CNT_NONFINITE], 1ull);
+          dtmin = fmin(dtmin, dta);
         }
         __syncthreads();
-        struct B {
-          const double2* F2;
-          const double* T;
-          const Stencil* st;
-          const Grid* g;
-          double alpha;
-          int n, K, sym;
-          const double* tab;
-          unsigned long long* ncoinc;
-          double xa, ya, za, vxa, vya, vza, ih2a, wBa, rinva, Xa, ca, a11, a12, a13, a22, a23, a33;
-          double fx, fy, fz, fu, vs;
-          __device__ __forceinline__ void begin(uint32_t i) {
-            xa = T[T_X * kTgt + i]; ya = T[T_Y * kTgt + i]; za = T[T_Z * kTgt + i];
-            vxa = T[T_VX * kTgt + i]; vya = T[T_VY * kTgt + i]; vza = T[T_VZ * kTgt + i];
-            ih2a = T[T_IH2 * kTgt + i]; wBa = T[T_WB * kTgt + i]; rinva = T[T_RINV * kTgt + i];
-            Xa = T[T_XP * kTgt + i]; ca = T[T_C * kTgt + i];
-            a11 = T[T_A11 * kTgt + i]; a12 = T[T_A12 * kTgt + i]; a13 = T[T_A13 * kTgt + i];
-            a22 = T[T_A22 * kTgt + i]; a23 = T[T_A23 * kTgt + i]; a33 = T[T_A33 * kTgt + i];
-            fx = fy = fz = fu = 0.0;
-            vs = -1.0;
-          }
-          __device__ __forceinline__ void operator()(int qi) {
-            const double2* q = F2 + qi;
-            const double2 p0 = q[0], p1 = q[kMomCap], p3 = q[3 * kMomCap];
-            double dx = p0.x - xa, dy = p0.y - ya, dz = p1.x - za;
-            delta3<W2>(*st, *g, dx, dy, dz);  // Delta_ab = x_b - x_a
-            const double r2 = dx * dx + dy * dy + dz * dz;
-            // coincident pair: Delta = 0 zeroes every term below; it is only
-            // kept out of v_sig and counted (no branch)
-            const bool coinc = r2 == 0.0;
-            *ncoinc += coinc;
-            const double ta = r2 * ih2a;
-            // symmetric extra pair (r >= 2 h_a): W(r, h_a) = 0, only the h_b terms remain
-            const double Sa = (sym && !(ta < 4.0)) ? 0.0 : kern_S<KM, N, true>(ta, n, tab, K);
-            const double Wa = wBa * Sa;
-            const double tb = r2 * p3.y;
-            double Sb = Sa;  // equal h: W(r, h_b) shares the kernel value
-            if (tb != ta) Sb = tb < 4.0 ? kern_S<KM, N, true>(tb, n, tab, K) : 0.0;
-            // R5: A_ab(h_a) = C_a Delta W_ab(h_a) = Wa u;  R4: A_ab(h_b) = C~_b Delta S_b = Sb w
-            const double ux = a11 * dx + a12 * dy + a13 * dz;
-            const double uy = a12 * dx + a22 * dy + a23 * dz;
-            const double uz = a13 * dx + a23 * dy + a33 * dz;
-            const double2 p5 = q[5 * kMomCap], p6 = q[6 * kMomCap], p7 = q[7 * kMomCap], p8 = q[8 * kMomCap];
-            const double b11 = p5.y, b12 = p6.x, b13 = p6.y, b22 = p7.x, b23 = p7.y, b33 = p8.x;
-            const double wx = b11 * dx + b12 * dy + b13 * dz;
-            const double wy = b12 * dx + b22 * dy + b23 * dz;
-            const double wz = b13 * dx + b23 * dy + b33 * dz;
-            const double2 p2 = q[2 * kMomCap], p4 = q[4 * kMomCap];
-            const double mb = p3.x, mXb = p4.y, mrb = p5.x, cb = p4.x;
-            const double vabx = vxa - p1.y, vaby = vya - p2.x, vabz = vza - p2.y;
-            const double vdotx = -(vabx * dx + vaby * dy + vabz * dz);  // v_ab . x_ab
-            // Eq. 5: w_ab = v_ab . x_ab / |x_ab|, Pi' only when approaching
-            const double w = vdotx < 0.0 ? vdotx * rsqrt(r2) : 0.0;
-            const double vsab = ca + cb - 3.0 * w;  // v_sig; w == min(w, 0)
-            const double hp = -0.25 * alpha * vsab * w;  // Pi'/2, Eq. 5
-            vs = (!coinc && vsab > vs) ? vsab : vs;
-            // Eq. 2 with R2 and Eq. 4: a += -m_b (X_a A_a + X_b A_b) - g,
-            //   g = (Pi'/2) (m_b/rho_a A_a + m_b/rho_b A_b), folded onto u and w
-            const double ka = mb * fma(hp, rinva, Xa) * Wa;
-            const double kb = fma(hp, mrb, mXb) * Sb;
-            fx -= fma(ka, ux, kb * wx);
-            fy -= fma(ka, uy, kb * wy);
-            fz -= fma(ka, uz, kb * wz);
-            // Eq. 3 with R1, R3: du += m_b X_a v_ab.A_a + (1/2) v_ab.g
-            const double vu = vabx * ux + vaby * uy + vabz * uz;
-            const double vw = vabx * wx + vaby * wy + vabz * wz;
-            fu += mb * fma(0.5 * hp, rinva, Xa) * Wa * vu + 0.5 * hp * mrb * Sb * vw;
-          }
-        } body;
-        body.F2 = F2; body.T = T; body.st = &st; body.g = &g; body.alpha = ph.alpha; body.n = n;
-        body.K = ph.tableK; body.tab = ph.table; body.sym = ph.sym;
-        body.ncoinc = &ncoinc;
-        walk_targets_half(t0, t1, nbr, maxn, s_n, s_cur, pend, S.cum, gb, &S.next[gi & 1], body,
-                          [&](bool act, uint32_t i, uint32_t c2) {
-                            double v[4] = {body.fx, body.fy, body.fz, body.fu};
-                            half_multi_sum<4>(v);
-                            const double e = half_max(body.vs);
-                            const int l16 = lane & 15;
-                            if (act) {
-                              if ((l16 & 3) == 0) acc[l16 >> 2][i] += v[0];
-                              if (l16 == 0) {
-                                s_cur[i] = c2;
-                                acc[4][i] = fmax(acc[4][i], e);
-                              }
-                            }
-                          });
-        __syncthreads();
       }
-      for (uint32_t t = t0 + threadIdx.x; t < t1; t += blockDim.x) {
-        const uint32_t i = t - t0;
-        double vsig = acc[4][i];
-        if (vsig < 0.0) vsig = 2.0 * T[T_C * kTgt + i];  // no interacting neighbour
-        out.ax[t] = acc[0][i];
-        out.ay[t] = acc[1][i];
-        out.az[t] = acc[2][i];
-        out.du[t] = acc[3][i];
-        out.vsig[t] = vsig;
-        const double dta = ph.courant * tg.h[t] / vsig;  // R19
-        if (!(dta > 0.0)) atomicAdd(&cnt[CNT_NONFINITE], 1ull);
-        dtmin = fmin(dtmin, dta);
       }
-      __syncthreads();
-    }
   }
   // block min dt -> one atomicMin per block (positive doubles order like uint64)
   dtmin = -wmax(-dtmin);
@@ -1273,9 +1318,10 @@ int launch_neighbors(sph_ctx* c) {
   auto kern = any_wrap2(c) ? (sym ? k_search<true, true> : k_search<true, false>)
                            : (sym ? k_search<false, true> : k_search<false, false>);
   set_smem(kern, smem);
+  cudaMemsetAsync(c->s.work + 0, 0, sizeof(uint32_t), c->stream);
   kern<<<cell_grid(c, 4), kCT, smem, c->stream>>>(
       c->P.x, c->P.y, c->P.z, c->P.h, c->grid, c->s.cell_start, c->s.cell_end, c->s.cell_hmax,
-      c->s.cell_list, c->s.ncell_list, c->s.nbr, c->s.ncount, c->maxn, c->s.nbr_maxcount);
+      c->s.cell_list, c->s.ncell_list, c->s.work + 0, c->s.nbr, c->s.ncount, c->maxn, c->s.nbr_maxcount);
   return 1;
 }
 
@@ -1284,9 +1330,10 @@ static void density_t(sph_ctx* c) {
   const size_t smem = 4 * kDensCap * sizeof(double);
   set_smem(k_density_c<N, W2, KM>, smem);
   sph_particles& P = c->P;
+  cudaMemsetAsync(c->s.work + 1, 0, sizeof(uint32_t), c->stream);
   k_density_c<N, W2, KM><<<cell_grid(c, 2), kCTD, smem, c->stream>>>(
       P.x, P.y, P.z, P.h, P.m, P.u, c->grid, c->s.cell_start, c->s.cell_end, c->s.cell_hmax,
-      c->s.cell_list, c->s.ncell_list, c->s.nbr, c->s.ncount, c->maxn, c->phys, P.rho, P.omega,
+      c->s.cell_list, c->s.ncell_list, c->s.work + 1, c->s.nbr, c->s.ncount, c->maxn, c->phys, P.rho, P.omega,
       P.p, P.c, c->s.wB, c->s.ih2, c->s.vol, c->s.rinv, c->s.X, c->s.mX, c->s.cnt);
 }
 
@@ -1320,9 +1367,10 @@ static void iad_t(sph_ctx* c) {
   const size_t smem = 4 * kDensCap * sizeof(double);
   set_smem(k_iad_c<N, W2, KM>, smem);
   sph_particles& P = c->P;
+  cudaMemsetAsync(c->s.work + 2, 0, sizeof(uint32_t), c->stream);
   k_iad_c<N, W2, KM><<<cell_grid(c, 2), kCTD, smem, c->stream>>>(
       P.x, P.y, P.z, c->grid, c->s.cell_start, c->s.cell_end, c->s.cell_hmax, c->s.cell_list,
-      c->s.ncell_list, c->s.nbr, c->s.ncount, c->maxn, c->phys, c->s.wB, c->s.ih2, c->s.vol,
+      c->s.ncell_list, c->s.work + 2, c->s.nbr, c->s.ncount, c->maxn, c->phys, c->s.wB, c->s.ih2, c->s.vol,
       P.c11, P.c12, P.c13, P.c22, P.c23, P.c33, c->s.ct, c->cap, c->s.cnt);
 }
 
@@ -1339,9 +1387,10 @@ static void momentum_t(sph_ctx* c) {
   MomSrc src = {P.x, P.y, P.z, P.vx, P.vy, P.vz, P.m, c->s.ih2, P.c, c->s.mX, c->s.vol, c->s.ct, c->cap};
   MomTgt tg = {P.h, c->s.wB, c->s.rinv, c->s.X, P.c11, P.c12, P.c13, P.c22, P.c23, P.c33};
   MomOut out = {P.ax, P.ay, P.az, P.du, P.vsig};
+  cudaMemsetAsync(c->s.work + 3, 0, sizeof(uint32_t), c->stream);
   k_momentum_c<N, W2, KM><<<cell_grid(c, 1), kCTM, smem, c->stream>>>(
       src, tg, out, c->grid, c->s.cell_start, c->s.cell_end, c->s.cell_hmax, c->s.cell_list,
-      c->s.ncell_list, c->s.nbr, c->s.ncount, c->maxn, c->phys, c->s.dts, c->s.cnt);
+      c->s.ncell_list, c->s.work + 3, c->s.nbr, c->s.ncount, c->maxn, c->phys, c->s.dts, c->s.cnt);
 }
 
 int launch_momentum(sph_ctx* c) {

@@ -280,6 +280,7 @@ sph_status sph_init(const sph_params* prm, int64_t capacity, sph_ctx** out) {
   AL(s.nbr, cap * (int64_t)c->maxn);
   AL(s.ncount, cap);
   AL(s.nbr_maxcount, 1);
+  AL(s.work, 4);
   AL(s.wB, cap);
   AL(s.ih2, cap);
   AL(s.vol, cap);
@@ -745,7 +746,7 @@ sph_status sph_destroy(sph_ctx* c) {
   Scratch& s = c->s;
   void* ptrs[] = {s.keys, s.keys_alt, s.idx, s.idx_alt, s.hist, s.scan_tmp, s.gather, s.gather_id,
                   s.cell_start, s.cell_end, s.cell_hmax, s.cell_flag, s.cell_rank, s.cell_list,
-                  s.ncell_list, s.nbr, s.ncount, s.nbr_maxcount, s.wB, s.ih2, s.vol, s.rinv, s.X,
+                  s.ncell_list, s.nbr, s.ncount, s.nbr_maxcount, s.work, s.wB, s.ih2, s.vol, s.rinv, s.X,
                   s.mX, s.ct, s.red, s.bbox, s.dts, s.cnt, s.diag, s.ktable};
   for (void* p : ptrs)
     if (p) cudaFree(p);

@@ -81,6 +81,7 @@ struct Scratch {
   uint32_t* nbr = nullptr;       // cap * maxn
   uint32_t* ncount = nullptr;    // cap
   unsigned int* nbr_maxcount = nullptr;  // device scalar
+  uint32_t* work = nullptr;              // per cell kernel: next cell chunk (reset per launch)
   // per-particle auxiliaries written by density, read by iad / momentum
   double* wB = nullptr;    // B / h^3
   double* ih2 = nullptr;   // 1 / h^2
