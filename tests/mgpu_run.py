@@ -29,7 +29,14 @@ def make_input():
         return inputs.square_patch(24, 24, pressure_ics=True)
     if CASE == "weak":
         return inputs.square_patch_weak(20, int(os.environ["WORLD_SIZE"]))
+    if CASE == "evrard":  # variable h (8x), open box, ideal gas
+        return inputs.evrard(30)
+    if CASE == "cloud_sym":  # variable h, periodic x and z, symmetric neighbour relation
+        return inputs.random_cloud(6000, box=12.0, h0=0.8, hspread=0.3, periodic=(1, 0, 1), seed=3)
     return inputs.jitter(inputs.square_patch(20, 16))
+
+
+KW = {"symmetric": 1} if CASE == "cloud_sym" else {}
 
 
 def main():
@@ -39,7 +46,7 @@ def main():
     d = make_input()
     mine = inputs.subset(d, np.arange(rank, d["x"].size, world))
     cap = int(d["x"].size * 1.2) + 1024  # any rank may end up owning a big share + halos
-    sim = sph.Simulation(mine, capacity=cap, rank=rank, nranks=world, unique_id=uid)
+    sim = sph.Simulation(mine, capacity=cap, rank=rank, nranks=world, unique_id=uid, **KW)
     dts = []
     for _ in range(STEPS):
         dts.append(sim.step(want_dt=True))
@@ -47,7 +54,7 @@ def main():
     got = dist.gather_by_id(sim.state(), world, FIELDS)
     ok, msg = True, ""
     if rank == 0:
-        ref = sph.Simulation(d, capacity=cap)
+        ref = sph.Simulation(d, capacity=cap, **KW)
         rdts = [ref.step(want_dt=True) for _ in range(STEPS)]
         rst = ref.state()
         o = np.argsort(rst["id"])

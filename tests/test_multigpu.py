@@ -24,7 +24,7 @@ def _port():
     return p
 
 
-@pytest.mark.parametrize("case", ["patch", "jitter", "weak"])
+@pytest.mark.parametrize("case", ["patch", "jitter", "weak", "evrard", "cloud_sym"])
 def test_multigpu_bit_identical_to_one_gpu(case):
     n = _ngpus()
     if n < 2:
