@@ -254,13 +254,22 @@ def run_ours(args):
         torch.cuda.synchronize()
         e2e_ms = max(ee0.elapsed_time(ee1), 1e3 * (time.perf_counter() - t0))
         peak64 = sph.measure_fp64_peak(stream.cuda_stream)
+    ms_rank = ms
     ms = max_over_ranks(ms, world)
     e2e_ms = max_over_ranks(e2e_ms, world)
+    per_rank = None
     if world > 1:
         import torch.distributed as dist
         t = torch.tensor([n_local], dtype=torch.int64, device="cuda")
         dist.all_reduce(t)
         n_total = int(t.item())
+        # per-rank view of the step (load balance, halo sizes): rank 0 reports it
+        sim._sync_n()
+        mine = {"ms_per_step": round(ms_rank / args.steps, 3), "n_owned": int(sim.n),
+                "n_halo": int(getattr(sim, "n_halo", 0)),
+                "phases": {k: round(v / args.steps, 3) for k, v in phase_ms.items() if v}}
+        per_rank = [None] * world
+        dist.all_gather_object(per_rank, mine)
     else:
         n_total = n_local
     if rank != 0:
@@ -316,6 +325,7 @@ def run_ours(args):
                      "avg_launch_ms": mom_ms},
         "pair_kernels_fp64": pair_kernels,
         "phases_ms_per_step": phases,
+        "per_rank": per_rank,
         "gpu_launches": int(sum(phase_launch.values())),
         "e2e": {"value": n_total * e2e_steps / (e2e_ms * 1e-3), "unit": UNIT,
                 "h2d_bytes_per_step": nbytes, "d2h_bytes_per_step": nbytes,

@@ -80,11 +80,21 @@ __device__ __forceinline__ int64_t key_bin(const Grid& g, uint64_t key, int shif
   return (int64_t)(m >> shift);
 }
 
+// Key-prefix histogram.  Particles are still in the previous step's (cell) order, so
+// a warp's 32 consecutive keys fall into one or two bins: one atomic per distinct
+// bin of the warp (match_any) instead of 32 atomics on the same address (which
+// serialised to ~9 ms per step at 25M particles, profiled per rank).
 __global__ void k_bin_hist(const uint64_t* __restrict__ keys, int64_t n, Grid g, int shift,
                            unsigned long long* __restrict__ hist) {
-  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
-       i += (int64_t)gridDim.x * blockDim.x)
-    atomicAdd(&hist[key_bin(g, keys[i], shift)], 1ull);
+  const int lane = threadIdx.x & 31;
+  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+  for (int64_t i0 = blockIdx.x * (int64_t)blockDim.x + (threadIdx.x & ~31); i0 < n; i0 += stride) {
+    const int64_t i = i0 + lane;
+    const bool ok = i < n;
+    const unsigned long long bin = ok ? (unsigned long long)key_bin(g, keys[i], shift) : ~0ull;
+    const unsigned grp = __match_any_sync(0xffffffffu, bin);
+    if (ok && lane == __ffs(grp) - 1) atomicAdd(&hist[bin], (unsigned long long)__popc(grp));
+  }
 }
 
 __device__ __forceinline__ int owner_dev(const int64_t* split, int G, int64_t bin) {
