@@ -621,7 +621,8 @@ __global__ void __launch_bounds__(kCT, 2) k_search(const double* __restrict__ x,
             // keep the row bases in registers (else ptxas re-derives nbr + t*maxn + p in 64-bit per store)
             asm volatile("" : "+l"(row0), "+l"(row1));
             // one staged candidate against both targets: fp32 band test, exact fp64 when inside it
-            auto test = [&](const float4 cd, const float2 cb, bool& hit0, bool& hit1) {
+            auto test = [&](const float4 cd, const float2 cb, bool& hit0, bool& hit1, bool& amb0,
+                            bool& amb1) {
               const uint32_t pk = __float_as_uint(cd.w);
               float dx0 = cd.x - ax0, dy0 = cd.y - ay0, dz0 = cd.z - az0;
               float dx1 = cd.x - ax1, dy1 = cd.y - ay1, dz1 = cd.z - az1;
@@ -632,7 +633,8 @@ __global__ void __launch_bounds__(kCT, 2) k_search(const double* __restrict__ x,
               const float r0 = fmaf(dz0, dz0, fmaf(dy0, dy0, dx0 * dx0));
               const float r1 = fmaf(dz1, dz1, fmaf(dy1, dy1, dx1 * dx1));
               bool in0 = r0 < lo0, in1 = r1 < lo1;
-              bool amb0 = (r0 >= lo0) & (r0 < hi0), amb1 = (r1 >= lo1) & (r1 < hi1);
+              amb0 = (r0 >= lo0) & (r0 < hi0);
+              amb1 = (r1 >= lo1) & (r1 < hi1);
               if constexpr (SYM) {  // either side's support
                 in0 |= r0 < cb.x;
                 in1 |= r1 < cb.x;
@@ -641,18 +643,20 @@ __global__ void __launch_bounds__(kCT, 2) k_search(const double* __restrict__ x,
               }
               hit0 = in0 & (pk != self0);
               hit1 = in1 & (pk != self1);
-              if (__ballot_sync(0xffffffffu, amb0 | amb1)) {  // rare: exact fp64 test
-                const uint32_t j = S.t_start[pk >> kLocalBits] + (pk & kLocalMask);
-                double limb = 0.0;
-                if constexpr (SYM) {
-                  if (amb0 | amb1) {
-                    const double thb = 2.0 * h[j];
-                    limb = __dmul_rn(thb, thb);
-                  }
+            };
+            // rare: exact fp64 test of the candidates inside a band (one ballot per step)
+            auto exact = [&](const float4 cd, bool& hit0, bool& hit1, bool amb0, bool amb1) {
+              const uint32_t pk = __float_as_uint(cd.w);
+              const uint32_t j = S.t_start[pk >> kLocalBits] + (pk & kLocalMask);
+              double limb = 0.0;
+              if constexpr (SYM) {
+                if (amb0 | amb1) {
+                  const double thb = 2.0 * h[j];
+                  limb = __dmul_rn(thb, thb);
                 }
-                if (amb0) hit0 = exact_hit(g, x, y, z, j, ta, TA.pos, fmax(TA.lim, limb));
-                if (amb1) hit1 = exact_hit(g, x, y, z, j, tb, TB.pos, fmax(TB.lim, limb));
               }
+              if (amb0) hit0 = exact_hit(g, x, y, z, j, ta, TA.pos, fmax(TA.lim, limb));
+              if (amb1) hit1 = exact_hit(g, x, y, z, j, tb, TB.pos, fmax(TB.lim, limb));
             };
             // Tiles either target can reach.  Box distance in the prefilter's own fp32
             // expression: rounding is monotone, so box d2 <= r2_32 of every member, and
@@ -709,9 +713,13 @@ __global__ void __launch_bounds__(kCT, 2) k_search(const double* __restrict__ x,
                 bA = candb[32 * qA + lane];
                 bB = candb[32 * qB + lane];
               }
-              bool hA0, hA1, hB0, hB1;
-              test(cA, bA, hA0, hA1);
-              test(cB, bB, hB0, hB1);
+              bool hA0, hA1, hB0, hB1, aA0, aA1, aB0, aB1;
+              test(cA, bA, hA0, hA1, aA0, aA1);
+              test(cB, bB, hB0, hB1, aB0, aB1);
+              if (__ballot_sync(0xffffffffu, aA0 | aA1 | aB0 | aB1)) {
+                exact(cA, hA0, hA1, aA0, aA1);
+                exact(cB, hB0, hB1, aB0, aB1);
+              }
               const unsigned bA0 = __ballot_sync(0xffffffffu, hA0), bA1 = __ballot_sync(0xffffffffu, hA1);
               const unsigned bB0 = __ballot_sync(0xffffffffu, hB0), bB1 = __ballot_sync(0xffffffffu, hB1);
               const uint32_t pA0 = cnt0 + __popc(bA0 & lt), pA1 = cnt1 + __popc(bA1 & lt);
