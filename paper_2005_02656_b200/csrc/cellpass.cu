@@ -22,17 +22,18 @@ namespace sphb {
 
 constexpr int kCT = 256;          // threads per CTA
 constexpr int kNW = kCT / 32;     // warps per CTA
-constexpr int kTgt = 128;         // targets per sub-block (per-target state in smem)
+constexpr int kTgt = 128;         // search: targets per sub-block (per-target state in smem)
+constexpr int kTgtU = 416;        // pair passes: targets per sub-block (a whole 2x2x1 unit, <= 9x9x5 at config 5)
 constexpr int kSlots = kKMax;     // slot tables: every stencil the grid chooser admits
 constexpr int kCellChunk = 4;     // consecutive cells per claim (L2 reuse of shared stencils)
 constexpr int kSearchCap = 3072;  // staged candidates per group (float4)
 constexpr int kSearchTiles = kSearchCap / 32 + 1;          // + the sentinel tile
 constexpr int kSearchWords = (kSearchCap / 32 + 31) / 32;  // tile bitmask words
-constexpr int kDensCap = 2560;    // staged particles per group, 4 fp64 fields
-constexpr int kMomCap = 1088;     // staged particles per group, 17 fp64 fields (1 CTA/SM; a 27-cell stencil in 2 groups)
+constexpr int kDensCap = 4096;    // density: staged particles per group, 4 fp64 fields
+constexpr int kIadCap = 4096;     // IAD: the same fields
+constexpr int kMomCap = 992;      // staged particles per group, 17 fp64 fields (1 CTA/SM; a 48-cell unit stencil in 4 groups)
 constexpr int kCTM = 512;         // momentum CTA: 16 warps, one CTA per SM
-constexpr int kCTD = 512;         // density / IAD CTA: 16 warps, two CTAs per SM
-constexpr int kNWD = kCTD / 32;
+constexpr int kCTD = 1024;        // density / IAD CTA: 32 warps, one CTA per SM (a unit stencil in one group)
 constexpr int kNWM = kCTM / 32;
 constexpr uint32_t kSent = 0xffffffffu;
 
@@ -185,52 +186,115 @@ __device__ __forceinline__ double min_img(double d, double L) {
   return d;
 }
 
-// CTA prologue for cell c (warp 0, one CTA barrier): stencil, per-slot tables and
-// their prefix (flat staging index of each slot).
+// Warp 0: per-slot tables of S.st and their prefix (flat staging index of each slot);
+// with umap, also the unit-stencil slot of every slot (search: rows are written in
+// unit numbering, stencil.cuh).  Lane 0 has set S.st / S.c3 / S.sc / S.ec.
+__device__ __forceinline__ void slot_tables(const Grid& g, const uint32_t* __restrict__ cstart,
+                                            const uint32_t* __restrict__ cend, CellSm& S,
+                                            uint16_t* umap, uint32_t* ustart, const Stencil* U) {
+  const int lane = threadIdx.x;
+  const int K = S.st.K;
+  uint32_t carry = 0;
+  for (int b = 0; b < K; b += 32) {
+    const int k = b + lane;
+    uint32_t cnt = 0;
+    if (k < K) {
+      int sh[3];
+      const int64_t cell = slot_cell(g, S.st, k, sh);
+      const uint32_t s0 = cstart[cell];
+      cnt = cend[cell] - s0;
+      S.t_start[k] = s0;
+      S.t_sh[k][0] = (signed char)sh[0];
+      S.t_sh[k][1] = (signed char)sh[1];
+      S.t_sh[k][2] = (signed char)sh[2];
+      if (umap) {
+        const int us = unit_slot(S.st, *U, k);
+        umap[k] = (uint16_t)us;
+        ustart[us] = s0;
+      }
+    }
+    uint32_t x = cnt;  // inclusive warp scan
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const uint32_t y = __shfl_up_sync(0xffffffffu, x, o);
+      if (lane >= o) x += y;
+    }
+    if (k < K) S.cum[k] = carry + x - cnt;
+    carry += __shfl_sync(0xffffffffu, x, 31);
+  }
+  if (lane == 0) {
+    S.cum[K] = carry;
+    S.total = carry;
+  }
+}
+
+// CTA prologue for search cell c (warp 0, one CTA barrier): the cell's own stencil,
+// its slot tables, and the map of its slots into its unit's stencil.
 __device__ void cell_setup(const Grid& g, uint32_t c, const uint32_t* __restrict__ cstart,
                            const uint32_t* __restrict__ cend,
-                           const unsigned long long* __restrict__ chmax, CellSm& S) {
+                           const unsigned long long* __restrict__ chmax, CellSm& S, uint16_t* umap,
+                           uint32_t* ustart) {
   if (threadIdx.x < 32) {
-    const int lane = threadIdx.x;
-    if (lane == 0) {
+    __shared__ Stencil U;
+    if (threadIdx.x == 0) {
       cell_coords(g, c, S.c3);
       S.sc = cstart[c];
       S.ec = cend[c];
       make_stencil(g, S.c3, cell_reach(g, __longlong_as_double((long long)chmax[c])), S.st);
       S.kself = self_slot(S.st, S.c3);
+      make_unit_stencil(g, S.c3, cstart, cend, chmax, U);
     }
     __syncwarp();
-    const int K = S.st.K;
-    uint32_t carry = 0;
-    for (int b = 0; b < K; b += 32) {
-      const int k = b + lane;
-      uint32_t cnt = 0;
-      if (k < K) {
-        int sh[3];
-        const int64_t cell = slot_cell(g, S.st, k, sh);
-        const uint32_t s0 = cstart[cell];
-        cnt = cend[cell] - s0;
-        S.t_start[k] = s0;
-        S.t_sh[k][0] = (signed char)sh[0];
-        S.t_sh[k][1] = (signed char)sh[1];
-        S.t_sh[k][2] = (signed char)sh[2];
-      }
-      uint32_t x = cnt;  // inclusive warp scan
-#pragma unroll
-      for (int o = 1; o < 32; o <<= 1) {
-        const uint32_t y = __shfl_up_sync(0xffffffffu, x, o);
-        if (lane >= o) x += y;
-      }
-      if (k < K) S.cum[k] = carry + x - cnt;
-      carry += __shfl_sync(0xffffffffu, x, 31);
-    }
-    if (lane == 0) {
-      S.cum[K] = carry;
-      S.total = carry;
-    }
+    slot_tables(g, cstart, cend, S, umap, ustart, &U);
   }
   __syncthreads();
 }
+
+// CTA prologue for pair-pass unit u (warp 0, one CTA barrier): the unit's target
+// range (its cells are consecutive in the cell list and in particle order), the
+// union stencil of its cells, and the slot tables.
+__device__ void unit_setup(const Grid& g, uint32_t u, const uint32_t* __restrict__ ulist,
+                           const uint32_t* __restrict__ clist, const uint32_t* __restrict__ cstart,
+                           const uint32_t* __restrict__ cend,
+                           const unsigned long long* __restrict__ chmax, CellSm& S) {
+  if (threadIdx.x < 32) {
+    if (threadIdx.x == 0) {
+      const uint32_t cf = clist[ulist[u]], cl = clist[ulist[u + 1] - 1];
+      cell_coords(g, cf, S.c3);
+      S.sc = cstart[cf];
+      S.ec = cend[cl];
+      make_unit_stencil(g, S.c3, cstart, cend, chmax, S.st);
+      S.kself = -1;
+    }
+    __syncwarp();
+    slot_tables(g, cstart, cend, S, nullptr, nullptr, nullptr);
+  }
+  __syncthreads();
+}
+
+// Dynamic claims of work chunks from a global counter, the next claim issued one
+// chunk ahead (its atomic's latency overlaps the current chunk instead of stalling
+// every warp at the claim barrier: ncu put 3-6 % of the pair passes there).
+struct ChunkClaim {
+  uint32_t* work;
+  uint32_t step, nxt;
+  __device__ __forceinline__ uint32_t first(uint32_t* s_chunk) {
+    if (threadIdx.x == 0) *s_chunk = atomicAdd(work, step);
+    __syncthreads();
+    const uint32_t v = *s_chunk;
+    __syncthreads();
+    if (threadIdx.x == 0) nxt = atomicAdd(work, step);  // lands while this chunk runs
+    return v;
+  }
+  __device__ __forceinline__ uint32_t next(uint32_t* s_chunk) {
+    if (threadIdx.x == 0) *s_chunk = nxt;
+    __syncthreads();
+    const uint32_t v = *s_chunk;
+    __syncthreads();
+    if (threadIdx.x == 0) nxt = atomicAdd(work, step);
+    return v;
+  }
+};
 
 // slot of flat index f: the largest k < K with cum[k] <= f (skips empty slots)
 __device__ __forceinline__ int slot_of(const CellSm& S, uint32_t f) {
@@ -508,6 +572,10 @@ __global__ void __launch_bounds__(kCT, 2) k_search(const double* __restrict__ x,
   __shared__ float4 tlo[kSearchTiles], thi[kSearchTiles];  // per staged tile: fp32 bounding box
   __shared__ uint32_t tcount[kTgt];
   __shared__ TgtW TW[kTgt];  // per target of the block: computed once, in parallel
+  // rows are written in unit-stencil numbering (stencil.cuh): cell slot -> unit slot,
+  // and the cell start of each unit slot the cell's stencil covers (exact test)
+  __shared__ uint16_t umap[kSlots];
+  __shared__ uint32_t ustart[kSlots];
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const unsigned lt = (1u << lane) - 1u;
   const uint32_t ncl = *nclist;
@@ -522,7 +590,7 @@ __global__ void __launch_bounds__(kCT, 2) k_search(const double* __restrict__ x,
     __syncthreads();
     if (cfirst >= ncl) break;
     for (uint32_t ci = cfirst; ci < min(ncl, cfirst + (uint32_t)kCellChunk); ++ci) {
-      cell_setup(g, clist[ci], cstart, cend, chmax, S);
+      cell_setup(g, clist[ci], cstart, cend, chmax, S, umap, ustart);
       const Stencil st = S.st;
       double org[3], M = 0.0;
   #pragma unroll
@@ -567,7 +635,7 @@ __global__ void __launch_bounds__(kCT, 2) k_search(const double* __restrict__ x,
             v.x = (float)((x[j] + sh[0]) - org[0]);
             v.y = (float)((y[j] + sh[1]) - org[1]);
             v.z = (float)((z[j] + sh[2]) - org[2]);
-            v.w = __uint_as_float(((uint32_t)slot << kLocalBits) | l);
+            v.w = __uint_as_float(((uint32_t)umap[slot] << kLocalBits) | l);
             cand[q] = v;
             if constexpr (SYM) candb[q] = band32(h[j], M);
           }
@@ -613,8 +681,9 @@ __global__ void __launch_bounds__(kCT, 2) k_search(const double* __restrict__ x,
             const TgtW& TB = TW[tb - t0];
             const float ax0 = TA.f[0], ay0 = TA.f[1], az0 = TA.f[2], lo0 = TA.f[3], hi0 = TA.f[4];
             const float ax1 = TB.f[0], ay1 = TB.f[1], az1 = TB.f[2], lo1 = TB.f[3], hi1 = TB.f[4];
-            const uint32_t self0 = ((uint32_t)S.kself << kLocalBits) | (ta - S.sc);
-            const uint32_t self1 = ((uint32_t)S.kself << kLocalBits) | (tb - S.sc);
+            const uint32_t uself = (uint32_t)umap[S.kself] << kLocalBits;
+            const uint32_t self0 = uself | (ta - S.sc);
+            const uint32_t self1 = uself | (tb - S.sc);
             uint32_t cnt0 = tcount[ta - t0], cnt1 = tcount[tb - t0];
             uint32_t* row0 = nbr + (size_t)ta * maxn;
             uint32_t* row1 = nbr + (size_t)tb * maxn;
@@ -647,7 +716,7 @@ __global__ void __launch_bounds__(kCT, 2) k_search(const double* __restrict__ x,
             // rare: exact fp64 test of the candidates inside a band (one ballot per step)
             auto exact = [&](const float4 cd, bool& hit0, bool& hit1, bool amb0, bool amb1) {
               const uint32_t pk = __float_as_uint(cd.w);
-              const uint32_t j = S.t_start[pk >> kLocalBits] + (pk & kLocalMask);
+              const uint32_t j = ustart[pk >> kLocalBits] + (pk & kLocalMask);
               double limb = 0.0;
               if constexpr (SYM) {
                 if (amb0 | amb1) {
@@ -798,12 +867,12 @@ struct DensBody {
 };
 
 template <int N, bool W2, int KM>
-__global__ void __launch_bounds__(kCTD, 2) k_density_c(
+__global__ void __launch_bounds__(kCTD, 1) k_density_c(
     const double* __restrict__ x, const double* __restrict__ y, const double* __restrict__ z,
     const double* __restrict__ h, const double* __restrict__ m, const double* __restrict__ u,
     Grid g, const uint32_t* __restrict__ cstart, const uint32_t* __restrict__ cend,
     const unsigned long long* __restrict__ chmax, const uint32_t* __restrict__ clist,
-    const uint32_t* __restrict__ nclist, uint32_t* __restrict__ work, const uint32_t* __restrict__ nbr,
+    const uint32_t* __restrict__ nclist, const uint32_t* __restrict__ ulist, const uint32_t* __restrict__ nulist, uint32_t* __restrict__ work, const uint32_t* __restrict__ nbr,
     const uint32_t* __restrict__ ncount, int maxn, Phys ph, double* __restrict__ rho,
     double* __restrict__ omega, double* __restrict__ p, double* __restrict__ cs,
     double* __restrict__ wB, double* __restrict__ ih2, double* __restrict__ vol,
@@ -813,26 +882,23 @@ __global__ void __launch_bounds__(kCTD, 2) k_density_c(
   double2* s01 = reinterpret_cast<double2*>(dsm);
   double2* s23 = s01 + kDensCap;
   __shared__ CellSm S;
-  __shared__ uint32_t s_n[kTgt], s_cur[kTgt];
-  __shared__ double tx[kTgt], ty[kTgt], tz[kTgt], tih2[kTgt], acc0[kTgt], acc1[kTgt];
+  __shared__ uint32_t s_n[kTgtU], s_cur[kTgtU];
+  __shared__ double tx[kTgtU], ty[kTgtU], tz[kTgtU], tih2[kTgtU], acc0[kTgtU], acc1[kTgtU];
   const int lane = threadIdx.x & 31;
-  const uint32_t ncl = *nclist;
   __shared__ uint32_t s_chunk;
   const int n = N > 0 ? N : ph.n;
   // cells in chunks of kCellChunk consecutive (Morton-order) cells claimed from a
   // counter: consecutive cells share most of their stencil, so a CTA's next staging
   // finds its sources in L2 (a grid stride left the re-reads to HBM)
-  for (;;) {
-    if (threadIdx.x == 0) s_chunk = atomicAdd(work, (uint32_t)kCellChunk);
-    __syncthreads();
-    const uint32_t cfirst = s_chunk;
-    __syncthreads();
-    if (cfirst >= ncl) break;
-    for (uint32_t ci = cfirst; ci < min(ncl, cfirst + (uint32_t)kCellChunk); ++ci) {
-      cell_setup(g, clist[ci], cstart, cend, chmax, S);
+  const uint32_t nun = *nulist;
+  const uint32_t uchunk = (uint32_t)kCellChunk >> g.ubits ? (uint32_t)kCellChunk >> g.ubits : 1u;
+  ChunkClaim claim{work, uchunk, 0u};
+  for (uint32_t cfirst = claim.first(&s_chunk); cfirst < nun; cfirst = claim.next(&s_chunk)) {
+    for (uint32_t ci = cfirst; ci < min(nun, cfirst + uchunk); ++ci) {
+      unit_setup(g, ci, ulist, clist, cstart, cend, chmax, S);
       const Stencil st = S.st;
-      for (uint32_t t0 = S.sc; t0 < S.ec; t0 += kTgt) {
-        const uint32_t t1 = min(S.ec, t0 + kTgt);
+      for (uint32_t t0 = S.sc; t0 < S.ec; t0 += kTgtU) {
+        const uint32_t t1 = min(S.ec, t0 + kTgtU);
         for (uint32_t t = t0 + threadIdx.x; t < t1; t += blockDim.x) {
           const uint32_t i = t - t0;
           s_n[i] = ncount[t];
@@ -937,11 +1003,11 @@ __global__ void __launch_bounds__(kCTD, 2) k_density_c(
 
 // ------------------------------------------------------------------ a8 IAD
 template <int N, bool W2, int KM>
-__global__ void __launch_bounds__(kCTD, 2) k_iad_c(
+__global__ void __launch_bounds__(kCTD, 1) k_iad_c(
     const double* __restrict__ x, const double* __restrict__ y, const double* __restrict__ z,
     Grid g, const uint32_t* __restrict__ cstart, const uint32_t* __restrict__ cend,
     const unsigned long long* __restrict__ chmax, const uint32_t* __restrict__ clist,
-    const uint32_t* __restrict__ nclist, uint32_t* __restrict__ work, const uint32_t* __restrict__ nbr,
+    const uint32_t* __restrict__ nclist, const uint32_t* __restrict__ ulist, const uint32_t* __restrict__ nulist, uint32_t* __restrict__ work, const uint32_t* __restrict__ nbr,
     const uint32_t* __restrict__ ncount, int maxn, Phys ph, const double* __restrict__ wB,
     const double* __restrict__ ih2, const double* __restrict__ vol, double* __restrict__ c11,
     double* __restrict__ c12, double* __restrict__ c13, double* __restrict__ c22,
@@ -949,29 +1015,26 @@ __global__ void __launch_bounds__(kCTD, 2) k_iad_c(
     int64_t ct_stride, unsigned long long* __restrict__ cnt) {
   extern __shared__ double dsm[];
   double2* s01 = reinterpret_cast<double2*>(dsm);
-  double2* s23 = s01 + kDensCap;
+  double2* s23 = s01 + kIadCap;
   __shared__ CellSm S;
-  __shared__ uint32_t s_n[kTgt], s_cur[kTgt];
-  __shared__ double tx[kTgt], ty[kTgt], tz[kTgt], tih2[kTgt];
-  __shared__ double acc[6][kTgt];
+  __shared__ uint32_t s_n[kTgtU], s_cur[kTgtU];
+  __shared__ double tx[kTgtU], ty[kTgtU], tz[kTgtU], tih2[kTgtU];
+  __shared__ double acc[6][kTgtU];
   const int lane = threadIdx.x & 31;
-  const uint32_t ncl = *nclist;
   __shared__ uint32_t s_chunk;
   const int n = N > 0 ? N : ph.n;
   // cells in chunks of kCellChunk consecutive (Morton-order) cells claimed from a
   // counter: consecutive cells share most of their stencil, so a CTA's next staging
   // finds its sources in L2 (a grid stride left the re-reads to HBM)
-  for (;;) {
-    if (threadIdx.x == 0) s_chunk = atomicAdd(work, (uint32_t)kCellChunk);
-    __syncthreads();
-    const uint32_t cfirst = s_chunk;
-    __syncthreads();
-    if (cfirst >= ncl) break;
-    for (uint32_t ci = cfirst; ci < min(ncl, cfirst + (uint32_t)kCellChunk); ++ci) {
-      cell_setup(g, clist[ci], cstart, cend, chmax, S);
+  const uint32_t nun = *nulist;
+  const uint32_t uchunk = (uint32_t)kCellChunk >> g.ubits ? (uint32_t)kCellChunk >> g.ubits : 1u;
+  ChunkClaim claim{work, uchunk, 0u};
+  for (uint32_t cfirst = claim.first(&s_chunk); cfirst < nun; cfirst = claim.next(&s_chunk)) {
+    for (uint32_t ci = cfirst; ci < min(nun, cfirst + uchunk); ++ci) {
+      unit_setup(g, ci, ulist, clist, cstart, cend, chmax, S);
       const Stencil st = S.st;
-      for (uint32_t t0 = S.sc; t0 < S.ec; t0 += kTgt) {
-        const uint32_t t1 = min(S.ec, t0 + kTgt);
+      for (uint32_t t0 = S.sc; t0 < S.ec; t0 += kTgtU) {
+        const uint32_t t1 = min(S.ec, t0 + kTgtU);
         for (uint32_t t = t0 + threadIdx.x; t < t1; t += blockDim.x) {
           const uint32_t i = t - t0;
           s_n[i] = ncount[t];
@@ -984,8 +1047,8 @@ __global__ void __launch_bounds__(kCTD, 2) k_iad_c(
         }
         if (threadIdx.x == 0) S.next[0] = 0;
         __syncthreads();
-        for (uint32_t gb = 0, gi = 0; gb < S.total; gb += kDensCap, ++gi) {
-          const uint32_t ge = min(S.total, gb + kDensCap), pend = pend_of(S, ge);
+        for (uint32_t gb = 0, gi = 0; gb < S.total; gb += kIadCap, ++gi) {
+          const uint32_t ge = min(S.total, gb + kIadCap), pend = pend_of(S, ge);
           if (threadIdx.x == 0) S.next[(gi + 1) & 1] = 0;
           stage2x2(g, S, gb, ge, x, y, z, vol, s01, s23);
           __syncthreads();
@@ -1094,19 +1157,19 @@ template <int N, bool W2, int KM>
 __global__ void __launch_bounds__(kCTM, 1) k_momentum_c(
     MomSrc src, MomTgt tg, MomOut out, Grid g, const uint32_t* __restrict__ cstart,
     const uint32_t* __restrict__ cend, const unsigned long long* __restrict__ chmax,
-    const uint32_t* __restrict__ clist, const uint32_t* __restrict__ nclist, uint32_t* __restrict__ work,
+    const uint32_t* __restrict__ clist, const uint32_t* __restrict__ nclist,
+    const uint32_t* __restrict__ ulist, const uint32_t* __restrict__ nulist, uint32_t* __restrict__ work,
     const uint32_t* __restrict__ nbr, const uint32_t* __restrict__ ncount, int maxn, Phys ph,
     double* __restrict__ dts, unsigned long long* __restrict__ cnt) {
-  extern __shared__ double dsm[];  // kMomPairs * kMomCap double2 staged + T_N * kTgt target fields
+  extern __shared__ double dsm[];  // kMomPairs * kMomCap double2 staged + T_N * kTgtU target fields
   double2* const F2 = reinterpret_cast<double2*>(dsm);
   double* const T = dsm + 2 * kMomPairs * kMomCap;
   __shared__ CellSm S;
-  __shared__ uint32_t s_n[kTgt], s_cur[kTgt];
-  __shared__ double acc[5][kTgt];
+  __shared__ uint32_t s_n[kTgtU], s_cur[kTgtU];
+  __shared__ double acc[5][kTgtU];
   __shared__ double shdt[kNWM];
   __shared__ unsigned long long shco;
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  const uint32_t ncl = *nclist;
   __shared__ uint32_t s_chunk;
   const int n = N > 0 ? N : ph.n;
   double dtmin = INFINITY;
@@ -1114,38 +1177,36 @@ __global__ void __launch_bounds__(kCTM, 1) k_momentum_c(
   // cells in chunks of kCellChunk consecutive (Morton-order) cells claimed from a
   // counter: consecutive cells share most of their stencil, so a CTA's next staging
   // finds its sources in L2 (a grid stride left the re-reads to HBM)
-  for (;;) {
-    if (threadIdx.x == 0) s_chunk = atomicAdd(work, (uint32_t)kCellChunk);
-    __syncthreads();
-    const uint32_t cfirst = s_chunk;
-    __syncthreads();
-    if (cfirst >= ncl) break;
-    for (uint32_t ci = cfirst; ci < min(ncl, cfirst + (uint32_t)kCellChunk); ++ci) {
-      cell_setup(g, clist[ci], cstart, cend, chmax, S);
+  const uint32_t nun = *nulist;
+  const uint32_t uchunk = (uint32_t)kCellChunk >> g.ubits ? (uint32_t)kCellChunk >> g.ubits : 1u;
+  ChunkClaim claim{work, uchunk, 0u};
+  for (uint32_t cfirst = claim.first(&s_chunk); cfirst < nun; cfirst = claim.next(&s_chunk)) {
+    for (uint32_t ci = cfirst; ci < min(nun, cfirst + uchunk); ++ci) {
+      unit_setup(g, ci, ulist, clist, cstart, cend, chmax, S);
       const Stencil st = S.st;
-      for (uint32_t t0 = S.sc; t0 < S.ec; t0 += kTgt) {
-        const uint32_t t1 = min(S.ec, t0 + kTgt);
+      for (uint32_t t0 = S.sc; t0 < S.ec; t0 += kTgtU) {
+        const uint32_t t1 = min(S.ec, t0 + kTgtU);
         for (uint32_t t = t0 + threadIdx.x; t < t1; t += blockDim.x) {
           const uint32_t i = t - t0;
           s_n[i] = ncount[t];
           s_cur[i] = 0;
-          T[T_X * kTgt + i] = src.x[t];
-          T[T_Y * kTgt + i] = src.y[t];
-          T[T_Z * kTgt + i] = src.z[t];
-          T[T_VX * kTgt + i] = src.vx[t];
-          T[T_VY * kTgt + i] = src.vy[t];
-          T[T_VZ * kTgt + i] = src.vz[t];
-          T[T_IH2 * kTgt + i] = src.ih2[t];
-          T[T_WB * kTgt + i] = tg.wB[t];
-          T[T_RINV * kTgt + i] = tg.rinv[t];
-          T[T_XP * kTgt + i] = tg.X[t];
-          T[T_C * kTgt + i] = src.c[t];
-          T[T_A11 * kTgt + i] = tg.c11[t];
-          T[T_A12 * kTgt + i] = tg.c12[t];
-          T[T_A13 * kTgt + i] = tg.c13[t];
-          T[T_A22 * kTgt + i] = tg.c22[t];
-          T[T_A23 * kTgt + i] = tg.c23[t];
-          T[T_A33 * kTgt + i] = tg.c33[t];
+          T[T_X * kTgtU + i] = src.x[t];
+          T[T_Y * kTgtU + i] = src.y[t];
+          T[T_Z * kTgtU + i] = src.z[t];
+          T[T_VX * kTgtU + i] = src.vx[t];
+          T[T_VY * kTgtU + i] = src.vy[t];
+          T[T_VZ * kTgtU + i] = src.vz[t];
+          T[T_IH2 * kTgtU + i] = src.ih2[t];
+          T[T_WB * kTgtU + i] = tg.wB[t];
+          T[T_RINV * kTgtU + i] = tg.rinv[t];
+          T[T_XP * kTgtU + i] = tg.X[t];
+          T[T_C * kTgtU + i] = src.c[t];
+          T[T_A11 * kTgtU + i] = tg.c11[t];
+          T[T_A12 * kTgtU + i] = tg.c12[t];
+          T[T_A13 * kTgtU + i] = tg.c13[t];
+          T[T_A22 * kTgtU + i] = tg.c22[t];
+          T[T_A23 * kTgtU + i] = tg.c23[t];
+          T[T_A33 * kTgtU + i] = tg.c33[t];
           acc[0][i] = 0.0;
           acc[1][i] = 0.0;
           acc[2][i] = 0.0;
@@ -1190,12 +1251,12 @@ __global__ void __launch_bounds__(kCTM, 1) k_momentum_c(
             double xa, ya, za, vxa, vya, vza, ih2a, wBa, rinva, Xa, ca, a11, a12, a13, a22, a23, a33;
             double fx, fy, fz, fu, vs;
             __device__ __forceinline__ void begin(uint32_t i) {
-              xa = T[T_X * kTgt + i]; ya = T[T_Y * kTgt + i]; za = T[T_Z * kTgt + i];
-              vxa = T[T_VX * kTgt + i]; vya = T[T_VY * kTgt + i]; vza = T[T_VZ * kTgt + i];
-              ih2a = T[T_IH2 * kTgt + i]; wBa = T[T_WB * kTgt + i]; rinva = T[T_RINV * kTgt + i];
-              Xa = T[T_XP * kTgt + i]; ca = T[T_C * kTgt + i];
-              a11 = T[T_A11 * kTgt + i]; a12 = T[T_A12 * kTgt + i]; a13 = T[T_A13 * kTgt + i];
-              a22 = T[T_A22 * kTgt + i]; a23 = T[T_A23 * kTgt + i]; a33 = T[T_A33 * kTgt + i];
+              xa = T[T_X * kTgtU + i]; ya = T[T_Y * kTgtU + i]; za = T[T_Z * kTgtU + i];
+              vxa = T[T_VX * kTgtU + i]; vya = T[T_VY * kTgtU + i]; vza = T[T_VZ * kTgtU + i];
+              ih2a = T[T_IH2 * kTgtU + i]; wBa = T[T_WB * kTgtU + i]; rinva = T[T_RINV * kTgtU + i];
+              Xa = T[T_XP * kTgtU + i]; ca = T[T_C * kTgtU + i];
+              a11 = T[T_A11 * kTgtU + i]; a12 = T[T_A12 * kTgtU + i]; a13 = T[T_A13 * kTgtU + i];
+              a22 = T[T_A22 * kTgtU + i]; a23 = T[T_A23 * kTgtU + i]; a33 = T[T_A33 * kTgtU + i];
               fx = fy = fz = fu = 0.0;
               vs = -1.0;
             }
@@ -1269,7 +1330,7 @@ __global__ void __launch_bounds__(kCTM, 1) k_momentum_c(
         for (uint32_t t = t0 + threadIdx.x; t < t1; t += blockDim.x) {
           const uint32_t i = t - t0;
           double vsig = acc[4][i];
-          if (vsig < 0.0) vsig = 2.0 * T[T_C * kTgt + i];  // no interacting neighbour
+          if (vsig < 0.0) vsig = 2.0 * T[T_C * kTgtU + i];  // no interacting neighbour
           out.ax[t] = acc[0][i];
           out.ay[t] = acc[1][i];
           out.az[t] = acc[2][i];
@@ -1339,9 +1400,9 @@ static void density_t(sph_ctx* c) {
   set_smem(k_density_c<N, W2, KM>, smem);
   sph_particles& P = c->P;
   cudaMemsetAsync(c->s.work + 1, 0, sizeof(uint32_t), c->stream);
-  k_density_c<N, W2, KM><<<cell_grid(c, 2), kCTD, smem, c->stream>>>(
+  k_density_c<N, W2, KM><<<cell_grid(c, 1), kCTD, smem, c->stream>>>(
       P.x, P.y, P.z, P.h, P.m, P.u, c->grid, c->s.cell_start, c->s.cell_end, c->s.cell_hmax,
-      c->s.cell_list, c->s.ncell_list, c->s.work + 1, c->s.nbr, c->s.ncount, c->maxn, c->phys, P.rho, P.omega,
+      c->s.cell_list, c->s.ncell_list, c->s.unit_list, c->s.nunit_list, c->s.work + 1, c->s.nbr, c->s.ncount, c->maxn, c->phys, P.rho, P.omega,
       P.p, P.c, c->s.wB, c->s.ih2, c->s.vol, c->s.rinv, c->s.X, c->s.mX, c->s.cnt);
 }
 
@@ -1372,13 +1433,13 @@ int launch_density(sph_ctx* c) {
 
 template <int N, bool W2, int KM>
 static void iad_t(sph_ctx* c) {
-  const size_t smem = 4 * kDensCap * sizeof(double);
+  const size_t smem = 4 * kIadCap * sizeof(double);
   set_smem(k_iad_c<N, W2, KM>, smem);
   sph_particles& P = c->P;
   cudaMemsetAsync(c->s.work + 2, 0, sizeof(uint32_t), c->stream);
-  k_iad_c<N, W2, KM><<<cell_grid(c, 2), kCTD, smem, c->stream>>>(
+  k_iad_c<N, W2, KM><<<cell_grid(c, 1), kCTD, smem, c->stream>>>(
       P.x, P.y, P.z, c->grid, c->s.cell_start, c->s.cell_end, c->s.cell_hmax, c->s.cell_list,
-      c->s.ncell_list, c->s.work + 2, c->s.nbr, c->s.ncount, c->maxn, c->phys, c->s.wB, c->s.ih2, c->s.vol,
+      c->s.ncell_list, c->s.unit_list, c->s.nunit_list, c->s.work + 2, c->s.nbr, c->s.ncount, c->maxn, c->phys, c->s.wB, c->s.ih2, c->s.vol,
       P.c11, P.c12, P.c13, P.c22, P.c23, P.c33, c->s.ct, c->cap, c->s.cnt);
 }
 
@@ -1389,7 +1450,7 @@ int launch_iad(sph_ctx* c) {
 
 template <int N, bool W2, int KM>
 static void momentum_t(sph_ctx* c) {
-  const size_t smem = ((size_t)2 * kMomPairs * kMomCap + (size_t)T_N * kTgt) * sizeof(double);
+  const size_t smem = ((size_t)2 * kMomPairs * kMomCap + (size_t)T_N * kTgtU) * sizeof(double);
   set_smem(k_momentum_c<N, W2, KM>, smem);
   sph_particles& P = c->P;
   MomSrc src = {P.x, P.y, P.z, P.vx, P.vy, P.vz, P.m, c->s.ih2, P.c, c->s.mX, c->s.vol, c->s.ct, c->cap};
@@ -1398,7 +1459,7 @@ static void momentum_t(sph_ctx* c) {
   cudaMemsetAsync(c->s.work + 3, 0, sizeof(uint32_t), c->stream);
   k_momentum_c<N, W2, KM><<<cell_grid(c, 1), kCTM, smem, c->stream>>>(
       src, tg, out, c->grid, c->s.cell_start, c->s.cell_end, c->s.cell_hmax, c->s.cell_list,
-      c->s.ncell_list, c->s.work + 3, c->s.nbr, c->s.ncount, c->maxn, c->phys, c->s.dts, c->s.cnt);
+      c->s.ncell_list, c->s.unit_list, c->s.nunit_list, c->s.work + 3, c->s.nbr, c->s.ncount, c->maxn, c->phys, c->s.dts, c->s.cnt);
 }
 
 int launch_momentum(sph_ctx* c) {

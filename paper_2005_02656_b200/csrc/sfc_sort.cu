@@ -417,6 +417,34 @@ __global__ void k_cell_hmax(const uint32_t* __restrict__ list, const uint32_t* _
   }
 }
 
+// first particle of each pair-pass unit (the cells sharing Morton code >> ubits)
+__global__ void k_unit_flags(const uint64_t* __restrict__ keys, int64_t n, Grid g,
+                             uint32_t* __restrict__ flag) {
+  const int sh = g.kshift + g.ubits;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    const uint64_t u = sh >= 64 ? 0 : keys[i] >> sh;
+    flag[i] = (i == 0 || (sh >= 64 ? 0 : keys[i - 1] >> sh) != u) ? 1u : 0u;
+  }
+}
+
+// unit list: index into the cell list of each unit's first cell, plus the end
+// sentinel list[nunit] = ncell_list (a unit spans cells list[u] .. list[u+1]-1)
+__global__ void k_unit_list(int64_t n, const uint32_t* __restrict__ uflag,
+                            const uint32_t* __restrict__ urank, const uint32_t* __restrict__ cflag,
+                            const uint32_t* __restrict__ crank, uint32_t* __restrict__ list,
+                            uint32_t* __restrict__ nlist) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    if (uflag[i]) list[urank[i]] = crank[i];  // the unit's first particle heads its first cell
+    if (i == n - 1) {
+      const uint32_t nu = urank[i] + uflag[i];
+      *nlist = nu;
+      list[nu] = crank[i] + cflag[i];
+    }
+  }
+}
+
 // cell ranges of the halo segment [i0, i0 + n) (sorted; cells disjoint from owned ones)
 __global__ void k_cells_range(const uint64_t* __restrict__ keys, int64_t i0, int64_t n, Grid g,
                               uint32_t* __restrict__ cstart, uint32_t* __restrict__ cend) {
@@ -446,6 +474,7 @@ int launch_cells(sph_ctx* c) {
   cudaMemsetAsync(c->s.cell_end, 0, sizeof(uint32_t) * c->grid.ncell, c->stream);
   if (n == 0) {  // a rank may own no particle
     cudaMemsetAsync(c->s.ncell_list, 0, sizeof(uint32_t), c->stream);
+    cudaMemsetAsync(c->s.nunit_list, 0, sizeof(uint32_t), c->stream);
     return 0;
   }
   const int nb = grid_blocks(c, n, 256, 8);
@@ -456,7 +485,12 @@ int launch_cells(sph_ctx* c) {
                                          c->s.cell_list, c->s.ncell_list);
   k_cell_hmax<<<grid_blocks(c, n, 256, 8), 256, 0, c->stream>>>(
       c->s.cell_list, c->s.ncell_list, c->s.cell_start, c->s.cell_end, c->P.h, c->s.cell_hmax);
-  return k + 2;
+  // pair-pass units (stencil.cuh): heads where the unit key changes, scanned into a list
+  k_unit_flags<<<nb, 256, 0, c->stream>>>(c->s.keys, n, c->grid, c->s.unit_flag);
+  k += scan_excl(c, c->s.unit_flag, c->s.unit_rank, n);
+  k_unit_list<<<nb, 256, 0, c->stream>>>(n, c->s.unit_flag, c->s.unit_rank, c->s.cell_flag,
+                                         c->s.cell_rank, c->s.unit_list, c->s.nunit_list);
+  return k + 4;
 }
 
 }  // namespace sphb

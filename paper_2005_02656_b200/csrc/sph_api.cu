@@ -166,6 +166,26 @@ sph_status choose_grid(sph_ctx* c, const double* bb, int64_t n) {
   g.sbits = std::max(0, std::min(3, (63 - 3 * g.cbits - g.idbits) / 3));
   g.kshift = g.idbits + 3 * g.sbits;
   g.hsym = c->phys.sym ? bb[6] : 0.0;
+  // pair-pass units (stencil.cuh): 2x2x1 cell blocks unless a periodic dim is so short
+  // that stencils wrap onto themselves, or the unit stencil would exceed kKMax slots
+  {
+    static const int want = [] {
+      const char* e = getenv("SPH_UNIT_BITS");  // A/B runs only
+      const int v = e ? atoi(e) : 2;
+      return v < 0 ? 0 : (v > 2 ? 2 : v);
+    }();
+    int ub = want;
+    for (int d = 0; d < 3; ++d)
+      if (g.periodic[d] && 2 * stencil_radius(g, d, reach_of(bb[6])) + 1 >= g.nc[d]) ub = 0;
+    for (; ub > 0; --ub) {
+      int64_t K = 1;
+      for (int d = 0; d < 3; ++d)
+        K *= std::min<int64_t>(2 * stencil_radius(g, d, reach_of(bb[6])) + 1 + (ub > d ? 1 : 0),
+                               g.nc[d]);
+      if (K <= kKMax) break;
+    }
+    g.ubits = ub;
+  }
   return SPH_OK;
 }
 
@@ -275,6 +295,10 @@ sph_status sph_init(const sph_params* prm, int64_t capacity, sph_ctx** out) {
   AL(s.cell_rank, cap);
   AL(s.cell_list, cap);
   AL(s.ncell_list, 1);
+  AL(s.unit_flag, cap);
+  AL(s.unit_rank, cap);
+  AL(s.unit_list, cap + 1);
+  AL(s.nunit_list, 1);
   AL(s.mX, cap);
   AL(s.ct, 6 * cap);
   AL(s.nbr, cap * (int64_t)c->maxn);
@@ -424,6 +448,7 @@ sph_status sph_find_neighbors(sph_ctx* c) {
   if (!multi && c->P.n == 0) {
     c->nbr_total = c->nbr_max = 0;
     CK(cudaMemsetAsync(c->s.ncell_list, 0, sizeof(uint32_t), c->stream));
+    CK(cudaMemsetAsync(c->s.nunit_list, 0, sizeof(uint32_t), c->stream));
     c->stage = 1;
     return SPH_OK;
   }
@@ -522,10 +547,8 @@ sph_status sph_get_neighbors(sph_ctx* c, int64_t* offsets, int64_t* ids, int64_t
       const int64_t cell = key_cell_hd(g, keys[r0 + i]);
       int c3[3];
       cell_coords(g, cell, c3);
-      double hm;
-      memcpy(&hm, &chm[cell], sizeof(double));
-      Stencil st;
-      make_stencil(g, c3, cell_reach(g, hm), st);
+      Stencil st;  // rows are numbered in the slots of the target's unit stencil
+      make_unit_stencil(g, c3, cs.data(), ce.data(), chm.data(), st);
       for (uint32_t k = 0; k < cnt[r0 + i]; ++k) {
         const uint32_t e = rows[(size_t)i * c->maxn + k];
         int sh[3];
@@ -746,7 +769,7 @@ sph_status sph_destroy(sph_ctx* c) {
   Scratch& s = c->s;
   void* ptrs[] = {s.keys, s.keys_alt, s.idx, s.idx_alt, s.hist, s.scan_tmp, s.gather, s.gather_id,
                   s.cell_start, s.cell_end, s.cell_hmax, s.cell_flag, s.cell_rank, s.cell_list,
-                  s.ncell_list, s.nbr, s.ncount, s.nbr_maxcount, s.work, s.wB, s.ih2, s.vol, s.rinv, s.X,
+                  s.ncell_list, s.unit_flag, s.unit_rank, s.unit_list, s.nunit_list, s.nbr, s.ncount, s.nbr_maxcount, s.work, s.wB, s.ih2, s.vol, s.rinv, s.X,
                   s.mX, s.ct, s.red, s.bbox, s.dts, s.cnt, s.diag, s.ktable};
   for (void* p : ptrs)
     if (p) cudaFree(p);

@@ -387,7 +387,10 @@ bool dist_splitters(sph_ctx* c) {
   Dist& D = *c->dist;
   const Grid& g = c->grid;
   const int mbits = 3 * g.cbits;
+  // bins are whole pair-pass units (shift >= ubits): a unit never straddles two ranks,
+  // so every rank stages the same unit stencils as one GPU does (bit-identical sums)
   D.shift = mbits > kBinBits ? mbits - kBinBits : 0;
+  if (D.shift < g.ubits) D.shift = g.ubits < mbits ? g.ubits : mbits;
   D.nbins = (int64_t)1 << (mbits - D.shift);
   CUK(cudaMemsetAsync(D.hist_d, 0, sizeof(unsigned long long) * D.nbins, c->stream));
   if (c->P.n) {

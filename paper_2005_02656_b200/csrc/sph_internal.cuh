@@ -34,6 +34,7 @@ struct Grid {
   int sbits;        // sub-cell Morton bits per dim between the cell code and the id
   int kshift;       // idbits + 3 sbits: key >> kshift = Morton code of the cell
   double hsym;      // symmetric relation: global h_max (every stencil reaches 2 max h); else 0
+  int ubits;        // pair-pass units: the cells sharing Morton code >> ubits (stencil.cuh)
   int64_t ncell;
 };
 
@@ -76,6 +77,10 @@ struct Scratch {
   uint32_t* cell_rank = nullptr;            // cap: exclusive scan of cell_flag
   uint32_t* cell_list = nullptr;            // non-empty cells in Morton order
   uint32_t* ncell_list = nullptr;           // device scalar
+  uint32_t* unit_flag = nullptr;            // cap: 1 at the first particle of a unit
+  uint32_t* unit_rank = nullptr;            // cap: exclusive scan of unit_flag
+  uint32_t* unit_list = nullptr;            // cap + 1: index into cell_list of each unit's first cell
+  uint32_t* nunit_list = nullptr;           // device scalar
   int64_t max_cells = 0;
   // neighbours
   uint32_t* nbr = nullptr;       // cap * maxn

@@ -9,6 +9,8 @@
 // particle order -- exactly the order in which candidates are staged.
 #pragma once
 
+#include <cstring>
+
 #include "sph_internal.cuh"
 
 namespace sphb {
@@ -106,6 +108,70 @@ __host__ __device__ __forceinline__ double reach_of(double hmax) {
 // particle that may reach into it (symmetric relation: the global h_max)
 __host__ __device__ __forceinline__ double cell_reach(const Grid& g, double cell_hmax) {
   return reach_of(cell_hmax > g.hsym ? cell_hmax : g.hsym);
+}
+
+// ---------------------------------------------------------------- pair-pass units
+// The pair passes give one CTA a UNIT of cells: the cells whose Morton codes agree
+// above the lowest g.ubits bits (ubits = 2: an aligned 2x2x1 block; 0: one cell).
+// Particles are sorted by cell Morton code, so a unit's targets are one contiguous
+// range, and the unit stages the UNION of its cells' stencils once: 4x4x3 = 48 cells
+// for four 27-cell stencils, i.e. 12 staged cells per target cell instead of 27.
+// Neighbour rows are written in the unit stencil's slot numbering; a cell's own
+// slots map into it monotonically (both enumerate z, then y, then x over unwrapped
+// coordinates), so rows stay sorted in the staging order.
+__host__ __device__ __forceinline__ void unit_base(const Grid& g, const int c3[3], int b3[3]) {
+  for (int d = 0; d < 3; ++d) b3[d] = g.ubits > d ? (c3[d] & ~1) : c3[d];
+}
+
+// Union (bounding box) of the stencils of the unit's non-empty cells; c3 is any
+// cell of the unit.  Depends only on those cells' ranges and h_max, so the search
+// (per cell) and the passes (per unit) build the same box on every rank.
+__host__ __device__ __forceinline__ void make_unit_stencil(const Grid& g, const int c3[3],
+                                                           const uint32_t* cstart, const uint32_t* cend,
+                                                           const unsigned long long* chmax, Stencil& u) {
+  int b3[3];
+  unit_base(g, c3, b3);
+  int lo[3] = {0, 0, 0}, hi[3] = {-1, -1, -1};
+  bool any = false;
+  const int w0 = g.ubits > 0 ? 2 : 1, w1 = g.ubits > 1 ? 2 : 1, w2 = g.ubits > 2 ? 2 : 1;
+  for (int dz = 0; dz < w2; ++dz)
+    for (int dy = 0; dy < w1; ++dy)
+      for (int dx = 0; dx < w0; ++dx) {
+        const int q[3] = {b3[0] + dx, b3[1] + dy, b3[2] + dz};
+        if (q[0] >= g.nc[0] || q[1] >= g.nc[1] || q[2] >= g.nc[2]) continue;
+        const int64_t cell = q[0] + (int64_t)g.nc[0] * (q[1] + (int64_t)g.nc[1] * q[2]);
+        const bool self = q[0] == c3[0] && q[1] == c3[1] && q[2] == c3[2];
+        if (!self && cstart[cell] >= cend[cell]) continue;  // empty cell: no stencil
+        const unsigned long long hb = chmax[cell];
+        double hm;
+#ifdef __CUDA_ARCH__
+        hm = __longlong_as_double((long long)hb);
+#else
+        memcpy(&hm, &hb, sizeof(double));
+#endif
+        Stencil s;
+        make_stencil(g, q, cell_reach(g, hm), s);
+        for (int d = 0; d < 3; ++d) {
+          const int l = s.lo[d], h = s.lo[d] + s.cnt[d] - 1;
+          lo[d] = any ? (l < lo[d] ? l : lo[d]) : l;
+          hi[d] = any ? (h > hi[d] ? h : hi[d]) : h;
+          u.wrap[d] = s.wrap[d];
+        }
+        any = true;
+      }
+  u.K = 1;
+  for (int d = 0; d < 3; ++d) {
+    u.lo[d] = lo[d];
+    u.cnt[d] = hi[d] - lo[d] + 1;
+    u.K *= u.cnt[d];
+  }
+}
+
+// unit-stencil slot of slot k of a cell stencil st (st's box lies inside u's)
+__host__ __device__ __forceinline__ int unit_slot(const Stencil& st, const Stencil& u, int k) {
+  const int i0 = k % st.cnt[0], i1 = (k / st.cnt[0]) % st.cnt[1], i2 = k / (st.cnt[0] * st.cnt[1]);
+  return (st.lo[0] + i0 - u.lo[0]) +
+         u.cnt[0] * ((st.lo[1] + i1 - u.lo[1]) + u.cnt[1] * (st.lo[2] + i2 - u.lo[2]));
 }
 
 }  // namespace sphb
