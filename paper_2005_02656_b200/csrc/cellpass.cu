@@ -27,8 +27,11 @@ constexpr int kTgtU = 416;        // pair passes: targets per sub-block (a whole
 constexpr int kSlots = kKMax;     // slot tables: every stencil the grid chooser admits
 constexpr int kCellChunk = 4;     // consecutive cells per claim (L2 reuse of shared stencils)
 constexpr int kSearchCap = 3072;  // staged candidates per group (float4)
-constexpr int kSearchTiles = kSearchCap / 32 + 1;          // + the sentinel tile
-constexpr int kSearchWords = (kSearchCap / 32 + 31) / 32;  // tile bitmask words
+constexpr int kTS = 32;           // search tile: candidates per fp32 bounding box (16 measured 2.7 ms slower)
+constexpr int kSearchTiles = kSearchCap / kTS + 1;          // + the sentinel tile
+constexpr int kSearchWords = (kSearchCap / kTS + 31) / 32;  // tile bitmask words
+static_assert(kTS == 16 || kTS == 32, "a tile is a half-warp or a warp of candidates");
+static_assert(kSearchWords <= 6, "tile mask held in six registers");
 constexpr int kDensCap = 4096;    // density: staged particles per group, 4 fp64 fields
 constexpr int kIadCap = 4096;     // IAD: the same fields
 constexpr int kMomCap = 992;      // staged particles per group, 17 fp64 fields (1 CTA/SM; a 48-cell unit stencil in 4 groups)
@@ -228,21 +231,60 @@ __device__ __forceinline__ void slot_tables(const Grid& g, const uint32_t* __res
   }
 }
 
-// CTA prologue for search cell c (warp 0, one CTA barrier): the cell's own stencil,
-// its slot tables, and the map of its slots into its unit's stencil.
-__device__ void cell_setup(const Grid& g, uint32_t c, const uint32_t* __restrict__ cstart,
-                           const uint32_t* __restrict__ cend,
+// Unit records (one thread per unit, once per step before the search): the union
+// stencil of the unit's cells and its target range, so a CTA prologue is one 48-byte
+// load instead of a serial chain of dependent cell-table loads (ncu: the prologue
+// barrier held 7-8 % of the search, density and IAD samples).
+__device__ __forceinline__ void pack_unit(const Stencil& u, uint32_t sc, uint32_t ec, int4* rec) {
+  rec[0] = make_int4(u.lo[0], u.lo[1], u.lo[2], u.K);
+  rec[1] = make_int4(u.cnt[0], u.cnt[1], u.cnt[2], u.wrap[0] | (u.wrap[1] << 2) | (u.wrap[2] << 4));
+  rec[2] = make_int4((int)sc, (int)ec, 0, 0);
+}
+__device__ __forceinline__ void unpack_unit(const int4* __restrict__ rec, Stencil& u, uint32_t& sc,
+                                            uint32_t& ec) {
+  const int4 a = rec[0], b = rec[1], c = rec[2];
+  u.lo[0] = a.x; u.lo[1] = a.y; u.lo[2] = a.z; u.K = a.w;
+  u.cnt[0] = b.x; u.cnt[1] = b.y; u.cnt[2] = b.z;
+  u.wrap[0] = b.w & 3; u.wrap[1] = (b.w >> 2) & 3; u.wrap[2] = (b.w >> 4) & 3;
+  sc = (uint32_t)c.x;
+  ec = (uint32_t)c.y;
+}
+
+__global__ void k_unit_prep(Grid g, const uint32_t* __restrict__ clist, const uint32_t* __restrict__ ulist,
+                            const uint32_t* __restrict__ nulist, const uint32_t* __restrict__ cstart,
+                            const uint32_t* __restrict__ cend, const unsigned long long* __restrict__ chmax,
+                            int4* __restrict__ urec, uint32_t* __restrict__ cunit) {
+  const uint32_t nu = *nulist;
+  for (uint32_t u = blockIdx.x * blockDim.x + threadIdx.x; u < nu; u += gridDim.x * blockDim.x) {
+    const uint32_t i0 = ulist[u], i1 = ulist[u + 1];
+    const uint32_t cf = clist[i0], cl = clist[i1 - 1];
+    int c3[3];
+    cell_coords(g, cf, c3);
+    Stencil st;
+    make_unit_stencil(g, c3, cstart, cend, chmax, st);
+    pack_unit(st, cstart[cf], cend[cl], urec + 3 * (size_t)u);
+    for (uint32_t i = i0; i < i1; ++i) cunit[i] = u;
+  }
+}
+
+// CTA prologue for search cell c = clist[ci] (warp 0, one CTA barrier): the cell's
+// own stencil, its slot tables, and the map of its slots into its unit's stencil.
+__device__ void cell_setup(const Grid& g, uint32_t ci, const uint32_t* __restrict__ clist,
+                           const uint32_t* __restrict__ cunit, const int4* __restrict__ urec,
+                           const uint32_t* __restrict__ cstart, const uint32_t* __restrict__ cend,
                            const unsigned long long* __restrict__ chmax, CellSm& S, uint16_t* umap,
                            uint32_t* ustart) {
   if (threadIdx.x < 32) {
     __shared__ Stencil U;
     if (threadIdx.x == 0) {
+      const uint32_t c = clist[ci], u = cunit[ci];
+      uint32_t usc, uec;
+      unpack_unit(urec + 3 * (size_t)u, U, usc, uec);
       cell_coords(g, c, S.c3);
       S.sc = cstart[c];
       S.ec = cend[c];
       make_stencil(g, S.c3, cell_reach(g, __longlong_as_double((long long)chmax[c])), S.st);
       S.kself = self_slot(S.st, S.c3);
-      make_unit_stencil(g, S.c3, cstart, cend, chmax, U);
     }
     __syncwarp();
     slot_tables(g, cstart, cend, S, umap, ustart, &U);
@@ -253,17 +295,15 @@ __device__ void cell_setup(const Grid& g, uint32_t c, const uint32_t* __restrict
 // CTA prologue for pair-pass unit u (warp 0, one CTA barrier): the unit's target
 // range (its cells are consecutive in the cell list and in particle order), the
 // union stencil of its cells, and the slot tables.
-__device__ void unit_setup(const Grid& g, uint32_t u, const uint32_t* __restrict__ ulist,
-                           const uint32_t* __restrict__ clist, const uint32_t* __restrict__ cstart,
-                           const uint32_t* __restrict__ cend,
-                           const unsigned long long* __restrict__ chmax, CellSm& S) {
+__device__ void unit_setup(const Grid& g, uint32_t u, const int4* __restrict__ urec,
+                           const uint32_t* __restrict__ cstart, const uint32_t* __restrict__ cend,
+                           CellSm& S) {
   if (threadIdx.x < 32) {
     if (threadIdx.x == 0) {
-      const uint32_t cf = clist[ulist[u]], cl = clist[ulist[u + 1] - 1];
-      cell_coords(g, cf, S.c3);
-      S.sc = cstart[cf];
-      S.ec = cend[cl];
-      make_unit_stencil(g, S.c3, cstart, cend, chmax, S.st);
+      uint32_t sc, ec;
+      unpack_unit(urec + 3 * (size_t)u, S.st, sc, ec);
+      S.sc = sc;
+      S.ec = ec;
       S.kself = -1;
     }
     __syncwarp();
@@ -562,7 +602,9 @@ __global__ void __launch_bounds__(kCT, 2) k_search(const double* __restrict__ x,
                                                 const uint32_t* __restrict__ cend,
                                                 const unsigned long long* __restrict__ chmax,
                                                 const uint32_t* __restrict__ clist,
-                                                const uint32_t* __restrict__ nclist, uint32_t* __restrict__ work,
+                                                const uint32_t* __restrict__ nclist,
+                                                const uint32_t* __restrict__ cunit,
+                                                const int4* __restrict__ urec, uint32_t* __restrict__ work,
                                                 uint32_t* __restrict__ nbr,
                                                 uint32_t* __restrict__ ncount, int maxn,
                                                 unsigned int* __restrict__ maxcount) {
@@ -590,7 +632,7 @@ __global__ void __launch_bounds__(kCT, 2) k_search(const double* __restrict__ x,
     __syncthreads();
     if (cfirst >= ncl) break;
     for (uint32_t ci = cfirst; ci < min(ncl, cfirst + (uint32_t)kCellChunk); ++ci) {
-      cell_setup(g, clist[ci], cstart, cend, chmax, S, umap, ustart);
+      cell_setup(g, ci, clist, cunit, urec, cstart, cend, chmax, S, umap, ustart);
       const Stencil st = S.st;
       double org[3], M = 0.0;
   #pragma unroll
@@ -640,24 +682,25 @@ __global__ void __launch_bounds__(kCT, 2) k_search(const double* __restrict__ x,
             if constexpr (SYM) candb[q] = band32(h[j], M);
           }
           // pad to whole tiles with far-away sentinels (never hit, never ambiguous), plus
-          // one all-sentinel tile (index ntile) that partners an odd last tile
-          const int ntile = (total + 31) >> 5;
-          for (int q = total + threadIdx.x; q < 32 * ntile + 32; q += blockDim.x) {
+          // one all-sentinel tile (index ntile) that partners a short last step
+          const int ntile = (total + kTS - 1) / kTS;
+          for (int q = total + threadIdx.x; q < kTS * ntile + kTS; q += blockDim.x) {
             cand[q] = make_float4(INFINITY, INFINITY, INFINITY, __uint_as_float(kSent));
             if constexpr (SYM) candb[q] = make_float2(-1.0f, -1.0f);
           }
           __syncthreads();
           // tile bounding boxes (staged candidates are Z-ordered within each cell, so a
-          // tile is a compact block)
-          for (int q = warp; q < ntile; q += kNW) {
-            const float4 v = cand[32 * q + lane];
+          // tile is a compact block); a warp reduces 32 / kTS tiles at once
+          for (int q0 = warp * (32 / kTS); q0 < ntile; q0 += kNW * (32 / kTS)) {
+            const int q = q0 + lane / kTS;
+            const float4 v = cand[kTS * q + lane % kTS];  // q <= ntile: sentinel at worst
             const bool ok = __float_as_uint(v.w) != kSent;
             float lx = ok ? v.x : INFINITY, ly = ok ? v.y : INFINITY, lz = ok ? v.z : INFINITY;
             float hx = ok ? v.x : -INFINITY, hy = ok ? v.y : -INFINITY, hz = ok ? v.z : -INFINITY;
             float hb = -1.0f;  // SYM: largest candidate band of the tile
-            if constexpr (SYM) hb = ok ? candb[32 * q + lane].y : -1.0f;
+            if constexpr (SYM) hb = ok ? candb[kTS * q + lane % kTS].y : -1.0f;
   #pragma unroll
-            for (int o = 16; o; o >>= 1) {
+            for (int o = kTS / 2; o; o >>= 1) {
               if constexpr (SYM) hb = fmaxf(hb, __shfl_xor_sync(0xffffffffu, hb, o));
               lx = fminf(lx, __shfl_xor_sync(0xffffffffu, lx, o));
               ly = fminf(ly, __shfl_xor_sync(0xffffffffu, ly, o));
@@ -666,7 +709,7 @@ __global__ void __launch_bounds__(kCT, 2) k_search(const double* __restrict__ x,
               hy = fmaxf(hy, __shfl_xor_sync(0xffffffffu, hy, o));
               hz = fmaxf(hz, __shfl_xor_sync(0xffffffffu, hz, o));
             }
-            if (lane == 0) {
+            if (lane % kTS == 0 && q < ntile) {
               tlo[q] = make_float4(lx, ly, lz, 0.f);
               thi[q] = make_float4(hx, hy, hz, hb);
             }
@@ -730,7 +773,7 @@ __global__ void __launch_bounds__(kCT, 2) k_search(const double* __restrict__ x,
             // Tiles either target can reach.  Box distance in the prefilter's own fp32
             // expression: rounding is monotone, so box d2 <= r2_32 of every member, and
             // box d2 >= hi excludes hits and ambiguous candidates alike (lists stay exact).
-            uint32_t need[kSearchWords];
+            uint32_t need[6] = {0u, 0u, 0u, 0u, 0u, 0u};
   #pragma unroll
             for (int w = 0; w < kSearchWords; ++w) {
               const int q = 32 * w + lane;
@@ -753,34 +796,42 @@ __global__ void __launch_bounds__(kCT, 2) k_search(const double* __restrict__ x,
               }
               need[w] = __ballot_sync(0xffffffffu, nd);
             }
-            static_assert(kSearchWords == 3, "tile mask held in three registers");
-            uint32_t n0 = need[0], n1 = need[1], n2 = need[2];
-            auto next_tile = [&]() -> int {  // lowest remaining needed tile (ascending: rows stay sorted)
-              int q;
-              if (n0) {
-                q = __ffs(n0) - 1;
-                n0 &= n0 - 1;
-              } else if (n1) {
-                q = 31 + __ffs(n1);
-                n1 &= n1 - 1;
-              } else if (n2) {
-                q = 63 + __ffs(n2);
-                n2 &= n2 - 1;
-              } else {
-                q = ntile;  // the sentinel tile
+            // lowest remaining needed tile (ascending: rows stay sorted); the word masks
+            // shift down as they empty (warp-uniform, no dynamic register indexing)
+            uint32_t m0 = need[0], m1 = need[1], m2 = need[2], m3 = need[3], m4 = need[4], m5 = need[5];
+            int base = 0, rem = (ntile + 31) / 32 - 1;
+            auto next_tile = [&]() -> int {
+              while (!m0 && rem > 0) {
+                m0 = m1; m1 = m2; m2 = m3; m3 = m4; m4 = m5; m5 = 0u;
+                base += 32;
+                --rem;
               }
+              if (!m0) return ntile;  // the sentinel tile
+              const int q = base + __ffs(m0) - 1;
+              m0 &= m0 - 1;
               return q;
             };
-            // two tiles per iteration: four independent test chains in flight
+            // per step two candidates per lane (kTS = 16: four tiles, lanes 0-15 on the
+            // lower tile of each pair): four independent test chains in flight, and the
+            // lane order of every ballot is the ascending staging order
             for (;;) {
               const int qA = next_tile();
               if (qA == ntile) break;
-              const int qB = next_tile();
-              const float4 cA = cand[32 * qA + lane], cB = cand[32 * qB + lane];
+              int qF, qS;
+              if constexpr (kTS == 32) {
+                qF = qA;
+                qS = next_tile();
+              } else {
+                const int qB = next_tile(), qC = next_tile(), qD = next_tile();
+                qF = lane < 16 ? qA : qB;
+                qS = lane < 16 ? qC : qD;
+              }
+              const int iF = kTS * qF + lane % kTS, iS = kTS * qS + lane % kTS;
+              const float4 cA = cand[iF], cB = cand[iS];
               float2 bA = make_float2(-1.0f, -1.0f), bB = bA;
               if constexpr (SYM) {
-                bA = candb[32 * qA + lane];
-                bB = candb[32 * qB + lane];
+                bA = candb[iF];
+                bB = candb[iS];
               }
               bool hA0, hA1, hB0, hB1, aA0, aA1, aB0, aB1;
               test(cA, bA, hA0, hA1, aA0, aA1);
@@ -872,7 +923,7 @@ __global__ void __launch_bounds__(kCTD, 1) k_density_c(
     const double* __restrict__ h, const double* __restrict__ m, const double* __restrict__ u,
     Grid g, const uint32_t* __restrict__ cstart, const uint32_t* __restrict__ cend,
     const unsigned long long* __restrict__ chmax, const uint32_t* __restrict__ clist,
-    const uint32_t* __restrict__ nclist, const uint32_t* __restrict__ ulist, const uint32_t* __restrict__ nulist, uint32_t* __restrict__ work, const uint32_t* __restrict__ nbr,
+    const uint32_t* __restrict__ nclist, const int4* __restrict__ urec, const uint32_t* __restrict__ nulist, uint32_t* __restrict__ work, const uint32_t* __restrict__ nbr,
     const uint32_t* __restrict__ ncount, int maxn, Phys ph, double* __restrict__ rho,
     double* __restrict__ omega, double* __restrict__ p, double* __restrict__ cs,
     double* __restrict__ wB, double* __restrict__ ih2, double* __restrict__ vol,
@@ -895,7 +946,7 @@ __global__ void __launch_bounds__(kCTD, 1) k_density_c(
   ChunkClaim claim{work, uchunk, 0u};
   for (uint32_t cfirst = claim.first(&s_chunk); cfirst < nun; cfirst = claim.next(&s_chunk)) {
     for (uint32_t ci = cfirst; ci < min(nun, cfirst + uchunk); ++ci) {
-      unit_setup(g, ci, ulist, clist, cstart, cend, chmax, S);
+      unit_setup(g, ci, urec, cstart, cend, S);
       const Stencil st = S.st;
       for (uint32_t t0 = S.sc; t0 < S.ec; t0 += kTgtU) {
         const uint32_t t1 = min(S.ec, t0 + kTgtU);
@@ -1007,7 +1058,7 @@ __global__ void __launch_bounds__(kCTD, 1) k_iad_c(
     const double* __restrict__ x, const double* __restrict__ y, const double* __restrict__ z,
     Grid g, const uint32_t* __restrict__ cstart, const uint32_t* __restrict__ cend,
     const unsigned long long* __restrict__ chmax, const uint32_t* __restrict__ clist,
-    const uint32_t* __restrict__ nclist, const uint32_t* __restrict__ ulist, const uint32_t* __restrict__ nulist, uint32_t* __restrict__ work, const uint32_t* __restrict__ nbr,
+    const uint32_t* __restrict__ nclist, const int4* __restrict__ urec, const uint32_t* __restrict__ nulist, uint32_t* __restrict__ work, const uint32_t* __restrict__ nbr,
     const uint32_t* __restrict__ ncount, int maxn, Phys ph, const double* __restrict__ wB,
     const double* __restrict__ ih2, const double* __restrict__ vol, double* __restrict__ c11,
     double* __restrict__ c12, double* __restrict__ c13, double* __restrict__ c22,
@@ -1031,7 +1082,7 @@ __global__ void __launch_bounds__(kCTD, 1) k_iad_c(
   ChunkClaim claim{work, uchunk, 0u};
   for (uint32_t cfirst = claim.first(&s_chunk); cfirst < nun; cfirst = claim.next(&s_chunk)) {
     for (uint32_t ci = cfirst; ci < min(nun, cfirst + uchunk); ++ci) {
-      unit_setup(g, ci, ulist, clist, cstart, cend, chmax, S);
+      unit_setup(g, ci, urec, cstart, cend, S);
       const Stencil st = S.st;
       for (uint32_t t0 = S.sc; t0 < S.ec; t0 += kTgtU) {
         const uint32_t t1 = min(S.ec, t0 + kTgtU);
@@ -1158,7 +1209,7 @@ __global__ void __launch_bounds__(kCTM, 1) k_momentum_c(
     MomSrc src, MomTgt tg, MomOut out, Grid g, const uint32_t* __restrict__ cstart,
     const uint32_t* __restrict__ cend, const unsigned long long* __restrict__ chmax,
     const uint32_t* __restrict__ clist, const uint32_t* __restrict__ nclist,
-    const uint32_t* __restrict__ ulist, const uint32_t* __restrict__ nulist, uint32_t* __restrict__ work,
+    const int4* __restrict__ urec, const uint32_t* __restrict__ nulist, uint32_t* __restrict__ work,
     const uint32_t* __restrict__ nbr, const uint32_t* __restrict__ ncount, int maxn, Phys ph,
     double* __restrict__ dts, unsigned long long* __restrict__ cnt) {
   extern __shared__ double dsm[];  // kMomPairs * kMomCap double2 staged + T_N * kTgtU target fields
@@ -1182,7 +1233,7 @@ __global__ void __launch_bounds__(kCTM, 1) k_momentum_c(
   ChunkClaim claim{work, uchunk, 0u};
   for (uint32_t cfirst = claim.first(&s_chunk); cfirst < nun; cfirst = claim.next(&s_chunk)) {
     for (uint32_t ci = cfirst; ci < min(nun, cfirst + uchunk); ++ci) {
-      unit_setup(g, ci, ulist, clist, cstart, cend, chmax, S);
+      unit_setup(g, ci, urec, cstart, cend, S);
       const Stencil st = S.st;
       for (uint32_t t0 = S.sc; t0 < S.ec; t0 += kTgtU) {
         const uint32_t t1 = min(S.ec, t0 + kTgtU);
@@ -1388,10 +1439,15 @@ int launch_neighbors(sph_ctx* c) {
                            : (sym ? k_search<false, true> : k_search<false, false>);
   set_smem(kern, smem);
   cudaMemsetAsync(c->s.work + 0, 0, sizeof(uint32_t), c->stream);
+  // unit records (union stencils + target ranges) for the search and the three passes
+  k_unit_prep<<<cell_grid(c, 8), 128, 0, c->stream>>>(c->grid, c->s.cell_list, c->s.unit_list,
+                                                      c->s.nunit_list, c->s.cell_start, c->s.cell_end,
+                                                      c->s.cell_hmax, c->s.unit_rec, c->s.cell_unit);
   kern<<<cell_grid(c, 4), kCT, smem, c->stream>>>(
       c->P.x, c->P.y, c->P.z, c->P.h, c->grid, c->s.cell_start, c->s.cell_end, c->s.cell_hmax,
-      c->s.cell_list, c->s.ncell_list, c->s.work + 0, c->s.nbr, c->s.ncount, c->maxn, c->s.nbr_maxcount);
-  return 1;
+      c->s.cell_list, c->s.ncell_list, c->s.cell_unit, c->s.unit_rec, c->s.work + 0, c->s.nbr,
+      c->s.ncount, c->maxn, c->s.nbr_maxcount);
+  return 2;
 }
 
 template <int N, bool W2, int KM>
@@ -1402,7 +1458,7 @@ static void density_t(sph_ctx* c) {
   cudaMemsetAsync(c->s.work + 1, 0, sizeof(uint32_t), c->stream);
   k_density_c<N, W2, KM><<<cell_grid(c, 1), kCTD, smem, c->stream>>>(
       P.x, P.y, P.z, P.h, P.m, P.u, c->grid, c->s.cell_start, c->s.cell_end, c->s.cell_hmax,
-      c->s.cell_list, c->s.ncell_list, c->s.unit_list, c->s.nunit_list, c->s.work + 1, c->s.nbr, c->s.ncount, c->maxn, c->phys, P.rho, P.omega,
+      c->s.cell_list, c->s.ncell_list, c->s.unit_rec, c->s.nunit_list, c->s.work + 1, c->s.nbr, c->s.ncount, c->maxn, c->phys, P.rho, P.omega,
       P.p, P.c, c->s.wB, c->s.ih2, c->s.vol, c->s.rinv, c->s.X, c->s.mX, c->s.cnt);
 }
 
@@ -1439,7 +1495,7 @@ static void iad_t(sph_ctx* c) {
   cudaMemsetAsync(c->s.work + 2, 0, sizeof(uint32_t), c->stream);
   k_iad_c<N, W2, KM><<<cell_grid(c, 1), kCTD, smem, c->stream>>>(
       P.x, P.y, P.z, c->grid, c->s.cell_start, c->s.cell_end, c->s.cell_hmax, c->s.cell_list,
-      c->s.ncell_list, c->s.unit_list, c->s.nunit_list, c->s.work + 2, c->s.nbr, c->s.ncount, c->maxn, c->phys, c->s.wB, c->s.ih2, c->s.vol,
+      c->s.ncell_list, c->s.unit_rec, c->s.nunit_list, c->s.work + 2, c->s.nbr, c->s.ncount, c->maxn, c->phys, c->s.wB, c->s.ih2, c->s.vol,
       P.c11, P.c12, P.c13, P.c22, P.c23, P.c33, c->s.ct, c->cap, c->s.cnt);
 }
 
@@ -1459,7 +1515,7 @@ static void momentum_t(sph_ctx* c) {
   cudaMemsetAsync(c->s.work + 3, 0, sizeof(uint32_t), c->stream);
   k_momentum_c<N, W2, KM><<<cell_grid(c, 1), kCTM, smem, c->stream>>>(
       src, tg, out, c->grid, c->s.cell_start, c->s.cell_end, c->s.cell_hmax, c->s.cell_list,
-      c->s.ncell_list, c->s.unit_list, c->s.nunit_list, c->s.work + 3, c->s.nbr, c->s.ncount, c->maxn, c->phys, c->s.dts, c->s.cnt);
+      c->s.ncell_list, c->s.unit_rec, c->s.nunit_list, c->s.work + 3, c->s.nbr, c->s.ncount, c->maxn, c->phys, c->s.dts, c->s.cnt);
 }
 
 int launch_momentum(sph_ctx* c) {

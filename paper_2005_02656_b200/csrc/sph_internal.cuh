@@ -81,6 +81,8 @@ struct Scratch {
   uint32_t* unit_rank = nullptr;            // cap: exclusive scan of unit_flag
   uint32_t* unit_list = nullptr;            // cap + 1: index into cell_list of each unit's first cell
   uint32_t* nunit_list = nullptr;           // device scalar
+  int4* unit_rec = nullptr;                 // 3 x cap: per unit, its union stencil + target range
+  uint32_t* cell_unit = nullptr;            // cap: unit of each cell-list entry
   int64_t max_cells = 0;
   // neighbours
   uint32_t* nbr = nullptr;       // cap * maxn
