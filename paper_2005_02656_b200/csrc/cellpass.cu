@@ -22,11 +22,10 @@ namespace sphb {
 
 constexpr int kCT = 256;          // threads per CTA
 constexpr int kNW = kCT / 32;     // warps per CTA
-constexpr int kTgt = 128;         // search: targets per sub-block (per-target state in smem)
-constexpr int kTgtU = 416;        // pair passes: targets per sub-block (a whole 2x2x1 unit, <= 9x9x5 at config 5)
+constexpr int kTgtU = 416;        // targets per sub-block (a whole 2x2x1 unit, <= 9x9x5 at config 5)
 constexpr int kSlots = kKMax;     // slot tables: every stencil the grid chooser admits
 constexpr int kCellChunk = 4;     // consecutive cells per claim (L2 reuse of shared stencils)
-constexpr int kSearchCap = 3072;  // staged candidates per group (float4)
+constexpr int kSearchCap = 4096;  // staged candidates per group (float4): a unit stencil in one group
 constexpr int kTS = 32;           // search tile: candidates per fp32 bounding box (16 measured 2.7 ms slower)
 constexpr int kSearchTiles = kSearchCap / kTS + 1;          // + the sentinel tile
 constexpr int kSearchWords = (kSearchCap / kTS + 31) / 32;  // tile bitmask words
@@ -189,12 +188,10 @@ __device__ __forceinline__ double min_img(double d, double L) {
   return d;
 }
 
-// Warp 0: per-slot tables of S.st and their prefix (flat staging index of each slot);
-// with umap, also the unit-stencil slot of every slot (search: rows are written in
-// unit numbering, stencil.cuh).  Lane 0 has set S.st / S.c3 / S.sc / S.ec.
+// Warp 0: per-slot tables of S.st and their prefix (flat staging index of each slot).
+// Lane 0 has set S.st / S.sc / S.ec.
 __device__ __forceinline__ void slot_tables(const Grid& g, const uint32_t* __restrict__ cstart,
-                                            const uint32_t* __restrict__ cend, CellSm& S,
-                                            uint16_t* umap, uint32_t* ustart, const Stencil* U) {
+                                            const uint32_t* __restrict__ cend, CellSm& S) {
   const int lane = threadIdx.x;
   const int K = S.st.K;
   uint32_t carry = 0;
@@ -210,11 +207,6 @@ __device__ __forceinline__ void slot_tables(const Grid& g, const uint32_t* __res
       S.t_sh[k][0] = (signed char)sh[0];
       S.t_sh[k][1] = (signed char)sh[1];
       S.t_sh[k][2] = (signed char)sh[2];
-      if (umap) {
-        const int us = unit_slot(S.st, *U, k);
-        umap[k] = (uint16_t)us;
-        ustart[us] = s0;
-      }
     }
     uint32_t x = cnt;  // inclusive warp scan
 #pragma unroll
@@ -235,14 +227,16 @@ __device__ __forceinline__ void slot_tables(const Grid& g, const uint32_t* __res
 // stencil of the unit's cells and its target range, so a CTA prologue is one 48-byte
 // load instead of a serial chain of dependent cell-table loads (ncu: the prologue
 // barrier held 7-8 % of the search, density and IAD samples).
-__device__ __forceinline__ void pack_unit(const Stencil& u, uint32_t sc, uint32_t ec, int4* rec) {
+__device__ __forceinline__ void pack_unit(const Stencil& u, uint32_t sc, uint32_t ec, uint32_t cf,
+                                          int4* rec) {
   rec[0] = make_int4(u.lo[0], u.lo[1], u.lo[2], u.K);
   rec[1] = make_int4(u.cnt[0], u.cnt[1], u.cnt[2], u.wrap[0] | (u.wrap[1] << 2) | (u.wrap[2] << 4));
-  rec[2] = make_int4((int)sc, (int)ec, 0, 0);
+  rec[2] = make_int4((int)sc, (int)ec, (int)cf, 0);
 }
 __device__ __forceinline__ void unpack_unit(const int4* __restrict__ rec, Stencil& u, uint32_t& sc,
-                                            uint32_t& ec) {
+                                            uint32_t& ec, uint32_t* cf = nullptr) {
   const int4 a = rec[0], b = rec[1], c = rec[2];
+  if (cf) *cf = (uint32_t)c.z;
   u.lo[0] = a.x; u.lo[1] = a.y; u.lo[2] = a.z; u.K = a.w;
   u.cnt[0] = b.x; u.cnt[1] = b.y; u.cnt[2] = b.z;
   u.wrap[0] = b.w & 3; u.wrap[1] = (b.w >> 2) & 3; u.wrap[2] = (b.w >> 4) & 3;
@@ -253,7 +247,7 @@ __device__ __forceinline__ void unpack_unit(const int4* __restrict__ rec, Stenci
 __global__ void k_unit_prep(Grid g, const uint32_t* __restrict__ clist, const uint32_t* __restrict__ ulist,
                             const uint32_t* __restrict__ nulist, const uint32_t* __restrict__ cstart,
                             const uint32_t* __restrict__ cend, const unsigned long long* __restrict__ chmax,
-                            int4* __restrict__ urec, uint32_t* __restrict__ cunit) {
+                            int4* __restrict__ urec) {
   const uint32_t nu = *nulist;
   for (uint32_t u = blockIdx.x * blockDim.x + threadIdx.x; u < nu; u += gridDim.x * blockDim.x) {
     const uint32_t i0 = ulist[u], i1 = ulist[u + 1];
@@ -262,34 +256,8 @@ __global__ void k_unit_prep(Grid g, const uint32_t* __restrict__ clist, const ui
     cell_coords(g, cf, c3);
     Stencil st;
     make_unit_stencil(g, c3, cstart, cend, chmax, st);
-    pack_unit(st, cstart[cf], cend[cl], urec + 3 * (size_t)u);
-    for (uint32_t i = i0; i < i1; ++i) cunit[i] = u;
+    pack_unit(st, cstart[cf], cend[cl], cf, urec + 3 * (size_t)u);
   }
-}
-
-// CTA prologue for search cell c = clist[ci] (warp 0, one CTA barrier): the cell's
-// own stencil, its slot tables, and the map of its slots into its unit's stencil.
-__device__ void cell_setup(const Grid& g, uint32_t ci, const uint32_t* __restrict__ clist,
-                           const uint32_t* __restrict__ cunit, const int4* __restrict__ urec,
-                           const uint32_t* __restrict__ cstart, const uint32_t* __restrict__ cend,
-                           const unsigned long long* __restrict__ chmax, CellSm& S, uint16_t* umap,
-                           uint32_t* ustart) {
-  if (threadIdx.x < 32) {
-    __shared__ Stencil U;
-    if (threadIdx.x == 0) {
-      const uint32_t c = clist[ci], u = cunit[ci];
-      uint32_t usc, uec;
-      unpack_unit(urec + 3 * (size_t)u, U, usc, uec);
-      cell_coords(g, c, S.c3);
-      S.sc = cstart[c];
-      S.ec = cend[c];
-      make_stencil(g, S.c3, cell_reach(g, __longlong_as_double((long long)chmax[c])), S.st);
-      S.kself = self_slot(S.st, S.c3);
-    }
-    __syncwarp();
-    slot_tables(g, cstart, cend, S, umap, ustart, &U);
-  }
-  __syncthreads();
 }
 
 // CTA prologue for pair-pass unit u (warp 0, one CTA barrier): the unit's target
@@ -300,14 +268,15 @@ __device__ void unit_setup(const Grid& g, uint32_t u, const int4* __restrict__ u
                            CellSm& S) {
   if (threadIdx.x < 32) {
     if (threadIdx.x == 0) {
-      uint32_t sc, ec;
-      unpack_unit(urec + 3 * (size_t)u, S.st, sc, ec);
+      uint32_t sc, ec, cf;
+      unpack_unit(urec + 3 * (size_t)u, S.st, sc, ec, &cf);
       S.sc = sc;
       S.ec = ec;
       S.kself = -1;
+      cell_coords(g, cf, S.c3);  // first cell of the unit
     }
     __syncwarp();
-    slot_tables(g, cstart, cend, S, nullptr, nullptr, nullptr);
+    slot_tables(g, cstart, cend, S);
   }
   __syncthreads();
 }
@@ -553,10 +522,11 @@ __device__ __forceinline__ void walk_targets_fast(uint32_t t0, uint32_t t1,
   }
 }
 
-struct TgtW {  // per-warp search target data (exact-test fp64 + fp32 band)
+struct TgtW {  // per-target search data (exact-test fp64 + fp32 band + own packed entry)
   double pos[3];
   double lim;
   float f[5];
+  uint32_t self;
 };
 
 __device__ __forceinline__ bool exact_hit(const Grid& g, const double* __restrict__ x,
@@ -601,10 +571,8 @@ __global__ void __launch_bounds__(kCT, 2) k_search(const double* __restrict__ x,
                                                 const uint32_t* __restrict__ cstart,
                                                 const uint32_t* __restrict__ cend,
                                                 const unsigned long long* __restrict__ chmax,
-                                                const uint32_t* __restrict__ clist,
-                                                const uint32_t* __restrict__ nclist,
-                                                const uint32_t* __restrict__ cunit,
-                                                const int4* __restrict__ urec, uint32_t* __restrict__ work,
+                                                const int4* __restrict__ urec,
+                                                const uint32_t* __restrict__ nulist, uint32_t* __restrict__ work,
                                                 uint32_t* __restrict__ nbr,
                                                 uint32_t* __restrict__ ncount, int maxn,
                                                 unsigned int* __restrict__ maxcount) {
@@ -612,41 +580,35 @@ __global__ void __launch_bounds__(kCT, 2) k_search(const double* __restrict__ x,
   float2* const candb = reinterpret_cast<float2*>(cand + kSearchCap + 64);  // SYM: per-candidate band
   __shared__ CellSm S;
   __shared__ float4 tlo[kSearchTiles], thi[kSearchTiles];  // per staged tile: fp32 bounding box
-  __shared__ uint32_t tcount[kTgt];
-  __shared__ TgtW TW[kTgt];  // per target of the block: computed once, in parallel
-  // rows are written in unit-stencil numbering (stencil.cuh): cell slot -> unit slot,
-  // and the cell start of each unit slot the cell's stencil covers (exact test)
-  __shared__ uint16_t umap[kSlots];
-  __shared__ uint32_t ustart[kSlots];
+  __shared__ uint32_t tcount[kTgtU];
+  __shared__ TgtW TW[kTgtU];  // per target of the block: computed once, in parallel
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const unsigned lt = (1u << lane) - 1u;
-  const uint32_t ncl = *nclist;
   __shared__ uint32_t s_chunk;
-  // cells in chunks of kCellChunk consecutive (Morton-order) cells claimed from a
-  // counter: consecutive cells share most of their stencil, so a CTA's next staging
-  // finds its sources in L2 (a grid stride left the re-reads to HBM)
-  for (;;) {
-    if (threadIdx.x == 0) s_chunk = atomicAdd(work, (uint32_t)kCellChunk);
-    __syncthreads();
-    const uint32_t cfirst = s_chunk;
-    __syncthreads();
-    if (cfirst >= ncl) break;
-    for (uint32_t ci = cfirst; ci < min(ncl, cfirst + (uint32_t)kCellChunk); ++ci) {
-      cell_setup(g, ci, clist, cunit, urec, cstart, cend, chmax, S, umap, ustart);
+  // one CTA per unit (stencil.cuh): the unit stencil is staged once for all its targets,
+  // and rows are written directly in its slot numbering
+  const uint32_t nun = *nulist;
+  const uint32_t uchunk = (uint32_t)kCellChunk >> g.ubits ? (uint32_t)kCellChunk >> g.ubits : 1u;
+  ChunkClaim claim{work, uchunk, 0u};
+  for (uint32_t cfirst = claim.first(&s_chunk); cfirst < nun; cfirst = claim.next(&s_chunk)) {
+    for (uint32_t ci = cfirst; ci < min(nun, cfirst + uchunk); ++ci) {
+      unit_setup(g, ci, urec, cstart, cend, S);
       const Stencil st = S.st;
+      int b3[3];
+      unit_base(g, S.c3, b3);
       double org[3], M = 0.0;
   #pragma unroll
       for (int d = 0; d < 3; ++d) {
         const double edge = g.inv[d] > 0.0 ? 1.0 / g.inv[d] : 0.0;
-        org[d] = g.lo[d] + S.c3[d] * edge;
-        // bound on |staged coordinate - org| (stencil cells + 1 cell of slack)
+        org[d] = g.lo[d] + b3[d] * edge;
+        // bound on |staged or target coordinate - org| (stencil cells + 1 cell of slack)
         const double Md = st.wrap[d] == 2
                               ? g.L[d]
-                              : (double)(max(S.c3[d] - st.lo[d], st.lo[d] + st.cnt[d] - S.c3[d]) + 1) * edge;
+                              : (double)(max(b3[d] - st.lo[d], st.lo[d] + st.cnt[d] - b3[d]) + 1) * edge;
         M = fmax(M, Md);
       }
-      for (uint32_t t0 = S.sc; t0 < S.ec; t0 += kTgt) {
-        const uint32_t t1 = min(S.ec, t0 + kTgt);
+      for (uint32_t t0 = S.sc; t0 < S.ec; t0 += kTgtU) {
+        const uint32_t t1 = min(S.ec, t0 + kTgtU);
         for (uint32_t t = t0 + threadIdx.x; t < t1; t += blockDim.x) {
           tcount[t - t0] = 0;
           const double ha = h[t], tha = 2.0 * ha;
@@ -663,6 +625,20 @@ __global__ void __launch_bounds__(kCT, 2) k_search(const double* __restrict__ x,
           w.f[2] = (float)(pz - org[2]);
           w.f[3] = bd.x;
           w.f[4] = bd.y;
+          // own packed entry (unit slot of the target's cell, index in it): never its own neighbour
+          w.self = kSent;
+          for (int dz = 0; dz < (g.ubits > 2 ? 2 : 1); ++dz)
+            for (int dy = 0; dy < (g.ubits > 1 ? 2 : 1); ++dy)
+              for (int dx = 0; dx < (g.ubits > 0 ? 2 : 1); ++dx) {
+                const int q0 = b3[0] + dx, q1 = b3[1] + dy, q2 = b3[2] + dz;
+                if (q0 >= g.nc[0] || q1 >= g.nc[1] || q2 >= g.nc[2]) continue;
+                const int64_t cell = q0 + (int64_t)g.nc[0] * (q1 + (int64_t)g.nc[1] * q2);
+                const uint32_t cs0 = cstart[cell];
+                if (t >= cs0 && t < cend[cell]) {
+                  const int us = (q0 - st.lo[0]) + st.cnt[0] * ((q1 - st.lo[1]) + st.cnt[1] * (q2 - st.lo[2]));
+                  w.self = ((uint32_t)us << kLocalBits) | (t - cs0);
+                }
+              }
         }
         __syncthreads();
         for (uint32_t gb = 0; gb < S.total; gb += kSearchCap) {
@@ -677,7 +653,7 @@ __global__ void __launch_bounds__(kCT, 2) k_search(const double* __restrict__ x,
             v.x = (float)((x[j] + sh[0]) - org[0]);
             v.y = (float)((y[j] + sh[1]) - org[1]);
             v.z = (float)((z[j] + sh[2]) - org[2]);
-            v.w = __uint_as_float(((uint32_t)umap[slot] << kLocalBits) | l);
+            v.w = __uint_as_float(((uint32_t)slot << kLocalBits) | l);
             cand[q] = v;
             if constexpr (SYM) candb[q] = band32(h[j], M);
           }
@@ -717,16 +693,14 @@ __global__ void __launch_bounds__(kCT, 2) k_search(const double* __restrict__ x,
           __syncthreads();
           // two targets per warp share every staged-candidate load (fp32 test data in
           // registers; the fp64 data of the rare exact test in shared memory)
-          for (uint32_t ta = t0 + 2 * warp; ta < t1; ta += 2 * kNW) {
+          for (uint32_t ta = t0 + 2 * warp; ta < t1; ta += 2 * kNW) {  // (static: ~18 pairs per warp)
             const bool has_b = ta + 1 < t1;
             const uint32_t tb = has_b ? ta + 1 : ta;  // odd tail: duplicate, identical writes
             const TgtW& TA = TW[ta - t0];
             const TgtW& TB = TW[tb - t0];
             const float ax0 = TA.f[0], ay0 = TA.f[1], az0 = TA.f[2], lo0 = TA.f[3], hi0 = TA.f[4];
             const float ax1 = TB.f[0], ay1 = TB.f[1], az1 = TB.f[2], lo1 = TB.f[3], hi1 = TB.f[4];
-            const uint32_t uself = (uint32_t)umap[S.kself] << kLocalBits;
-            const uint32_t self0 = uself | (ta - S.sc);
-            const uint32_t self1 = uself | (tb - S.sc);
+            const uint32_t self0 = TA.self, self1 = TB.self;
             uint32_t cnt0 = tcount[ta - t0], cnt1 = tcount[tb - t0];
             uint32_t* row0 = nbr + (size_t)ta * maxn;
             uint32_t* row1 = nbr + (size_t)tb * maxn;
@@ -759,7 +733,7 @@ __global__ void __launch_bounds__(kCT, 2) k_search(const double* __restrict__ x,
             // rare: exact fp64 test of the candidates inside a band (one ballot per step)
             auto exact = [&](const float4 cd, bool& hit0, bool& hit1, bool amb0, bool amb1) {
               const uint32_t pk = __float_as_uint(cd.w);
-              const uint32_t j = ustart[pk >> kLocalBits] + (pk & kLocalMask);
+              const uint32_t j = S.t_start[pk >> kLocalBits] + (pk & kLocalMask);
               double limb = 0.0;
               if constexpr (SYM) {
                 if (amb0 | amb1) {
@@ -1185,6 +1159,34 @@ __global__ void __launch_bounds__(kCTD, 1) k_iad_c(
 }
 
 // ------------------------------------------------------------------ a10-a11 momentum + energy + AV + dt
+// ---- TMA bulk copies (cp.async.bulk) completing on an mbarrier (sm_90+; SASS UBLKCP)
+__device__ __forceinline__ uint32_t smem_u32(const void* p) {
+  return (uint32_t)__cvta_generic_to_shared(p);
+}
+__device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;\n" ::"r"(smem_u32(bar)), "r"(count) : "memory");
+}
+__device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, uint32_t bytes) {
+  asm volatile("{\n .reg .b64 st;\n mbarrier.arrive.expect_tx.shared::cta.b64 st, [%0], %1;\n}\n" ::"r"(
+                   smem_u32(bar)), "r"(bytes)
+               : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t phase) {
+  uint32_t ok = 0;
+  do {
+    asm volatile("{\n .reg .pred p;\n mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n selp.u32 %0, 1, 0, p;\n}\n"
+                 : "=r"(ok)
+                 : "r"(smem_u32(bar)), "r"(phase)
+                 : "memory");
+  } while (!ok);
+}
+__device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t bytes, uint64_t* bar) {
+  asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];\n" ::"r"(
+                   smem_u32(dst)), "l"(src), "r"(bytes), "r"(smem_u32(bar))
+               : "memory");
+}
+__device__ __forceinline__ void fence_proxy_async() { asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory"); }
+
 struct MomSrc {  // per-particle arrays staged for the source side of a pair
   const double *x, *y, *z, *vx, *vy, *vz, *m, *ih2, *c, *mX, *mr;
   const double* ct;  // 6 x stride: C~ = (B/h^3) C
@@ -1201,6 +1203,26 @@ struct MomOut {
 //   0 (x, y)  1 (z, vx)  2 (vy, vz)  3 (m, 1/h^2)  4 (c, m X)  5 (m/rho, C~11)
 //   6 (C~12, C~13)  7 (C~22, C~23)  8 (C~33, -)
 constexpr int kMomPairs = 9;
+
+// Momentum source records: the kMomPairs double2 a pair reads from its source, one
+// contiguous 144-byte record per particle, built once per step after IAD (owned +
+// halo).  A staging group is then a handful of bulk copies (one per stencil slot).
+__global__ void k_mom_records(MomSrc src, int64_t n, double2* __restrict__ rec) {
+  for (int64_t j = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; j < n;
+       j += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t cs = src.ct_stride;
+    double2* r = rec + j * kMomPairs;
+    r[0] = make_double2(src.x[j], src.y[j]);
+    r[1] = make_double2(src.z[j], src.vx[j]);
+    r[2] = make_double2(src.vy[j], src.vz[j]);
+    r[3] = make_double2(src.m[j], src.ih2[j]);
+    r[4] = make_double2(src.c[j], src.mX[j]);
+    r[5] = make_double2(src.mr[j], src.ct[j]);
+    r[6] = make_double2(src.ct[cs + j], src.ct[2 * cs + j]);
+    r[7] = make_double2(src.ct[3 * cs + j], src.ct[4 * cs + j]);
+    r[8] = make_double2(src.ct[5 * cs + j], 0.0);
+  }
+}
 // per-target smem fields
 enum { T_X, T_Y, T_Z, T_VX, T_VY, T_VZ, T_IH2, T_WB, T_RINV, T_XP, T_C, T_A11, T_A12, T_A13, T_A22, T_A23, T_A33, T_N };
 
@@ -1211,8 +1233,8 @@ __global__ void __launch_bounds__(kCTM, 1) k_momentum_c(
     const uint32_t* __restrict__ clist, const uint32_t* __restrict__ nclist,
     const int4* __restrict__ urec, const uint32_t* __restrict__ nulist, uint32_t* __restrict__ work,
     const uint32_t* __restrict__ nbr, const uint32_t* __restrict__ ncount, int maxn, Phys ph,
-    double* __restrict__ dts, unsigned long long* __restrict__ cnt) {
-  extern __shared__ double dsm[];  // kMomPairs * kMomCap double2 staged + T_N * kTgtU target fields
+    double* __restrict__ dts, unsigned long long* __restrict__ cnt, const double2* __restrict__ mrec) {
+  extern __shared__ double dsm[];  // kMomCap staged source records + T_N * kTgtU target fields
   double2* const F2 = reinterpret_cast<double2*>(dsm);
   double* const T = dsm + 2 * kMomPairs * kMomCap;
   __shared__ CellSm S;
@@ -1225,6 +1247,11 @@ __global__ void __launch_bounds__(kCTM, 1) k_momentum_c(
   const int n = N > 0 ? N : ph.n;
   double dtmin = INFINITY;
   unsigned long long ncoinc = 0;
+  __shared__ __align__(8) uint64_t mbar;  // staging: bulk copies complete on it
+  __shared__ int s_wrap;
+  uint32_t mphase = 0;
+  if (threadIdx.x == 0) mbar_init(&mbar, 1);
+  __syncthreads();
   // cells in chunks of kCellChunk consecutive (Morton-order) cells claimed from a
   // counter: consecutive cells share most of their stencil, so a CTA's next staging
   // finds its sources in L2 (a grid stride left the re-reads to HBM)
@@ -1269,27 +1296,45 @@ __global__ void __launch_bounds__(kCTM, 1) k_momentum_c(
         for (uint32_t gb = 0, gi = 0; gb < S.total; gb += kMomCap, ++gi) {
           const uint32_t ge = min(S.total, gb + kMomCap), pend = pend_of(S, ge);
           if (threadIdx.x == 0) S.next[(gi + 1) & 1] = 0;
-          for (uint32_t qq = threadIdx.x; qq < ge - gb; qq += blockDim.x) {  // flat staging
-            {
-              const uint32_t fi = gb + qq;
-              const int k = slot_of(S, fi);
-              const uint32_t j = S.t_start[k] + (fi - S.cum[k]);
-              double sh[3];
-              shifts_of(g, S, k, sh);
-              double2* q = F2 + qq;
-              const int64_t cs = src.ct_stride;
-              q[0 * kMomCap] = make_double2(src.x[j] + sh[0], src.y[j] + sh[1]);
-              q[1 * kMomCap] = make_double2(src.z[j] + sh[2], src.vx[j]);
-              q[2 * kMomCap] = make_double2(src.vy[j], src.vz[j]);
-              q[3 * kMomCap] = make_double2(src.m[j], src.ih2[j]);
-              q[4 * kMomCap] = make_double2(src.c[j], src.mX[j]);
-              q[5 * kMomCap] = make_double2(src.mr[j], src.ct[j]);
-              q[6 * kMomCap] = make_double2(src.ct[cs + j], src.ct[2 * cs + j]);
-              q[7 * kMomCap] = make_double2(src.ct[3 * cs + j], src.ct[4 * cs + j]);
-              q[8 * kMomCap] = make_double2(src.ct[5 * cs + j], 0.0);
+          // stage [gb, ge): warp 0 issues one bulk copy of consecutive records per slot
+          // (the slot's cell is a contiguous range), all complete on one mbarrier
+          if (warp == 0) {
+            if (lane == 0) {
+              fence_proxy_async();  // the buffer's previous group was read through the generic proxy
+              mbar_expect_tx(&mbar, (ge - gb) * (uint32_t)sizeof(double2) * kMomPairs);
             }
+            __syncwarp();
+            const int k0 = slot_of(S, gb), k1 = slot_of(S, ge - 1);
+            int wr = 0;
+            for (int k = k0 + lane; k <= k1; k += 32) {
+              const uint32_t f0 = max(S.cum[k], gb), f1 = min(S.cum[k + 1], ge);
+              if (f1 > f0) {
+                bulk_g2s(F2 + (size_t)(f0 - gb) * kMomPairs,
+                         mrec + (size_t)(S.t_start[k] + (f0 - S.cum[k])) * kMomPairs,
+                         (f1 - f0) * (uint32_t)sizeof(double2) * kMomPairs, &mbar);
+                wr |= S.t_sh[k][0] | S.t_sh[k][1] | S.t_sh[k][2];
+              }
+            }
+            wr = __any_sync(0xffffffffu, wr != 0);
+            if (lane == 0) s_wrap = wr;
           }
-          __syncthreads();
+          mbar_wait(&mbar, mphase);
+          mphase ^= 1;
+          __syncthreads();  // s_wrap
+          if (s_wrap) {  // periodic images: shift the staged positions of wrapped slots
+            for (uint32_t qq = threadIdx.x; qq < ge - gb; qq += blockDim.x) {
+              const int k = slot_of(S, gb + qq);
+              if (S.t_sh[k][0] | S.t_sh[k][1] | S.t_sh[k][2]) {
+                double sh[3];
+                shifts_of(g, S, k, sh);
+                double2* q = F2 + (size_t)qq * kMomPairs;
+                q[0].x += sh[0];
+                q[0].y += sh[1];
+                q[1].x += sh[2];
+              }
+            }
+            __syncthreads();
+          }
           struct B {
             const double2* F2;
             const double* T;
@@ -1312,8 +1357,8 @@ __global__ void __launch_bounds__(kCTM, 1) k_momentum_c(
               vs = -1.0;
             }
             __device__ __forceinline__ void operator()(int qi) {
-              const double2* q = F2 + qi;
-              const double2 p0 = q[0], p1 = q[kMomCap], p3 = q[3 * kMomCap];
+              const double2* q = F2 + (size_t)qi * kMomPairs;
+              const double2 p0 = q[0], p1 = q[1], p3 = q[3];
               double dx = p0.x - xa, dy = p0.y - ya, dz = p1.x - za;
               delta3<W2>(*st, *g, dx, dy, dz);  // Delta_ab = x_b - x_a
               const double r2 = dx * dx + dy * dy + dz * dz;
@@ -1332,12 +1377,12 @@ __global__ void __launch_bounds__(kCTM, 1) k_momentum_c(
               const double ux = a11 * dx + a12 * dy + a13 * dz;
               const double uy = a12 * dx + a22 * dy + a23 * dz;
               const double uz = a13 * dx + a23 * dy + a33 * dz;
-              const double2 p5 = q[5 * kMomCap], p6 = q[6 * kMomCap], p7 = q[7 * kMomCap], p8 = q[8 * kMomCap];
+              const double2 p5 = q[5], p6 = q[6], p7 = q[7], p8 = q[8];
               const double b11 = p5.y, b12 = p6.x, b13 = p6.y, b22 = p7.x, b23 = p7.y, b33 = p8.x;
               const double wx = b11 * dx + b12 * dy + b13 * dz;
               const double wy = b12 * dx + b22 * dy + b23 * dz;
               const double wz = b13 * dx + b23 * dy + b33 * dz;
-              const double2 p2 = q[2 * kMomCap], p4 = q[4 * kMomCap];
+              const double2 p2 = q[2], p4 = q[4];
               const double mb = p3.x, mXb = p4.y, mrb = p5.x, cb = p4.x;
               const double vabx = vxa - p1.y, vaby = vya - p2.x, vabz = vza - p2.y;
               const double vdotx = -(vabx * dx + vaby * dy + vabz * dz);  // v_ab . x_ab
@@ -1442,11 +1487,11 @@ int launch_neighbors(sph_ctx* c) {
   // unit records (union stencils + target ranges) for the search and the three passes
   k_unit_prep<<<cell_grid(c, 8), 128, 0, c->stream>>>(c->grid, c->s.cell_list, c->s.unit_list,
                                                       c->s.nunit_list, c->s.cell_start, c->s.cell_end,
-                                                      c->s.cell_hmax, c->s.unit_rec, c->s.cell_unit);
-  kern<<<cell_grid(c, 4), kCT, smem, c->stream>>>(
+                                                      c->s.cell_hmax, c->s.unit_rec);
+  kern<<<cell_grid(c, 2), kCT, smem, c->stream>>>(
       c->P.x, c->P.y, c->P.z, c->P.h, c->grid, c->s.cell_start, c->s.cell_end, c->s.cell_hmax,
-      c->s.cell_list, c->s.ncell_list, c->s.cell_unit, c->s.unit_rec, c->s.work + 0, c->s.nbr,
-      c->s.ncount, c->maxn, c->s.nbr_maxcount);
+      c->s.unit_rec, c->s.nunit_list, c->s.work + 0, c->s.nbr, c->s.ncount, c->maxn,
+      c->s.nbr_maxcount);
   return 2;
 }
 
@@ -1513,14 +1558,18 @@ static void momentum_t(sph_ctx* c) {
   MomTgt tg = {P.h, c->s.wB, c->s.rinv, c->s.X, P.c11, P.c12, P.c13, P.c22, P.c23, P.c33};
   MomOut out = {P.ax, P.ay, P.az, P.du, P.vsig};
   cudaMemsetAsync(c->s.work + 3, 0, sizeof(uint32_t), c->stream);
+  const int64_t nall = P.n + c->n_halo;  // owned + halo sources
+  k_mom_records<<<grid_blocks(c, nall, 256, 8), 256, 0, c->stream>>>(src, nall,
+                                                                     reinterpret_cast<double2*>(c->s.mrec));
   k_momentum_c<N, W2, KM><<<cell_grid(c, 1), kCTM, smem, c->stream>>>(
       src, tg, out, c->grid, c->s.cell_start, c->s.cell_end, c->s.cell_hmax, c->s.cell_list,
-      c->s.ncell_list, c->s.unit_rec, c->s.nunit_list, c->s.work + 3, c->s.nbr, c->s.ncount, c->maxn, c->phys, c->s.dts, c->s.cnt);
+      c->s.ncell_list, c->s.unit_rec, c->s.nunit_list, c->s.work + 3, c->s.nbr, c->s.ncount, c->maxn, c->phys, c->s.dts, c->s.cnt,
+      reinterpret_cast<const double2*>(c->s.mrec));
 }
 
 int launch_momentum(sph_ctx* c) {
   SPH_DISPATCH(momentum_t);
-  return 1;
+  return 2;  // source records + the pass
 }
 
 }  // namespace sphb

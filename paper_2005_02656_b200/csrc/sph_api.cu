@@ -299,10 +299,10 @@ sph_status sph_init(const sph_params* prm, int64_t capacity, sph_ctx** out) {
   AL(s.unit_rank, cap);
   AL(s.unit_list, cap + 1);
   AL(s.unit_rec, 3 * cap);
-  AL(s.cell_unit, cap);
   AL(s.nunit_list, 1);
   AL(s.mX, cap);
   AL(s.ct, 6 * cap);
+  AL(s.mrec, 18 * cap);
   AL(s.nbr, cap * (int64_t)c->maxn);
   AL(s.ncount, cap);
   AL(s.nbr_maxcount, 1);
@@ -771,8 +771,8 @@ sph_status sph_destroy(sph_ctx* c) {
   Scratch& s = c->s;
   void* ptrs[] = {s.keys, s.keys_alt, s.idx, s.idx_alt, s.hist, s.scan_tmp, s.gather, s.gather_id,
                   s.cell_start, s.cell_end, s.cell_hmax, s.cell_flag, s.cell_rank, s.cell_list,
-                  s.ncell_list, s.unit_flag, s.unit_rank, s.unit_list, s.nunit_list, s.unit_rec, s.cell_unit, s.nbr, s.ncount, s.nbr_maxcount, s.work, s.wB, s.ih2, s.vol, s.rinv, s.X,
-                  s.mX, s.ct, s.red, s.bbox, s.dts, s.cnt, s.diag, s.ktable};
+                  s.ncell_list, s.unit_flag, s.unit_rank, s.unit_list, s.nunit_list, s.unit_rec, s.nbr, s.ncount, s.nbr_maxcount, s.work, s.wB, s.ih2, s.vol, s.rinv, s.X,
+                  s.mX, s.ct, s.mrec, s.red, s.bbox, s.dts, s.cnt, s.diag, s.ktable};
   for (void* p : ptrs)
     if (p) cudaFree(p);
   delete c;

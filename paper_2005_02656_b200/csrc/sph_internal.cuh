@@ -82,7 +82,6 @@ struct Scratch {
   uint32_t* unit_list = nullptr;            // cap + 1: index into cell_list of each unit's first cell
   uint32_t* nunit_list = nullptr;           // device scalar
   int4* unit_rec = nullptr;                 // 3 x cap: per unit, its union stencil + target range
-  uint32_t* cell_unit = nullptr;            // cap: unit of each cell-list entry
   int64_t max_cells = 0;
   // neighbours
   uint32_t* nbr = nullptr;       // cap * maxn
@@ -96,7 +95,8 @@ struct Scratch {
   double* rinv = nullptr;  // 1 / rho
   double* X = nullptr;     // P / (Omega rho^2)   (reading R1)
   double* mX = nullptr;    // m P / (Omega rho^2)
-  double* ct = nullptr;    // 6 x cap: (B/h^3) C, written by IAD, staged by momentum
+  double* ct = nullptr;    // 6 x cap: (B/h^3) C, written by IAD (and exchanged as halo #3)
+  double* mrec = nullptr;  // 18 x cap: momentum source records (144 B each), bulk-copied into smem
   // reductions
   double* red = nullptr;   // block partials
   double* bbox = nullptr;  // 8 doubles (device)

@@ -116,9 +116,8 @@ __host__ __device__ __forceinline__ double cell_reach(const Grid& g, double cell
 // Particles are sorted by cell Morton code, so a unit's targets are one contiguous
 // range, and the unit stages the UNION of its cells' stencils once: 4x4x3 = 48 cells
 // for four 27-cell stencils, i.e. 12 staged cells per target cell instead of 27.
-// Neighbour rows are written in the unit stencil's slot numbering; a cell's own
-// slots map into it monotonically (both enumerate z, then y, then x over unwrapped
-// coordinates), so rows stay sorted in the staging order.
+// The search stages the same unit stencil and writes neighbour rows in its slot
+// numbering, so rows are sorted in the passes' staging order.
 __host__ __device__ __forceinline__ void unit_base(const Grid& g, const int c3[3], int b3[3]) {
   for (int d = 0; d < 3; ++d) b3[d] = g.ubits > d ? (c3[d] & ~1) : c3[d];
 }
@@ -165,13 +164,6 @@ __host__ __device__ __forceinline__ void make_unit_stencil(const Grid& g, const 
     u.cnt[d] = hi[d] - lo[d] + 1;
     u.K *= u.cnt[d];
   }
-}
-
-// unit-stencil slot of slot k of a cell stencil st (st's box lies inside u's)
-__host__ __device__ __forceinline__ int unit_slot(const Stencil& st, const Stencil& u, int k) {
-  const int i0 = k % st.cnt[0], i1 = (k / st.cnt[0]) % st.cnt[1], i2 = k / (st.cnt[0] * st.cnt[1]);
-  return (st.lo[0] + i0 - u.lo[0]) +
-         u.cnt[0] * ((st.lo[1] + i1 - u.lo[1]) + u.cnt[1] * (st.lo[2] + i2 - u.lo[2]));
 }
 
 }  // namespace sphb
