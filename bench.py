@@ -217,7 +217,7 @@ def run_ours(args):
     with torch.cuda.stream(stream):
         sim = sph.Simulation(d, capacity=cap, stream=stream.cuda_stream, rank=rank, nranks=world,
                              unique_id=uid, kernel_mode=sph.KERNEL_MODES[args.kernel_mode],
-                             symmetric=int(args.symmetric))
+                             symmetric=int(args.symmetric), redecomp_every=args.redecomp_every)
         for _ in range(args.warmup):
             sim.step()
         torch.cuda.synchronize()
@@ -312,6 +312,7 @@ def run_ours(args):
         "config": {"workload": workload_label(args), "description": desc,
                    "particles_per_gpu": n_local, "particles_total": n_total,
                    "kernel_mode": args.kernel_mode, "symmetric": bool(args.symmetric),
+                   "redecomp_every": args.redecomp_every,
                    "neighbors_mean": diag["nbr_total"] / max(1, diag["n_owned"]),
                    "l2": "no flush: every SoA field array >= 200 MB > 126 MB L2",
                    "parallelism": f"sfc{max(world, 1)}" if world > 1 else "1 GPU"},
@@ -348,6 +349,8 @@ def main():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--kernel-mode", default="poly", choices=["poly", "table", "sin"],
                     help="kernel evaluation in the pair passes (sph.h SPH_KERNEL_*; A/B of P:248)")
+    ap.add_argument("--redecomp-every", type=int, default=1,
+                    help="multi-GPU: recompute splitters every k-th step (sph_params.redecomp_every)")
     ap.add_argument("--symmetric", action="store_true",
                     help="neighbour relation r < 2 max(h_a, h_b) (sph_params.symmetric)")
     args = ap.parse_args()

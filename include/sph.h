@@ -42,7 +42,7 @@
 extern "C" {
 #endif
 
-#define SPH_ABI_VERSION 3
+#define SPH_ABI_VERSION 4
 
 typedef struct sph_ctx sph_ctx;
 
@@ -94,6 +94,10 @@ typedef struct {
   int    symmetric;       /* 0: N(a) = {b : r < 2 h_a} (gather, R10);                     */
                           /* 1: r < 2 max(h_a, h_b) -- b in N(a) iff a in N(b), pair forces */
                           /* antisymmetric, exact conservation for variable h (closes R24) */
+  int    redecomp_every;  /* multi-GPU: recompute the key-prefix histogram + splitters    */
+                          /* every k-th step only (the top tree changes slowly;    */
+                          /* SURVEY 8(f) NEXT-3); migration still runs every step against */
+                          /* the kept splitters.  0 or 1: every step.  Ignored on 1 GPU.  */
 } sph_params;
 
 typedef struct {          /* caller-owned DEVICE buffers, each >= capacity elements       */

@@ -389,8 +389,16 @@ bool dist_splitters(sph_ctx* c) {
   const int mbits = 3 * g.cbits;
   // bins are whole pair-pass units (shift >= ubits): a unit never straddles two ranks,
   // so every rank stages the same unit stencils as one GPU does (bit-identical sums)
-  D.shift = mbits > kBinBits ? mbits - kBinBits : 0;
-  if (D.shift < g.ubits) D.shift = g.ubits < mbits ? g.ubits : mbits;
+  int shift = mbits > kBinBits ? mbits - kBinBits : 0;
+  if (shift < g.ubits) shift = g.ubits < mbits ? g.ubits : mbits;
+  // lazy re-decomposition: keep the splitters for `every` steps while the bin
+  // space is unchanged; migration below still moves every particle to its owner
+  const bool keep = D.have_split && D.every > 1 && (D.decomp_calls % D.every) != 0 && shift == D.shift &&
+                    ((int64_t)1 << (mbits - shift)) == D.nbins;
+  ++D.decomp_calls;
+  if (keep) return true;
+  D.shift = shift;
+  D.have_split = true;
   D.nbins = (int64_t)1 << (mbits - D.shift);
   CUK(cudaMemsetAsync(D.hist_d, 0, sizeof(unsigned long long) * D.nbins, c->stream));
   if (c->P.n) {
@@ -551,6 +559,7 @@ bool dist_init(sph_ctx* c, const sph_params* prm) {
   c->dist = D;
   D->G = prm->nranks;
   D->rank = prm->rank;
+  D->every = prm->redecomp_every > 1 ? prm->redecomp_every : 1;
   D->split.assign(D->G + 1, 0);
   D->soff.assign(D->G, 0);
   D->scnt.assign(D->G, 0);

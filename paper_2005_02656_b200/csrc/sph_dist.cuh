@@ -18,6 +18,9 @@ struct Dist {
   ncclComm_t comm = nullptr;
 #endif
   int shift = 0;            // bin = Morton(cell) >> shift
+  int every = 1;            // recompute splitters every k-th step (sph_params.redecomp_every)
+  int64_t decomp_calls = 0; // dist_splitters calls so far
+  bool have_split = false;
   int64_t nbins = 1;
   int64_t n_total = 0;      // particles over all ranks
   int64_t n_halo = 0;

@@ -16,7 +16,7 @@ _HERE = os.path.dirname(os.path.abspath(__file__))
 # SPH_LIB selects another in-tree build of the same library (A/B runs of kernel variants)
 LIB_PATH = os.environ.get("SPH_LIB") or os.path.join(_HERE, "libsph.so")
 
-ABI_VERSION = 3
+ABI_VERSION = 4
 KERNEL_MODES = {"poly": 0, "table": 1, "sin": 2}
 EOS = {"linear": 0, "ideal": 1}
 STATUS = {0: "SPH_OK", 1: "SPH_ERR_NUMERIC", 2: "SPH_ERR_CONFIG", 3: "SPH_ERR_CAPACITY",
@@ -84,6 +84,7 @@ class Params(C.Structure):
         ("rank", C.c_int), ("nranks", C.c_int), ("nccl_unique_id", C.c_void_p),
         ("stream", C.c_void_p),
         ("kernel_mode", C.c_int), ("table_size", C.c_int), ("symmetric", C.c_int),
+        ("redecomp_every", C.c_int),
     ]
 
 
@@ -166,7 +167,8 @@ def make_params(d: dict, *, n: float = 6.0, alpha: float = 1.0, omega_mode: int 
                 courant: float = 0.3, dt_growth: float = 1.1, h_min: float = 0.0,
                 h_max: float = 0.0, u_floor: float = -np.inf, max_neighbors: int = 0,
                 cell_factor: float = 0.0, rank: int = 0, nranks: int = 1, stream=None,
-                kernel_mode: int = 0, table_size: int = 0, symmetric: int = 0) -> Params:
+                kernel_mode: int = 0, table_size: int = 0, symmetric: int = 0,
+                redecomp_every: int = 1) -> Params:
     p = Params()
     p.abi_version = ABI_VERSION
     p.sinc_n = n
@@ -189,6 +191,7 @@ def make_params(d: dict, *, n: float = 6.0, alpha: float = 1.0, omega_mode: int 
     p.kernel_mode = kernel_mode
     p.table_size = table_size
     p.symmetric = int(symmetric)
+    p.redecomp_every = int(redecomp_every)
     return p
 
 

@@ -37,6 +37,9 @@ def make_input():
 
 
 KW = {"symmetric": 1} if CASE == "cloud_sym" else {}
+# lazy re-decomposition (splitters kept for k steps): the 1-GPU
+# reference ignores it, so bit-identity also checks that kept splitters stay correct
+KW_MG = dict(KW, redecomp_every=int(os.environ.get("MGPU_REDECOMP", "1")))
 
 
 def main():
@@ -46,7 +49,7 @@ def main():
     d = make_input()
     mine = inputs.subset(d, np.arange(rank, d["x"].size, world))
     cap = int(d["x"].size * 1.2) + 1024  # any rank may end up owning a big share + halos
-    sim = sph.Simulation(mine, capacity=cap, rank=rank, nranks=world, unique_id=uid, **KW)
+    sim = sph.Simulation(mine, capacity=cap, rank=rank, nranks=world, unique_id=uid, **KW_MG)
     dts = []
     for _ in range(STEPS):
         dts.append(sim.step(want_dt=True))

@@ -24,13 +24,14 @@ def _port():
     return p
 
 
-@pytest.mark.parametrize("case", ["patch", "jitter", "weak", "evrard", "cloud_sym"])
-def test_multigpu_bit_identical_to_one_gpu(case):
+@pytest.mark.parametrize("case,redecomp", [("patch", 1), ("jitter", 1), ("weak", 1), ("evrard", 1),
+                                           ("cloud_sym", 1), ("jitter", 3)])
+def test_multigpu_bit_identical_to_one_gpu(case, redecomp):
     n = _ngpus()
     if n < 2:
         pytest.skip("needs >= 2 GPUs")
     world = min(n, 4)
-    env = dict(os.environ, MGPU_CASE=case, MGPU_STEPS="4")
+    env = dict(os.environ, MGPU_CASE=case, MGPU_STEPS="4", MGPU_REDECOMP=str(redecomp))
     cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={world}",
            "--master-addr", "127.0.0.1", "--master-port", str(_port()),
            os.path.join(ROOT, "tests", "mgpu_run.py")]
