@@ -49,12 +49,11 @@ void set_poly_constants(const double* poly, const double* dpoly) {
   cudaMemcpyToSymbol(c_dpoly, dpoly, sizeof(double) * kPolyTerms);
 }
 
-// Per-cell stencil tables.  The stencil's particles form one flat sequence (slots
+// Per-unit stencil tables.  The stencil's particles form one flat sequence (slots
 // in order, each slot a contiguous cell range); cum[k] is the flat index of slot
-// k's first particle.  A staging group is the flat range [gb, ge): slot k's local
-// particle l sits at shared index cum[k] + l - gb, and a row entry (k << 20 | l)
-// belongs to the group iff it lies in [pack(gb), pack(ge)) -- row entries ascend in
-// flat order, so "entry < pend" selects a target's segment of the group.
+// k's first particle.  A row entry IS a flat index f: the neighbour sits at shared
+// index f - gb of the staging group [gb, ge), and since rows ascend, "entry < ge"
+// selects a target's segment of the group (no table lookup per pair).
 struct CellSm {
   uint32_t t_start[kSlots];     // first sorted index of slot k's cell
   uint32_t cum[kSlots + 1];     // exclusive prefix of the slot counts
@@ -315,15 +314,10 @@ __device__ __forceinline__ int slot_of(const CellSm& S, uint32_t f) {
   }
   return lo;
 }
-// packed row entry of flat index ge (the first entry past the group), kSent at the end
-__device__ __forceinline__ uint32_t pend_of(const CellSm& S, uint32_t ge) {
-  if (ge >= S.total) return kSent;
-  const int k = slot_of(S, ge);
-  return ((uint32_t)k << kLocalBits) | (ge - S.cum[k]);
-}
 // shared-memory index of row entry e in the group starting at flat index gb
 __device__ __forceinline__ int qidx(const uint32_t* cum, uint32_t gb, uint32_t e) {
-  return (int)(cum[e >> kLocalBits] + (e & kLocalMask) - gb);
+  (void)cum;
+  return (int)(e - gb);  // row entries are flat staging indices of the unit stencil
 }
 
 __device__ __forceinline__ void shifts_of(const Grid& g, const CellSm& S, int slot, double sh[3]) {
@@ -507,7 +501,7 @@ __device__ __forceinline__ void walk_targets_fast(uint32_t t0, uint32_t t1,
     R = (m == 32 && off < lim) ? *rp : kSent;                                        \
     rp += 32;                                                                        \
     off += 32;                                                                       \
-    body(in ? (int)(cum[e >> kLocalBits] + (e & kLocalMask) - gb) : 0, in);          \
+    body(in ? (int)(e - gb) : 0, in);                                                \
     cur += m;                                                                        \
     if (m < 32) break;                                                               \
   }
@@ -636,7 +630,7 @@ __global__ void __launch_bounds__(kCT, 2) k_search(const double* __restrict__ x,
                 const uint32_t cs0 = cstart[cell];
                 if (t >= cs0 && t < cend[cell]) {
                   const int us = (q0 - st.lo[0]) + st.cnt[0] * ((q1 - st.lo[1]) + st.cnt[1] * (q2 - st.lo[2]));
-                  w.self = ((uint32_t)us << kLocalBits) | (t - cs0);
+                  w.self = S.cum[us] + (t - cs0);  // flat staging index of the target itself
                 }
               }
         }
@@ -653,7 +647,7 @@ __global__ void __launch_bounds__(kCT, 2) k_search(const double* __restrict__ x,
             v.x = (float)((x[j] + sh[0]) - org[0]);
             v.y = (float)((y[j] + sh[1]) - org[1]);
             v.z = (float)((z[j] + sh[2]) - org[2]);
-            v.w = __uint_as_float(((uint32_t)slot << kLocalBits) | l);
+            v.w = __uint_as_float(f);  // row entry: flat staging index in the unit stencil
             cand[q] = v;
             if constexpr (SYM) candb[q] = band32(h[j], M);
           }
@@ -733,7 +727,8 @@ __global__ void __launch_bounds__(kCT, 2) k_search(const double* __restrict__ x,
             // rare: exact fp64 test of the candidates inside a band (one ballot per step)
             auto exact = [&](const float4 cd, bool& hit0, bool& hit1, bool amb0, bool amb1) {
               const uint32_t pk = __float_as_uint(cd.w);
-              const uint32_t j = S.t_start[pk >> kLocalBits] + (pk & kLocalMask);
+              const int kq = slot_of(S, pk);
+              const uint32_t j = S.t_start[kq] + (pk - S.cum[kq]);
               double limb = 0.0;
               if constexpr (SYM) {
                 if (amb0 | amb1) {
@@ -939,7 +934,7 @@ __global__ void __launch_bounds__(kCTD, 1) k_density_c(
         if (threadIdx.x == 0) S.next[0] = 0;
         __syncthreads();
         for (uint32_t gb = 0, gi = 0; gb < S.total; gb += kDensCap, ++gi) {
-          const uint32_t ge = min(S.total, gb + kDensCap), pend = pend_of(S, ge);
+          const uint32_t ge = min(S.total, gb + kDensCap), pend = ge;
           if (threadIdx.x == 0) S.next[(gi + 1) & 1] = 0;
           stage2x2(g, S, gb, ge, x, y, z, m, s01, s23);
           __syncthreads();
@@ -1073,7 +1068,7 @@ __global__ void __launch_bounds__(kCTD, 1) k_iad_c(
         if (threadIdx.x == 0) S.next[0] = 0;
         __syncthreads();
         for (uint32_t gb = 0, gi = 0; gb < S.total; gb += kIadCap, ++gi) {
-          const uint32_t ge = min(S.total, gb + kIadCap), pend = pend_of(S, ge);
+          const uint32_t ge = min(S.total, gb + kIadCap), pend = ge;
           if (threadIdx.x == 0) S.next[(gi + 1) & 1] = 0;
           stage2x2(g, S, gb, ge, x, y, z, vol, s01, s23);
           __syncthreads();
@@ -1207,20 +1202,32 @@ constexpr int kMomPairs = 9;
 // Momentum source records: the kMomPairs double2 a pair reads from its source, one
 // contiguous 144-byte record per particle, built once per step after IAD (owned +
 // halo).  A staging group is then a handful of bulk copies (one per stencil slot).
-__global__ void k_mom_records(MomSrc src, int64_t n, double2* __restrict__ rec) {
-  for (int64_t j = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; j < n;
-       j += (int64_t)gridDim.x * blockDim.x) {
-    const int64_t cs = src.ct_stride;
-    double2* r = rec + j * kMomPairs;
-    r[0] = make_double2(src.x[j], src.y[j]);
-    r[1] = make_double2(src.z[j], src.vx[j]);
-    r[2] = make_double2(src.vy[j], src.vz[j]);
-    r[3] = make_double2(src.m[j], src.ih2[j]);
-    r[4] = make_double2(src.c[j], src.mX[j]);
-    r[5] = make_double2(src.mr[j], src.ct[j]);
-    r[6] = make_double2(src.ct[cs + j], src.ct[2 * cs + j]);
-    r[7] = make_double2(src.ct[3 * cs + j], src.ct[4 * cs + j]);
-    r[8] = make_double2(src.ct[5 * cs + j], 0.0);
+constexpr int kRecThreads = 256;  // k_mom_records block: records transposed through smem
+__global__ void __launch_bounds__(kRecThreads) k_mom_records(MomSrc src, int64_t n, double2* __restrict__ rec) {
+  // each thread assembles one record in shared memory, then the block writes its
+  // kRecThreads consecutive records as one contiguous, fully coalesced range
+  // (per-thread 144-byte-strided stores wrote each L2 sector piecemeal: 3.0 ms at 25M)
+  __shared__ double2 buf[kRecThreads * kMomPairs];
+  for (int64_t b0 = (int64_t)blockIdx.x * kRecThreads; b0 < n; b0 += (int64_t)gridDim.x * kRecThreads) {
+    const int64_t j = b0 + threadIdx.x;
+    if (j < n) {
+      const int64_t cs = src.ct_stride;
+      double2* r = buf + threadIdx.x * kMomPairs;
+      r[0] = make_double2(src.x[j], src.y[j]);
+      r[1] = make_double2(src.z[j], src.vx[j]);
+      r[2] = make_double2(src.vy[j], src.vz[j]);
+      r[3] = make_double2(src.m[j], src.ih2[j]);
+      r[4] = make_double2(src.c[j], src.mX[j]);
+      r[5] = make_double2(src.mr[j], src.ct[j]);
+      r[6] = make_double2(src.ct[cs + j], src.ct[2 * cs + j]);
+      r[7] = make_double2(src.ct[3 * cs + j], src.ct[4 * cs + j]);
+      r[8] = make_double2(src.ct[5 * cs + j], 0.0);
+    }
+    __syncthreads();
+    const int64_t cnt = min((int64_t)kRecThreads, n - b0) * kMomPairs;
+    double2* out = rec + b0 * kMomPairs;
+    for (int64_t e = threadIdx.x; e < cnt; e += kRecThreads) out[e] = buf[e];
+    __syncthreads();
   }
 }
 // per-target smem fields
@@ -1294,7 +1301,7 @@ __global__ void __launch_bounds__(kCTM, 1) k_momentum_c(
         if (threadIdx.x == 0) S.next[0] = 0;
         __syncthreads();
         for (uint32_t gb = 0, gi = 0; gb < S.total; gb += kMomCap, ++gi) {
-          const uint32_t ge = min(S.total, gb + kMomCap), pend = pend_of(S, ge);
+          const uint32_t ge = min(S.total, gb + kMomCap), pend = ge;
           if (threadIdx.x == 0) S.next[(gi + 1) & 1] = 0;
           // stage [gb, ge): warp 0 issues one bulk copy of consecutive records per slot
           // (the slot's cell is a contiguous range), all complete on one mbarrier
@@ -1559,7 +1566,7 @@ static void momentum_t(sph_ctx* c) {
   MomOut out = {P.ax, P.ay, P.az, P.du, P.vsig};
   cudaMemsetAsync(c->s.work + 3, 0, sizeof(uint32_t), c->stream);
   const int64_t nall = P.n + c->n_halo;  // owned + halo sources
-  k_mom_records<<<grid_blocks(c, nall, 256, 8), 256, 0, c->stream>>>(src, nall,
+  k_mom_records<<<grid_blocks(c, nall, kRecThreads, 6), kRecThreads, 0, c->stream>>>(src, nall,
                                                                      reinterpret_cast<double2*>(c->s.mrec));
   k_momentum_c<N, W2, KM><<<cell_grid(c, 1), kCTM, smem, c->stream>>>(
       src, tg, out, c->grid, c->s.cell_start, c->s.cell_end, c->s.cell_hmax, c->s.cell_list,

@@ -529,7 +529,7 @@ sph_status sph_get_neighbors(sph_ctx* c, int64_t* offsets, int64_t* ids, int64_t
   for (int64_t i = 0; i < n; ++i) offsets[i + 1] = offsets[i] + cnt[i];
   if (offsets[n] > cap) return SPH_ERR_CAPACITY;  // not sticky: caller retries with room
   if (!ids) return SPH_OK;
-  // rows hold packed (stencil slot, local) entries: decode with the cell tables
+  // rows hold flat indices into unit stencils: decode with the cell tables
   const Grid& g = c->grid;
   std::vector<uint64_t> keys(n);
   std::vector<uint32_t> cs(g.ncell), ce(g.ncell);
@@ -541,6 +541,9 @@ sph_status sph_get_neighbors(sph_ctx* c, int64_t* offsets, int64_t* ids, int64_t
                 cudaMemcpyDeviceToHost));
   const int64_t chunk = 1 << 14;
   std::vector<uint32_t> rows((size_t)chunk * c->maxn);
+  std::vector<int64_t> ucum, ucell;
+  int ub3[3] = {-1, -1, -1};
+  Stencil st;
   for (int64_t r0 = 0; r0 < n; r0 += chunk) {
     int64_t nr = std::min(chunk, n - r0);
     CK(cudaMemcpy(rows.data(), c->s.nbr + (size_t)r0 * c->maxn, sizeof(uint32_t) * nr * c->maxn,
@@ -549,13 +552,25 @@ sph_status sph_get_neighbors(sph_ctx* c, int64_t* offsets, int64_t* ids, int64_t
       const int64_t cell = key_cell_hd(g, keys[r0 + i]);
       int c3[3];
       cell_coords(g, cell, c3);
-      Stencil st;  // rows are numbered in the slots of the target's unit stencil
-      make_unit_stencil(g, c3, cs.data(), ce.data(), chm.data(), st);
+      // rows hold flat indices into the target's unit stencil (slots in order, each
+      // slot its cell's range): rebuild the slot prefix when the unit changes
+      int b3[3];
+      unit_base(g, c3, b3);
+      if (b3[0] != ub3[0] || b3[1] != ub3[1] || b3[2] != ub3[2]) {
+        memcpy(ub3, b3, sizeof(b3));
+        make_unit_stencil(g, c3, cs.data(), ce.data(), chm.data(), st);
+        ucum.assign(st.K + 1, 0);
+        ucell.assign(st.K, 0);
+        for (int k = 0; k < st.K; ++k) {
+          int sh[3];
+          ucell[k] = slot_cell(g, st, k, sh);
+          ucum[k + 1] = ucum[k] + (ce[ucell[k]] - cs[ucell[k]]);
+        }
+      }
       for (uint32_t k = 0; k < cnt[r0 + i]; ++k) {
         const uint32_t e = rows[(size_t)i * c->maxn + k];
-        int sh[3];
-        const int64_t sc = slot_cell(g, st, (int)(e >> kLocalBits), sh);
-        ids[offsets[r0 + i] + k] = id[cs[sc] + (e & kLocalMask)];
+        const int slot = (int)(std::upper_bound(ucum.begin(), ucum.end(), (int64_t)e) - ucum.begin()) - 1;
+        ids[offsets[r0 + i] + k] = id[cs[ucell[slot]] + (e - ucum[slot])];
       }
     }
   }

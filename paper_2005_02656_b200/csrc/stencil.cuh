@@ -4,9 +4,9 @@
 // A search cell c with largest smoothing length h_max(c) needs, per dimension,
 // the cells within R_d = ceil(2 h_max (1 + 2^-20) / edge_d) of c (all cells of
 // the dimension when 2R+1 >= nc).  Slots enumerate that box z-major, then y,
-// then x; a neighbour-row entry is packed as (slot << 20) | local index in the
-// slot's cell, so rows sorted by the packed value are sorted by slot, then by
-// particle order -- exactly the order in which candidates are staged.
+// then x.  A pair pass stages the stencil of a unit of cells (below) as one flat
+// sequence, slot by slot; a neighbour-row entry is the flat index in it, so rows
+// sorted by entry are in staging order.
 #pragma once
 
 #include <cstring>
@@ -16,8 +16,6 @@
 namespace sphb {
 
 constexpr int kKMax = 1024;       // max slots per stencil (R <= 4 in every dim)
-constexpr int kLocalBits = 20;    // local index bits of a packed row entry
-constexpr uint32_t kLocalMask = (1u << kLocalBits) - 1u;
 
 struct Stencil {
   int lo[3];    // first cell coordinate per dim (may be < 0 or run past nc when periodic)
@@ -116,8 +114,8 @@ __host__ __device__ __forceinline__ double cell_reach(const Grid& g, double cell
 // Particles are sorted by cell Morton code, so a unit's targets are one contiguous
 // range, and the unit stages the UNION of its cells' stencils once: 4x4x3 = 48 cells
 // for four 27-cell stencils, i.e. 12 staged cells per target cell instead of 27.
-// The search stages the same unit stencil and writes neighbour rows in its slot
-// numbering, so rows are sorted in the passes' staging order.
+// The search stages the same unit stencil and writes neighbour rows as flat
+// indices into it, so rows are sorted in the passes' staging order.
 __host__ __device__ __forceinline__ void unit_base(const Grid& g, const int c3[3], int b3[3]) {
   for (int d = 0; d < 3; ++d) b3[d] = g.ubits > d ? (c3[d] & ~1) : c3[d];
 }
