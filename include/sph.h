@@ -42,7 +42,7 @@
 extern "C" {
 #endif
 
-#define SPH_ABI_VERSION 4
+#define SPH_ABI_VERSION 5
 
 typedef struct sph_ctx sph_ctx;
 
@@ -124,7 +124,9 @@ typedef struct {
 /* per-phase device time, accumulated while profiling is on (sph_set_profiling) */
 enum {
   SPH_PH_BBOX = 0, SPH_PH_KEYS, SPH_PH_SORT, SPH_PH_PERMUTE, SPH_PH_CELLS, SPH_PH_NEIGHBORS,
-  SPH_PH_DENSITY, SPH_PH_IAD, SPH_PH_MOMENTUM, SPH_PH_UPDATE, SPH_PH_HALO, SPH_PH_COUNT
+  SPH_PH_DENSITY, SPH_PH_IAD, SPH_PH_MOMENTUM, SPH_PH_UPDATE, SPH_PH_HALO,
+  SPH_PH_RECORDS,  /* momentum source records (144 B/particle) built before the momentum pass */
+  SPH_PH_COUNT
 };
 
 int         sph_abi_version(void);

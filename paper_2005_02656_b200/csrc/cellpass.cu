@@ -1565,9 +1565,6 @@ static void momentum_t(sph_ctx* c) {
   MomTgt tg = {P.h, c->s.wB, c->s.rinv, c->s.X, P.c11, P.c12, P.c13, P.c22, P.c23, P.c33};
   MomOut out = {P.ax, P.ay, P.az, P.du, P.vsig};
   cudaMemsetAsync(c->s.work + 3, 0, sizeof(uint32_t), c->stream);
-  const int64_t nall = P.n + c->n_halo;  // owned + halo sources
-  k_mom_records<<<grid_blocks(c, nall, kRecThreads, 6), kRecThreads, 0, c->stream>>>(src, nall,
-                                                                     reinterpret_cast<double2*>(c->s.mrec));
   k_momentum_c<N, W2, KM><<<cell_grid(c, 1), kCTM, smem, c->stream>>>(
       src, tg, out, c->grid, c->s.cell_start, c->s.cell_end, c->s.cell_hmax, c->s.cell_list,
       c->s.ncell_list, c->s.unit_rec, c->s.nunit_list, c->s.work + 3, c->s.nbr, c->s.ncount, c->maxn, c->phys, c->s.dts, c->s.cnt,
@@ -1576,7 +1573,16 @@ static void momentum_t(sph_ctx* c) {
 
 int launch_momentum(sph_ctx* c) {
   SPH_DISPATCH(momentum_t);
-  return 2;  // source records + the pass
+  return 1;
+}
+
+int launch_mom_records(sph_ctx* c) {
+  sph_particles& P = c->P;
+  MomSrc src = {P.x, P.y, P.z, P.vx, P.vy, P.vz, P.m, c->s.ih2, P.c, c->s.mX, c->s.vol, c->s.ct, c->cap};
+  const int64_t nall = P.n + c->n_halo;  // owned + halo sources
+  k_mom_records<<<grid_blocks(c, nall, kRecThreads, 6), kRecThreads, 0, c->stream>>>(
+      src, nall, reinterpret_cast<double2*>(c->s.mrec));
+  return 1;
 }
 
 }  // namespace sphb

@@ -619,6 +619,12 @@ sph_status sph_momentum_energy(sph_ctx* c, double* dt_out) {
   if (!c) return SPH_ERR_CONFIG;
   if (c->status != SPH_OK) return c->status;
   if (c->stage < 3) return fail(c, SPH_ERR_STATE, "sph_momentum_energy before sph_iad");
+  if (c->P.n) {  // source records of owned + halo particles for the pass's bulk staging
+    Phase ph(c, SPH_PH_RECORDS);
+    int k = launch_mom_records(c);
+    CKL();
+    ph.done(k);
+  }
   {
     Phase ph(c, SPH_PH_MOMENTUM);
     int k = c->P.n ? launch_momentum(c) : 0;

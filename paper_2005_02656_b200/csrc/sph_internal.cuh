@@ -161,6 +161,7 @@ int launch_neighbors(sph_ctx* c);
 int launch_density(sph_ctx* c);
 int launch_iad(sph_ctx* c);
 int launch_momentum(sph_ctx* c);
+int launch_mom_records(sph_ctx* c);
 int launch_dt_finalize(sph_ctx* c);
 int launch_update(sph_ctx* c);
 int launch_diag(sph_ctx* c);

@@ -16,13 +16,13 @@ _HERE = os.path.dirname(os.path.abspath(__file__))
 # SPH_LIB selects another in-tree build of the same library (A/B runs of kernel variants)
 LIB_PATH = os.environ.get("SPH_LIB") or os.path.join(_HERE, "libsph.so")
 
-ABI_VERSION = 4
+ABI_VERSION = 5
 KERNEL_MODES = {"poly": 0, "table": 1, "sin": 2}
 EOS = {"linear": 0, "ideal": 1}
 STATUS = {0: "SPH_OK", 1: "SPH_ERR_NUMERIC", 2: "SPH_ERR_CONFIG", 3: "SPH_ERR_CAPACITY",
           4: "SPH_ERR_CUDA", 5: "SPH_ERR_COMM", 6: "SPH_ERR_STATE"}
 PHASES = ("bbox", "keys", "sort", "permute", "cells", "neighbors", "density", "iad", "momentum",
-          "update", "halo")
+          "update", "halo", "records")
 
 STATE_FIELDS = ("x", "y", "z", "vx", "vy", "vz", "h", "m", "u", "vhx", "vhy", "vhz", "du_prev")
 OUT_FIELDS = ("rho", "omega", "p", "c", "c11", "c12", "c13", "c22", "c23", "c33", "ax", "ay", "az",
