@@ -392,12 +392,17 @@ __device__ __forceinline__ void walk_targets(uint32_t t0, uint32_t t1, const uin
 // the per-(target, group) setup and reduction is shared by two targets and the
 // unused lanes at the end of a segment drop from up to 31 to up to 15.  Both
 // halves step together; a half whose segment ended idles until the other is done.
+// Row chunks stream through a 2-deep ring consumed in place (unrolled by two): a
+// shifted ring (e0 = e1; e1 = e2 <- load) made every step wait for the load it had
+// just issued (ncu: long_sb on the ring move), and a momentum step is long enough
+// that two chunks of prefetch cover the load latency.
 template <class Body, class Finish>
 __device__ __forceinline__ void walk_targets_half(uint32_t t0, uint32_t t1,
                                                   const uint32_t* __restrict__ nbr, int maxn,
                                                   const uint32_t* s_n, uint32_t* s_cur,
                                                   uint32_t pend, const uint32_t* cum, uint32_t gb,
                                                   uint32_t* s_next, Body&& body, Finish&& finish) {
+  (void)cum;
   const int lane = threadIdx.x & 31, l16 = lane & 15;
   const unsigned hmask = (threadIdx.x & 16) ? 0xffff0000u : 0x0000ffffu;
   auto claim = [&]() {
@@ -406,46 +411,51 @@ __device__ __forceinline__ void walk_targets_half(uint32_t t0, uint32_t t1,
     return __shfl_sync(0xffffffffu, v, lane & 16);
   };
   uint32_t t = claim();
-  uint32_t f0 = kSent, f1 = kSent, f2 = kSent;
+  uint32_t f0 = kSent, f1 = kSent;
   if (t < t1) {
     const uint32_t c0 = s_cur[t - t0] + l16, nn = s_n[t - t0];
     const uint32_t* r = nbr + (size_t)t * maxn;
     f0 = row_chunk(r, c0, nn);
     f1 = row_chunk(r, c0 + 16, nn);
-    f2 = row_chunk(r, c0 + 32, nn);
   }
   while (__any_sync(0xffffffffu, t < t1)) {
     const bool act = t < t1;
     const uint32_t i = act ? t - t0 : 0;
     const uint32_t n = act ? s_n[i] : 0;
-    const uint32_t* row = nbr + (size_t)(act ? t : 0) * maxn;
     uint32_t cur = act ? s_cur[i] : 0;
-    uint32_t e0 = f0, e1 = f1, e2 = f2;
+    uint32_t off = cur + l16 + 32;  // row position of the next chunk to load (two ahead)
+    const uint32_t* rp = nbr + (size_t)(act ? t : 0) * maxn + off;
+    uint32_t e0 = f0, e1 = f1;
     const uint32_t tn = claim();
-    f0 = f1 = f2 = kSent;
+    f0 = f1 = kSent;
     if (tn < t1) {
       const uint32_t cn = s_cur[tn - t0] + l16, nn = s_n[tn - t0];
       const uint32_t* r = nbr + (size_t)tn * maxn;
       f0 = row_chunk(r, cn, nn);
       f1 = row_chunk(r, cn + 16, nn);
-      f2 = row_chunk(r, cn + 32, nn);
     }
     if (act) body.begin(i);
     bool live = act;
+#define SPH_HALF_STEP(R)                                                       \
+  {                                                                            \
+    const uint32_t e = R;                                                      \
+    const bool in = live && e < pend;                                          \
+    const int m = __popc(__ballot_sync(0xffffffffu, in) & hmask);              \
+    const bool more = live && m == 16;                                         \
+    const int qi = (int)(e - gb);                                              \
+    R = (more && off < n) ? *rp : kSent;                                       \
+    rp += 16;                                                                  \
+    off += 16;                                                                 \
+    if (in) body(qi);                                                          \
+    cur += m;                                                                  \
+    live = more;                                                               \
+    if (!__any_sync(0xffffffffu, live)) break;                                 \
+  }
     for (;;) {
-      const bool in = live && e0 < pend;
-      const unsigned b = __ballot_sync(0xffffffffu, in);
-      const int m = __popc(b & hmask);
-      const bool more = live && m == 16;
-      const uint32_t e3 = more ? row_chunk(row, cur + 48 + l16, n) : kSent;
-      if (in) body(qidx(cum, gb, e0));
-      cur += m;
-      live = more;
-      if (!__any_sync(0xffffffffu, live)) break;
-      e0 = e1;
-      e1 = e2;
-      e2 = e3;
+      SPH_HALF_STEP(e0)
+      SPH_HALF_STEP(e1)
     }
+#undef SPH_HALF_STEP
     finish(act, i, cur);
     t = tn;
   }
@@ -498,10 +508,11 @@ __device__ __forceinline__ void walk_targets_fast(uint32_t t0, uint32_t t1,
     const uint32_t e = R;                                                            \
     const bool in = e < pend;                                                        \
     const int m = __popc(__ballot_sync(0xffffffffu, in));                            \
+    const int qi = in ? (int)(e - gb) : 0; /* e dies here: the refill can reuse R */ \
     R = (m == 32 && off < lim) ? *rp : kSent;                                        \
     rp += 32;                                                                        \
     off += 32;                                                                       \
-    body(in ? (int)(e - gb) : 0, in);                                                \
+    body(qi, in);                                                                    \
     cur += m;                                                                        \
     if (m < 32) break;                                                               \
   }
