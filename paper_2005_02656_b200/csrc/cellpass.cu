@@ -26,6 +26,7 @@ constexpr int kTgtU = 416;        // targets per sub-block (a whole 2x2x1 unit, 
 constexpr int kSlots = kKMax;     // slot tables: every stencil the grid chooser admits
 constexpr int kCellChunk = 4;     // consecutive cells per claim (L2 reuse of shared stencils)
 constexpr int kSearchCap = 4096;  // staged candidates per group (float4): a unit stencil in one group
+constexpr int kNT = 4;            // search: targets per warp sharing each candidate load
 constexpr int kTS = 32;           // search tile: candidates per fp32 bounding box (16 measured 2.7 ms slower)
 constexpr int kSearchTiles = kSearchCap / kTS + 1;          // + the sentinel tile
 constexpr int kSearchWords = (kSearchCap / kTS + 31) / 32;  // tile bitmask words
@@ -698,59 +699,63 @@ __global__ void __launch_bounds__(kCT, 2) k_search(const double* __restrict__ x,
           __syncthreads();
           // two targets per warp share every staged-candidate load (fp32 test data in
           // registers; the fp64 data of the rare exact test in shared memory)
-          for (uint32_t ta = t0 + 2 * warp; ta < t1; ta += 2 * kNW) {  // (static: ~18 pairs per warp)
-            const bool has_b = ta + 1 < t1;
-            const uint32_t tb = has_b ? ta + 1 : ta;  // odd tail: duplicate, identical writes
-            const TgtW& TA = TW[ta - t0];
-            const TgtW& TB = TW[tb - t0];
-            const float ax0 = TA.f[0], ay0 = TA.f[1], az0 = TA.f[2], lo0 = TA.f[3], hi0 = TA.f[4];
-            const float ax1 = TB.f[0], ay1 = TB.f[1], az1 = TB.f[2], lo1 = TB.f[3], hi1 = TB.f[4];
-            const uint32_t self0 = TA.self, self1 = TB.self;
-            uint32_t cnt0 = tcount[ta - t0], cnt1 = tcount[tb - t0];
-            uint32_t* row0 = nbr + (size_t)ta * maxn;
-            uint32_t* row1 = nbr + (size_t)tb * maxn;
-            // keep the row bases in registers (else ptxas re-derives nbr + t*maxn + p in 64-bit per store)
-            asm volatile("" : "+l"(row0), "+l"(row1));
-            // one staged candidate against both targets: fp32 band test, exact fp64 when inside it
-            auto test = [&](const float4 cd, const float2 cb, bool& hit0, bool& hit1, bool& amb0,
-                            bool& amb1) {
+          // kNT targets per warp share every staged-candidate load (fp32 test data in
+          // registers; the fp64 data of the rare exact test in shared memory)
+          for (uint32_t tq = t0 + kNT * warp; tq < t1; tq += kNT * kNW) {
+            uint32_t tt[kNT];
+            float ax[kNT], ay[kNT], az[kNT], lo[kNT], hi[kNT];
+            uint32_t self[kNT], cnt[kNT];
+            uint32_t* row[kNT];
+  #pragma unroll
+            for (int u = 0; u < kNT; ++u) {
+              tt[u] = min(tq + u, t1 - 1);  // short tail: duplicates, identical writes
+              const TgtW& T = TW[tt[u] - t0];
+              ax[u] = T.f[0]; ay[u] = T.f[1]; az[u] = T.f[2]; lo[u] = T.f[3]; hi[u] = T.f[4];
+              self[u] = T.self;
+              cnt[u] = tcount[tt[u] - t0];
+              row[u] = nbr + (size_t)tt[u] * maxn;
+              // keep the row bases in registers (else ptxas re-derives nbr + t*maxn + p in 64-bit per store)
+              asm volatile("" : "+l"(row[u]));
+            }
+            // one staged candidate against every target: fp32 band test, exact fp64 inside the band
+            auto test = [&](const float4 cd, const float2 cb, bool (&hit)[kNT], bool (&amb)[kNT]) {
               const uint32_t pk = __float_as_uint(cd.w);
-              float dx0 = cd.x - ax0, dy0 = cd.y - ay0, dz0 = cd.z - az0;
-              float dx1 = cd.x - ax1, dy1 = cd.y - ay1, dz1 = cd.z - az1;
-              if constexpr (W2) {
-                wrap32(st, g, dx0, dy0, dz0);
-                wrap32(st, g, dx1, dy1, dz1);
+  #pragma unroll
+              for (int u = 0; u < kNT; ++u) {
+                float dx = cd.x - ax[u], dy = cd.y - ay[u], dz = cd.z - az[u];
+                if constexpr (W2) wrap32(st, g, dx, dy, dz);
+                const float r = fmaf(dz, dz, fmaf(dy, dy, dx * dx));
+                bool in = r < lo[u];
+                bool a = (r >= lo[u]) & (r < hi[u]);
+                if constexpr (SYM) {  // either side's support
+                  in |= r < cb.x;
+                  a = !in & (a | (r < cb.y));
+                }
+                amb[u] = a;
+                hit[u] = in & (pk != self[u]);
               }
-              const float r0 = fmaf(dz0, dz0, fmaf(dy0, dy0, dx0 * dx0));
-              const float r1 = fmaf(dz1, dz1, fmaf(dy1, dy1, dx1 * dx1));
-              bool in0 = r0 < lo0, in1 = r1 < lo1;
-              amb0 = (r0 >= lo0) & (r0 < hi0);
-              amb1 = (r1 >= lo1) & (r1 < hi1);
-              if constexpr (SYM) {  // either side's support
-                in0 |= r0 < cb.x;
-                in1 |= r1 < cb.x;
-                amb0 = !in0 & (amb0 | (r0 < cb.y));
-                amb1 = !in1 & (amb1 | (r1 < cb.y));
-              }
-              hit0 = in0 & (pk != self0);
-              hit1 = in1 & (pk != self1);
             };
             // rare: exact fp64 test of the candidates inside a band (one ballot per step)
-            auto exact = [&](const float4 cd, bool& hit0, bool& hit1, bool amb0, bool amb1) {
+            auto exact = [&](const float4 cd, bool (&hit)[kNT], const bool (&amb)[kNT]) {
+              bool any = false;
+  #pragma unroll
+              for (int u = 0; u < kNT; ++u) any |= amb[u];
+              if (!any) return;
               const uint32_t pk = __float_as_uint(cd.w);
               const int kq = slot_of(S, pk);
               const uint32_t j = S.t_start[kq] + (pk - S.cum[kq]);
               double limb = 0.0;
               if constexpr (SYM) {
-                if (amb0 | amb1) {
-                  const double thb = 2.0 * h[j];
-                  limb = __dmul_rn(thb, thb);
-                }
+                const double thb = 2.0 * h[j];
+                limb = __dmul_rn(thb, thb);
               }
-              if (amb0) hit0 = exact_hit(g, x, y, z, j, ta, TA.pos, fmax(TA.lim, limb));
-              if (amb1) hit1 = exact_hit(g, x, y, z, j, tb, TB.pos, fmax(TB.lim, limb));
+  #pragma unroll
+              for (int u = 0; u < kNT; ++u) {
+                const TgtW& T = TW[tt[u] - t0];
+                if (amb[u]) hit[u] = exact_hit(g, x, y, z, j, tt[u], T.pos, fmax(T.lim, limb));
+              }
             };
-            // Tiles either target can reach.  Box distance in the prefilter's own fp32
+            // Tiles any target can reach.  Box distance in the prefilter's own fp32
             // expression: rounding is monotone, so box d2 <= r2_32 of every member, and
             // box d2 >= hi excludes hits and ambiguous candidates alike (lists stay exact).
             uint32_t need[6] = {0u, 0u, 0u, 0u, 0u, 0u};
@@ -763,15 +768,14 @@ __global__ void __launch_bounds__(kCT, 2) k_search(const double* __restrict__ x,
                   nd = true;
                 } else {
                   const float4 L = tlo[q], H = thi[q];
-                  const float bx0 = fmaxf(fmaxf(L.x - ax0, ax0 - H.x), 0.f);
-                  const float by0 = fmaxf(fmaxf(L.y - ay0, ay0 - H.y), 0.f);
-                  const float bz0 = fmaxf(fmaxf(L.z - az0, az0 - H.z), 0.f);
-                  const float bx1 = fmaxf(fmaxf(L.x - ax1, ax1 - H.x), 0.f);
-                  const float by1 = fmaxf(fmaxf(L.y - ay1, ay1 - H.y), 0.f);
-                  const float bz1 = fmaxf(fmaxf(L.z - az1, az1 - H.z), 0.f);
                   const float hb = SYM ? H.w : -1.0f;
-                  nd = (fmaf(bz0, bz0, fmaf(by0, by0, bx0 * bx0)) < fmaxf(hi0, hb)) |
-                       (fmaf(bz1, bz1, fmaf(by1, by1, bx1 * bx1)) < fmaxf(hi1, hb));
+  #pragma unroll
+                  for (int u = 0; u < kNT; ++u) {
+                    const float bx = fmaxf(fmaxf(L.x - ax[u], ax[u] - H.x), 0.f);
+                    const float by = fmaxf(fmaxf(L.y - ay[u], ay[u] - H.y), 0.f);
+                    const float bz = fmaxf(fmaxf(L.z - az[u], az[u] - H.z), 0.f);
+                    nd |= fmaf(bz, bz, fmaf(by, by, bx * bx)) < fmaxf(hi[u], hb);
+                  }
                 }
               }
               need[w] = __ballot_sync(0xffffffffu, nd);
@@ -791,9 +795,8 @@ __global__ void __launch_bounds__(kCT, 2) k_search(const double* __restrict__ x,
               m0 &= m0 - 1;
               return q;
             };
-            // per step two candidates per lane (kTS = 16: four tiles, lanes 0-15 on the
-            // lower tile of each pair): four independent test chains in flight, and the
-            // lane order of every ballot is the ascending staging order
+            // per step two candidates per lane (two tiles): kNT x 2 independent test chains,
+            // and the lane order of every ballot is the ascending staging order
             for (;;) {
               const int qA = next_tile();
               if (qA == ntile) break;
@@ -813,28 +816,32 @@ __global__ void __launch_bounds__(kCT, 2) k_search(const double* __restrict__ x,
                 bA = candb[iF];
                 bB = candb[iS];
               }
-              bool hA0, hA1, hB0, hB1, aA0, aA1, aB0, aB1;
-              test(cA, bA, hA0, hA1, aA0, aA1);
-              test(cB, bB, hB0, hB1, aB0, aB1);
-              if (__ballot_sync(0xffffffffu, aA0 | aA1 | aB0 | aB1)) {
-                exact(cA, hA0, hA1, aA0, aA1);
-                exact(cB, hB0, hB1, aB0, aB1);
+              bool hA[kNT], hB[kNT], aA[kNT], aB[kNT];
+              test(cA, bA, hA, aA);
+              test(cB, bB, hB, aB);
+              bool anyamb = false;
+  #pragma unroll
+              for (int u = 0; u < kNT; ++u) anyamb |= aA[u] | aB[u];
+              if (__ballot_sync(0xffffffffu, anyamb)) {
+                exact(cA, hA, aA);
+                exact(cB, hB, aB);
               }
-              const unsigned bA0 = __ballot_sync(0xffffffffu, hA0), bA1 = __ballot_sync(0xffffffffu, hA1);
-              const unsigned bB0 = __ballot_sync(0xffffffffu, hB0), bB1 = __ballot_sync(0xffffffffu, hB1);
-              const uint32_t pA0 = cnt0 + __popc(bA0 & lt), pA1 = cnt1 + __popc(bA1 & lt);
-              const uint32_t pB0 = cnt0 + __popc(bA0) + __popc(bB0 & lt);
-              const uint32_t pB1 = cnt1 + __popc(bA1) + __popc(bB1 & lt);
-              if (hA0 & (pA0 < (uint32_t)maxn)) row0[pA0] = __float_as_uint(cA.w);
-              if (hA1 & (pA1 < (uint32_t)maxn)) row1[pA1] = __float_as_uint(cA.w);
-              if (hB0 & (pB0 < (uint32_t)maxn)) row0[pB0] = __float_as_uint(cB.w);
-              if (hB1 & (pB1 < (uint32_t)maxn)) row1[pB1] = __float_as_uint(cB.w);
-              cnt0 += __popc(bA0) + __popc(bB0);
-              cnt1 += __popc(bA1) + __popc(bB1);
+              const uint32_t wA = __float_as_uint(cA.w), wB = __float_as_uint(cB.w);
+  #pragma unroll
+              for (int u = 0; u < kNT; ++u) {
+                const unsigned bAu = __ballot_sync(0xffffffffu, hA[u]);
+                const unsigned bBu = __ballot_sync(0xffffffffu, hB[u]);
+                const uint32_t pA = cnt[u] + __popc(bAu & lt);
+                const uint32_t pB = cnt[u] + __popc(bAu) + __popc(bBu & lt);
+                if (hA[u] & (pA < (uint32_t)maxn)) row[u][pA] = wA;
+                if (hB[u] & (pB < (uint32_t)maxn)) row[u][pB] = wB;
+                cnt[u] += __popc(bAu) + __popc(bBu);
+              }
             }
             if (lane == 0) {
-              tcount[ta - t0] = cnt0;
-              if (has_b) tcount[tb - t0] = cnt1;
+  #pragma unroll
+              for (int u = 0; u < kNT; ++u)
+                if (u == 0 || tq + u < t1) tcount[tt[u] - t0] = cnt[u];
             }
             __syncwarp();
           }
