@@ -42,7 +42,7 @@
 extern "C" {
 #endif
 
-#define SPH_ABI_VERSION 5
+#define SPH_ABI_VERSION 6
 
 typedef struct sph_ctx sph_ctx;
 
@@ -116,6 +116,8 @@ typedef struct {
   int64_t n_owned, n_halo, nbr_total, nbr_max;
   int64_t omega_clamped, iad_singular, coincident_pairs, u_floored, h_clamped;
   int64_t steps;
+  int64_t first_bad_id;   /* smallest id with a non-finite / non-positive x, h, m or update,
+                             -1 if none; the call that found it returned SPH_ERR_NUMERIC     */
   double  dt, dt_prev, time;
   double  momentum[3], ang_momentum[3], energy;   /* sum m v, sum m x x v, sum m (u + v^2/2) */
   int     grid[3];                                /* search cells per dimension             */
@@ -170,6 +172,14 @@ sph_status  sph_destroy(sph_ctx* ctx);
  * The caller broadcasts it (e.g. torch.distributed) and passes it as params.nccl_unique_id
  * to sph_init on every rank (one process per GPU).  SPH_ERR_CONFIG if built without NCCL. */
 sph_status  sph_nccl_unique_id(void* out, int size);
+/* In-process transport (testing and single-GPU runs of the multi-rank path): create a hub
+ * for `nranks` ranks and write its 128-byte id to out (host memory, size >= 128).  Passing
+ * that id as params.nccl_unique_id makes every sph_init of the same process join the hub
+ * instead of NCCL; each rank is then driven by its own host thread (the collectives are
+ * blocking rendezvous of those threads; data moves by device-to-device copies).  The
+ * decomposition, migration, halo plan and the three exchanges run exactly as over NCCL,
+ * so G ranks on one GPU reproduce the NCCL run.  SPH_ERR_CONFIG on bad arguments. */
+sph_status  sph_local_comm_id(int nranks, void* out, int size);
 /* Host-side decomposition helpers (no GPU needed; used by the library and by CPU tests).
  * splitters: rank r owns key-prefix bins [split[r], split[r+1]) of a global histogram
  * hist[nbins], split[G+1] at equal particle counts (the paper's global tree + bucket rule,

@@ -518,6 +518,10 @@ void orc_update(const orc_params* p, int64_t N, double dt, double dt_prev, int f
         double L = p->box_hi[k] - p->box_lo[k];
         if (xn >= p->box_hi[k]) xn -= L;
         else if (xn < p->box_lo[k]) xn += L;
+        /* reading R30: the wrapped coordinate stays in [lo, hi) when the wrap rounds
+         * onto an end (x = -1e-15 in [0, 100) wraps to 100.0 exactly)                */
+        if (xn < p->box_lo[k]) xn = p->box_lo[k];
+        if (xn >= p->box_hi[k]) xn = nextafter(p->box_hi[k], p->box_lo[k]);
       }
       X[k][a] = xn;
       VH[k][a] = vb;

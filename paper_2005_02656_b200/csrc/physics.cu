@@ -10,67 +10,27 @@ __device__ __forceinline__ double wsum(double v) {
   for (int o = 16; o; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
   return v;
 }
-__device__ __forceinline__ double wmax(double v) {
-#pragma unroll
-  for (int o = 16; o; o >>= 1) v = fmax(v, __shfl_xor_sync(0xffffffffu, v, o));
-  return v;
-}
-
-__device__ __forceinline__ double sinc_poly(const Phys& ph, double t) {
-  double p = ph.poly[kPolyTerms - 1];
-#pragma unroll
-  for (int k = kPolyTerms - 2; k >= 0; --k) p = fma(p, t, ph.poly[k]);
-  return p;
-}
-__device__ __forceinline__ double sinc_dpoly(const Phys& ph, double t) {
-  double p = ph.dpoly[kPolyTerms - 2];
-#pragma unroll
-  for (int k = kPolyTerms - 3; k >= 0; --k) p = fma(p, t, ph.dpoly[k]);
-  return p;
-}
-// "inline x*x*x*x..."
-__device__ __forceinline__ double ipow(double s, int n) {
-  if (n == 6) {
-    double s2 = s * s;
-    double s4 = s2 * s2;
-    return s4 * s2;
-  }
-  double r = 1.0;
-  for (int k = 0; k < n; ++k) r *= s;
-  return r;
-}
-
-// minimum image on periodic dims -- same branch formula as the oracle
-__device__ __forceinline__ double min_image(double d, int periodic, double L) {
-  if (periodic) {
-    if (d > 0.5 * L) d -= L;
-    else if (d < -0.5 * L) d += L;
-  }
-  return d;
-}
-
-__device__ __forceinline__ int cell_coord(const Grid& g, int d, double v) {
-  double q = (v - g.lo[d]) * g.inv[d];
-  int c = (int)floor(q);
-  c = c < 0 ? 0 : c;
-  c = c > g.nc[d] - 1 ? g.nc[d] - 1 : c;
-  return c;
-}
-
 // dt = min(raw, growth * dt_prev) except on the first step; dt_prev := dt on the first step
-__global__ void k_dt_finalize(double* dts, int first, double growth) {
+// A non-finite or non-positive dt sets DT_BAD: k_update then leaves the state
+// untouched and the next sph_find_neighbors / sph_diagnostics returns SPH_ERR_NUMERIC,
+// whether or not the caller asked for dt on the host.
+__global__ void k_dt_finalize(double* dts, int first, double growth, int nonempty, unsigned long long* cnt) {
   double raw = __longlong_as_double((long long)*(unsigned long long*)&dts[DT_RAW_BITS]);
   double prev = first ? raw : dts[DT_COMMITTED];
   double dt = raw;
   if (!first && growth * prev < dt) dt = growth * prev;
   dts[DT_CUR] = dt;
   dts[DT_PREV] = first ? dt : prev;
+  const bool bad = nonempty && !(dt > 0.0 && dt < INFINITY);  // no particle anywhere: dt = inf
+  dts[DT_BAD] = bad ? 1.0 : 0.0;
+  if (bad) atomicAdd(&cnt[CNT_NONFINITE], 1ull);
   // re-arm the atomic-min slot for the next momentum pass (+inf)
   *(unsigned long long*)&dts[DT_RAW_BITS] = 0x7ff0000000000000ull;
 }
 
-int launch_dt_finalize(sph_ctx* c) {
-  k_dt_finalize<<<1, 1, 0, c->stream>>>(c->s.dts, c->first ? 1 : 0, c->phys.dt_growth);
+int launch_dt_finalize(sph_ctx* c, bool nonempty) {
+  k_dt_finalize<<<1, 1, 0, c->stream>>>(c->s.dts, c->first ? 1 : 0, c->phys.dt_growth, nonempty ? 1 : 0,
+                                        c->s.cnt);
   return 1;
 }
 
@@ -81,7 +41,9 @@ struct UpdState {
 };
 
 __global__ void k_update(UpdState s, int64_t n, const uint32_t* __restrict__ ncount, Phys ph,
-                         int first, double* __restrict__ dts, unsigned long long* __restrict__ cnt) {
+                         int first, double* __restrict__ dts, unsigned long long* __restrict__ cnt,
+                         const int64_t* __restrict__ id, unsigned long long* __restrict__ bad_id) {
+  if (dts[DT_BAD] != 0.0) return;  // invalid dt: keep the state, the error surfaces next call
   const double dt = dts[DT_CUR], dtp = dts[DT_PREV];
   const double q = dt / dtp;
   unsigned long long nfl = 0, nhc = 0;
@@ -100,7 +62,11 @@ __global__ void k_update(UpdState s, int64_t n, const uint32_t* __restrict__ nco
       if (ph.periodic[k]) {
         if (xn >= ph.box_hi[k]) xn -= ph.L[k];
         else if (xn < ph.box_lo[k]) xn += ph.L[k];
+        // reading R30: the wrapped value stays in [lo, hi) against rounding
+        if (xn < ph.box_lo[k]) xn = ph.box_lo[k];
+        if (xn >= ph.box_hi[k]) xn = nextafter(ph.box_hi[k], ph.box_lo[k]);
       }
+      if (!isfinite(xn) || !isfinite(vb)) atomicMin(bad_id, (unsigned long long)id[i]);
       X[k][i] = xn;
       VH[k][i] = vb;
       V[k][i] = vb + 0.5 * ak * dt;
@@ -126,6 +92,7 @@ __global__ void k_update(UpdState s, int64_t n, const uint32_t* __restrict__ nco
       hn = ph.h_max;
       ++nhc;
     }
+    if (!isfinite(un) || !(hn > 0.0 && hn < INFINITY)) atomicMin(bad_id, (unsigned long long)id[i]);
     s.h[i] = hn;
   }
   if (nfl) atomicAdd(&cnt[CNT_U_FLOOR], nfl);
@@ -141,7 +108,8 @@ int launch_update(sph_ctx* c) {
   UpdState s = {P.x, P.y, P.z, P.vx, P.vy, P.vz, P.vhx, P.vhy, P.vhz, P.u, P.du_prev, P.h,
                 P.ax, P.ay, P.az, P.du};
   k_update<<<grid_blocks(c, P.n, 256, 8), 256, 0, c->stream>>>(s, P.n, c->s.ncount, c->phys,
-                                                               c->first ? 1 : 0, c->s.dts, c->s.cnt);
+                                                               c->first ? 1 : 0, c->s.dts, c->s.cnt,
+                                                               P.id, c->s.bad_id);
   return 1;
 }
 

@@ -34,12 +34,19 @@ __global__ void __launch_bounds__(kRedThreads) k_bbox(const double* __restrict__
                                                       const double* __restrict__ y,
                                                       const double* __restrict__ z,
                                                       const double* __restrict__ h,
+                                                      const double* __restrict__ m,
                                                       const int64_t* __restrict__ id, int64_t n,
-                                                      double* __restrict__ part) {
+                                                      double* __restrict__ part,
+                                                      unsigned long long* __restrict__ bad_id) {
   double v[kBB] = {INFINITY, INFINITY, INFINITY, -INFINITY, -INFINITY, -INFINITY, 0.0, 0.0, 0.0};
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
        i += (int64_t)gridDim.x * blockDim.x) {
-    double xi = x[i], yi = y[i], zi = z[i], hi = h[i];
+    double xi = x[i], yi = y[i], zi = z[i], hi = h[i], mi = m[i];
+    // positions finite, h and m finite and positive; the smallest offending id is
+    // reported (sph_diag.first_bad_id) and the step fails with SPH_ERR_NUMERIC
+    if (!(isfinite(xi) && isfinite(yi) && isfinite(zi) && hi > 0.0 && hi < INFINITY && mi > 0.0 &&
+          mi < INFINITY))
+      atomicMin(bad_id, (unsigned long long)id[i]);
     v[0] = fmin(v[0], xi); v[1] = fmin(v[1], yi); v[2] = fmin(v[2], zi);
     v[3] = fmax(v[3], xi); v[4] = fmax(v[4], yi); v[5] = fmax(v[5], zi);
     v[6] = fmax(v[6], hi); v[7] += hi;
@@ -75,8 +82,8 @@ __global__ void k_bbox_final(const double* __restrict__ part, int nblk, double* 
 int launch_bbox(sph_ctx* c) {
   int64_t n = c->P.n;
   int nb = grid_blocks(c, n, kRedThreads, 4);
-  k_bbox<<<nb, kRedThreads, 0, c->stream>>>(c->P.x, c->P.y, c->P.z, c->P.h, c->P.id, n,
-                                              c->s.red);
+  k_bbox<<<nb, kRedThreads, 0, c->stream>>>(c->P.x, c->P.y, c->P.z, c->P.h, c->P.m, c->P.id, n,
+                                              c->s.red, c->s.bad_id);
   k_bbox_final<<<1, 32, 0, c->stream>>>(c->s.red, nb, c->s.bbox);
   return 2;
 }

@@ -329,9 +329,11 @@ sph_status sph_init(const sph_params* prm, int64_t capacity, sph_ctx** out) {
   AL(s.bbox, 16);
   AL(s.dts, DT_SLOTS);
   AL(s.cnt, kCounters);
+  AL(s.bad_id, 1);
   AL(s.diag, 8);
 #undef AL
   cudaMemsetAsync(s.cnt, 0, sizeof(unsigned long long) * kCounters, c->stream);
+  cudaMemsetAsync(s.bad_id, 0xff, sizeof(unsigned long long), c->stream);
   cudaMemsetAsync(s.dts, 0, sizeof(double) * DT_SLOTS, c->stream);
   cudaMemsetAsync(s.ncount, 0, sizeof(uint32_t) * cap, c->stream);
   {
@@ -361,12 +363,17 @@ sph_status sph_attach(sph_ctx* c, const sph_particles* p) {
   if (c->status != SPH_OK) return c->status;
   if (p->n < 0 || p->n > c->cap || p->capacity < p->n)
     return fail(c, SPH_ERR_CAPACITY, "n exceeds the context capacity");
+  // multi-GPU: migration and halo unpack write up to the context capacity (sph_init)
+  if (c->dist && p->capacity < c->cap)
+    return fail(c, SPH_ERR_CAPACITY, "multi-GPU: particle arrays must hold the sph_init capacity");
   const void* ptrs[] = {p->id, p->x, p->y, p->z, p->vx, p->vy, p->vz, p->h, p->m, p->u, p->rho,
                         p->omega, p->p, p->c, p->c11, p->c12, p->c13, p->c22, p->c23, p->c33,
                         p->ax, p->ay, p->az, p->du, p->vsig, p->vhx, p->vhy, p->vhz, p->du_prev};
   for (const void* q : ptrs)
     if (!q) return fail(c, SPH_ERR_CONFIG, "null particle array");
   c->P = *p;
+  c->first_bad_id = -1;
+  CK(cudaMemsetAsync(c->s.bad_id, 0xff, sizeof(unsigned long long), c->stream));
   c->attached = true;
   c->first = true;
   c->stage = 0;
@@ -462,13 +469,27 @@ sph_status sph_find_neighbors(sph_ctx* c) {
     ph.done(k);
   }
   int64_t n_total = c->P.n;
-  if (multi) {  // global domain size + h statistics (P:194 allreduce)
-    if (!dist_global_bbox(c, bb)) return fail(c, SPH_ERR_COMM, c->dist_err);
+  // S:90 / S:274: a non-finite or non-positive input (k_bbox) or an invalid dt / update of
+  // the previous step (k_dt_finalize, k_update) stops here, read with the bbox (no extra sync)
+  unsigned long long bad[2] = {~0ull, 0ull};
+  bool bad_any = false;
+  if (multi) {  // global domain size + h statistics (P:194 allreduce); the flag is global too
+    if (!dist_global_bbox(c, bb, &bad_any)) return fail(c, SPH_ERR_COMM, c->dist_err);
     n_total = dist_n_total(c);
-  } else {
-    CK(cudaMemcpyAsync(bb, c->s.bbox, 9 * sizeof(double), cudaMemcpyDeviceToHost, c->stream));
-    CK(cudaStreamSynchronize(c->stream));
   }
+  if (!multi) CK(cudaMemcpyAsync(bb, c->s.bbox, 9 * sizeof(double), cudaMemcpyDeviceToHost, c->stream));
+  CK(cudaMemcpyAsync(&bad[0], c->s.bad_id, sizeof(unsigned long long), cudaMemcpyDeviceToHost, c->stream));
+  CK(cudaMemcpyAsync(&bad[1], c->s.cnt + CNT_NONFINITE, sizeof(unsigned long long), cudaMemcpyDeviceToHost,
+                     c->stream));
+  CK(cudaStreamSynchronize(c->stream));
+  if (bad[0] != ~0ull) c->first_bad_id = (int64_t)bad[0];
+  if (bad_any || bad[0] != ~0ull || bad[1])
+    return fail(c, SPH_ERR_NUMERIC,
+                bad[0] != ~0ull ? "non-finite or non-positive state (x, h, m) of particle id " +
+                                      std::to_string(bad[0]) + " (sph_diag.first_bad_id)"
+                                : (bad[1] ? std::string("non-finite or non-positive dt in the previous step")
+                                          : std::string("non-finite state on another rank")));
+  c->n_global = n_total;
   if (n_total == 0) {
     c->stage = 1;
     return SPH_OK;
@@ -629,7 +650,7 @@ sph_status sph_momentum_energy(sph_ctx* c, double* dt_out) {
     Phase ph(c, SPH_PH_MOMENTUM);
     int k = c->P.n ? launch_momentum(c) : 0;
     if (c->dist && !dist_allreduce_dt(c)) return fail(c, SPH_ERR_COMM, c->dist_err);  // a11
-    k += launch_dt_finalize(c);
+    k += launch_dt_finalize(c, c->n_global > 0);
     CKL();
     ph.done(k);
   }
@@ -714,9 +735,14 @@ sph_status sph_download(sph_ctx* c, sph_particles* host) {
 
 sph_status sph_diagnostics(sph_ctx* c, sph_diag* out) {
   if (!c || !out) return SPH_ERR_CONFIG;
-  if (c->status != SPH_OK) return c->status;
   memset(out, 0, sizeof(*out));
+  if (c->status != SPH_OK) {  // sticky error: report what the host knows (which particle, when)
+    out->first_bad_id = c->first_bad_id;
+    out->steps = c->steps;
+    return c->status;
+  }
   double d[8] = {0};
+  unsigned long long badid = ~0ull;
   if (c->attached && c->P.n) {
     launch_diag(c);
     CKL();
@@ -734,7 +760,10 @@ sph_status sph_diagnostics(sph_ctx* c, sph_diag* out) {
   CK(cudaMemcpyAsync(cnt, c->dist ? dist_counters(c) : c->s.cnt, sizeof(cnt), cudaMemcpyDeviceToHost,
                      c->stream));
   CK(cudaMemcpyAsync(dts, c->s.dts, sizeof(dts), cudaMemcpyDeviceToHost, c->stream));
+  CK(cudaMemcpyAsync(&badid, c->s.bad_id, sizeof(badid), cudaMemcpyDeviceToHost, c->stream));
   CK(cudaStreamSynchronize(c->stream));
+  if (badid != ~0ull) c->first_bad_id = (int64_t)badid;
+  out->first_bad_id = c->first_bad_id;
   out->n_owned = n_owned;
   out->n_halo = c->n_halo;
   out->nbr_total = (int64_t)d[7];
@@ -754,6 +783,8 @@ sph_status sph_diagnostics(sph_ctx* c, sph_diag* out) {
   }
   out->energy = d[6];
   if (cnt[CNT_NONFINITE]) return fail(c, SPH_ERR_NUMERIC, "non-finite dt encountered");
+  if (badid != ~0ull)
+    return fail(c, SPH_ERR_NUMERIC, "non-finite state of particle id " + std::to_string(badid));
   return SPH_OK;
 }
 
@@ -793,7 +824,7 @@ sph_status sph_destroy(sph_ctx* c) {
   void* ptrs[] = {s.keys, s.keys_alt, s.idx, s.idx_alt, s.hist, s.scan_tmp, s.gather, s.gather_id,
                   s.cell_start, s.cell_end, s.cell_hmax, s.cell_flag, s.cell_rank, s.cell_list,
                   s.ncell_list, s.unit_flag, s.unit_rank, s.unit_list, s.nunit_list, s.unit_rec, s.nbr, s.ncount, s.nbr_maxcount, s.work, s.wB, s.ih2, s.vol, s.rinv, s.X,
-                  s.mX, s.ct, s.mrec, s.red, s.bbox, s.dts, s.cnt, s.diag, s.ktable};
+                  s.mX, s.ct, s.mrec, s.red, s.bbox, s.dts, s.cnt, s.bad_id, s.diag, s.ktable};
   for (void* p : ptrs)
     if (p) cudaFree(p);
   delete c;

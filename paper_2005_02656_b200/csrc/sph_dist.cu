@@ -15,6 +15,9 @@
 
 #include "stencil.cuh"
 #include "sph_dist.cuh"
+#ifdef SPH_WITH_NCCL
+#include <nccl.h>
+#endif
 
 namespace sphb {
 
@@ -45,15 +48,11 @@ int owner_of_bin(const int64_t* split, int G, int64_t bin) {
   return lo;
 }
 
-#ifdef SPH_WITH_NCCL
-
-#define NCK(call)                                                                           \
+// every collective goes through the rank's transport (comm.cuh: NCCL, or the in-process
+// hub that runs G ranks as threads of one process on one GPU)
+#define COMM(call)                                                                          \
   do {                                                                                      \
-    ncclResult_t r_ = (call);                                                               \
-    if (r_ != ncclSuccess) {                                                                \
-      c->dist_err = std::string(#call) + ": " + ncclGetErrorString(r_);                     \
-      return false;                                                                         \
-    }                                                                                       \
+    if (!(c->dist->comm->call)) return false;                                               \
   } while (0)
 #define CUK(call)                                                                           \
   do {                                                                                      \
@@ -258,12 +257,14 @@ __global__ void k_unpack(FieldSet fs, const uint64_t* __restrict__ buf, int64_t 
        k += (int64_t)gridDim.x * blockDim.x)
     for (int f = 0; f < fs.nf; ++f) fs.f[f][dst0 + k] = buf[base * fs.nf + f * n + k];
 }
-__global__ void k_bbox_pack(const double* __restrict__ bb, int64_t n, double* __restrict__ mx,
+__global__ void k_bbox_pack(const double* __restrict__ bb, int64_t n, const unsigned long long* __restrict__ bad_id,
+                            const unsigned long long* __restrict__ cnt, double* __restrict__ mx,
                             double* __restrict__ sm) {
-  // MAX of {-min x,y,z, max x,y,z, max h, max id}; SUM of {sum h, n}
+  // MAX of {-min x,y,z, max x,y,z, max h, max id, bad state flag}; SUM of {sum h, n}
   mx[0] = -bb[0]; mx[1] = -bb[1]; mx[2] = -bb[2];
   mx[3] = bb[3]; mx[4] = bb[4]; mx[5] = bb[5];
   mx[6] = bb[6]; mx[7] = bb[8];
+  mx[8] = (*bad_id != ~0ull || cnt[CNT_NONFINITE]) ? 1.0 : 0.0;
   sm[0] = n ? bb[7] : 0.0;
   sm[1] = (double)n;
 }
@@ -297,18 +298,16 @@ static bool exchange(sph_ctx* c, const FieldSet& fs) {
     if (r != me) sbase += D.scnt[r];
   }
   CUK(cudaGetLastError());
-  NCK(ncclGroupStart());
+  std::vector<Xfer> sends, recvs;
   sbase = 0;
   for (int r = 0; r < G; ++r) {
     if (r == me) continue;
-    if (D.scnt[r])
-      NCK(ncclSend(D.sendbuf + sbase * F, (size_t)D.scnt[r] * F, ncclUint64, r, D.comm, c->stream));
-    if (D.rcnt[r])
-      NCK(ncclRecv(D.recvbuf + rbase * F, (size_t)D.rcnt[r] * F, ncclUint64, r, D.comm, c->stream));
+    if (D.scnt[r]) sends.push_back({r, D.sendbuf + sbase * F, (size_t)D.scnt[r] * F * sizeof(uint64_t)});
+    if (D.rcnt[r]) recvs.push_back({r, D.recvbuf + rbase * F, (size_t)D.rcnt[r] * F * sizeof(uint64_t)});
     sbase += D.scnt[r];
     rbase += D.rcnt[r];
   }
-  NCK(ncclGroupEnd());
+  COMM(exchange(sends, recvs, c->stream, c->dist_err));
   return true;
 }
 
@@ -341,7 +340,7 @@ static bool swap_counts(sph_ctx* c, int64_t base, Need&& need) {
   for (int r = 0; r < G; ++r) row[r] = D.scnt[r];
   row[G] = base;
   CUK(cudaMemcpyAsync(D.cnt_d, row.data(), sizeof(int64_t) * W, cudaMemcpyHostToDevice, c->stream));
-  NCK(ncclAllGather(D.cnt_d, D.cnt_all_d, W, ncclInt64, D.comm, c->stream));
+  COMM(allgather(D.cnt_d, D.cnt_all_d, W, DType::I64, c->stream, c->dist_err));
   std::vector<int64_t> all((size_t)G * W);
   CUK(cudaMemcpyAsync(all.data(), D.cnt_all_d, sizeof(int64_t) * G * W, cudaMemcpyDeviceToHost, c->stream));
   CUK(cudaStreamSynchronize(c->stream));
@@ -365,20 +364,19 @@ static bool swap_counts(sph_ctx* c, int64_t base, Need&& need) {
   return true;
 }
 
-bool dist_global_bbox(sph_ctx* c, double* bb_out) {
+bool dist_global_bbox(sph_ctx* c, double* bb_out, bool* bad_any) {
   Dist& D = *c->dist;
-  k_bbox_pack<<<1, 1, 0, c->stream>>>(c->s.bbox, c->P.n, D.red_d, D.red_d + 8);
-  NCK(ncclGroupStart());
-  NCK(ncclAllReduce(D.red_d, D.red_d, 8, ncclFloat64, ncclMax, D.comm, c->stream));
-  NCK(ncclAllReduce(D.red_d + 8, D.red_d + 8, 2, ncclFloat64, ncclSum, D.comm, c->stream));
-  NCK(ncclGroupEnd());
-  double v[10];
+  k_bbox_pack<<<1, 1, 0, c->stream>>>(c->s.bbox, c->P.n, c->s.bad_id, c->s.cnt, D.red_d, D.red_d + 9);
+  COMM(allreduce(D.red_d, D.red_d, 9, DType::F64, ROp::Max, c->stream, c->dist_err));
+  COMM(allreduce(D.red_d + 9, D.red_d + 9, 2, DType::F64, ROp::Sum, c->stream, c->dist_err));
+  double v[11];
   CUK(cudaMemcpyAsync(v, D.red_d, sizeof(v), cudaMemcpyDeviceToHost, c->stream));
   CUK(cudaStreamSynchronize(c->stream));
   bb_out[0] = -v[0]; bb_out[1] = -v[1]; bb_out[2] = -v[2];
   bb_out[3] = v[3]; bb_out[4] = v[4]; bb_out[5] = v[5];
-  bb_out[6] = v[6]; bb_out[7] = v[8]; bb_out[8] = v[7];
-  D.n_total = (int64_t)v[9];
+  bb_out[6] = v[6]; bb_out[7] = v[9]; bb_out[8] = v[7];
+  *bad_any = v[8] != 0.0;
+  D.n_total = (int64_t)v[10];
   return true;
 }
 
@@ -405,7 +403,7 @@ bool dist_splitters(sph_ctx* c) {
     k_bin_hist<<<grid_blocks(c, c->P.n, 256, 8), 256, 0, c->stream>>>(c->s.keys, c->P.n, g, D.shift, D.hist_d);
     c->launches++;
   }
-  NCK(ncclAllReduce(D.hist_d, D.hist_d, D.nbins, ncclUint64, ncclSum, D.comm, c->stream));
+  COMM(allreduce(D.hist_d, D.hist_d, D.nbins, DType::U64, ROp::Sum, c->stream, c->dist_err));
   std::vector<int64_t> hist(D.nbins);
   CUK(cudaMemcpyAsync(hist.data(), D.hist_d, sizeof(int64_t) * D.nbins, cudaMemcpyDeviceToHost, c->stream));
   CUK(cudaStreamSynchronize(c->stream));
@@ -540,17 +538,15 @@ bool dist_exchange3(sph_ctx* c) {  // after IAD: C~ = (B/h^3) C of the sources
 }
 
 bool dist_allreduce_dt(sph_ctx* c) {
-  Dist& D = *c->dist;
-  NCK(ncclAllReduce(c->s.dts + DT_RAW_BITS, c->s.dts + DT_RAW_BITS, 1, ncclUint64, ncclMin, D.comm, c->stream));
+  COMM(allreduce(c->s.dts + DT_RAW_BITS, c->s.dts + DT_RAW_BITS, 1, DType::U64, ROp::Min, c->stream,
+                 c->dist_err));
   return true;
 }
 
 bool dist_allreduce_diag(sph_ctx* c, double* d_dev, unsigned long long* cnt_dev) {
   Dist& D = *c->dist;
-  NCK(ncclGroupStart());
-  NCK(ncclAllReduce(d_dev, d_dev, 8, ncclFloat64, ncclSum, D.comm, c->stream));
-  NCK(ncclAllReduce(cnt_dev, D.cntred_d, kCounters, ncclUint64, ncclSum, D.comm, c->stream));
-  NCK(ncclGroupEnd());
+  COMM(allreduce(d_dev, d_dev, 8, DType::F64, ROp::Sum, c->stream, c->dist_err));
+  COMM(allreduce(cnt_dev, D.cntred_d, kCounters, DType::U64, ROp::Sum, c->stream, c->dist_err));
   return true;
 }
 
@@ -564,9 +560,8 @@ bool dist_init(sph_ctx* c, const sph_params* prm) {
   D->soff.assign(D->G, 0);
   D->scnt.assign(D->G, 0);
   D->rcnt.assign(D->G, 0);
-  ncclUniqueId id;
-  memcpy(&id, prm->nccl_unique_id, sizeof(id));
-  NCK(ncclCommInitRank(&D->comm, D->G, id, D->rank));
+  D->comm = comm_create(prm->nccl_unique_id, D->G, D->rank, c->dist_err);
+  if (!D->comm) return false;
   D->xcap = c->cap;
   const int64_t cap = c->cap;
   CUK(cudaMalloc(&D->hist_d, sizeof(unsigned long long) << kBinBits));
@@ -590,7 +585,7 @@ bool dist_init(sph_ctx* c, const sph_params* prm) {
 void dist_destroy(sph_ctx* c) {
   Dist* D = c->dist;
   if (!D) return;
-  if (D->comm) ncclCommDestroy(D->comm);
+  delete D->comm;
   void* ptrs[] = {D->hist_d, D->split_d, D->off_d, D->cnt_d, D->cnt_all_d, D->tot_d, D->red_d,
                   D->mask_d, D->pcnt_d, D->poff_d, D->send_idx, D->sendbuf, D->recvbuf, D->cntred_d,
                   D->hm_d};
@@ -600,23 +595,14 @@ void dist_destroy(sph_ctx* c) {
   c->dist = nullptr;
 }
 
-#else  // !SPH_WITH_NCCL
-bool dist_init(sph_ctx* c, const sph_params*) {
-  c->dist_err = "built without NCCL";
-  return false;
-}
-void dist_destroy(sph_ctx*) {}
-bool dist_global_bbox(sph_ctx*, double*) { return false; }
-bool dist_splitters(sph_ctx*) { return false; }
-bool dist_migrate(sph_ctx*, int64_t*, int64_t*) { return false; }
-bool dist_halo_plan_and_exchange1(sph_ctx*) { return false; }
-bool dist_exchange2(sph_ctx*) { return false; }
-bool dist_exchange3(sph_ctx*) { return false; }
-bool dist_allreduce_dt(sph_ctx*) { return false; }
-bool dist_allreduce_diag(sph_ctx*, double*, unsigned long long*) { return false; }
-#endif
+
 
 }  // namespace sphb
+
+extern "C" sph_status sph_local_comm_id(int nranks, void* out, int size) {
+  if (!out || size < sphb::kCommIdBytes || nranks < 1 || nranks > 64) return SPH_ERR_CONFIG;
+  return sphb::local_hub_create(nranks, out) ? SPH_OK : SPH_ERR_CONFIG;
+}
 
 extern "C" sph_status sph_nccl_unique_id(void* out, int size) {
 #ifdef SPH_WITH_NCCL

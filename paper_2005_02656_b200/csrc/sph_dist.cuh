@@ -3,10 +3,8 @@
 
 #include <vector>
 
+#include "comm.cuh"
 #include "sph_internal.cuh"
-#ifdef SPH_WITH_NCCL
-#include <nccl.h>
-#endif
 
 namespace sphb {
 
@@ -14,9 +12,7 @@ constexpr int kBinBits = 16;  // key-prefix histogram: 2^16 bins (top Morton bit
 
 struct Dist {
   int G = 1, rank = 0;
-#ifdef SPH_WITH_NCCL
-  ncclComm_t comm = nullptr;
-#endif
+  Comm* comm = nullptr;     // NCCL or the in-process hub (comm.cuh)
   int shift = 0;            // bin = Morton(cell) >> shift
   int every = 1;            // recompute splitters every k-th step (sph_params.redecomp_every)
   int64_t decomp_calls = 0; // dist_splitters calls so far
@@ -46,7 +42,7 @@ inline int64_t dist_n_total(const sph_ctx* c) { return c->dist->n_total; }
 inline int64_t dist_n_halo(const sph_ctx* c) { return c->dist->n_halo; }
 inline unsigned long long* dist_counters(const sph_ctx* c) { return c->dist->cntred_d; }
 void dist_destroy(sph_ctx* c);
-bool dist_global_bbox(sph_ctx* c, double* bb_out);
+bool dist_global_bbox(sph_ctx* c, double* bb_out, bool* bad_any);
 bool dist_splitters(sph_ctx* c);
 bool dist_migrate(sph_ctx* c, int64_t* nleave, int64_t* nrecv);
 bool dist_halo_plan_and_exchange1(sph_ctx* c);

@@ -56,7 +56,7 @@ struct Phys {
 };
 
 // Device-side scalars of the integrator: written by kernels, read by kernels.
-enum { DT_RAW_BITS = 0, DT_CUR = 1, DT_PREV = 2, DT_COMMITTED = 3, DT_TIME = 4, DT_SLOTS = 8 };
+enum { DT_RAW_BITS = 0, DT_CUR = 1, DT_PREV = 2, DT_COMMITTED = 3, DT_TIME = 4, DT_BAD = 5, DT_SLOTS = 8 };
 
 struct Scratch {
   // sort
@@ -102,6 +102,7 @@ struct Scratch {
   double* bbox = nullptr;  // 8 doubles (device)
   double* dts = nullptr;   // DT_SLOTS
   unsigned long long* cnt = nullptr;  // kCounters
+  unsigned long long* bad_id = nullptr;  // smallest id with a non-finite / non-positive state (~0: none)
   double* diag = nullptr;  // 8
 };
 
@@ -133,6 +134,8 @@ struct sph_ctx {
   double hmax = 0.0;        // global max h of the current step (grid geometry)
   int64_t nbr_max = 0;
   sph_status status = SPH_OK;
+  int64_t first_bad_id = -1;  // sph_diag.first_bad_id
+  int64_t n_global = 0;       // particles over all ranks in the current step
   std::string err;
   // profiling
   bool prof = false;
@@ -162,7 +165,7 @@ int launch_density(sph_ctx* c);
 int launch_iad(sph_ctx* c);
 int launch_momentum(sph_ctx* c);
 int launch_mom_records(sph_ctx* c);
-int launch_dt_finalize(sph_ctx* c);
+int launch_dt_finalize(sph_ctx* c, bool nonempty);
 int launch_update(sph_ctx* c);
 int launch_diag(sph_ctx* c);
 void set_poly_constants(const double* poly, const double* dpoly);

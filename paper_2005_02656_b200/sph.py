@@ -16,7 +16,7 @@ _HERE = os.path.dirname(os.path.abspath(__file__))
 # SPH_LIB selects another in-tree build of the same library (A/B runs of kernel variants)
 LIB_PATH = os.environ.get("SPH_LIB") or os.path.join(_HERE, "libsph.so")
 
-ABI_VERSION = 5
+ABI_VERSION = 6
 KERNEL_MODES = {"poly": 0, "table": 1, "sin": 2}
 EOS = {"linear": 0, "ideal": 1}
 STATUS = {0: "SPH_OK", 1: "SPH_ERR_NUMERIC", 2: "SPH_ERR_CONFIG", 3: "SPH_ERR_CAPACITY",
@@ -36,6 +36,16 @@ def nccl_unique_id() -> bytes:
     st = lib().sph_nccl_unique_id(buf, 128)
     if st != 0:
         raise SphError(st, "sph_nccl_unique_id failed (built without NCCL?)")
+    return buf.raw
+
+
+def local_comm_id(nranks: int) -> bytes:
+    """128-byte id of a new in-process hub (sph_local_comm_id): pass it as ``unique_id`` to
+    ``nranks`` Simulations of this process, one per rank, each driven by its own thread."""
+    buf = C.create_string_buffer(128)
+    st = lib().sph_local_comm_id(int(nranks), buf, 128)
+    if st != 0:
+        raise SphError(st, "sph_local_comm_id failed")
     return buf.raw
 
 
@@ -103,7 +113,7 @@ class Particles(C.Structure):
 class Diag(C.Structure):
     _fields_ = ([(k, C.c_int64) for k in ("n_owned", "n_halo", "nbr_total", "nbr_max",
                                           "omega_clamped", "iad_singular", "coincident_pairs",
-                                          "u_floored", "h_clamped", "steps")] +
+                                          "u_floored", "h_clamped", "steps", "first_bad_id")] +
                 [("dt", C.c_double), ("dt_prev", C.c_double), ("time", C.c_double),
                  ("momentum", C.c_double * 3), ("ang_momentum", C.c_double * 3),
                  ("energy", C.c_double), ("grid", C.c_int * 3)])
@@ -147,6 +157,8 @@ def lib():
         L.sph_local_count.restype = C.c_int
         L.sph_nccl_unique_id.argtypes = [vp, C.c_int]
         L.sph_nccl_unique_id.restype = C.c_int
+        L.sph_local_comm_id.argtypes = [C.c_int, vp, C.c_int]
+        L.sph_local_comm_id.restype = C.c_int
         L.sph_decomp_splitters.argtypes = [C.POINTER(C.c_int64), C.c_int64, C.c_int,
                                            C.POINTER(C.c_int64)]
         L.sph_decomp_splitters.restype = C.c_int
@@ -354,10 +366,16 @@ class Simulation:
         self._check(lib().sph_download(self._ctx, C.byref(s)))
         host.n = s.n
 
-    def diagnostics(self) -> dict:
+    def diagnostics(self, check: bool = True) -> dict:
+        """Conserved sums and counters (sph_diagnostics).  check=False returns what the
+        library reports even after a sticky error (first_bad_id, steps)."""
         d = Diag()
-        self._check(lib().sph_diagnostics(self._ctx, C.byref(d)))
-        return d.as_dict()
+        st = lib().sph_diagnostics(self._ctx, C.byref(d))
+        if check:
+            self._check(st)
+        out = d.as_dict()
+        out["status"] = st
+        return out
 
     def set_profiling(self, on: bool):
         self._check(lib().sph_set_profiling(self._ctx, int(on)))

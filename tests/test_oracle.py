@@ -543,6 +543,17 @@ def test_periodic_wrap_in_update(O):
     acc = {"ax": np.zeros(1), "ay": np.zeros(1), "az": np.zeros(1), "du": np.zeros(1)}
     o.update(st, acc, 0.1, 0.1, True)
     assert abs(st["z"][0] - (49.9 + 1.0 - 100.0)) < 1e-12
+    # reading R30: a wrap that rounds onto the open end stays inside [lo, hi): z = -1e-15
+    # in [0, 100) wraps to 100 - 1e-15, which rounds to 100.0 -> the largest double below 100
+    d2 = dict(d, box_lo=np.array([-50.0, -50.0, 0.0]), box_hi=np.array([50.0, 50.0, 100.0]))
+    o = mk(O, d2)
+    st["z"][0], st["vz"][0] = 0.0, -1e-15
+    o.update(st, acc, 1.0, 1.0, True)
+    assert st["z"][0] == np.nextafter(100.0, 0.0)
+    # a wrap from above that would round below lo is kept at lo
+    st["z"][0], st["vz"][0] = np.nextafter(100.0, 0.0), 1e-14
+    o.update(st, acc, 1.0, 1.0, True)
+    assert 0.0 <= st["z"][0] < 100.0
 
 
 # ------------------------------------------------------------------ O11 + ICs + config 1
