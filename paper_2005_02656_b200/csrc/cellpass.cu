@@ -1,46 +1,20 @@
-// cellpass.cu -- a5 neighbour search, a6 density + Omega + EOS, a8 IAD and
-// a10-a11 momentum + energy + AV + dt, each as ONE CTA PER SEARCH CELL.
+// cellpass.cu -- a6 density + Omega + EOS, a8 IAD and a10-a11 momentum + energy +
+// AV + dt, each as ONE CTA PER PAIR-PASS UNIT (stencil.cuh; the search is in
+// search.cu, shared helpers in pairpass.cuh).
 //
-// A CTA owns a search cell (~72 targets at the paper's 300 neighbours), stages
-// the source particles of the cell's stencil into shared memory with coalesced
-// loads (each cell is a contiguous range of the Morton order; periodic images
-// are shifted at staging time, so no pair needs a minimum image), and one warp
-// per target walks the target's neighbour row, lanes striding over entries.
-// Every source particle is read from L2/HBM once per target CELL instead of once
-// per pair (profiles/r1_ncu_summary.md has the measurements behind this).
-//
-// Neighbour rows hold packed entries (slot << 20 | local): the shared-memory
-// index of a neighbour is cum[slot] + local - (group start) -- no search, no global gather.
-// Row chunks are prefetched one chunk ahead, across target boundaries.
-//
-// The search tests r^2 < (2 h_a)^2 first in fp32 on cell-relative coordinates
-// inside an error band derived in DESIGN.md §6; candidates inside the band get
-// the exact fp64 test in the oracle's association, so lists stay bit-exact.
-#include "stencil.cuh"
+// A CTA owns a unit of 2x2x1 search cells (~290 targets at the paper's 300
+// neighbours), stages the source particles of the unit's union stencil into shared
+// memory in groups with coalesced loads (density, IAD) or TMA bulk copies of
+// per-particle records (momentum); periodic images are shifted at staging time, so
+// no pair needs a minimum image.  A warp (density, IAD) or half-warp (momentum) per
+// target expands the target's neighbour SEGMENTS of the current group (tile +
+// 32-bit mask, pairpass.cuh) into staging indices in a small per-warp buffer -- one
+// lane per segment -- and runs the pair body over them.  The segment list of the
+// next target is loaded while the current one runs (one coalesced 8-byte load per
+// lane), so no pair step waits on a global load.
+#include "pairpass.cuh"
 
 namespace sphb {
-
-constexpr int kCT = 256;          // threads per CTA
-constexpr int kNW = kCT / 32;     // warps per CTA
-constexpr int kTgtU = 416;        // targets per sub-block (a whole 2x2x1 unit, <= 9x9x5 at config 5)
-constexpr int kSlots = kKMax;     // slot tables: every stencil the grid chooser admits
-constexpr int kCellChunk = 4;     // consecutive cells per claim (L2 reuse of shared stencils)
-constexpr int kSearchCap = 4096;  // staged candidates per group (float4): a unit stencil in one group
-constexpr int kNT = 4;            // search: targets per warp sharing each candidate load
-constexpr int kTS = 32;           // search tile: candidates per fp32 bounding box (16 measured 2.7 ms slower)
-constexpr int kSearchTiles = kSearchCap / kTS + 1;          // + the sentinel tile
-constexpr int kSearchWords = (kSearchCap / kTS + 31) / 32;  // tile bitmask words
-static_assert(kTS == 16 || kTS == 32, "a tile is a half-warp or a warp of candidates");
-static_assert(kSearchWords <= 6, "tile mask held in six registers");
-constexpr int kDensCap = 4096;    // density: staged particles per group, 4 fp64 fields
-constexpr int kIadCap = 4096;     // IAD: the same fields
-constexpr int kMomCap = 992;      // staged particles per group, 17 fp64 fields (1 CTA/SM; a 48-cell unit stencil in 4 groups)
-constexpr int kCTM = 512;         // momentum CTA: 16 warps, one CTA per SM
-constexpr int kCTD = 1024;        // density / IAD CTA: 32 warps, one CTA per SM (a unit stencil in one group)
-constexpr int kNWM = kCTM / 32;
-constexpr uint32_t kSent = 0xffffffffu;
-
-static_assert(kSlots >= kKMax, "slot tables must hold the largest admitted stencil");
 
 __constant__ double c_poly[kPolyTerms];   // sinc(pi sqrt(t)/2) = sum c_poly[k] t^k
 __constant__ double c_dpoly[kPolyTerms];  // derivative in t
@@ -48,77 +22,6 @@ __constant__ double c_dpoly[kPolyTerms];  // derivative in t
 void set_poly_constants(const double* poly, const double* dpoly) {
   cudaMemcpyToSymbol(c_poly, poly, sizeof(double) * kPolyTerms);
   cudaMemcpyToSymbol(c_dpoly, dpoly, sizeof(double) * kPolyTerms);
-}
-
-// Per-unit stencil tables.  The stencil's particles form one flat sequence (slots
-// in order, each slot a contiguous cell range); cum[k] is the flat index of slot
-// k's first particle.  A row entry IS a flat index f: the neighbour sits at shared
-// index f - gb of the staging group [gb, ge), and since rows ascend, "entry < ge"
-// selects a target's segment of the group (no table lookup per pair).
-struct CellSm {
-  uint32_t t_start[kSlots];     // first sorted index of slot k's cell
-  uint32_t cum[kSlots + 1];     // exclusive prefix of the slot counts
-  signed char t_sh[kSlots][3];  // periodic image shift of slot k (in periods)
-  uint32_t next[2];             // dynamic target counters, by group parity
-  Stencil st;
-  int c3[3];
-  uint32_t sc, ec, total;
-  int kself;
-};
-
-__device__ __forceinline__ double wsum(double v) {
-#pragma unroll
-  for (int o = 16; o; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
-  return v;
-}
-__device__ __forceinline__ double wmax(double v) {
-#pragma unroll
-  for (int o = 16; o; o >>= 1) v = fmax(v, __shfl_xor_sync(0xffffffffu, v, o));
-  return v;
-}
-
-// Sum NV (power of two) per-lane values over the warp by transpose-reduce: each
-// exchange step halves the values a lane keeps, so the cost is NV-1+log2(32/NV)
-// shuffles instead of NV*5.  On return v[0] of lane k*(32/NV) holds the sum of
-// value k (lanes in between hold the same sums).
-template <int NV>
-__device__ __forceinline__ void warp_multi_sum(double (&v)[NV]) {
-  const int lane = threadIdx.x & 31;
-#pragma unroll
-  for (int cnt = NV, off = 16; cnt > 1; cnt >>= 1, off >>= 1) {
-    const bool upper = (lane & off) != 0;
-#pragma unroll
-    for (int i = 0; i < cnt / 2; ++i) {
-      const double send = upper ? v[i] : v[i + cnt / 2];
-      const double keep = upper ? v[i + cnt / 2] : v[i];
-      v[i] = keep + __shfl_xor_sync(0xffffffffu, send, off);
-    }
-  }
-#pragma unroll
-  for (int off = 16 / NV; off > 0; off >>= 1) v[0] += __shfl_xor_sync(0xffffffffu, v[0], off);
-}
-
-// transpose-reduce over each 16-lane half: value k of a half ends in its lane 4k (NV = 4)
-template <int NV>
-__device__ __forceinline__ void half_multi_sum(double (&v)[NV]) {
-  const int lane = threadIdx.x & 31;
-#pragma unroll
-  for (int cnt = NV, off = 8; cnt > 1; cnt >>= 1, off >>= 1) {
-    const bool upper = (lane & off) != 0;
-#pragma unroll
-    for (int i = 0; i < cnt / 2; ++i) {
-      const double send = upper ? v[i] : v[i + cnt / 2];
-      const double keep = upper ? v[i + cnt / 2] : v[i];
-      v[i] = keep + __shfl_xor_sync(0xffffffffu, send, off);
-    }
-  }
-#pragma unroll
-  for (int off = 8 / NV; off > 0; off >>= 1) v[0] += __shfl_xor_sync(0xffffffffu, v[0], off);
-}
-__device__ __forceinline__ double half_max(double v) {
-#pragma unroll
-  for (int o = 8; o; o >>= 1) v = fmax(v, __shfl_xor_sync(0xffffffffu, v, o));
-  return v;
 }
 
 __device__ __forceinline__ double sinc_poly(double t) {  // Horner
@@ -182,682 +85,6 @@ __device__ __forceinline__ double kern_S(double t, int n, const double* __restri
   }
 }
 
-__device__ __forceinline__ double min_img(double d, double L) {
-  if (d > 0.5 * L) d -= L;
-  else if (d < -0.5 * L) d += L;
-  return d;
-}
-
-// Warp 0: per-slot tables of S.st and their prefix (flat staging index of each slot).
-// Lane 0 has set S.st / S.sc / S.ec.
-__device__ __forceinline__ void slot_tables(const Grid& g, const uint32_t* __restrict__ cstart,
-                                            const uint32_t* __restrict__ cend, CellSm& S) {
-  const int lane = threadIdx.x;
-  const int K = S.st.K;
-  uint32_t carry = 0;
-  for (int b = 0; b < K; b += 32) {
-    const int k = b + lane;
-    uint32_t cnt = 0;
-    if (k < K) {
-      int sh[3];
-      const int64_t cell = slot_cell(g, S.st, k, sh);
-      const uint32_t s0 = cstart[cell];
-      cnt = cend[cell] - s0;
-      S.t_start[k] = s0;
-      S.t_sh[k][0] = (signed char)sh[0];
-      S.t_sh[k][1] = (signed char)sh[1];
-      S.t_sh[k][2] = (signed char)sh[2];
-    }
-    uint32_t x = cnt;  // inclusive warp scan
-#pragma unroll
-    for (int o = 1; o < 32; o <<= 1) {
-      const uint32_t y = __shfl_up_sync(0xffffffffu, x, o);
-      if (lane >= o) x += y;
-    }
-    if (k < K) S.cum[k] = carry + x - cnt;
-    carry += __shfl_sync(0xffffffffu, x, 31);
-  }
-  if (lane == 0) {
-    S.cum[K] = carry;
-    S.total = carry;
-  }
-}
-
-// Unit records (one thread per unit, once per step before the search): the union
-// stencil of the unit's cells and its target range, so a CTA prologue is one 48-byte
-// load instead of a serial chain of dependent cell-table loads (ncu: the prologue
-// barrier held 7-8 % of the search, density and IAD samples).
-__device__ __forceinline__ void pack_unit(const Stencil& u, uint32_t sc, uint32_t ec, uint32_t cf,
-                                          int4* rec) {
-  rec[0] = make_int4(u.lo[0], u.lo[1], u.lo[2], u.K);
-  rec[1] = make_int4(u.cnt[0], u.cnt[1], u.cnt[2], u.wrap[0] | (u.wrap[1] << 2) | (u.wrap[2] << 4));
-  rec[2] = make_int4((int)sc, (int)ec, (int)cf, 0);
-}
-__device__ __forceinline__ void unpack_unit(const int4* __restrict__ rec, Stencil& u, uint32_t& sc,
-                                            uint32_t& ec, uint32_t* cf = nullptr) {
-  const int4 a = rec[0], b = rec[1], c = rec[2];
-  if (cf) *cf = (uint32_t)c.z;
-  u.lo[0] = a.x; u.lo[1] = a.y; u.lo[2] = a.z; u.K = a.w;
-  u.cnt[0] = b.x; u.cnt[1] = b.y; u.cnt[2] = b.z;
-  u.wrap[0] = b.w & 3; u.wrap[1] = (b.w >> 2) & 3; u.wrap[2] = (b.w >> 4) & 3;
-  sc = (uint32_t)c.x;
-  ec = (uint32_t)c.y;
-}
-
-__global__ void k_unit_prep(Grid g, const uint32_t* __restrict__ clist, const uint32_t* __restrict__ ulist,
-                            const uint32_t* __restrict__ nulist, const uint32_t* __restrict__ cstart,
-                            const uint32_t* __restrict__ cend, const unsigned long long* __restrict__ chmax,
-                            int4* __restrict__ urec) {
-  const uint32_t nu = *nulist;
-  for (uint32_t u = blockIdx.x * blockDim.x + threadIdx.x; u < nu; u += gridDim.x * blockDim.x) {
-    const uint32_t i0 = ulist[u], i1 = ulist[u + 1];
-    const uint32_t cf = clist[i0], cl = clist[i1 - 1];
-    int c3[3];
-    cell_coords(g, cf, c3);
-    Stencil st;
-    make_unit_stencil(g, c3, cstart, cend, chmax, st);
-    pack_unit(st, cstart[cf], cend[cl], cf, urec + 3 * (size_t)u);
-  }
-}
-
-// CTA prologue for pair-pass unit u (warp 0, one CTA barrier): the unit's target
-// range (its cells are consecutive in the cell list and in particle order), the
-// union stencil of its cells, and the slot tables.
-__device__ void unit_setup(const Grid& g, uint32_t u, const int4* __restrict__ urec,
-                           const uint32_t* __restrict__ cstart, const uint32_t* __restrict__ cend,
-                           CellSm& S) {
-  if (threadIdx.x < 32) {
-    if (threadIdx.x == 0) {
-      uint32_t sc, ec, cf;
-      unpack_unit(urec + 3 * (size_t)u, S.st, sc, ec, &cf);
-      S.sc = sc;
-      S.ec = ec;
-      S.kself = -1;
-      cell_coords(g, cf, S.c3);  // first cell of the unit
-    }
-    __syncwarp();
-    slot_tables(g, cstart, cend, S);
-  }
-  __syncthreads();
-}
-
-// Dynamic claims of work chunks from a global counter, the next claim issued one
-// chunk ahead (its atomic's latency overlaps the current chunk instead of stalling
-// every warp at the claim barrier: ncu put 3-6 % of the pair passes there).
-struct ChunkClaim {
-  uint32_t* work;
-  uint32_t step, nxt;
-  __device__ __forceinline__ uint32_t first(uint32_t* s_chunk) {
-    if (threadIdx.x == 0) *s_chunk = atomicAdd(work, step);
-    __syncthreads();
-    const uint32_t v = *s_chunk;
-    __syncthreads();
-    if (threadIdx.x == 0) nxt = atomicAdd(work, step);  // lands while this chunk runs
-    return v;
-  }
-  __device__ __forceinline__ uint32_t next(uint32_t* s_chunk) {
-    if (threadIdx.x == 0) *s_chunk = nxt;
-    __syncthreads();
-    const uint32_t v = *s_chunk;
-    __syncthreads();
-    if (threadIdx.x == 0) nxt = atomicAdd(work, step);
-    return v;
-  }
-};
-
-// slot of flat index f: the largest k < K with cum[k] <= f (skips empty slots)
-__device__ __forceinline__ int slot_of(const CellSm& S, uint32_t f) {
-  int lo = 0, hi = S.st.K - 1;
-  while (lo < hi) {
-    const int mid = (lo + hi + 1) >> 1;
-    if (S.cum[mid] <= f) lo = mid;
-    else hi = mid - 1;
-  }
-  return lo;
-}
-// shared-memory index of row entry e in the group starting at flat index gb
-__device__ __forceinline__ int qidx(const uint32_t* cum, uint32_t gb, uint32_t e) {
-  (void)cum;
-  return (int)(e - gb);  // row entries are flat staging indices of the unit stencil
-}
-
-__device__ __forceinline__ void shifts_of(const Grid& g, const CellSm& S, int slot, double sh[3]) {
-  sh[0] = S.t_sh[slot][0] * g.L[0];
-  sh[1] = S.t_sh[slot][1] * g.L[1];
-  sh[2] = S.t_sh[slot][2] * g.L[2];
-}
-
-// Warp-level walk over the entries of target rows that fall in the current
-// group [.., pend).  Targets are handed out dynamically (shared counter, reset by
-// the group loop) so warps reach the group barrier together.  Row chunks (32
-// entries) stream through a 3-deep register ring (ncu: with one chunk of
-// prefetch the row load was the top stall), and the first three chunks of the
-// warp's next target are issued before the current target's work.
-__device__ __forceinline__ uint32_t row_chunk(const uint32_t* row, uint32_t pos, uint32_t n) {
-  return pos < n ? row[pos] : kSent;
-}
-
-template <int NW, class Body, class Finish>
-__device__ __forceinline__ void walk_targets(uint32_t t0, uint32_t t1, const uint32_t* __restrict__ nbr,
-                                             int maxn, const uint32_t* s_n, uint32_t* s_cur,
-                                             uint32_t pend, const uint32_t* cum, uint32_t gb,
-                                             uint32_t* s_next, Body&& body, Finish&& finish) {
-  const int lane = threadIdx.x & 31;
-  uint32_t t = 0;
-  if (lane == 0) t = t0 + atomicAdd(s_next, 1u);
-  t = __shfl_sync(0xffffffffu, t, 0);
-  uint32_t f0 = kSent, f1 = kSent, f2 = kSent;
-  if (t < t1) {
-    const uint32_t c0 = s_cur[t - t0] + lane, nn = s_n[t - t0];
-    const uint32_t* r = nbr + (size_t)t * maxn;
-    f0 = row_chunk(r, c0, nn);
-    f1 = row_chunk(r, c0 + 32, nn);
-    f2 = row_chunk(r, c0 + 64, nn);
-  }
-  while (t < t1) {
-    const uint32_t i = t - t0;
-    const uint32_t n = s_n[i];
-    const uint32_t* row = nbr + (size_t)t * maxn;
-    uint32_t cur = s_cur[i];
-    uint32_t e0 = f0, e1 = f1, e2 = f2;
-    // claim the next target and prefetch its first three chunks
-    uint32_t tn = 0;
-    if (lane == 0) tn = t0 + atomicAdd(s_next, 1u);
-    tn = __shfl_sync(0xffffffffu, tn, 0);
-    if (tn < t1) {
-      const uint32_t cn = s_cur[tn - t0] + lane, nn = s_n[tn - t0];
-      const uint32_t* r = nbr + (size_t)tn * maxn;
-      f0 = row_chunk(r, cn, nn);
-      f1 = row_chunk(r, cn + 32, nn);
-      f2 = row_chunk(r, cn + 64, nn);
-    }
-    body.begin(i);
-    for (;;) {
-      const bool in = e0 < pend;
-      const unsigned b = __ballot_sync(0xffffffffu, in);
-      const int m = __popc(b);
-      const uint32_t e3 = m == 32 ? row_chunk(row, cur + 96 + lane, n) : kSent;
-      if (in) body(qidx(cum, gb, e0));
-      cur += m;
-      if (m < 32) break;
-      e0 = e1;
-      e1 = e2;
-      e2 = e3;
-    }
-    finish(i, cur);
-    t = tn;
-  }
-}
-
-// Same walk with 16 lanes per target (two targets per warp, one per half-warp):
-// the per-(target, group) setup and reduction is shared by two targets and the
-// unused lanes at the end of a segment drop from up to 31 to up to 15.  Both
-// halves step together; a half whose segment ended idles until the other is done.
-// Row chunks stream through a 2-deep ring consumed in place (unrolled by two): a
-// shifted ring (e0 = e1; e1 = e2 <- load) made every step wait for the load it had
-// just issued (ncu: long_sb on the ring move), and a momentum step is long enough
-// that two chunks of prefetch cover the load latency.
-template <class Body, class Finish>
-__device__ __forceinline__ void walk_targets_half(uint32_t t0, uint32_t t1,
-                                                  const uint32_t* __restrict__ nbr, int maxn,
-                                                  const uint32_t* s_n, uint32_t* s_cur,
-                                                  uint32_t pend, const uint32_t* cum, uint32_t gb,
-                                                  uint32_t* s_next, Body&& body, Finish&& finish) {
-  (void)cum;
-  const int lane = threadIdx.x & 31, l16 = lane & 15;
-  const unsigned hmask = (threadIdx.x & 16) ? 0xffff0000u : 0x0000ffffu;
-  auto claim = [&]() {
-    uint32_t v = 0;
-    if (l16 == 0) v = t0 + atomicAdd(s_next, 1u);
-    return __shfl_sync(0xffffffffu, v, lane & 16);
-  };
-  uint32_t t = claim();
-  uint32_t f0 = kSent, f1 = kSent;
-  if (t < t1) {
-    const uint32_t c0 = s_cur[t - t0] + l16, nn = s_n[t - t0];
-    const uint32_t* r = nbr + (size_t)t * maxn;
-    f0 = row_chunk(r, c0, nn);
-    f1 = row_chunk(r, c0 + 16, nn);
-  }
-  while (__any_sync(0xffffffffu, t < t1)) {
-    const bool act = t < t1;
-    const uint32_t i = act ? t - t0 : 0;
-    const uint32_t n = act ? s_n[i] : 0;
-    uint32_t cur = act ? s_cur[i] : 0;
-    uint32_t off = cur + l16 + 32;  // row position of the next chunk to load (two ahead)
-    const uint32_t* rp = nbr + (size_t)(act ? t : 0) * maxn + off;
-    uint32_t e0 = f0, e1 = f1;
-    const uint32_t tn = claim();
-    f0 = f1 = kSent;
-    if (tn < t1) {
-      const uint32_t cn = s_cur[tn - t0] + l16, nn = s_n[tn - t0];
-      const uint32_t* r = nbr + (size_t)tn * maxn;
-      f0 = row_chunk(r, cn, nn);
-      f1 = row_chunk(r, cn + 16, nn);
-    }
-    if (act) body.begin(i);
-    bool live = act;
-#define SPH_HALF_STEP(R)                                                       \
-  {                                                                            \
-    const uint32_t e = R;                                                      \
-    const bool in = live && e < pend;                                          \
-    const int m = __popc(__ballot_sync(0xffffffffu, in) & hmask);              \
-    const bool more = live && m == 16;                                         \
-    const int qi = (int)(e - gb);                                              \
-    R = (more && off < n) ? *rp : kSent;                                       \
-    rp += 16;                                                                  \
-    off += 16;                                                                 \
-    if (in) body(qi);                                                          \
-    cur += m;                                                                  \
-    live = more;                                                               \
-    if (!__any_sync(0xffffffffu, live)) break;                                 \
-  }
-    for (;;) {
-      SPH_HALF_STEP(e0)
-      SPH_HALF_STEP(e1)
-    }
-#undef SPH_HALF_STEP
-    finish(act, i, cur);
-    t = tn;
-  }
-}
-
-// Lean full-warp walk (density, IAD): the ring of three row chunks is consumed in
-// place -- each step refills the register it just used with the chunk three steps
-// ahead (a shifted ring makes every move wait for the latest load) -- through a
-// running row pointer, and the body runs on every lane with a validity flag instead
-// of a divergent branch (ncu: per-step bookkeeping was as large as the pair math).
-template <class Body, class Finish>
-__device__ __forceinline__ void walk_targets_fast(uint32_t t0, uint32_t t1,
-                                                  const uint32_t* __restrict__ nbr, int maxn,
-                                                  const uint32_t* s_n, const uint32_t* s_cur,
-                                                  uint32_t pend, const uint32_t* cum, uint32_t gb,
-                                                  uint32_t* s_next, Body&& body, Finish&& finish) {
-  const uint32_t lane = threadIdx.x & 31;
-  auto claim = [&]() {
-    uint32_t v = 0;
-    if (lane == 0) v = t0 + atomicAdd(s_next, 1u);
-    return __shfl_sync(0xffffffffu, v, 0);
-  };
-  uint32_t t = claim();
-  uint32_t f0 = kSent, f1 = kSent, f2 = kSent;
-  if (t < t1) {
-    const uint32_t c0 = s_cur[t - t0] + lane, nn = s_n[t - t0];
-    const uint32_t* r = nbr + (size_t)t * maxn;
-    f0 = row_chunk(r, c0, nn);
-    f1 = row_chunk(r, c0 + 32, nn);
-    f2 = row_chunk(r, c0 + 64, nn);
-  }
-  while (t < t1) {
-    const uint32_t i = t - t0, n = s_n[i];
-    uint32_t cur = s_cur[i];
-    const uint32_t lim = n - cur;  // valid positions: offset < lim from cur
-    const uint32_t* rp = nbr + (size_t)t * maxn + cur + lane + 96;
-    uint32_t off = lane + 96;
-    uint32_t e0 = f0, e1 = f1, e2 = f2;
-    const uint32_t tn = claim();
-    if (tn < t1) {  // the next target's first three chunks
-      const uint32_t cn = s_cur[tn - t0] + lane, nn = s_n[tn - t0];
-      const uint32_t* r = nbr + (size_t)tn * maxn;
-      f0 = row_chunk(r, cn, nn);
-      f1 = row_chunk(r, cn + 32, nn);
-      f2 = row_chunk(r, cn + 64, nn);
-    }
-    body.begin(i);
-#define SPH_FAST_STEP(R)                                                             \
-  {                                                                                  \
-    const uint32_t e = R;                                                            \
-    const bool in = e < pend;                                                        \
-    const int m = __popc(__ballot_sync(0xffffffffu, in));                            \
-    const int qi = in ? (int)(e - gb) : 0; /* e dies here: the refill can reuse R */ \
-    R = (m == 32 && off < lim) ? *rp : kSent;                                        \
-    rp += 32;                                                                        \
-    off += 32;                                                                       \
-    body(qi, in);                                                                    \
-    cur += m;                                                                        \
-    if (m < 32) break;                                                               \
-  }
-    for (;;) {
-      SPH_FAST_STEP(e0)
-      SPH_FAST_STEP(e1)
-      SPH_FAST_STEP(e2)
-    }
-#undef SPH_FAST_STEP
-    finish(i, cur);
-    t = tn;
-  }
-}
-
-struct TgtW {  // per-target search data (exact-test fp64 + fp32 band + own packed entry)
-  double pos[3];
-  double lim;
-  float f[5];
-  uint32_t self;
-};
-
-__device__ __forceinline__ bool exact_hit(const Grid& g, const double* __restrict__ x,
-                                          const double* __restrict__ y, const double* __restrict__ z,
-                                          uint32_t j, uint32_t t, const double* pos, double lim) {
-  // r^2 in the oracle's association, no FMA, minimum image (Eq. 6; R10)
-  if (j == t) return false;
-  double ex = __dsub_rn(x[j], pos[0]), ey = __dsub_rn(y[j], pos[1]), ez = __dsub_rn(z[j], pos[2]);
-  if (g.periodic[0]) ex = min_img(ex, g.L[0]);
-  if (g.periodic[1]) ey = min_img(ey, g.L[1]);
-  if (g.periodic[2]) ez = min_img(ez, g.L[2]);
-  return __dadd_rn(__dadd_rn(__dmul_rn(ex, ex), __dmul_rn(ey, ey)), __dmul_rn(ez, ez)) < lim;
-}
-
-__device__ __forceinline__ void wrap32(const Stencil& st, const Grid& g, float& dx, float& dy,
-                                       float& dz) {
-  const float L0 = (float)g.L[0], L1 = (float)g.L[1], L2 = (float)g.L[2];
-  if (st.wrap[0] == 2) dx = dx > 0.5f * L0 ? dx - L0 : (dx < -0.5f * L0 ? dx + L0 : dx);
-  if (st.wrap[1] == 2) dy = dy > 0.5f * L1 ? dy - L1 : (dy < -0.5f * L1 ? dy + L1 : dy);
-  if (st.wrap[2] == 2) dz = dz > 0.5f * L2 ? dz - L2 : (dz < -0.5f * L2 ? dz + L2 : dz);
-}
-
-// ------------------------------------------------------------------ a5 search
-// fp32 band [lo, hi) around lim = (2h)^2 for a staged-coordinate bound M (DESIGN.md
-// §6): r2_32 < lo implies r2 < lim, r2_32 >= hi implies r2 >= lim
-__device__ __forceinline__ float2 band32(double hh, double M) {
-  const double th = 2.0 * hh, lim = __dmul_rn(th, th);
-  const double mh = M / hh;
-  const double delta = 0x1p-20 * (2.0 + 2.0 * mh + 0x1p-20 * mh * mh);
-  if (!(delta < 0.25)) return make_float2(-1.0f, INFINITY);
-  return make_float2((float)(lim * (1.0 - delta)), (float)(lim * (1.0 + delta)));
-}
-
-// SYM: symmetric relation r < 2 max(h_a, h_b) -- each staged candidate carries its
-// own band (candidate side) next to the target's, and the exact test uses the larger
-// of the two limits (the oracle's (2 max h)^2)
-template <bool W2, bool SYM>
-__global__ void __launch_bounds__(kCT, 2) k_search(const double* __restrict__ x,
-                                                const double* __restrict__ y,
-                                                const double* __restrict__ z,
-                                                const double* __restrict__ h, Grid g,
-                                                const uint32_t* __restrict__ cstart,
-                                                const uint32_t* __restrict__ cend,
-                                                const unsigned long long* __restrict__ chmax,
-                                                const int4* __restrict__ urec,
-                                                const uint32_t* __restrict__ nulist, uint32_t* __restrict__ work,
-                                                uint32_t* __restrict__ nbr,
-                                                uint32_t* __restrict__ ncount, int maxn,
-                                                unsigned int* __restrict__ maxcount) {
-  extern __shared__ float4 cand[];  // kSearchCap + 32 (tile round-up) + 32 (sentinel tile)
-  float2* const candb = reinterpret_cast<float2*>(cand + kSearchCap + 64);  // SYM: per-candidate band
-  __shared__ CellSm S;
-  __shared__ float4 tlo[kSearchTiles], thi[kSearchTiles];  // per staged tile: fp32 bounding box
-  __shared__ uint32_t tcount[kTgtU];
-  __shared__ TgtW TW[kTgtU];  // per target of the block: computed once, in parallel
-  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  const unsigned lt = (1u << lane) - 1u;
-  __shared__ uint32_t s_chunk;
-  // one CTA per unit (stencil.cuh): the unit stencil is staged once for all its targets,
-  // and rows are written directly in its slot numbering
-  const uint32_t nun = *nulist;
-  const uint32_t uchunk = (uint32_t)kCellChunk >> g.ubits ? (uint32_t)kCellChunk >> g.ubits : 1u;
-  ChunkClaim claim{work, uchunk, 0u};
-  for (uint32_t cfirst = claim.first(&s_chunk); cfirst < nun; cfirst = claim.next(&s_chunk)) {
-    for (uint32_t ci = cfirst; ci < min(nun, cfirst + uchunk); ++ci) {
-      unit_setup(g, ci, urec, cstart, cend, S);
-      const Stencil st = S.st;
-      int b3[3];
-      unit_base(g, S.c3, b3);
-      double org[3], M = 0.0;
-  #pragma unroll
-      for (int d = 0; d < 3; ++d) {
-        const double edge = g.inv[d] > 0.0 ? 1.0 / g.inv[d] : 0.0;
-        org[d] = g.lo[d] + b3[d] * edge;
-        // bound on |staged or target coordinate - org| (stencil cells + 1 cell of slack)
-        const double Md = st.wrap[d] == 2
-                              ? g.L[d]
-                              : (double)(max(b3[d] - st.lo[d], st.lo[d] + st.cnt[d] - b3[d]) + 1) * edge;
-        M = fmax(M, Md);
-      }
-      for (uint32_t t0 = S.sc; t0 < S.ec; t0 += kTgtU) {
-        const uint32_t t1 = min(S.ec, t0 + kTgtU);
-        for (uint32_t t = t0 + threadIdx.x; t < t1; t += blockDim.x) {
-          tcount[t - t0] = 0;
-          const double ha = h[t], tha = 2.0 * ha;
-          // fp32 error band: |r2_32 - r2| <= delta lim, delta = 2^-20 (2 + 2 M/h + 2^-20 (M/h)^2)
-          const float2 bd = band32(ha, M);
-          const double px = x[t], py = y[t], pz = z[t];
-          TgtW& w = TW[t - t0];
-          w.pos[0] = px;
-          w.pos[1] = py;
-          w.pos[2] = pz;
-          w.lim = __dmul_rn(tha, tha);
-          w.f[0] = (float)(px - org[0]);
-          w.f[1] = (float)(py - org[1]);
-          w.f[2] = (float)(pz - org[2]);
-          w.f[3] = bd.x;
-          w.f[4] = bd.y;
-          // own packed entry (unit slot of the target's cell, index in it): never its own neighbour
-          w.self = kSent;
-          for (int dz = 0; dz < (g.ubits > 2 ? 2 : 1); ++dz)
-            for (int dy = 0; dy < (g.ubits > 1 ? 2 : 1); ++dy)
-              for (int dx = 0; dx < (g.ubits > 0 ? 2 : 1); ++dx) {
-                const int q0 = b3[0] + dx, q1 = b3[1] + dy, q2 = b3[2] + dz;
-                if (q0 >= g.nc[0] || q1 >= g.nc[1] || q2 >= g.nc[2]) continue;
-                const int64_t cell = q0 + (int64_t)g.nc[0] * (q1 + (int64_t)g.nc[1] * q2);
-                const uint32_t cs0 = cstart[cell];
-                if (t >= cs0 && t < cend[cell]) {
-                  const int us = (q0 - st.lo[0]) + st.cnt[0] * ((q1 - st.lo[1]) + st.cnt[1] * (q2 - st.lo[2]));
-                  w.self = S.cum[us] + (t - cs0);  // flat staging index of the target itself
-                }
-              }
-        }
-        __syncthreads();
-        for (uint32_t gb = 0; gb < S.total; gb += kSearchCap) {
-          const int total = (int)(min(S.total, gb + kSearchCap) - gb);
-          for (int q = threadIdx.x; q < total; q += blockDim.x) {  // flat staging, all threads
-            const uint32_t f = gb + q;
-            const int slot = slot_of(S, f);
-            const uint32_t l = f - S.cum[slot], j = S.t_start[slot] + l;
-            double sh[3];
-            shifts_of(g, S, slot, sh);
-            float4 v;
-            v.x = (float)((x[j] + sh[0]) - org[0]);
-            v.y = (float)((y[j] + sh[1]) - org[1]);
-            v.z = (float)((z[j] + sh[2]) - org[2]);
-            v.w = __uint_as_float(f);  // row entry: flat staging index in the unit stencil
-            cand[q] = v;
-            if constexpr (SYM) candb[q] = band32(h[j], M);
-          }
-          // pad to whole tiles with far-away sentinels (never hit, never ambiguous), plus
-          // one all-sentinel tile (index ntile) that partners a short last step
-          const int ntile = (total + kTS - 1) / kTS;
-          for (int q = total + threadIdx.x; q < kTS * ntile + kTS; q += blockDim.x) {
-            cand[q] = make_float4(INFINITY, INFINITY, INFINITY, __uint_as_float(kSent));
-            if constexpr (SYM) candb[q] = make_float2(-1.0f, -1.0f);
-          }
-          __syncthreads();
-          // tile bounding boxes (staged candidates are Z-ordered within each cell, so a
-          // tile is a compact block); a warp reduces 32 / kTS tiles at once
-          for (int q0 = warp * (32 / kTS); q0 < ntile; q0 += kNW * (32 / kTS)) {
-            const int q = q0 + lane / kTS;
-            const float4 v = cand[kTS * q + lane % kTS];  // q <= ntile: sentinel at worst
-            const bool ok = __float_as_uint(v.w) != kSent;
-            float lx = ok ? v.x : INFINITY, ly = ok ? v.y : INFINITY, lz = ok ? v.z : INFINITY;
-            float hx = ok ? v.x : -INFINITY, hy = ok ? v.y : -INFINITY, hz = ok ? v.z : -INFINITY;
-            float hb = -1.0f;  // SYM: largest candidate band of the tile
-            if constexpr (SYM) hb = ok ? candb[kTS * q + lane % kTS].y : -1.0f;
-  #pragma unroll
-            for (int o = kTS / 2; o; o >>= 1) {
-              if constexpr (SYM) hb = fmaxf(hb, __shfl_xor_sync(0xffffffffu, hb, o));
-              lx = fminf(lx, __shfl_xor_sync(0xffffffffu, lx, o));
-              ly = fminf(ly, __shfl_xor_sync(0xffffffffu, ly, o));
-              lz = fminf(lz, __shfl_xor_sync(0xffffffffu, lz, o));
-              hx = fmaxf(hx, __shfl_xor_sync(0xffffffffu, hx, o));
-              hy = fmaxf(hy, __shfl_xor_sync(0xffffffffu, hy, o));
-              hz = fmaxf(hz, __shfl_xor_sync(0xffffffffu, hz, o));
-            }
-            if (lane % kTS == 0 && q < ntile) {
-              tlo[q] = make_float4(lx, ly, lz, 0.f);
-              thi[q] = make_float4(hx, hy, hz, hb);
-            }
-          }
-          __syncthreads();
-          // two targets per warp share every staged-candidate load (fp32 test data in
-          // registers; the fp64 data of the rare exact test in shared memory)
-          // kNT targets per warp share every staged-candidate load (fp32 test data in
-          // registers; the fp64 data of the rare exact test in shared memory)
-          for (uint32_t tq = t0 + kNT * warp; tq < t1; tq += kNT * kNW) {
-            uint32_t tt[kNT];
-            float ax[kNT], ay[kNT], az[kNT], lo[kNT], hi[kNT];
-            uint32_t self[kNT], cnt[kNT];
-            uint32_t* row[kNT];
-  #pragma unroll
-            for (int u = 0; u < kNT; ++u) {
-              tt[u] = min(tq + u, t1 - 1);  // short tail: duplicates, identical writes
-              const TgtW& T = TW[tt[u] - t0];
-              ax[u] = T.f[0]; ay[u] = T.f[1]; az[u] = T.f[2]; lo[u] = T.f[3]; hi[u] = T.f[4];
-              self[u] = T.self;
-              cnt[u] = tcount[tt[u] - t0];
-              row[u] = nbr + (size_t)tt[u] * maxn;
-              // keep the row bases in registers (else ptxas re-derives nbr + t*maxn + p in 64-bit per store)
-              asm volatile("" : "+l"(row[u]));
-            }
-            // one staged candidate against every target: fp32 band test, exact fp64 inside the band
-            auto test = [&](const float4 cd, const float2 cb, bool (&hit)[kNT], bool (&amb)[kNT]) {
-              const uint32_t pk = __float_as_uint(cd.w);
-  #pragma unroll
-              for (int u = 0; u < kNT; ++u) {
-                float dx = cd.x - ax[u], dy = cd.y - ay[u], dz = cd.z - az[u];
-                if constexpr (W2) wrap32(st, g, dx, dy, dz);
-                const float r = fmaf(dz, dz, fmaf(dy, dy, dx * dx));
-                bool in = r < lo[u];
-                bool a = (r >= lo[u]) & (r < hi[u]);
-                if constexpr (SYM) {  // either side's support
-                  in |= r < cb.x;
-                  a = !in & (a | (r < cb.y));
-                }
-                amb[u] = a;
-                hit[u] = in & (pk != self[u]);
-              }
-            };
-            // rare: exact fp64 test of the candidates inside a band (one ballot per step)
-            auto exact = [&](const float4 cd, bool (&hit)[kNT], const bool (&amb)[kNT]) {
-              bool any = false;
-  #pragma unroll
-              for (int u = 0; u < kNT; ++u) any |= amb[u];
-              if (!any) return;
-              const uint32_t pk = __float_as_uint(cd.w);
-              const int kq = slot_of(S, pk);
-              const uint32_t j = S.t_start[kq] + (pk - S.cum[kq]);
-              double limb = 0.0;
-              if constexpr (SYM) {
-                const double thb = 2.0 * h[j];
-                limb = __dmul_rn(thb, thb);
-              }
-  #pragma unroll
-              for (int u = 0; u < kNT; ++u) {
-                const TgtW& T = TW[tt[u] - t0];
-                if (amb[u]) hit[u] = exact_hit(g, x, y, z, j, tt[u], T.pos, fmax(T.lim, limb));
-              }
-            };
-            // Tiles any target can reach.  Box distance in the prefilter's own fp32
-            // expression: rounding is monotone, so box d2 <= r2_32 of every member, and
-            // box d2 >= hi excludes hits and ambiguous candidates alike (lists stay exact).
-            uint32_t need[6] = {0u, 0u, 0u, 0u, 0u, 0u};
-  #pragma unroll
-            for (int w = 0; w < kSearchWords; ++w) {
-              const int q = 32 * w + lane;
-              bool nd = false;
-              if (q < ntile) {
-                if constexpr (W2) {
-                  nd = true;
-                } else {
-                  const float4 L = tlo[q], H = thi[q];
-                  const float hb = SYM ? H.w : -1.0f;
-  #pragma unroll
-                  for (int u = 0; u < kNT; ++u) {
-                    const float bx = fmaxf(fmaxf(L.x - ax[u], ax[u] - H.x), 0.f);
-                    const float by = fmaxf(fmaxf(L.y - ay[u], ay[u] - H.y), 0.f);
-                    const float bz = fmaxf(fmaxf(L.z - az[u], az[u] - H.z), 0.f);
-                    nd |= fmaf(bz, bz, fmaf(by, by, bx * bx)) < fmaxf(hi[u], hb);
-                  }
-                }
-              }
-              need[w] = __ballot_sync(0xffffffffu, nd);
-            }
-            // lowest remaining needed tile (ascending: rows stay sorted); the word masks
-            // shift down as they empty (warp-uniform, no dynamic register indexing)
-            uint32_t m0 = need[0], m1 = need[1], m2 = need[2], m3 = need[3], m4 = need[4], m5 = need[5];
-            int base = 0, rem = (ntile + 31) / 32 - 1;
-            auto next_tile = [&]() -> int {
-              while (!m0 && rem > 0) {
-                m0 = m1; m1 = m2; m2 = m3; m3 = m4; m4 = m5; m5 = 0u;
-                base += 32;
-                --rem;
-              }
-              if (!m0) return ntile;  // the sentinel tile
-              const int q = base + __ffs(m0) - 1;
-              m0 &= m0 - 1;
-              return q;
-            };
-            // per step two candidates per lane (two tiles): kNT x 2 independent test chains,
-            // and the lane order of every ballot is the ascending staging order
-            for (;;) {
-              const int qA = next_tile();
-              if (qA == ntile) break;
-              int qF, qS;
-              if constexpr (kTS == 32) {
-                qF = qA;
-                qS = next_tile();
-              } else {
-                const int qB = next_tile(), qC = next_tile(), qD = next_tile();
-                qF = lane < 16 ? qA : qB;
-                qS = lane < 16 ? qC : qD;
-              }
-              const int iF = kTS * qF + lane % kTS, iS = kTS * qS + lane % kTS;
-              const float4 cA = cand[iF], cB = cand[iS];
-              float2 bA = make_float2(-1.0f, -1.0f), bB = bA;
-              if constexpr (SYM) {
-                bA = candb[iF];
-                bB = candb[iS];
-              }
-              bool hA[kNT], hB[kNT], aA[kNT], aB[kNT];
-              test(cA, bA, hA, aA);
-              test(cB, bB, hB, aB);
-              bool anyamb = false;
-  #pragma unroll
-              for (int u = 0; u < kNT; ++u) anyamb |= aA[u] | aB[u];
-              if (__ballot_sync(0xffffffffu, anyamb)) {
-                exact(cA, hA, aA);
-                exact(cB, hB, aB);
-              }
-              const uint32_t wA = __float_as_uint(cA.w), wB = __float_as_uint(cB.w);
-  #pragma unroll
-              for (int u = 0; u < kNT; ++u) {
-                const unsigned bAu = __ballot_sync(0xffffffffu, hA[u]);
-                const unsigned bBu = __ballot_sync(0xffffffffu, hB[u]);
-                const uint32_t pA = cnt[u] + __popc(bAu & lt);
-                const uint32_t pB = cnt[u] + __popc(bAu) + __popc(bBu & lt);
-                if (hA[u] & (pA < (uint32_t)maxn)) row[u][pA] = wA;
-                if (hB[u] & (pB < (uint32_t)maxn)) row[u][pB] = wB;
-                cnt[u] += __popc(bAu) + __popc(bBu);
-              }
-            }
-            if (lane == 0) {
-  #pragma unroll
-              for (int u = 0; u < kNT; ++u)
-                if (u == 0 || tq + u < t1) tcount[tt[u] - t0] = cnt[u];
-            }
-            __syncwarp();
-          }
-          __syncthreads();
-        }
-        for (uint32_t t = t0 + threadIdx.x; t < t1; t += blockDim.x) {
-          const uint32_t cn = tcount[t - t0];
-          ncount[t] = cn;
-          if (cn > (uint32_t)maxn) atomicMax(maxcount, cn);
-        }
-        __syncthreads();
-      }
-      }
-  }
-}
-
 // stage (x, y) and (z, f) of the current group as double2 pairs: one 16-byte LDS
 // per pair of fields, bank conflicts only within 8-lane quarters (ncu: the
 // 8-byte SoA layout cost ~3x the ideal shared-memory wavefronts)
@@ -887,6 +114,98 @@ __device__ __forceinline__ void delta3(const Stencil& st, const Grid& g, double&
   }
 }
 
+// Full-warp walk over the targets [t0, t1) of a sub-block for the staging group
+// [gb, ge) (tiles < tend): targets handed out by a shared counter so warps reach the
+// group barrier together; each target's segments of the group are expanded into the
+// warp's buffer and consumed 32 entries per step; the body runs on every lane with a
+// validity flag (ok == false: padding lane, its terms are discarded by selects).
+template <class Body, class Finish>
+__device__ __forceinline__ void walk_seg_warp(uint32_t t0, uint32_t t1, const uint2* __restrict__ seg,
+                                              int maxs, const uint32_t* s_n, const uint32_t* s_cur,
+                                              uint32_t tend, uint32_t gb, uint32_t* s_next,
+                                              uint16_t* buf, Body&& body, Finish&& finish) {
+  const uint32_t lane = threadIdx.x & 31;
+  const uint2 none = make_uint2(0u, 0xffffffffu);
+  auto claim = [&]() {
+    uint32_t v = 0;
+    if (lane == 0) v = t0 + atomicAdd(s_next, 1u);
+    return __shfl_sync(0xffffffffu, v, 0);
+  };
+  uint32_t t = claim();
+  uint2 f = t < t1 ? seg_load(seg, t, maxs, s_cur[t - t0] + lane, s_n[t - t0]) : none;
+  while (t < t1) {
+    const uint32_t i = t - t0, n = s_n[i];
+    uint32_t cur = s_cur[i];
+    uint2 sg = f;
+    const uint32_t tn = claim();  // the next target's first segment chunk lands meanwhile
+    f = tn < t1 ? seg_load(seg, tn, maxs, s_cur[tn - t0] + lane, s_n[tn - t0]) : none;
+    body.begin(i);
+    for (;;) {
+      uint32_t nfit, nval;
+      const uint32_t tot = expand_segments<32, kBufD>(sg, tend, gb, buf, &nfit, &nval);
+      for (uint32_t p0 = 0; p0 < tot; p0 += 32) {
+        const uint32_t p = p0 + lane;
+        const bool ok = p < tot;
+        body(ok ? (int)buf[p] : 0, ok);
+      }
+      __syncwarp();
+      cur += nfit;
+      if ((nfit == nval && nval < 32) || cur >= n) break;
+      sg = seg_load(seg, t, maxs, cur + lane, n);  // > 32 segments in the group, or a full buffer
+    }
+    finish(i, cur);
+    t = tn;
+  }
+}
+
+// Half-warp walk (momentum): two targets per warp, one per 16-lane half, in lockstep;
+// a half whose target is done idles until the other is.  Fewer idle lanes at the end
+// of a target's group segment (up to 15 instead of 31), and the per-target set-up and
+// reduction is shared by two targets.
+template <class Body, class Finish>
+__device__ __forceinline__ void walk_seg_half(uint32_t t0, uint32_t t1, const uint2* __restrict__ seg,
+                                              int maxs, const uint32_t* s_n, const uint32_t* s_cur,
+                                              uint32_t tend, uint32_t gb, uint32_t* s_next,
+                                              uint16_t* buf2, Body&& body, Finish&& finish) {
+  const uint32_t lane = threadIdx.x & 31, l16 = lane & 15;
+  uint16_t* const buf = buf2 + (lane >> 4) * kBufM;
+  const uint2 none = make_uint2(0u, 0xffffffffu);
+  auto claim = [&]() {
+    uint32_t v = 0;
+    if (l16 == 0) v = t0 + atomicAdd(s_next, 1u);
+    return __shfl_sync(0xffffffffu, v, lane & 16);
+  };
+  uint32_t t = claim();
+  uint2 f = t < t1 ? seg_load(seg, t, maxs, s_cur[t - t0] + l16, s_n[t - t0]) : none;
+  while (__any_sync(0xffffffffu, t < t1)) {
+    const bool act = t < t1;
+    const uint32_t i = act ? t - t0 : 0;
+    const uint32_t n = act ? s_n[i] : 0;
+    uint32_t cur = act ? s_cur[i] : 0;
+    uint2 sg = f;
+    const uint32_t tn = claim();
+    f = tn < t1 ? seg_load(seg, tn, maxs, s_cur[tn - t0] + l16, s_n[tn - t0]) : none;
+    if (act) body.begin(i);
+    bool more = act;
+    while (__any_sync(0xffffffffu, more)) {
+      uint32_t nfit, nval;
+      const uint32_t tot = expand_segments<16, kBufM>(more ? sg : none, tend, gb, buf, &nfit, &nval);
+      for (uint32_t p0 = 0; __any_sync(0xffffffffu, p0 < tot); p0 += 16) {
+        const uint32_t p = p0 + l16;
+        if (p < tot) body((int)buf[p]);
+      }
+      __syncwarp();
+      if (more) {
+        cur += nfit;
+        if ((nfit == nval && nval < 16) || cur >= n) more = false;
+        else sg = seg_load(seg, t, maxs, cur + l16, n);
+      }
+    }
+    finish(act, i, cur);
+    t = tn;
+  }
+}
+
 // ------------------------------------------------------------------ a6 density + Omega + EOS
 struct DensBody {
   const double2 *s01, *s23;
@@ -910,8 +229,8 @@ __global__ void __launch_bounds__(kCTD, 1) k_density_c(
     const double* __restrict__ h, const double* __restrict__ m, const double* __restrict__ u,
     Grid g, const uint32_t* __restrict__ cstart, const uint32_t* __restrict__ cend,
     const unsigned long long* __restrict__ chmax, const uint32_t* __restrict__ clist,
-    const uint32_t* __restrict__ nclist, const int4* __restrict__ urec, const uint32_t* __restrict__ nulist, uint32_t* __restrict__ work, const uint32_t* __restrict__ nbr,
-    const uint32_t* __restrict__ ncount, int maxn, Phys ph, double* __restrict__ rho,
+    const uint32_t* __restrict__ nclist, const int4* __restrict__ urec, const uint32_t* __restrict__ nulist, uint32_t* __restrict__ work, const uint2* __restrict__ seg,
+    const uint32_t* __restrict__ nseg, int maxs, Phys ph, double* __restrict__ rho,
     double* __restrict__ omega, double* __restrict__ p, double* __restrict__ cs,
     double* __restrict__ wB, double* __restrict__ ih2, double* __restrict__ vol,
     double* __restrict__ rinv, double* __restrict__ X, double* __restrict__ mX,
@@ -919,10 +238,11 @@ __global__ void __launch_bounds__(kCTD, 1) k_density_c(
   extern __shared__ double dsm[];
   double2* s01 = reinterpret_cast<double2*>(dsm);
   double2* s23 = s01 + kDensCap;
+  uint16_t* const ebuf = reinterpret_cast<uint16_t*>(s23 + kDensCap);  // expanded entries, kBufD per warp
   __shared__ CellSm S;
   __shared__ uint32_t s_n[kTgtU], s_cur[kTgtU];
   __shared__ double tx[kTgtU], ty[kTgtU], tz[kTgtU], tih2[kTgtU], acc0[kTgtU], acc1[kTgtU];
-  const int lane = threadIdx.x & 31;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   __shared__ uint32_t s_chunk;
   const int n = N > 0 ? N : ph.n;
   // cells in chunks of kCellChunk consecutive (Morton-order) cells claimed from a
@@ -939,7 +259,7 @@ __global__ void __launch_bounds__(kCTD, 1) k_density_c(
         const uint32_t t1 = min(S.ec, t0 + kTgtU);
         for (uint32_t t = t0 + threadIdx.x; t < t1; t += blockDim.x) {
           const uint32_t i = t - t0;
-          s_n[i] = ncount[t];
+          s_n[i] = nseg[t];
           s_cur[i] = 0;
           tx[i] = x[t];
           ty[i] = y[t];
@@ -952,7 +272,7 @@ __global__ void __launch_bounds__(kCTD, 1) k_density_c(
         if (threadIdx.x == 0) S.next[0] = 0;
         __syncthreads();
         for (uint32_t gb = 0, gi = 0; gb < S.total; gb += kDensCap, ++gi) {
-          const uint32_t ge = min(S.total, gb + kDensCap), pend = ge;
+          const uint32_t ge = min(S.total, gb + kDensCap);
           if (threadIdx.x == 0) S.next[(gi + 1) & 1] = 0;
           stage2x2(g, S, gb, ge, x, y, z, m, s01, s23);
           __syncthreads();
@@ -988,7 +308,7 @@ __global__ void __launch_bounds__(kCTD, 1) k_density_c(
           body.tx = tx; body.ty = ty; body.tz = tz; body.tih2 = tih2;
           body.st = &st; body.g = &g; body.n = n; body.K = ph.tableK; body.tab = ph.table;
           body.sym = ph.sym;
-          walk_targets_fast(t0, t1, nbr, maxn, s_n, s_cur, pend, S.cum, gb, &S.next[gi & 1], body,
+          walk_seg_warp(t0, t1, seg, maxs, s_n, s_cur, (ge + 31) >> 5, gb, &S.next[gi & 1], ebuf + warp * kBufD, body,
                             [&](uint32_t i, uint32_t c2) {
                               double v[2] = {body.sr, body.sd};
                               warp_multi_sum<2>(v);
@@ -1045,8 +365,8 @@ __global__ void __launch_bounds__(kCTD, 1) k_iad_c(
     const double* __restrict__ x, const double* __restrict__ y, const double* __restrict__ z,
     Grid g, const uint32_t* __restrict__ cstart, const uint32_t* __restrict__ cend,
     const unsigned long long* __restrict__ chmax, const uint32_t* __restrict__ clist,
-    const uint32_t* __restrict__ nclist, const int4* __restrict__ urec, const uint32_t* __restrict__ nulist, uint32_t* __restrict__ work, const uint32_t* __restrict__ nbr,
-    const uint32_t* __restrict__ ncount, int maxn, Phys ph, const double* __restrict__ wB,
+    const uint32_t* __restrict__ nclist, const int4* __restrict__ urec, const uint32_t* __restrict__ nulist, uint32_t* __restrict__ work, const uint2* __restrict__ seg,
+    const uint32_t* __restrict__ nseg, int maxs, Phys ph, const double* __restrict__ wB,
     const double* __restrict__ ih2, const double* __restrict__ vol, double* __restrict__ c11,
     double* __restrict__ c12, double* __restrict__ c13, double* __restrict__ c22,
     double* __restrict__ c23, double* __restrict__ c33, double* __restrict__ ct,
@@ -1054,11 +374,12 @@ __global__ void __launch_bounds__(kCTD, 1) k_iad_c(
   extern __shared__ double dsm[];
   double2* s01 = reinterpret_cast<double2*>(dsm);
   double2* s23 = s01 + kIadCap;
+  uint16_t* const ebuf = reinterpret_cast<uint16_t*>(s23 + kIadCap);  // expanded entries, kBufD per warp
   __shared__ CellSm S;
   __shared__ uint32_t s_n[kTgtU], s_cur[kTgtU];
   __shared__ double tx[kTgtU], ty[kTgtU], tz[kTgtU], tih2[kTgtU];
   __shared__ double acc[6][kTgtU];
-  const int lane = threadIdx.x & 31;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   __shared__ uint32_t s_chunk;
   const int n = N > 0 ? N : ph.n;
   // cells in chunks of kCellChunk consecutive (Morton-order) cells claimed from a
@@ -1075,7 +396,7 @@ __global__ void __launch_bounds__(kCTD, 1) k_iad_c(
         const uint32_t t1 = min(S.ec, t0 + kTgtU);
         for (uint32_t t = t0 + threadIdx.x; t < t1; t += blockDim.x) {
           const uint32_t i = t - t0;
-          s_n[i] = ncount[t];
+          s_n[i] = nseg[t];
           s_cur[i] = 0;
           tx[i] = x[t];
           ty[i] = y[t];
@@ -1086,7 +407,7 @@ __global__ void __launch_bounds__(kCTD, 1) k_iad_c(
         if (threadIdx.x == 0) S.next[0] = 0;
         __syncthreads();
         for (uint32_t gb = 0, gi = 0; gb < S.total; gb += kIadCap, ++gi) {
-          const uint32_t ge = min(S.total, gb + kIadCap), pend = ge;
+          const uint32_t ge = min(S.total, gb + kIadCap);
           if (threadIdx.x == 0) S.next[(gi + 1) & 1] = 0;
           stage2x2(g, S, gb, ge, x, y, z, vol, s01, s23);
           __syncthreads();
@@ -1126,7 +447,7 @@ __global__ void __launch_bounds__(kCTD, 1) k_iad_c(
           body.tx = tx; body.ty = ty; body.tz = tz; body.tih2 = tih2;
           body.st = &st; body.g = &g; body.n = n; body.K = ph.tableK; body.tab = ph.table;
           body.sym = ph.sym;
-          walk_targets_fast(t0, t1, nbr, maxn, s_n, s_cur, pend, S.cum, gb, &S.next[gi & 1], body,
+          walk_seg_warp(t0, t1, seg, maxs, s_n, s_cur, (ge + 31) >> 5, gb, &S.next[gi & 1], ebuf + warp * kBufD, body,
                             [&](uint32_t i, uint32_t c2) {
                               double v[8] = {body.t11, body.t12, body.t13, body.t22,
                                              body.t23, body.t33, 0.0, 0.0};
@@ -1257,7 +578,7 @@ __global__ void __launch_bounds__(kCTM, 1) k_momentum_c(
     const uint32_t* __restrict__ cend, const unsigned long long* __restrict__ chmax,
     const uint32_t* __restrict__ clist, const uint32_t* __restrict__ nclist,
     const int4* __restrict__ urec, const uint32_t* __restrict__ nulist, uint32_t* __restrict__ work,
-    const uint32_t* __restrict__ nbr, const uint32_t* __restrict__ ncount, int maxn, Phys ph,
+    const uint2* __restrict__ seg, const uint32_t* __restrict__ nseg, int maxs, Phys ph,
     double* __restrict__ dts, unsigned long long* __restrict__ cnt, const double2* __restrict__ mrec) {
   extern __shared__ double dsm[];  // kMomCap staged source records + T_N * kTgtU target fields
   double2* const F2 = reinterpret_cast<double2*>(dsm);
@@ -1267,6 +588,7 @@ __global__ void __launch_bounds__(kCTM, 1) k_momentum_c(
   __shared__ double acc[5][kTgtU];
   __shared__ double shdt[kNWM];
   __shared__ unsigned long long shco;
+  __shared__ uint16_t ebuf[kNWM][2 * kBufM];  // expanded neighbour entries, per half-warp
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   __shared__ uint32_t s_chunk;
   const int n = N > 0 ? N : ph.n;
@@ -1291,7 +613,7 @@ __global__ void __launch_bounds__(kCTM, 1) k_momentum_c(
         const uint32_t t1 = min(S.ec, t0 + kTgtU);
         for (uint32_t t = t0 + threadIdx.x; t < t1; t += blockDim.x) {
           const uint32_t i = t - t0;
-          s_n[i] = ncount[t];
+          s_n[i] = nseg[t];
           s_cur[i] = 0;
           T[T_X * kTgtU + i] = src.x[t];
           T[T_Y * kTgtU + i] = src.y[t];
@@ -1319,7 +641,7 @@ __global__ void __launch_bounds__(kCTM, 1) k_momentum_c(
         if (threadIdx.x == 0) S.next[0] = 0;
         __syncthreads();
         for (uint32_t gb = 0, gi = 0; gb < S.total; gb += kMomCap, ++gi) {
-          const uint32_t ge = min(S.total, gb + kMomCap), pend = ge;
+          const uint32_t ge = min(S.total, gb + kMomCap);
           if (threadIdx.x == 0) S.next[(gi + 1) & 1] = 0;
           // stage [gb, ge): warp 0 issues one bulk copy of consecutive records per slot
           // (the slot's cell is a contiguous range), all complete on one mbarrier
@@ -1432,7 +754,7 @@ __global__ void __launch_bounds__(kCTM, 1) k_momentum_c(
           body.F2 = F2; body.T = T; body.st = &st; body.g = &g; body.alpha = ph.alpha; body.n = n;
           body.K = ph.tableK; body.tab = ph.table; body.sym = ph.sym;
           body.ncoinc = &ncoinc;
-          walk_targets_half(t0, t1, nbr, maxn, s_n, s_cur, pend, S.cum, gb, &S.next[gi & 1], body,
+          walk_seg_half(t0, t1, seg, maxs, s_n, s_cur, (ge + 31) >> 5, gb, &S.next[gi & 1], ebuf[warp], body,
                             [&](bool act, uint32_t i, uint32_t c2) {
                               double v[4] = {body.fx, body.fy, body.fz, body.fu};
                               half_multi_sum<4>(v);
@@ -1501,34 +823,15 @@ static void set_smem(K kern, size_t bytes) {
   cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes);
 }
 
-int launch_neighbors(sph_ctx* c) {
-  const bool sym = c->phys.sym != 0;
-  // + tile round-up + sentinel tile; symmetric: + the candidates' own bands
-  const size_t smem = (kSearchCap + 64) * sizeof(float4) + (sym ? (kSearchCap + 64) * sizeof(float2) : 0);
-  auto kern = any_wrap2(c) ? (sym ? k_search<true, true> : k_search<true, false>)
-                           : (sym ? k_search<false, true> : k_search<false, false>);
-  set_smem(kern, smem);
-  cudaMemsetAsync(c->s.work + 0, 0, sizeof(uint32_t), c->stream);
-  // unit records (union stencils + target ranges) for the search and the three passes
-  k_unit_prep<<<cell_grid(c, 8), 128, 0, c->stream>>>(c->grid, c->s.cell_list, c->s.unit_list,
-                                                      c->s.nunit_list, c->s.cell_start, c->s.cell_end,
-                                                      c->s.cell_hmax, c->s.unit_rec);
-  kern<<<cell_grid(c, 2), kCT, smem, c->stream>>>(
-      c->P.x, c->P.y, c->P.z, c->P.h, c->grid, c->s.cell_start, c->s.cell_end, c->s.cell_hmax,
-      c->s.unit_rec, c->s.nunit_list, c->s.work + 0, c->s.nbr, c->s.ncount, c->maxn,
-      c->s.nbr_maxcount);
-  return 2;
-}
-
 template <int N, bool W2, int KM>
 static void density_t(sph_ctx* c) {
-  const size_t smem = 4 * kDensCap * sizeof(double);
+  const size_t smem = 4 * kDensCap * sizeof(double) + kNWD * kBufD * sizeof(uint16_t);
   set_smem(k_density_c<N, W2, KM>, smem);
   sph_particles& P = c->P;
   cudaMemsetAsync(c->s.work + 1, 0, sizeof(uint32_t), c->stream);
   k_density_c<N, W2, KM><<<cell_grid(c, 1), kCTD, smem, c->stream>>>(
       P.x, P.y, P.z, P.h, P.m, P.u, c->grid, c->s.cell_start, c->s.cell_end, c->s.cell_hmax,
-      c->s.cell_list, c->s.ncell_list, c->s.unit_rec, c->s.nunit_list, c->s.work + 1, c->s.nbr, c->s.ncount, c->maxn, c->phys, P.rho, P.omega,
+      c->s.cell_list, c->s.ncell_list, c->s.unit_rec, c->s.nunit_list, c->s.work + 1, c->s.seg, c->s.nseg, c->maxs, c->phys, P.rho, P.omega,
       P.p, P.c, c->s.wB, c->s.ih2, c->s.vol, c->s.rinv, c->s.X, c->s.mX, c->s.cnt);
 }
 
@@ -1559,13 +862,13 @@ int launch_density(sph_ctx* c) {
 
 template <int N, bool W2, int KM>
 static void iad_t(sph_ctx* c) {
-  const size_t smem = 4 * kIadCap * sizeof(double);
+  const size_t smem = 4 * kIadCap * sizeof(double) + kNWD * kBufD * sizeof(uint16_t);
   set_smem(k_iad_c<N, W2, KM>, smem);
   sph_particles& P = c->P;
   cudaMemsetAsync(c->s.work + 2, 0, sizeof(uint32_t), c->stream);
   k_iad_c<N, W2, KM><<<cell_grid(c, 1), kCTD, smem, c->stream>>>(
       P.x, P.y, P.z, c->grid, c->s.cell_start, c->s.cell_end, c->s.cell_hmax, c->s.cell_list,
-      c->s.ncell_list, c->s.unit_rec, c->s.nunit_list, c->s.work + 2, c->s.nbr, c->s.ncount, c->maxn, c->phys, c->s.wB, c->s.ih2, c->s.vol,
+      c->s.ncell_list, c->s.unit_rec, c->s.nunit_list, c->s.work + 2, c->s.seg, c->s.nseg, c->maxs, c->phys, c->s.wB, c->s.ih2, c->s.vol,
       P.c11, P.c12, P.c13, P.c22, P.c23, P.c33, c->s.ct, c->cap, c->s.cnt);
 }
 
@@ -1585,7 +888,7 @@ static void momentum_t(sph_ctx* c) {
   cudaMemsetAsync(c->s.work + 3, 0, sizeof(uint32_t), c->stream);
   k_momentum_c<N, W2, KM><<<cell_grid(c, 1), kCTM, smem, c->stream>>>(
       src, tg, out, c->grid, c->s.cell_start, c->s.cell_end, c->s.cell_hmax, c->s.cell_list,
-      c->s.ncell_list, c->s.unit_rec, c->s.nunit_list, c->s.work + 3, c->s.nbr, c->s.ncount, c->maxn, c->phys, c->s.dts, c->s.cnt,
+      c->s.ncell_list, c->s.unit_rec, c->s.nunit_list, c->s.work + 3, c->s.seg, c->s.nseg, c->maxs, c->phys, c->s.dts, c->s.cnt,
       reinterpret_cast<const double2*>(c->s.mrec));
 }
 

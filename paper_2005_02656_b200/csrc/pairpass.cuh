@@ -1,0 +1,277 @@
+// pairpass.cuh -- device helpers shared by the neighbour search (search.cu) and the
+// pair passes (cellpass.cu): unit stencils in shared memory, work claiming, warp
+// reductions, the kernel polynomial, and the neighbour-list format.
+//
+// Neighbour lists.  A pair-pass UNIT (stencil.cuh) stages the
+// particles of its union stencil as one flat sequence (slots in order, each slot
+// a contiguous cell range).  The flat sequence is cut into TILES of 32; target t's
+// list is nseg[t] SEGMENTS seg[t * maxs + k] = (mask, tile), tiles ascending, where
+// bit b of mask marks the staged particle with flat index 32 tile + b as a
+// neighbour.  The search produces one 32-bit mask per (target, tile) straight from
+// its candidate tests, and a pass expands a target's segments into staging indices
+// with one lane per segment (expand_segments below): ~8 bytes per ~10 neighbours
+// in HBM instead of 4 bytes per neighbour, loaded with one coalesced 8-byte load
+// per lane per target.
+#pragma once
+
+#include "stencil.cuh"
+
+namespace sphb {
+
+constexpr int kCT = 256;          // search CTA threads
+constexpr int kNW = kCT / 32;
+constexpr int kTgtU = 416;        // targets per sub-block (a whole 2x2x1 unit, <= 9x9x5 at config 5)
+constexpr int kSlots = kKMax;     // slot tables: every stencil the grid chooser admits
+constexpr int kCellChunk = 4;     // consecutive cells per claim (L2 reuse of shared stencils)
+constexpr int kSearchCap = 4096;  // staged candidates per group (float4): a unit stencil in one group
+constexpr int kSearchTiles = kSearchCap / 32;
+constexpr int kSearchWords = kSearchTiles / 32;  // tile bitmask words
+constexpr int kDensCap = 4096;    // density: staged particles per group, 4 fp64 fields
+constexpr int kIadCap = 4096;     // IAD: the same fields
+constexpr int kMomCap = 896;      // momentum: staged 144-byte records per group (28 tiles)
+constexpr int kCTM = 512;         // momentum CTA: 16 warps, one CTA per SM
+constexpr int kCTD = 1024;        // density / IAD CTA: 32 warps, one CTA per SM
+constexpr int kNWM = kCTM / 32;
+constexpr int kNWD = kCTD / 32;
+constexpr int kBufD = 512;        // density / IAD: expanded entries per warp buffer
+constexpr int kBufM = 128;        // momentum: expanded entries per half-warp buffer (smem budget)
+static_assert(kSearchCap % 32 == 0 && kDensCap % 32 == 0 && kIadCap % 32 == 0 && kMomCap % 32 == 0,
+              "staging groups are whole tiles");
+static_assert(kSlots >= kKMax, "slot tables must hold the largest admitted stencil");
+
+// Per-unit stencil tables.  cum[k] is the flat index of slot k's first particle.
+struct CellSm {
+  uint32_t t_start[kSlots];     // first sorted index of slot k's cell
+  uint32_t cum[kSlots + 1];     // exclusive prefix of the slot counts
+  signed char t_sh[kSlots][3];  // periodic image shift of slot k (in periods)
+  uint32_t next[2];             // dynamic target counters, by group parity
+  Stencil st;
+  int c3[3];
+  uint32_t sc, ec, total;
+  int kself;
+};
+
+__device__ __forceinline__ double wsum(double v) {
+#pragma unroll
+  for (int o = 16; o; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+  return v;
+}
+__device__ __forceinline__ double wmax(double v) {
+#pragma unroll
+  for (int o = 16; o; o >>= 1) v = fmax(v, __shfl_xor_sync(0xffffffffu, v, o));
+  return v;
+}
+
+// Sum NV (power of two) per-lane values over the warp by transpose-reduce: each
+// exchange step halves the values a lane keeps, so the cost is NV-1+log2(32/NV)
+// shuffles instead of NV*5.  On return v[0] of lane k*(32/NV) holds the sum of
+// value k (lanes in between hold the same sums).
+template <int NV>
+__device__ __forceinline__ void warp_multi_sum(double (&v)[NV]) {
+  const int lane = threadIdx.x & 31;
+#pragma unroll
+  for (int cnt = NV, off = 16; cnt > 1; cnt >>= 1, off >>= 1) {
+    const bool upper = (lane & off) != 0;
+#pragma unroll
+    for (int i = 0; i < cnt / 2; ++i) {
+      const double send = upper ? v[i] : v[i + cnt / 2];
+      const double keep = upper ? v[i + cnt / 2] : v[i];
+      v[i] = keep + __shfl_xor_sync(0xffffffffu, send, off);
+    }
+  }
+#pragma unroll
+  for (int off = 16 / NV; off > 0; off >>= 1) v[0] += __shfl_xor_sync(0xffffffffu, v[0], off);
+}
+
+// transpose-reduce over each 16-lane half: value k of a half ends in its lane 4k (NV = 4)
+template <int NV>
+__device__ __forceinline__ void half_multi_sum(double (&v)[NV]) {
+  const int lane = threadIdx.x & 31;
+#pragma unroll
+  for (int cnt = NV, off = 8; cnt > 1; cnt >>= 1, off >>= 1) {
+    const bool upper = (lane & off) != 0;
+#pragma unroll
+    for (int i = 0; i < cnt / 2; ++i) {
+      const double send = upper ? v[i] : v[i + cnt / 2];
+      const double keep = upper ? v[i + cnt / 2] : v[i];
+      v[i] = keep + __shfl_xor_sync(0xffffffffu, send, off);
+    }
+  }
+#pragma unroll
+  for (int off = 8 / NV; off > 0; off >>= 1) v[0] += __shfl_xor_sync(0xffffffffu, v[0], off);
+}
+__device__ __forceinline__ double half_max(double v) {
+#pragma unroll
+  for (int o = 8; o; o >>= 1) v = fmax(v, __shfl_xor_sync(0xffffffffu, v, o));
+  return v;
+}
+
+__device__ __forceinline__ double min_img(double d, double L) {
+  if (d > 0.5 * L) d -= L;
+  else if (d < -0.5 * L) d += L;
+  return d;
+}
+
+// Warp 0: per-slot tables of S.st and their prefix (flat staging index of each slot).
+// Lane 0 has set S.st / S.sc / S.ec.
+__device__ __forceinline__ void slot_tables(const Grid& g, const uint32_t* __restrict__ cstart,
+                                            const uint32_t* __restrict__ cend, CellSm& S) {
+  const int lane = threadIdx.x;
+  const int K = S.st.K;
+  uint32_t carry = 0;
+  for (int b = 0; b < K; b += 32) {
+    const int k = b + lane;
+    uint32_t cnt = 0;
+    if (k < K) {
+      int sh[3];
+      const int64_t cell = slot_cell(g, S.st, k, sh);
+      const uint32_t s0 = cstart[cell];
+      cnt = cend[cell] - s0;
+      S.t_start[k] = s0;
+      S.t_sh[k][0] = (signed char)sh[0];
+      S.t_sh[k][1] = (signed char)sh[1];
+      S.t_sh[k][2] = (signed char)sh[2];
+    }
+    uint32_t x = cnt;  // inclusive warp scan
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const uint32_t y = __shfl_up_sync(0xffffffffu, x, o);
+      if (lane >= o) x += y;
+    }
+    if (k < K) S.cum[k] = carry + x - cnt;
+    carry += __shfl_sync(0xffffffffu, x, 31);
+  }
+  if (lane == 0) {
+    S.cum[K] = carry;
+    S.total = carry;
+  }
+}
+
+// Unit records (one thread per unit, once per step before the search): the union
+// stencil of the unit's cells and its target range, so a CTA prologue is one 48-byte
+// load instead of a serial chain of dependent cell-table loads.
+__device__ __forceinline__ void pack_unit(const Stencil& u, uint32_t sc, uint32_t ec, uint32_t cf,
+                                          int4* rec) {
+  rec[0] = make_int4(u.lo[0], u.lo[1], u.lo[2], u.K);
+  rec[1] = make_int4(u.cnt[0], u.cnt[1], u.cnt[2], u.wrap[0] | (u.wrap[1] << 2) | (u.wrap[2] << 4));
+  rec[2] = make_int4((int)sc, (int)ec, (int)cf, 0);
+}
+__device__ __forceinline__ void unpack_unit(const int4* __restrict__ rec, Stencil& u, uint32_t& sc,
+                                            uint32_t& ec, uint32_t* cf = nullptr) {
+  const int4 a = rec[0], b = rec[1], c = rec[2];
+  if (cf) *cf = (uint32_t)c.z;
+  u.lo[0] = a.x; u.lo[1] = a.y; u.lo[2] = a.z; u.K = a.w;
+  u.cnt[0] = b.x; u.cnt[1] = b.y; u.cnt[2] = b.z;
+  u.wrap[0] = b.w & 3; u.wrap[1] = (b.w >> 2) & 3; u.wrap[2] = (b.w >> 4) & 3;
+  sc = (uint32_t)c.x;
+  ec = (uint32_t)c.y;
+}
+
+// CTA prologue for pair-pass unit u (warp 0, one CTA barrier): the unit's target
+// range (its cells are consecutive in the cell list and in particle order), the
+// union stencil of its cells, and the slot tables.
+__device__ __forceinline__ void unit_setup(const Grid& g, uint32_t u, const int4* __restrict__ urec,
+                                           const uint32_t* __restrict__ cstart,
+                                           const uint32_t* __restrict__ cend, CellSm& S) {
+  if (threadIdx.x < 32) {
+    if (threadIdx.x == 0) {
+      uint32_t sc, ec, cf;
+      unpack_unit(urec + 3 * (size_t)u, S.st, sc, ec, &cf);
+      S.sc = sc;
+      S.ec = ec;
+      S.kself = -1;
+      cell_coords(g, cf, S.c3);  // first cell of the unit
+    }
+    __syncwarp();
+    slot_tables(g, cstart, cend, S);
+  }
+  __syncthreads();
+}
+
+// Dynamic claims of work chunks from a global counter, the next claim issued one
+// chunk ahead (its atomic's latency overlaps the current chunk).
+struct ChunkClaim {
+  uint32_t* work;
+  uint32_t step, nxt;
+  __device__ __forceinline__ uint32_t first(uint32_t* s_chunk) {
+    if (threadIdx.x == 0) *s_chunk = atomicAdd(work, step);
+    __syncthreads();
+    const uint32_t v = *s_chunk;
+    __syncthreads();
+    if (threadIdx.x == 0) nxt = atomicAdd(work, step);  // lands while this chunk runs
+    return v;
+  }
+  __device__ __forceinline__ uint32_t next(uint32_t* s_chunk) {
+    if (threadIdx.x == 0) *s_chunk = nxt;
+    __syncthreads();
+    const uint32_t v = *s_chunk;
+    __syncthreads();
+    if (threadIdx.x == 0) nxt = atomicAdd(work, step);
+    return v;
+  }
+};
+
+// slot of flat index f: the largest k < K with cum[k] <= f (skips empty slots)
+__device__ __forceinline__ int slot_of(const CellSm& S, uint32_t f) {
+  int lo = 0, hi = S.st.K - 1;
+  while (lo < hi) {
+    const int mid = (lo + hi + 1) >> 1;
+    if (S.cum[mid] <= f) lo = mid;
+    else hi = mid - 1;
+  }
+  return lo;
+}
+
+__device__ __forceinline__ void shifts_of(const Grid& g, const CellSm& S, int slot, double sh[3]) {
+  sh[0] = S.t_sh[slot][0] * g.L[0];
+  sh[1] = S.t_sh[slot][1] * g.L[1];
+  sh[2] = S.t_sh[slot][2] * g.L[2];
+}
+
+// ------------------------------------------------------------------ neighbour segments
+// Lane-held chunk of a target's segment list: lane lw of a W-lane group holds segment
+// cur + lw (mask 0 past the end).
+__device__ __forceinline__ uint2 seg_load(const uint2* __restrict__ seg, uint32_t t, int maxs,
+                                          uint32_t k, uint32_t n) {
+  return k < n ? __ldg(seg + (size_t)t * maxs + k) : make_uint2(0u, 0xffffffffu);
+}
+
+// One expansion round over a W-lane group's chunk: the leading segments with tile <
+// tend whose expansion fits BUF entries are written to buf as group-relative staging
+// indices (32 tile + bit - gb), in list order, ONE LANE PER SEGMENT (each lane walks
+// its own mask).  Returns the entries written; *nfit = segments consumed, *nval =
+// segments of the chunk inside the group.  W = 32 (warp) or 16 (half-warp, width-16
+// shuffles: the two halves expand independent targets).
+template <int W, int BUF>
+__device__ __forceinline__ uint32_t expand_segments(uint2 sg, uint32_t tend, uint32_t gb, uint16_t* buf,
+                                                    uint32_t* nfit, uint32_t* nval) {
+  const uint32_t lane = threadIdx.x & 31, lw = lane & (W - 1);
+  const uint32_t gshift = W == 32 ? 0u : (lane & 16u);
+  const uint32_t gm = W == 32 ? 0xffffffffu : (0xffffu << gshift);
+  const bool valid = sg.x != 0u && sg.y < tend;  // tiles ascend: the valid lanes are a prefix
+  const uint32_t pc = valid ? __popc(sg.x) : 0u;
+  uint32_t incl = pc;
+#pragma unroll
+  for (int o = 1; o < W; o <<= 1) {
+    const uint32_t v = __shfl_up_sync(0xffffffffu, incl, o, W);
+    if (lw >= (uint32_t)o) incl += v;
+  }
+  const bool fit = valid && incl <= (uint32_t)BUF;
+  const uint32_t nf = __popc(__ballot_sync(0xffffffffu, fit) & gm);
+  *nval = __popc(__ballot_sync(0xffffffffu, valid) & gm);
+  *nfit = nf;
+  const uint32_t tot = __shfl_sync(0xffffffffu, incl, nf ? nf - 1 : 0, W);
+  if (fit) {
+    uint32_t mm = sg.x, pos = incl - pc;
+    const uint32_t base = 32u * sg.y - gb;
+    while (mm) {
+      const uint32_t b = __ffs(mm) - 1;
+      mm &= mm - 1;
+      buf[pos++] = (uint16_t)(base + b);
+    }
+  }
+  __syncwarp();
+  return nf ? tot : 0u;
+}
+
+}  // namespace sphb

@@ -1,0 +1,356 @@
+// search.cu -- a5 neighbour search N(a) = {b != a : r_ab^2 < (2 h_a)^2} (P:103,
+// P:149 / Eq. 6 support, reading R10; symmetric variant r < 2 max(h_a, h_b), R24).
+//
+// One CTA per pair-pass UNIT (stencil.cuh): the unit's union stencil is staged in
+// shared memory as fp32 coordinates relative to the unit's base-cell corner
+// (periodic images shifted at staging time), cut into 32-candidate tiles with fp32
+// bounding boxes.  LANE PER TARGET: a warp takes 32 consecutive (Z-ordered, so
+// compact) targets, culls the tiles no member can reach with one box-to-box test,
+// and streams the surviving tiles' candidates from shared memory as broadcasts --
+// every lane tests the same candidate against its own target, so a test is ~10
+// instructions with no per-hit bookkeeping, and a tile's hits of a target are ONE
+// 32-bit mask: the neighbour-list segment (mask, tile) the pair passes consume
+// (pairpass.cuh).
+//
+// Exactness: fp32 test with an error band, the exact fp64 test in
+// the oracle's association (__dmul_rn/__dadd_rn, minimum image) for candidates
+// inside the band, so lists are bit-exact.
+#include "pairpass.cuh"
+
+namespace sphb {
+
+constexpr int kCTS = 320;             // search CTA: 10 warps = one 32-target block each per round
+constexpr int kNWS = kCTS / 32;
+
+struct TgtW {  // per-target search data (exact-test fp64 + fp32 band + own flat index)
+  double pos[3];
+  double lim;
+  float f[5];
+  uint32_t self;
+};
+
+__device__ __forceinline__ bool exact_hit(const Grid& g, const double* __restrict__ x,
+                                          const double* __restrict__ y, const double* __restrict__ z,
+                                          uint32_t j, uint32_t t, const double* pos, double lim) {
+  // r^2 in the oracle's association, no FMA, minimum image (Eq. 6; R10)
+  if (j == t) return false;
+  double ex = __dsub_rn(x[j], pos[0]), ey = __dsub_rn(y[j], pos[1]), ez = __dsub_rn(z[j], pos[2]);
+  if (g.periodic[0]) ex = min_img(ex, g.L[0]);
+  if (g.periodic[1]) ey = min_img(ey, g.L[1]);
+  if (g.periodic[2]) ez = min_img(ez, g.L[2]);
+  return __dadd_rn(__dadd_rn(__dmul_rn(ex, ex), __dmul_rn(ey, ey)), __dmul_rn(ez, ez)) < lim;
+}
+
+__device__ __forceinline__ float wrap1(float d, float L) {
+  return d > 0.5f * L ? d - L : (d < -0.5f * L ? d + L : d);
+}
+
+// fp32 band [lo, hi) around lim = (2h)^2 for a staged-coordinate bound M (DESIGN.md
+// §6): r2_32 < lo implies r2 < lim, r2_32 >= hi implies r2 >= lim
+__device__ __forceinline__ float2 band32(double hh, double M) {
+  const double th = 2.0 * hh, lim = __dmul_rn(th, th);
+  const double mh = M / hh;
+  const double delta = 0x1p-20 * (2.0 + 2.0 * mh + 0x1p-20 * mh * mh);
+  if (!(delta < 0.25)) return make_float2(-1.0f, INFINITY);
+  return make_float2((float)(lim * (1.0 - delta)), (float)(lim * (1.0 + delta)));
+}
+
+// Unit records (one thread per unit, once per step before the search).
+__global__ void k_unit_prep(Grid g, const uint32_t* __restrict__ clist, const uint32_t* __restrict__ ulist,
+                            const uint32_t* __restrict__ nulist, const uint32_t* __restrict__ cstart,
+                            const uint32_t* __restrict__ cend, const unsigned long long* __restrict__ chmax,
+                            int4* __restrict__ urec) {
+  const uint32_t nu = *nulist;
+  for (uint32_t u = blockIdx.x * blockDim.x + threadIdx.x; u < nu; u += gridDim.x * blockDim.x) {
+    const uint32_t i0 = ulist[u], i1 = ulist[u + 1];
+    const uint32_t cf = clist[i0], cl = clist[i1 - 1];
+    int c3[3];
+    cell_coords(g, cf, c3);
+    Stencil st;
+    make_unit_stencil(g, c3, cstart, cend, chmax, st);
+    pack_unit(st, cstart[cf], cend[cl], cf, urec + 3 * (size_t)u);
+  }
+}
+
+// W2: a periodic dim whose stencil spans every cell (per-pair minimum image in fp32).
+// SYM: symmetric relation -- each staged candidate carries its own band, and the exact
+// test uses the larger of the two limits (the oracle's (2 max h)^2).
+template <bool W2, bool SYM>
+__global__ void __launch_bounds__(kCTS, 2) k_search(const double* __restrict__ x,
+                                                 const double* __restrict__ y,
+                                                 const double* __restrict__ z,
+                                                 const double* __restrict__ h, Grid g,
+                                                 const uint32_t* __restrict__ cstart,
+                                                 const uint32_t* __restrict__ cend,
+                                                 const int4* __restrict__ urec,
+                                                 const uint32_t* __restrict__ nulist,
+                                                 uint32_t* __restrict__ work, uint2* __restrict__ seg,
+                                                 uint32_t* __restrict__ nseg, uint32_t* __restrict__ ncount,
+                                                 int maxs, unsigned int* __restrict__ maxima) {
+  extern __shared__ float4 cand[];  // kSearchCap + 32 (last tile padded with sentinels)
+  float2* const candb = reinterpret_cast<float2*>(cand + kSearchCap + 32);  // SYM: per-candidate band
+  __shared__ CellSm S;
+  __shared__ float4 tlo[kSearchTiles], thi[kSearchTiles];  // per staged tile: fp32 bounding box
+  __shared__ uint32_t tseg[kTgtU], tcnt[kTgtU];             // per target: segments / neighbours so far
+  __shared__ TgtW TW[kTgtU];
+  __shared__ uint32_t s_chunk;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  unsigned int mxseg = 0, mxcnt = 0;
+  const uint32_t nun = *nulist;
+  const uint32_t uchunk = (uint32_t)kCellChunk >> g.ubits ? (uint32_t)kCellChunk >> g.ubits : 1u;
+  ChunkClaim claim{work, uchunk, 0u};
+  for (uint32_t cfirst = claim.first(&s_chunk); cfirst < nun; cfirst = claim.next(&s_chunk)) {
+    for (uint32_t ci = cfirst; ci < min(nun, cfirst + uchunk); ++ci) {
+      unit_setup(g, ci, urec, cstart, cend, S);
+      const Stencil st = S.st;
+      int b3[3];
+      unit_base(g, S.c3, b3);
+      double org[3], M = 0.0;
+#pragma unroll
+      for (int d = 0; d < 3; ++d) {
+        const double edge = g.inv[d] > 0.0 ? 1.0 / g.inv[d] : 0.0;
+        org[d] = g.lo[d] + b3[d] * edge;
+        // bound on |staged or target coordinate - org| (stencil cells + 1 cell of slack)
+        const double Md = st.wrap[d] == 2
+                              ? g.L[d]
+                              : (double)(max(b3[d] - st.lo[d], st.lo[d] + st.cnt[d] - b3[d]) + 1) * edge;
+        M = fmax(M, Md);
+      }
+      for (uint32_t t0 = S.sc; t0 < S.ec; t0 += kTgtU) {
+        const uint32_t t1 = min(S.ec, t0 + kTgtU);
+        for (uint32_t t = t0 + threadIdx.x; t < t1; t += blockDim.x) {
+          tseg[t - t0] = 0;
+          tcnt[t - t0] = 0;
+          const double ha = h[t], tha = 2.0 * ha;
+          const float2 bd = band32(ha, M);
+          const double px = x[t], py = y[t], pz = z[t];
+          TgtW& w = TW[t - t0];
+          w.pos[0] = px;
+          w.pos[1] = py;
+          w.pos[2] = pz;
+          w.lim = __dmul_rn(tha, tha);
+          w.f[0] = (float)(px - org[0]);
+          w.f[1] = (float)(py - org[1]);
+          w.f[2] = (float)(pz - org[2]);
+          w.f[3] = bd.x;
+          w.f[4] = bd.y;
+          // own flat staging index (the unit slot of the target's cell): never its own neighbour
+          w.self = 0xffffffffu;
+          for (int dz = 0; dz < (g.ubits > 2 ? 2 : 1); ++dz)
+            for (int dy = 0; dy < (g.ubits > 1 ? 2 : 1); ++dy)
+              for (int dx = 0; dx < (g.ubits > 0 ? 2 : 1); ++dx) {
+                const int q0 = b3[0] + dx, q1 = b3[1] + dy, q2 = b3[2] + dz;
+                if (q0 >= g.nc[0] || q1 >= g.nc[1] || q2 >= g.nc[2]) continue;
+                const int64_t cell = q0 + (int64_t)g.nc[0] * (q1 + (int64_t)g.nc[1] * q2);
+                const uint32_t cs0 = cstart[cell];
+                if (t >= cs0 && t < cend[cell]) {
+                  const int us = (q0 - st.lo[0]) + st.cnt[0] * ((q1 - st.lo[1]) + st.cnt[1] * (q2 - st.lo[2]));
+                  w.self = S.cum[us] + (t - cs0);
+                }
+              }
+        }
+        __syncthreads();
+        for (uint32_t gb = 0; gb < S.total; gb += kSearchCap) {
+          const int total = (int)(min(S.total, gb + kSearchCap) - gb);
+          for (int q = threadIdx.x; q < total; q += blockDim.x) {  // flat staging, all threads
+            const uint32_t f = gb + q;
+            const int slot = slot_of(S, f);
+            const uint32_t j = S.t_start[slot] + (f - S.cum[slot]);
+            double sh[3];
+            shifts_of(g, S, slot, sh);
+            float4 v;
+            v.x = (float)((x[j] + sh[0]) - org[0]);
+            v.y = (float)((y[j] + sh[1]) - org[1]);
+            v.z = (float)((z[j] + sh[2]) - org[2]);
+            v.w = 0.0f;
+            cand[q] = v;
+            if constexpr (SYM) candb[q] = band32(h[j], M);
+          }
+          // pad the last tile with far-away sentinels (never a hit, never ambiguous)
+          const int ntile = (total + 31) / 32;
+          for (int q = total + threadIdx.x; q < 32 * ntile; q += blockDim.x) {
+            cand[q] = make_float4(INFINITY, INFINITY, INFINITY, 0.0f);
+            if constexpr (SYM) candb[q] = make_float2(-1.0f, -1.0f);
+          }
+          __syncthreads();
+          // tile bounding boxes (staged candidates are Z-ordered within each cell, so a
+          // tile is a compact block); one warp per tile
+          for (int q = warp; q < ntile; q += kNWS) {
+            const float4 v = cand[32 * q + lane];
+            const bool ok = v.x != INFINITY;
+            float lx = ok ? v.x : INFINITY, ly = ok ? v.y : INFINITY, lz = ok ? v.z : INFINITY;
+            float hx = ok ? v.x : -INFINITY, hy = ok ? v.y : -INFINITY, hz = ok ? v.z : -INFINITY;
+            float hb = -1.0f;  // SYM: largest candidate band of the tile
+            if constexpr (SYM) hb = ok ? candb[32 * q + lane].y : -1.0f;
+#pragma unroll
+            for (int o = 16; o; o >>= 1) {
+              if constexpr (SYM) hb = fmaxf(hb, __shfl_xor_sync(0xffffffffu, hb, o));
+              lx = fminf(lx, __shfl_xor_sync(0xffffffffu, lx, o));
+              ly = fminf(ly, __shfl_xor_sync(0xffffffffu, ly, o));
+              lz = fminf(lz, __shfl_xor_sync(0xffffffffu, lz, o));
+              hx = fmaxf(hx, __shfl_xor_sync(0xffffffffu, hx, o));
+              hy = fmaxf(hy, __shfl_xor_sync(0xffffffffu, hy, o));
+              hz = fmaxf(hz, __shfl_xor_sync(0xffffffffu, hz, o));
+            }
+            if (lane == 0) {
+              tlo[q] = make_float4(lx, ly, lz, 0.f);
+              thi[q] = make_float4(hx, hy, hz, hb);
+            }
+          }
+          __syncthreads();
+          const uint32_t tile0 = gb >> 5;
+          // lane per target: 32 consecutive targets per warp
+          for (uint32_t tb = t0 + 32u * warp; tb < t1; tb += 32u * kNWS) {
+            const uint32_t t = tb + lane;
+            const bool act = t < t1;
+            const TgtW& T = TW[act ? t - t0 : 0];
+            const float ax = T.f[0], ay = T.f[1], az = T.f[2];
+            const float lo = act ? T.f[3] : -1.0f, hi = act ? T.f[4] : -1.0f;
+            const uint32_t selff = T.self - gb;  // >= ntile*32 (wraps) when not in this group
+            const uint32_t selfq = selff >> 5, selfbit = 1u << (selff & 31u);
+            uint32_t nsg = act ? tseg[t - t0] : 0u, ncn = act ? tcnt[t - t0] : 0u;
+            uint2* const row = seg + (size_t)(act ? t : 0) * maxs;
+            // the block's bounding box and largest band (box-to-box culling)
+            float blx = act ? ax : INFINITY, bly = act ? ay : INFINITY, blz = act ? az : INFINITY;
+            float bhx = act ? ax : -INFINITY, bhy = act ? ay : -INFINITY, bhz = act ? az : -INFINITY;
+            float bhi = hi;
+#pragma unroll
+            for (int o = 16; o; o >>= 1) {
+              blx = fminf(blx, __shfl_xor_sync(0xffffffffu, blx, o));
+              bly = fminf(bly, __shfl_xor_sync(0xffffffffu, bly, o));
+              blz = fminf(blz, __shfl_xor_sync(0xffffffffu, blz, o));
+              bhx = fmaxf(bhx, __shfl_xor_sync(0xffffffffu, bhx, o));
+              bhy = fmaxf(bhy, __shfl_xor_sync(0xffffffffu, bhy, o));
+              bhz = fmaxf(bhz, __shfl_xor_sync(0xffffffffu, bhz, o));
+              bhi = fmaxf(bhi, __shfl_xor_sync(0xffffffffu, bhi, o));
+            }
+            // Tiles any member can reach.  Box gap per dim in the prefilter's own fp32
+            // expression: rounding is monotone, so the gap never exceeds |c - a| of a
+            // member pair, box d2 <= r2_32, and box d2 >= every hi excludes hits and
+            // ambiguous candidates alike (lists stay exact).
+            uint32_t need[kSearchWords];
+#pragma unroll
+            for (int w = 0; w < kSearchWords; ++w) {
+              const int q = 32 * w + lane;
+              bool nd = false;
+              if (q < ntile) {
+                if constexpr (W2) {
+                  nd = true;
+                } else {
+                  const float4 L = tlo[q], H = thi[q];
+                  const float bx = fmaxf(fmaxf(L.x - bhx, blx - H.x), 0.f);
+                  const float by = fmaxf(fmaxf(L.y - bhy, bly - H.y), 0.f);
+                  const float bz = fmaxf(fmaxf(L.z - bhz, blz - H.z), 0.f);
+                  nd = fmaf(bz, bz, fmaf(by, by, bx * bx)) < fmaxf(bhi, SYM ? H.w : -1.0f);
+                }
+              }
+              need[w] = __ballot_sync(0xffffffffu, nd);
+            }
+#pragma unroll 1
+            for (int w = 0; w < kSearchWords; ++w) {
+              uint32_t nm = need[w];
+              while (nm) {
+                const int q = 32 * w + __ffs(nm) - 1;
+                nm &= nm - 1;
+                const float4* cq = cand + 32 * q;
+                uint32_t in = 0u, near = 0u;
+#pragma unroll
+                for (int k = 0; k < 32; ++k) {
+                  const float4 c = cq[k];
+                  float dx = c.x - ax, dy = c.y - ay, dz = c.z - az;
+                  if constexpr (W2) {
+                    if (st.wrap[0] == 2) dx = wrap1(dx, (float)g.L[0]);
+                    if (st.wrap[1] == 2) dy = wrap1(dy, (float)g.L[1]);
+                    if (st.wrap[2] == 2) dz = wrap1(dz, (float)g.L[2]);
+                  }
+                  const float r = fmaf(dz, dz, fmaf(dy, dy, dx * dx));
+                  float l2 = lo, h2 = hi;
+                  if constexpr (SYM) {  // either side's support
+                    const float2 cb = candb[32 * q + k];
+                    l2 = fmaxf(l2, cb.x);
+                    h2 = fmaxf(h2, cb.y);
+                  }
+                  if (r < l2) in |= 1u << k;
+                  if (r < h2) near |= 1u << k;
+                }
+                if (!act) in = near = 0u;  // SYM: a padding lane must not pick up candidate bands
+                uint32_t amb = near & ~in;
+                if (__any_sync(0xffffffffu, amb != 0u)) {  // rare: exact fp64 test inside the band
+                  while (amb) {
+                    const uint32_t b = __ffs(amb) - 1;
+                    amb &= amb - 1;
+                    const uint32_t f = gb + 32u * q + b;
+                    const int kq = slot_of(S, f);
+                    const uint32_t j = S.t_start[kq] + (f - S.cum[kq]);
+                    double lim = T.lim;
+                    if constexpr (SYM) {
+                      const double thb = 2.0 * h[j];
+                      lim = fmax(lim, __dmul_rn(thb, thb));
+                    }
+                    if (exact_hit(g, x, y, z, j, t, T.pos, lim)) in |= 1u << b;
+                  }
+                }
+                if ((uint32_t)q == selfq) in &= ~selfbit;
+                if (in) {
+                  if (nsg < (uint32_t)maxs) row[nsg] = make_uint2(in, tile0 + (uint32_t)q);
+                  ++nsg;
+                  ncn += __popc(in);
+                }
+              }
+            }
+            if (act) {
+              tseg[t - t0] = nsg;
+              tcnt[t - t0] = ncn;
+            }
+          }
+          __syncthreads();
+        }
+        for (uint32_t t = t0 + threadIdx.x; t < t1; t += blockDim.x) {
+          const uint32_t ns = tseg[t - t0], nc = tcnt[t - t0];
+          nseg[t] = ns;
+          ncount[t] = nc;
+          mxseg = max(mxseg, ns);
+          mxcnt = max(mxcnt, nc);
+        }
+        __syncthreads();
+      }
+    }
+  }
+  // largest segment list / neighbour count of the launch (capacity check, diagnostics)
+  for (int o = 16; o; o >>= 1) {
+    mxseg = max(mxseg, __shfl_xor_sync(0xffffffffu, mxseg, o));
+    mxcnt = max(mxcnt, __shfl_xor_sync(0xffffffffu, mxcnt, o));
+  }
+  if (lane == 0) {
+    if (mxseg) atomicMax(&maxima[0], mxseg);
+    if (mxcnt) atomicMax(&maxima[1], mxcnt);
+  }
+}
+
+static bool any_wrap2_s(const sph_ctx* c) {
+  const Grid& g = c->grid;
+  for (int d = 0; d < 3; ++d)
+    if (g.periodic[d] && 2 * stencil_radius(g, d, reach_of(c->hmax)) + 1 >= g.nc[d]) return true;
+  return false;
+}
+
+int launch_neighbors(sph_ctx* c) {
+  const bool sym = c->phys.sym != 0;
+  const size_t smem = (kSearchCap + 32) * sizeof(float4) + (sym ? (kSearchCap + 32) * sizeof(float2) : 0);
+  auto kern = any_wrap2_s(c) ? (sym ? k_search<true, true> : k_search<true, false>)
+                             : (sym ? k_search<false, true> : k_search<false, false>);
+  cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  cudaMemsetAsync(c->s.work + 0, 0, sizeof(uint32_t), c->stream);
+  const int64_t cells = c->grid.ncell < c->P.n ? c->grid.ncell : c->P.n;
+  // unit records (union stencils + target ranges) for the search and the three passes
+  const int gprep = (int)std::min<int64_t>(std::max<int64_t>(cells, 1), (int64_t)c->num_sms * 8);
+  k_unit_prep<<<gprep, 128, 0, c->stream>>>(c->grid, c->s.cell_list, c->s.unit_list, c->s.nunit_list,
+                                            c->s.cell_start, c->s.cell_end, c->s.cell_hmax, c->s.unit_rec);
+  const int gs = (int)std::min<int64_t>(std::max<int64_t>(cells, 1), (int64_t)c->num_sms * 2);
+  kern<<<gs, kCTS, smem, c->stream>>>(c->P.x, c->P.y, c->P.z, c->P.h, c->grid, c->s.cell_start,
+                                      c->s.cell_end, c->s.unit_rec, c->s.nunit_list, c->s.work + 0,
+                                      c->s.seg, c->s.nseg, c->s.ncount, c->maxs, c->s.nbr_max);
+  return 2;
+}
+
+}  // namespace sphb

@@ -1,9 +1,9 @@
 // sph_internal.cuh -- shared definitions of the CUDA path (sm_100a).
 //
 // Layout in HBM: every per-particle quantity is its own fp64
-// array (SoA) in Morton-cell order; neighbour lists are uint32 rows of fixed
-// stride `maxn` (row-major: the warp that owns a target reads its row with
-// coalesced 128-byte loads); the search grid is a dense table of cell ranges
+// array (SoA) in Morton-cell order; neighbour lists are per-target lists of
+// (32-bit mask, tile) segments over the target's unit stencil, fixed stride `maxs`
+// (pairpass.cuh); the search grid is a dense table of cell ranges
 // [cell_start, cell_end) into the sorted order.
 #pragma once
 
@@ -84,9 +84,10 @@ struct Scratch {
   int4* unit_rec = nullptr;                 // 3 x cap: per unit, its union stencil + target range
   int64_t max_cells = 0;
   // neighbours
-  uint32_t* nbr = nullptr;       // cap * maxn
-  uint32_t* ncount = nullptr;    // cap
-  unsigned int* nbr_maxcount = nullptr;  // device scalar
+  uint2* seg = nullptr;          // cap * maxs neighbour segments (mask, tile)
+  uint32_t* nseg = nullptr;      // cap: segments per target
+  uint32_t* ncount = nullptr;    // cap: neighbours per target
+  unsigned int* nbr_max = nullptr;  // [0] largest segment count, [1] largest neighbour count
   uint32_t* work = nullptr;              // per cell kernel: next cell chunk (reset per launch)
   // per-particle auxiliaries written by density, read by iad / momentum
   double* wB = nullptr;    // B / h^3
@@ -119,7 +120,8 @@ struct sph_ctx {
   sph_params prm;
   cudaStream_t stream = nullptr;
   int64_t cap = 0;
-  int maxn = 512;
+  int maxn = 0;             // user limit on neighbours per particle (0: none)
+  int maxs = 64;            // segment capacity per particle
   sph_particles P{};
   bool attached = false;
   int stage = 0;            // 0 none, 1 neighbours, 2 density, 3 iad, 4 momentum
