@@ -82,7 +82,9 @@ typedef struct {
   double n_target;        /* neighbour target of the h update (300)                */
   double h_min, h_max;    /* h clamp after the update; h_max <= 0: no upper clamp        */
   double u_floor;         /* u clamp after the update                                     */
-  int    max_neighbors;   /* limit on neighbours per particle (0: none); more -> SPH_ERR_CAPACITY */
+  int    max_neighbors;   /* hard limit on neighbours per particle: more -> SPH_ERR_CAPACITY.  */
+                          /* 0: no limit -- the library sizes the rows (384 entries, grown */
+                          /* on demand; never truncated, R23)                              */
   double cell_factor;     /* search-cell edge = cell_factor * 2 * mean(h) (0: 1.0)        */
   double box_lo[3], box_hi[3]; /* periodic dims: the period is box_hi - box_lo            */
   int    periodic[3];     /* square patch: {0,0,1}                               */
@@ -98,10 +100,6 @@ typedef struct {
                           /* every k-th step only (the top tree changes slowly;    */
                           /* SURVEY 8(f) NEXT-3); migration still runs every step against */
                           /* the kept splitters.  0 or 1: every step.  Ignored on 1 GPU.  */
-  int    max_segments;    /* neighbour-list capacity per particle in (mask, tile) segments   */
-                          /* of 32 staged candidates (0: 64 = 512 bytes; a square-patch     */
-                          /* particle uses ~30); overflow -> SPH_ERR_CAPACITY, never        */
-                          /* truncation (R23)                                               */
 } sph_params;
 
 typedef struct {          /* caller-owned DEVICE buffers, each >= capacity elements       */

@@ -4,17 +4,22 @@
 //
 // A CTA owns a unit of 2x2x1 search cells (~290 targets at the paper's 300
 // neighbours), stages the source particles of the unit's union stencil into shared
-// memory in groups with coalesced loads (density, IAD) or TMA bulk copies of
+// memory in groups -- coalesced loads (density, IAD) or TMA bulk copies of
 // per-particle records (momentum); periodic images are shifted at staging time, so
-// no pair needs a minimum image.  A warp (density, IAD) or half-warp (momentum) per
-// target expands the target's neighbour SEGMENTS of the current group (tile +
-// 32-bit mask, pairpass.cuh) into staging indices in a small per-warp buffer -- one
-// lane per segment -- and runs the pair body over them.  The segment list of the
-// next target is loaded while the current one runs (one coalesced 8-byte load per
-// lane), so no pair step waits on a global load.
+// no pair needs a minimum image -- and a warp (density, IAD) or half-warp
+// (momentum) per target walks the target's neighbour row, lanes striding over
+// entries.  Row entries are flat staging indices of the unit stencil (16-bit unless
+// a unit stencil exceeds 65,535 particles): the shared-memory index of a neighbour
+// is entry - (group start), and "entry < group end" selects a target's segment of
+// the group.  Row chunks are prefetched ahead, across target boundaries.
 #include "pairpass.cuh"
 
 namespace sphb {
+
+__device__ __forceinline__ int qidx(const uint32_t* cum, uint32_t gb, uint32_t e) {
+  (void)cum;
+  return (int)(e - gb);  // row entries are flat staging indices of the unit stencil
+}
 
 __constant__ double c_poly[kPolyTerms];   // sinc(pi sqrt(t)/2) = sum c_poly[k] t^k
 __constant__ double c_dpoly[kPolyTerms];  // derivative in t
@@ -85,6 +90,208 @@ __device__ __forceinline__ double kern_S(double t, int n, const double* __restri
   }
 }
 
+// Warp-level walk over the entries of target rows that fall in the current
+// group [.., pend).  Targets are handed out dynamically (shared counter, reset by
+// the group loop) so warps reach the group barrier together.  Row chunks (32
+// entries) stream through a 3-deep register ring (ncu: with one chunk of
+// prefetch the row load was the top stall), and the first three chunks of the
+// warp's next target are issued before the current target's work.
+template <typename E>
+__device__ __forceinline__ uint32_t row_chunk(const E* row, uint32_t pos, uint32_t n) {
+  return pos < n ? (uint32_t)row[pos] : kSent;
+}
+
+template <int NW, typename E, class Body, class Finish>
+__device__ __forceinline__ void walk_targets(uint32_t t0, uint32_t t1, const E* __restrict__ nbr,
+                                             int maxn, const uint32_t* s_n, uint32_t* s_cur,
+                                             uint32_t pend, const uint32_t* cum, uint32_t gb,
+                                             uint32_t* s_next, Body&& body, Finish&& finish) {
+  const int lane = threadIdx.x & 31;
+  uint32_t t = 0;
+  if (lane == 0) t = t0 + atomicAdd(s_next, 1u);
+  t = __shfl_sync(0xffffffffu, t, 0);
+  uint32_t f0 = kSent, f1 = kSent, f2 = kSent;
+  if (t < t1) {
+    const uint32_t c0 = s_cur[t - t0] + lane, nn = s_n[t - t0];
+    const E* r = nbr + (size_t)t * maxn;
+    f0 = row_chunk(r, c0, nn);
+    f1 = row_chunk(r, c0 + 32, nn);
+    f2 = row_chunk(r, c0 + 64, nn);
+  }
+  while (t < t1) {
+    const uint32_t i = t - t0;
+    const uint32_t n = s_n[i];
+    const E* row = nbr + (size_t)t * maxn;
+    uint32_t cur = s_cur[i];
+    uint32_t e0 = f0, e1 = f1, e2 = f2;
+    // claim the next target and prefetch its first three chunks
+    uint32_t tn = 0;
+    if (lane == 0) tn = t0 + atomicAdd(s_next, 1u);
+    tn = __shfl_sync(0xffffffffu, tn, 0);
+    if (tn < t1) {
+      const uint32_t cn = s_cur[tn - t0] + lane, nn = s_n[tn - t0];
+      const E* r = nbr + (size_t)tn * maxn;
+      f0 = row_chunk(r, cn, nn);
+      f1 = row_chunk(r, cn + 32, nn);
+      f2 = row_chunk(r, cn + 64, nn);
+    }
+    body.begin(i);
+    for (;;) {
+      const bool in = e0 < pend;
+      const unsigned b = __ballot_sync(0xffffffffu, in);
+      const int m = __popc(b);
+      const uint32_t e3 = m == 32 ? row_chunk(row, cur + 96 + lane, n) : kSent;
+      if (in) body(qidx(cum, gb, e0));
+      cur += m;
+      if (m < 32) break;
+      e0 = e1;
+      e1 = e2;
+      e2 = e3;
+    }
+    finish(i, cur);
+    t = tn;
+  }
+}
+
+// Same walk with 16 lanes per target (two targets per warp, one per half-warp):
+// the per-(target, group) setup and reduction is shared by two targets and the
+// unused lanes at the end of a segment drop from up to 31 to up to 15.  Both
+// halves step together; a half whose segment ended idles until the other is done.
+// Row chunks stream through a 2-deep ring consumed in place (unrolled by two): a
+// shifted ring (e0 = e1; e1 = e2 <- load) made every step wait for the load it had
+// just issued (ncu: long_sb on the ring move), and a momentum step is long enough
+// that two chunks of prefetch cover the load latency.
+template <typename E, class Body, class Finish>
+__device__ __forceinline__ void walk_targets_half(uint32_t t0, uint32_t t1,
+                                                  const E* __restrict__ nbr, int maxn,
+                                                  const uint32_t* s_n, uint32_t* s_cur,
+                                                  uint32_t pend, const uint32_t* cum, uint32_t gb,
+                                                  uint32_t* s_next, Body&& body, Finish&& finish) {
+  (void)cum;
+  const int lane = threadIdx.x & 31, l16 = lane & 15;
+  const unsigned hmask = (threadIdx.x & 16) ? 0xffff0000u : 0x0000ffffu;
+  auto claim = [&]() {
+    uint32_t v = 0;
+    if (l16 == 0) v = t0 + atomicAdd(s_next, 1u);
+    return __shfl_sync(0xffffffffu, v, lane & 16);
+  };
+  uint32_t t = claim();
+  uint32_t f0 = kSent, f1 = kSent;
+  if (t < t1) {
+    const uint32_t c0 = s_cur[t - t0] + l16, nn = s_n[t - t0];
+    const E* r = nbr + (size_t)t * maxn;
+    f0 = row_chunk(r, c0, nn);
+    f1 = row_chunk(r, c0 + 16, nn);
+  }
+  while (__any_sync(0xffffffffu, t < t1)) {
+    const bool act = t < t1;
+    const uint32_t i = act ? t - t0 : 0;
+    const uint32_t n = act ? s_n[i] : 0;
+    uint32_t cur = act ? s_cur[i] : 0;
+    uint32_t off = cur + l16 + 32;  // row position of the next chunk to load (two ahead)
+    const E* rp = nbr + (size_t)(act ? t : 0) * maxn + off;
+    uint32_t e0 = f0, e1 = f1;
+    const uint32_t tn = claim();
+    f0 = f1 = kSent;
+    if (tn < t1) {
+      const uint32_t cn = s_cur[tn - t0] + l16, nn = s_n[tn - t0];
+      const E* r = nbr + (size_t)tn * maxn;
+      f0 = row_chunk(r, cn, nn);
+      f1 = row_chunk(r, cn + 16, nn);
+    }
+    if (act) body.begin(i);
+    bool live = act;
+#define SPH_HALF_STEP(R)                                                       \
+  {                                                                            \
+    const uint32_t e = R;                                                      \
+    const bool in = live && e < pend;                                          \
+    const int m = __popc(__ballot_sync(0xffffffffu, in) & hmask);              \
+    const bool more = live && m == 16;                                         \
+    const int qi = (int)(e - gb);                                              \
+    R = (more && off < n) ? (uint32_t)*rp : kSent;                                       \
+    rp += 16;                                                                  \
+    off += 16;                                                                 \
+    if (in) body(qi);                                                          \
+    cur += m;                                                                  \
+    live = more;                                                               \
+    if (!__any_sync(0xffffffffu, live)) break;                                 \
+  }
+    for (;;) {
+      SPH_HALF_STEP(e0)
+      SPH_HALF_STEP(e1)
+    }
+#undef SPH_HALF_STEP
+    finish(act, i, cur);
+    t = tn;
+  }
+}
+
+// Lean full-warp walk (density, IAD): the ring of three row chunks is consumed in
+// place -- each step refills the register it just used with the chunk three steps
+// ahead (a shifted ring makes every move wait for the latest load) -- through a
+// running row pointer, and the body runs on every lane with a validity flag instead
+// of a divergent branch (ncu: per-step bookkeeping was as large as the pair math).
+template <typename E, class Body, class Finish>
+__device__ __forceinline__ void walk_targets_fast(uint32_t t0, uint32_t t1,
+                                                  const E* __restrict__ nbr, int maxn,
+                                                  const uint32_t* s_n, const uint32_t* s_cur,
+                                                  uint32_t pend, const uint32_t* cum, uint32_t gb,
+                                                  uint32_t* s_next, Body&& body, Finish&& finish) {
+  const uint32_t lane = threadIdx.x & 31;
+  auto claim = [&]() {
+    uint32_t v = 0;
+    if (lane == 0) v = t0 + atomicAdd(s_next, 1u);
+    return __shfl_sync(0xffffffffu, v, 0);
+  };
+  uint32_t t = claim();
+  uint32_t f0 = kSent, f1 = kSent, f2 = kSent;
+  if (t < t1) {
+    const uint32_t c0 = s_cur[t - t0] + lane, nn = s_n[t - t0];
+    const E* r = nbr + (size_t)t * maxn;
+    f0 = row_chunk(r, c0, nn);
+    f1 = row_chunk(r, c0 + 32, nn);
+    f2 = row_chunk(r, c0 + 64, nn);
+  }
+  while (t < t1) {
+    const uint32_t i = t - t0, n = s_n[i];
+    uint32_t cur = s_cur[i];
+    const uint32_t lim = n - cur;  // valid positions: offset < lim from cur
+    const E* rp = nbr + (size_t)t * maxn + cur + lane + 96;
+    uint32_t off = lane + 96;
+    uint32_t e0 = f0, e1 = f1, e2 = f2;
+    const uint32_t tn = claim();
+    if (tn < t1) {  // the next target's first three chunks
+      const uint32_t cn = s_cur[tn - t0] + lane, nn = s_n[tn - t0];
+      const E* r = nbr + (size_t)tn * maxn;
+      f0 = row_chunk(r, cn, nn);
+      f1 = row_chunk(r, cn + 32, nn);
+      f2 = row_chunk(r, cn + 64, nn);
+    }
+    body.begin(i);
+#define SPH_FAST_STEP(R)                                                             \
+  {                                                                                  \
+    const uint32_t e = R;                                                            \
+    const bool in = e < pend;                                                        \
+    const int m = __popc(__ballot_sync(0xffffffffu, in));                            \
+    const int qi = in ? (int)(e - gb) : 0; /* e dies here: the refill can reuse R */ \
+    R = (m == 32 && off < lim) ? (uint32_t)*rp : kSent;                                        \
+    rp += 32;                                                                        \
+    off += 32;                                                                       \
+    body(qi, in);                                                                    \
+    cur += m;                                                                        \
+    if (m < 32) break;                                                               \
+  }
+    for (;;) {
+      SPH_FAST_STEP(e0)
+      SPH_FAST_STEP(e1)
+      SPH_FAST_STEP(e2)
+    }
+#undef SPH_FAST_STEP
+    finish(i, cur);
+    t = tn;
+  }
+}
+
 // stage (x, y) and (z, f) of the current group as double2 pairs: one 16-byte LDS
 // per pair of fields, bank conflicts only within 8-lane quarters (ncu: the
 // 8-byte SoA layout cost ~3x the ideal shared-memory wavefronts)
@@ -114,98 +321,6 @@ __device__ __forceinline__ void delta3(const Stencil& st, const Grid& g, double&
   }
 }
 
-// Full-warp walk over the targets [t0, t1) of a sub-block for the staging group
-// [gb, ge) (tiles < tend): targets handed out by a shared counter so warps reach the
-// group barrier together; each target's segments of the group are expanded into the
-// warp's buffer and consumed 32 entries per step; the body runs on every lane with a
-// validity flag (ok == false: padding lane, its terms are discarded by selects).
-template <class Body, class Finish>
-__device__ __forceinline__ void walk_seg_warp(uint32_t t0, uint32_t t1, const uint2* __restrict__ seg,
-                                              int maxs, const uint32_t* s_n, const uint32_t* s_cur,
-                                              uint32_t tend, uint32_t gb, uint32_t* s_next,
-                                              uint16_t* buf, Body&& body, Finish&& finish) {
-  const uint32_t lane = threadIdx.x & 31;
-  const uint2 none = make_uint2(0u, 0xffffffffu);
-  auto claim = [&]() {
-    uint32_t v = 0;
-    if (lane == 0) v = t0 + atomicAdd(s_next, 1u);
-    return __shfl_sync(0xffffffffu, v, 0);
-  };
-  uint32_t t = claim();
-  uint2 f = t < t1 ? seg_load(seg, t, maxs, s_cur[t - t0] + lane, s_n[t - t0]) : none;
-  while (t < t1) {
-    const uint32_t i = t - t0, n = s_n[i];
-    uint32_t cur = s_cur[i];
-    uint2 sg = f;
-    const uint32_t tn = claim();  // the next target's first segment chunk lands meanwhile
-    f = tn < t1 ? seg_load(seg, tn, maxs, s_cur[tn - t0] + lane, s_n[tn - t0]) : none;
-    body.begin(i);
-    for (;;) {
-      uint32_t nfit, nval;
-      const uint32_t tot = expand_segments<32, kBufD>(sg, tend, gb, buf, &nfit, &nval);
-      for (uint32_t p0 = 0; p0 < tot; p0 += 32) {
-        const uint32_t p = p0 + lane;
-        const bool ok = p < tot;
-        body(ok ? (int)buf[p] : 0, ok);
-      }
-      __syncwarp();
-      cur += nfit;
-      if ((nfit == nval && nval < 32) || cur >= n) break;
-      sg = seg_load(seg, t, maxs, cur + lane, n);  // > 32 segments in the group, or a full buffer
-    }
-    finish(i, cur);
-    t = tn;
-  }
-}
-
-// Half-warp walk (momentum): two targets per warp, one per 16-lane half, in lockstep;
-// a half whose target is done idles until the other is.  Fewer idle lanes at the end
-// of a target's group segment (up to 15 instead of 31), and the per-target set-up and
-// reduction is shared by two targets.
-template <class Body, class Finish>
-__device__ __forceinline__ void walk_seg_half(uint32_t t0, uint32_t t1, const uint2* __restrict__ seg,
-                                              int maxs, const uint32_t* s_n, const uint32_t* s_cur,
-                                              uint32_t tend, uint32_t gb, uint32_t* s_next,
-                                              uint16_t* buf2, Body&& body, Finish&& finish) {
-  const uint32_t lane = threadIdx.x & 31, l16 = lane & 15;
-  uint16_t* const buf = buf2 + (lane >> 4) * kBufM;
-  const uint2 none = make_uint2(0u, 0xffffffffu);
-  auto claim = [&]() {
-    uint32_t v = 0;
-    if (l16 == 0) v = t0 + atomicAdd(s_next, 1u);
-    return __shfl_sync(0xffffffffu, v, lane & 16);
-  };
-  uint32_t t = claim();
-  uint2 f = t < t1 ? seg_load(seg, t, maxs, s_cur[t - t0] + l16, s_n[t - t0]) : none;
-  while (__any_sync(0xffffffffu, t < t1)) {
-    const bool act = t < t1;
-    const uint32_t i = act ? t - t0 : 0;
-    const uint32_t n = act ? s_n[i] : 0;
-    uint32_t cur = act ? s_cur[i] : 0;
-    uint2 sg = f;
-    const uint32_t tn = claim();
-    f = tn < t1 ? seg_load(seg, tn, maxs, s_cur[tn - t0] + l16, s_n[tn - t0]) : none;
-    if (act) body.begin(i);
-    bool more = act;
-    while (__any_sync(0xffffffffu, more)) {
-      uint32_t nfit, nval;
-      const uint32_t tot = expand_segments<16, kBufM>(more ? sg : none, tend, gb, buf, &nfit, &nval);
-      for (uint32_t p0 = 0; __any_sync(0xffffffffu, p0 < tot); p0 += 16) {
-        const uint32_t p = p0 + l16;
-        if (p < tot) body((int)buf[p]);
-      }
-      __syncwarp();
-      if (more) {
-        cur += nfit;
-        if ((nfit == nval && nval < 16) || cur >= n) more = false;
-        else sg = seg_load(seg, t, maxs, cur + l16, n);
-      }
-    }
-    finish(act, i, cur);
-    t = tn;
-  }
-}
-
 // ------------------------------------------------------------------ a6 density + Omega + EOS
 struct DensBody {
   const double2 *s01, *s23;
@@ -223,14 +338,14 @@ struct DensBody {
   }
 };
 
-template <int N, bool W2, int KM>
+template <int N, bool W2, int KM, typename E>
 __global__ void __launch_bounds__(kCTD, 1) k_density_c(
     const double* __restrict__ x, const double* __restrict__ y, const double* __restrict__ z,
     const double* __restrict__ h, const double* __restrict__ m, const double* __restrict__ u,
     Grid g, const uint32_t* __restrict__ cstart, const uint32_t* __restrict__ cend,
     const unsigned long long* __restrict__ chmax, const uint32_t* __restrict__ clist,
-    const uint32_t* __restrict__ nclist, const int4* __restrict__ urec, const uint32_t* __restrict__ nulist, uint32_t* __restrict__ work, const uint2* __restrict__ seg,
-    const uint32_t* __restrict__ nseg, int maxs, Phys ph, double* __restrict__ rho,
+    const uint32_t* __restrict__ nclist, const int4* __restrict__ urec, const uint32_t* __restrict__ nulist, uint32_t* __restrict__ work, const E* __restrict__ nbr,
+    const uint32_t* __restrict__ ncount, int maxn, Phys ph, double* __restrict__ rho,
     double* __restrict__ omega, double* __restrict__ p, double* __restrict__ cs,
     double* __restrict__ wB, double* __restrict__ ih2, double* __restrict__ vol,
     double* __restrict__ rinv, double* __restrict__ X, double* __restrict__ mX,
@@ -238,11 +353,10 @@ __global__ void __launch_bounds__(kCTD, 1) k_density_c(
   extern __shared__ double dsm[];
   double2* s01 = reinterpret_cast<double2*>(dsm);
   double2* s23 = s01 + kDensCap;
-  uint16_t* const ebuf = reinterpret_cast<uint16_t*>(s23 + kDensCap);  // expanded entries, kBufD per warp
   __shared__ CellSm S;
   __shared__ uint32_t s_n[kTgtU], s_cur[kTgtU];
   __shared__ double tx[kTgtU], ty[kTgtU], tz[kTgtU], tih2[kTgtU], acc0[kTgtU], acc1[kTgtU];
-  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int lane = threadIdx.x & 31;
   __shared__ uint32_t s_chunk;
   const int n = N > 0 ? N : ph.n;
   // cells in chunks of kCellChunk consecutive (Morton-order) cells claimed from a
@@ -259,7 +373,7 @@ __global__ void __launch_bounds__(kCTD, 1) k_density_c(
         const uint32_t t1 = min(S.ec, t0 + kTgtU);
         for (uint32_t t = t0 + threadIdx.x; t < t1; t += blockDim.x) {
           const uint32_t i = t - t0;
-          s_n[i] = nseg[t];
+          s_n[i] = ncount[t];
           s_cur[i] = 0;
           tx[i] = x[t];
           ty[i] = y[t];
@@ -272,7 +386,7 @@ __global__ void __launch_bounds__(kCTD, 1) k_density_c(
         if (threadIdx.x == 0) S.next[0] = 0;
         __syncthreads();
         for (uint32_t gb = 0, gi = 0; gb < S.total; gb += kDensCap, ++gi) {
-          const uint32_t ge = min(S.total, gb + kDensCap);
+          const uint32_t ge = min(S.total, gb + kDensCap), pend = ge;
           if (threadIdx.x == 0) S.next[(gi + 1) & 1] = 0;
           stage2x2(g, S, gb, ge, x, y, z, m, s01, s23);
           __syncthreads();
@@ -308,7 +422,7 @@ __global__ void __launch_bounds__(kCTD, 1) k_density_c(
           body.tx = tx; body.ty = ty; body.tz = tz; body.tih2 = tih2;
           body.st = &st; body.g = &g; body.n = n; body.K = ph.tableK; body.tab = ph.table;
           body.sym = ph.sym;
-          walk_seg_warp(t0, t1, seg, maxs, s_n, s_cur, (ge + 31) >> 5, gb, &S.next[gi & 1], ebuf + warp * kBufD, body,
+          walk_targets_fast(t0, t1, nbr, maxn, s_n, s_cur, pend, S.cum, gb, &S.next[gi & 1], body,
                             [&](uint32_t i, uint32_t c2) {
                               double v[2] = {body.sr, body.sd};
                               warp_multi_sum<2>(v);
@@ -360,13 +474,13 @@ __global__ void __launch_bounds__(kCTD, 1) k_density_c(
 }
 
 // ------------------------------------------------------------------ a8 IAD
-template <int N, bool W2, int KM>
+template <int N, bool W2, int KM, typename E>
 __global__ void __launch_bounds__(kCTD, 1) k_iad_c(
     const double* __restrict__ x, const double* __restrict__ y, const double* __restrict__ z,
     Grid g, const uint32_t* __restrict__ cstart, const uint32_t* __restrict__ cend,
     const unsigned long long* __restrict__ chmax, const uint32_t* __restrict__ clist,
-    const uint32_t* __restrict__ nclist, const int4* __restrict__ urec, const uint32_t* __restrict__ nulist, uint32_t* __restrict__ work, const uint2* __restrict__ seg,
-    const uint32_t* __restrict__ nseg, int maxs, Phys ph, const double* __restrict__ wB,
+    const uint32_t* __restrict__ nclist, const int4* __restrict__ urec, const uint32_t* __restrict__ nulist, uint32_t* __restrict__ work, const E* __restrict__ nbr,
+    const uint32_t* __restrict__ ncount, int maxn, Phys ph, const double* __restrict__ wB,
     const double* __restrict__ ih2, const double* __restrict__ vol, double* __restrict__ c11,
     double* __restrict__ c12, double* __restrict__ c13, double* __restrict__ c22,
     double* __restrict__ c23, double* __restrict__ c33, double* __restrict__ ct,
@@ -374,12 +488,11 @@ __global__ void __launch_bounds__(kCTD, 1) k_iad_c(
   extern __shared__ double dsm[];
   double2* s01 = reinterpret_cast<double2*>(dsm);
   double2* s23 = s01 + kIadCap;
-  uint16_t* const ebuf = reinterpret_cast<uint16_t*>(s23 + kIadCap);  // expanded entries, kBufD per warp
   __shared__ CellSm S;
   __shared__ uint32_t s_n[kTgtU], s_cur[kTgtU];
   __shared__ double tx[kTgtU], ty[kTgtU], tz[kTgtU], tih2[kTgtU];
   __shared__ double acc[6][kTgtU];
-  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int lane = threadIdx.x & 31;
   __shared__ uint32_t s_chunk;
   const int n = N > 0 ? N : ph.n;
   // cells in chunks of kCellChunk consecutive (Morton-order) cells claimed from a
@@ -396,7 +509,7 @@ __global__ void __launch_bounds__(kCTD, 1) k_iad_c(
         const uint32_t t1 = min(S.ec, t0 + kTgtU);
         for (uint32_t t = t0 + threadIdx.x; t < t1; t += blockDim.x) {
           const uint32_t i = t - t0;
-          s_n[i] = nseg[t];
+          s_n[i] = ncount[t];
           s_cur[i] = 0;
           tx[i] = x[t];
           ty[i] = y[t];
@@ -407,7 +520,7 @@ __global__ void __launch_bounds__(kCTD, 1) k_iad_c(
         if (threadIdx.x == 0) S.next[0] = 0;
         __syncthreads();
         for (uint32_t gb = 0, gi = 0; gb < S.total; gb += kIadCap, ++gi) {
-          const uint32_t ge = min(S.total, gb + kIadCap);
+          const uint32_t ge = min(S.total, gb + kIadCap), pend = ge;
           if (threadIdx.x == 0) S.next[(gi + 1) & 1] = 0;
           stage2x2(g, S, gb, ge, x, y, z, vol, s01, s23);
           __syncthreads();
@@ -447,7 +560,7 @@ __global__ void __launch_bounds__(kCTD, 1) k_iad_c(
           body.tx = tx; body.ty = ty; body.tz = tz; body.tih2 = tih2;
           body.st = &st; body.g = &g; body.n = n; body.K = ph.tableK; body.tab = ph.table;
           body.sym = ph.sym;
-          walk_seg_warp(t0, t1, seg, maxs, s_n, s_cur, (ge + 31) >> 5, gb, &S.next[gi & 1], ebuf + warp * kBufD, body,
+          walk_targets_fast(t0, t1, nbr, maxn, s_n, s_cur, pend, S.cum, gb, &S.next[gi & 1], body,
                             [&](uint32_t i, uint32_t c2) {
                               double v[8] = {body.t11, body.t12, body.t13, body.t22,
                                              body.t23, body.t33, 0.0, 0.0};
@@ -572,13 +685,13 @@ __global__ void __launch_bounds__(kRecThreads) k_mom_records(MomSrc src, int64_t
 // per-target smem fields
 enum { T_X, T_Y, T_Z, T_VX, T_VY, T_VZ, T_IH2, T_WB, T_RINV, T_XP, T_C, T_A11, T_A12, T_A13, T_A22, T_A23, T_A33, T_N };
 
-template <int N, bool W2, int KM>
+template <int N, bool W2, int KM, typename E>
 __global__ void __launch_bounds__(kCTM, 1) k_momentum_c(
     MomSrc src, MomTgt tg, MomOut out, Grid g, const uint32_t* __restrict__ cstart,
     const uint32_t* __restrict__ cend, const unsigned long long* __restrict__ chmax,
     const uint32_t* __restrict__ clist, const uint32_t* __restrict__ nclist,
     const int4* __restrict__ urec, const uint32_t* __restrict__ nulist, uint32_t* __restrict__ work,
-    const uint2* __restrict__ seg, const uint32_t* __restrict__ nseg, int maxs, Phys ph,
+    const E* __restrict__ nbr, const uint32_t* __restrict__ ncount, int maxn, Phys ph,
     double* __restrict__ dts, unsigned long long* __restrict__ cnt, const double2* __restrict__ mrec) {
   extern __shared__ double dsm[];  // kMomCap staged source records + T_N * kTgtU target fields
   double2* const F2 = reinterpret_cast<double2*>(dsm);
@@ -588,7 +701,6 @@ __global__ void __launch_bounds__(kCTM, 1) k_momentum_c(
   __shared__ double acc[5][kTgtU];
   __shared__ double shdt[kNWM];
   __shared__ unsigned long long shco;
-  __shared__ uint16_t ebuf[kNWM][2 * kBufM];  // expanded neighbour entries, per half-warp
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   __shared__ uint32_t s_chunk;
   const int n = N > 0 ? N : ph.n;
@@ -613,7 +725,7 @@ __global__ void __launch_bounds__(kCTM, 1) k_momentum_c(
         const uint32_t t1 = min(S.ec, t0 + kTgtU);
         for (uint32_t t = t0 + threadIdx.x; t < t1; t += blockDim.x) {
           const uint32_t i = t - t0;
-          s_n[i] = nseg[t];
+          s_n[i] = ncount[t];
           s_cur[i] = 0;
           T[T_X * kTgtU + i] = src.x[t];
           T[T_Y * kTgtU + i] = src.y[t];
@@ -641,7 +753,7 @@ __global__ void __launch_bounds__(kCTM, 1) k_momentum_c(
         if (threadIdx.x == 0) S.next[0] = 0;
         __syncthreads();
         for (uint32_t gb = 0, gi = 0; gb < S.total; gb += kMomCap, ++gi) {
-          const uint32_t ge = min(S.total, gb + kMomCap);
+          const uint32_t ge = min(S.total, gb + kMomCap), pend = ge;
           if (threadIdx.x == 0) S.next[(gi + 1) & 1] = 0;
           // stage [gb, ge): warp 0 issues one bulk copy of consecutive records per slot
           // (the slot's cell is a contiguous range), all complete on one mbarrier
@@ -754,7 +866,7 @@ __global__ void __launch_bounds__(kCTM, 1) k_momentum_c(
           body.F2 = F2; body.T = T; body.st = &st; body.g = &g; body.alpha = ph.alpha; body.n = n;
           body.K = ph.tableK; body.tab = ph.table; body.sym = ph.sym;
           body.ncoinc = &ncoinc;
-          walk_seg_half(t0, t1, seg, maxs, s_n, s_cur, (ge + 31) >> 5, gb, &S.next[gi & 1], ebuf[warp], body,
+          walk_targets_half(t0, t1, nbr, maxn, s_n, s_cur, pend, S.cum, gb, &S.next[gi & 1], body,
                             [&](bool act, uint32_t i, uint32_t c2) {
                               double v[4] = {body.fx, body.fy, body.fz, body.fu};
                               half_multi_sum<4>(v);
@@ -823,36 +935,41 @@ static void set_smem(K kern, size_t bytes) {
   cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes);
 }
 
-template <int N, bool W2, int KM>
+template <int N, bool W2, int KM, typename E>
 static void density_t(sph_ctx* c) {
-  const size_t smem = 4 * kDensCap * sizeof(double) + kNWD * kBufD * sizeof(uint16_t);
-  set_smem(k_density_c<N, W2, KM>, smem);
+  const size_t smem = 4 * kDensCap * sizeof(double);
+  set_smem(k_density_c<N, W2, KM, E>, smem);
   sph_particles& P = c->P;
   cudaMemsetAsync(c->s.work + 1, 0, sizeof(uint32_t), c->stream);
-  k_density_c<N, W2, KM><<<cell_grid(c, 1), kCTD, smem, c->stream>>>(
+  k_density_c<N, W2, KM, E><<<cell_grid(c, 1), kCTD, smem, c->stream>>>(
       P.x, P.y, P.z, P.h, P.m, P.u, c->grid, c->s.cell_start, c->s.cell_end, c->s.cell_hmax,
-      c->s.cell_list, c->s.ncell_list, c->s.unit_rec, c->s.nunit_list, c->s.work + 1, c->s.seg, c->s.nseg, c->maxs, c->phys, P.rho, P.omega,
+      c->s.cell_list, c->s.ncell_list, c->s.unit_rec, c->s.nunit_list, c->s.work + 1, reinterpret_cast<const E*>(c->s.nbr), c->s.ncount, c->maxn_cap, c->phys, P.rho, P.omega,
       P.p, P.c, c->s.wB, c->s.ih2, c->s.vol, c->s.rinv, c->s.X, c->s.mX, c->s.cnt);
 }
 
-// kernel-mode x exponent x wrap dispatch of a pair pass
-#define SPH_DISPATCH(fn)                                                              \
+// row type x kernel-mode x exponent x wrap dispatch of a pair pass
+#define SPH_DISPATCH_E(fn, E)                                                         \
   do {                                                                                \
     const bool w2 = any_wrap2(c);                                                     \
     const bool n6 = c->phys.n == 6;                                                   \
     switch (c->phys.kmode) {                                                          \
       case SPH_KERNEL_TABLE:                                                          \
-        n6 ? (w2 ? fn<6, true, 1>(c) : fn<6, false, 1>(c))                            \
-           : (w2 ? fn<0, true, 1>(c) : fn<0, false, 1>(c));                           \
+        n6 ? (w2 ? fn<6, true, 1, E>(c) : fn<6, false, 1, E>(c))                      \
+           : (w2 ? fn<0, true, 1, E>(c) : fn<0, false, 1, E>(c));                     \
         break;                                                                        \
       case SPH_KERNEL_SIN:                                                            \
-        n6 ? (w2 ? fn<6, true, 2>(c) : fn<6, false, 2>(c))                            \
-           : (w2 ? fn<0, true, 2>(c) : fn<0, false, 2>(c));                           \
+        n6 ? (w2 ? fn<6, true, 2, E>(c) : fn<6, false, 2, E>(c))                      \
+           : (w2 ? fn<0, true, 2, E>(c) : fn<0, false, 2, E>(c));                     \
         break;                                                                        \
       default:                                                                        \
-        n6 ? (w2 ? fn<6, true, 0>(c) : fn<6, false, 0>(c))                            \
-           : (w2 ? fn<0, true, 0>(c) : fn<0, false, 0>(c));                           \
+        n6 ? (w2 ? fn<6, true, 0, E>(c) : fn<6, false, 0, E>(c))                      \
+           : (w2 ? fn<0, true, 0, E>(c) : fn<0, false, 0, E>(c));                     \
     }                                                                                 \
+  } while (0)
+#define SPH_DISPATCH(fn)                                                              \
+  do {                                                                                \
+    if (c->wide_rows) SPH_DISPATCH_E(fn, uint32_t);                                   \
+    else SPH_DISPATCH_E(fn, uint16_t);                                                \
   } while (0)
 
 int launch_density(sph_ctx* c) {
@@ -860,15 +977,15 @@ int launch_density(sph_ctx* c) {
   return 1;
 }
 
-template <int N, bool W2, int KM>
+template <int N, bool W2, int KM, typename E>
 static void iad_t(sph_ctx* c) {
-  const size_t smem = 4 * kIadCap * sizeof(double) + kNWD * kBufD * sizeof(uint16_t);
-  set_smem(k_iad_c<N, W2, KM>, smem);
+  const size_t smem = 4 * kIadCap * sizeof(double);
+  set_smem(k_iad_c<N, W2, KM, E>, smem);
   sph_particles& P = c->P;
   cudaMemsetAsync(c->s.work + 2, 0, sizeof(uint32_t), c->stream);
-  k_iad_c<N, W2, KM><<<cell_grid(c, 1), kCTD, smem, c->stream>>>(
+  k_iad_c<N, W2, KM, E><<<cell_grid(c, 1), kCTD, smem, c->stream>>>(
       P.x, P.y, P.z, c->grid, c->s.cell_start, c->s.cell_end, c->s.cell_hmax, c->s.cell_list,
-      c->s.ncell_list, c->s.unit_rec, c->s.nunit_list, c->s.work + 2, c->s.seg, c->s.nseg, c->maxs, c->phys, c->s.wB, c->s.ih2, c->s.vol,
+      c->s.ncell_list, c->s.unit_rec, c->s.nunit_list, c->s.work + 2, reinterpret_cast<const E*>(c->s.nbr), c->s.ncount, c->maxn_cap, c->phys, c->s.wB, c->s.ih2, c->s.vol,
       P.c11, P.c12, P.c13, P.c22, P.c23, P.c33, c->s.ct, c->cap, c->s.cnt);
 }
 
@@ -877,18 +994,18 @@ int launch_iad(sph_ctx* c) {
   return 1;
 }
 
-template <int N, bool W2, int KM>
+template <int N, bool W2, int KM, typename E>
 static void momentum_t(sph_ctx* c) {
   const size_t smem = ((size_t)2 * kMomPairs * kMomCap + (size_t)T_N * kTgtU) * sizeof(double);
-  set_smem(k_momentum_c<N, W2, KM>, smem);
+  set_smem(k_momentum_c<N, W2, KM, E>, smem);
   sph_particles& P = c->P;
   MomSrc src = {P.x, P.y, P.z, P.vx, P.vy, P.vz, P.m, c->s.ih2, P.c, c->s.mX, c->s.vol, c->s.ct, c->cap};
   MomTgt tg = {P.h, c->s.wB, c->s.rinv, c->s.X, P.c11, P.c12, P.c13, P.c22, P.c23, P.c33};
   MomOut out = {P.ax, P.ay, P.az, P.du, P.vsig};
   cudaMemsetAsync(c->s.work + 3, 0, sizeof(uint32_t), c->stream);
-  k_momentum_c<N, W2, KM><<<cell_grid(c, 1), kCTM, smem, c->stream>>>(
+  k_momentum_c<N, W2, KM, E><<<cell_grid(c, 1), kCTM, smem, c->stream>>>(
       src, tg, out, c->grid, c->s.cell_start, c->s.cell_end, c->s.cell_hmax, c->s.cell_list,
-      c->s.ncell_list, c->s.unit_rec, c->s.nunit_list, c->s.work + 3, c->s.seg, c->s.nseg, c->maxs, c->phys, c->s.dts, c->s.cnt,
+      c->s.ncell_list, c->s.unit_rec, c->s.nunit_list, c->s.work + 3, reinterpret_cast<const E*>(c->s.nbr), c->s.ncount, c->maxn_cap, c->phys, c->s.dts, c->s.cnt,
       reinterpret_cast<const double2*>(c->s.mrec));
 }
 

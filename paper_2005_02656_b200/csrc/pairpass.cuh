@@ -1,17 +1,14 @@
 // pairpass.cuh -- device helpers shared by the neighbour search (search.cu) and the
-// pair passes (cellpass.cu): unit stencils in shared memory, work claiming, warp
-// reductions, the kernel polynomial, and the neighbour-list format.
+// pair passes (cellpass.cu): unit stencils in shared memory, work claiming and warp
+// reductions.
 //
 // Neighbour lists.  A pair-pass UNIT (stencil.cuh) stages the
-// particles of its union stencil as one flat sequence (slots in order, each slot
-// a contiguous cell range).  The flat sequence is cut into TILES of 32; target t's
-// list is nseg[t] SEGMENTS seg[t * maxs + k] = (mask, tile), tiles ascending, where
-// bit b of mask marks the staged particle with flat index 32 tile + b as a
-// neighbour.  The search produces one 32-bit mask per (target, tile) straight from
-// its candidate tests, and a pass expands a target's segments into staging indices
-// with one lane per segment (expand_segments below): ~8 bytes per ~10 neighbours
-// in HBM instead of 4 bytes per neighbour, loaded with one coalesced 8-byte load
-// per lane per target.
+// particles of its union stencil as one flat sequence (slots in order, each slot a
+// contiguous cell range).  Target t's row holds the FLAT INDICES of its neighbours
+// in that sequence, ascending (fixed row stride, 16-bit entries unless a unit
+// stencil exceeds 65,535 particles): a pass reads a neighbour's staged data at
+// shared index entry - (group start) with no table lookup, and the host decodes
+// entries to global ids with the cell tables (sph_get_neighbors).
 #pragma once
 
 #include "stencil.cuh"
@@ -28,13 +25,12 @@ constexpr int kSearchTiles = kSearchCap / 32;
 constexpr int kSearchWords = kSearchTiles / 32;  // tile bitmask words
 constexpr int kDensCap = 4096;    // density: staged particles per group, 4 fp64 fields
 constexpr int kIadCap = 4096;     // IAD: the same fields
-constexpr int kMomCap = 896;      // momentum: staged 144-byte records per group (28 tiles)
+constexpr int kMomCap = 992;      // momentum: staged 144-byte records per group (a 48-cell unit in 4 groups)
 constexpr int kCTM = 512;         // momentum CTA: 16 warps, one CTA per SM
 constexpr int kCTD = 1024;        // density / IAD CTA: 32 warps, one CTA per SM
 constexpr int kNWM = kCTM / 32;
 constexpr int kNWD = kCTD / 32;
-constexpr int kBufD = 512;        // density / IAD: expanded entries per warp buffer
-constexpr int kBufM = 128;        // momentum: expanded entries per half-warp buffer (smem budget)
+constexpr uint32_t kSent = 0xffffffffu;  // past-the-end row entry
 static_assert(kSearchCap % 32 == 0 && kDensCap % 32 == 0 && kIadCap % 32 == 0 && kMomCap % 32 == 0,
               "staging groups are whole tiles");
 static_assert(kSlots >= kKMax, "slot tables must hold the largest admitted stencil");
@@ -226,52 +222,6 @@ __device__ __forceinline__ void shifts_of(const Grid& g, const CellSm& S, int sl
   sh[0] = S.t_sh[slot][0] * g.L[0];
   sh[1] = S.t_sh[slot][1] * g.L[1];
   sh[2] = S.t_sh[slot][2] * g.L[2];
-}
-
-// ------------------------------------------------------------------ neighbour segments
-// Lane-held chunk of a target's segment list: lane lw of a W-lane group holds segment
-// cur + lw (mask 0 past the end).
-__device__ __forceinline__ uint2 seg_load(const uint2* __restrict__ seg, uint32_t t, int maxs,
-                                          uint32_t k, uint32_t n) {
-  return k < n ? __ldg(seg + (size_t)t * maxs + k) : make_uint2(0u, 0xffffffffu);
-}
-
-// One expansion round over a W-lane group's chunk: the leading segments with tile <
-// tend whose expansion fits BUF entries are written to buf as group-relative staging
-// indices (32 tile + bit - gb), in list order, ONE LANE PER SEGMENT (each lane walks
-// its own mask).  Returns the entries written; *nfit = segments consumed, *nval =
-// segments of the chunk inside the group.  W = 32 (warp) or 16 (half-warp, width-16
-// shuffles: the two halves expand independent targets).
-template <int W, int BUF>
-__device__ __forceinline__ uint32_t expand_segments(uint2 sg, uint32_t tend, uint32_t gb, uint16_t* buf,
-                                                    uint32_t* nfit, uint32_t* nval) {
-  const uint32_t lane = threadIdx.x & 31, lw = lane & (W - 1);
-  const uint32_t gshift = W == 32 ? 0u : (lane & 16u);
-  const uint32_t gm = W == 32 ? 0xffffffffu : (0xffffu << gshift);
-  const bool valid = sg.x != 0u && sg.y < tend;  // tiles ascend: the valid lanes are a prefix
-  const uint32_t pc = valid ? __popc(sg.x) : 0u;
-  uint32_t incl = pc;
-#pragma unroll
-  for (int o = 1; o < W; o <<= 1) {
-    const uint32_t v = __shfl_up_sync(0xffffffffu, incl, o, W);
-    if (lw >= (uint32_t)o) incl += v;
-  }
-  const bool fit = valid && incl <= (uint32_t)BUF;
-  const uint32_t nf = __popc(__ballot_sync(0xffffffffu, fit) & gm);
-  *nval = __popc(__ballot_sync(0xffffffffu, valid) & gm);
-  *nfit = nf;
-  const uint32_t tot = __shfl_sync(0xffffffffu, incl, nf ? nf - 1 : 0, W);
-  if (fit) {
-    uint32_t mm = sg.x, pos = incl - pc;
-    const uint32_t base = 32u * sg.y - gb;
-    while (mm) {
-      const uint32_t b = __ffs(mm) - 1;
-      mm &= mm - 1;
-      buf[pos++] = (uint16_t)(base + b);
-    }
-  }
-  __syncwarp();
-  return nf ? tot : 0u;
 }
 
 }  // namespace sphb

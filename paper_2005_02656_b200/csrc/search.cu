@@ -8,13 +8,18 @@
 // compact) targets, culls the tiles no member can reach with one box-to-box test,
 // and streams the surviving tiles' candidates from shared memory as broadcasts --
 // every lane tests the same candidate against its own target, so a test is ~10
-// instructions with no per-hit bookkeeping, and a tile's hits of a target are ONE
-// 32-bit mask: the neighbour-list segment (mask, tile) the pair passes consume
-// (pairpass.cuh).
+// instructions with no per-hit bookkeeping: a tile's hits of a target accumulate in
+// ONE 32-bit mask, and the lane appends the segment (mask, tile) to its target's row
+// region (one 8-byte store per non-empty tile).  k_expand_rows then rewrites every
+// row in place as flat staging indices (pairpass.cuh), a warp per row through shared
+// memory, so the row stores are coalesced (per-bit stores from the lane-per-target
+// loop touched 32 rows per instruction and doubled the search time).
 //
 // Exactness: fp32 test with an error band, the exact fp64 test in
 // the oracle's association (__dmul_rn/__dadd_rn, minimum image) for candidates
 // inside the band, so lists are bit-exact.
+#include <algorithm>
+
 #include "pairpass.cuh"
 
 namespace sphb {
@@ -75,7 +80,7 @@ __global__ void k_unit_prep(Grid g, const uint32_t* __restrict__ clist, const ui
 // W2: a periodic dim whose stencil spans every cell (per-pair minimum image in fp32).
 // SYM: symmetric relation -- each staged candidate carries its own band, and the exact
 // test uses the larger of the two limits (the oracle's (2 max h)^2).
-template <bool W2, bool SYM>
+template <bool W2, bool SYM, typename E>
 __global__ void __launch_bounds__(kCTS, 2) k_search(const double* __restrict__ x,
                                                  const double* __restrict__ y,
                                                  const double* __restrict__ z,
@@ -84,18 +89,19 @@ __global__ void __launch_bounds__(kCTS, 2) k_search(const double* __restrict__ x
                                                  const uint32_t* __restrict__ cend,
                                                  const int4* __restrict__ urec,
                                                  const uint32_t* __restrict__ nulist,
-                                                 uint32_t* __restrict__ work, uint2* __restrict__ seg,
-                                                 uint32_t* __restrict__ nseg, uint32_t* __restrict__ ncount,
-                                                 int maxs, unsigned int* __restrict__ maxima) {
+                                                 uint32_t* __restrict__ work, E* __restrict__ nbr,
+                                                 uint32_t* __restrict__ ncount, uint32_t* __restrict__ nseg,
+                                                 int maxn, unsigned int* __restrict__ maxima) {
   extern __shared__ float4 cand[];  // kSearchCap + 32 (last tile padded with sentinels)
   float2* const candb = reinterpret_cast<float2*>(cand + kSearchCap + 32);  // SYM: per-candidate band
   __shared__ CellSm S;
   __shared__ float4 tlo[kSearchTiles], thi[kSearchTiles];  // per staged tile: fp32 bounding box
-  __shared__ uint32_t tseg[kTgtU], tcnt[kTgtU];             // per target: segments / neighbours so far
+  __shared__ uint32_t tcnt[kTgtU], tseg[kTgtU];            // per target: neighbours / segments so far
   __shared__ TgtW TW[kTgtU];
   __shared__ uint32_t s_chunk;
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  unsigned int mxseg = 0, mxcnt = 0;
+  unsigned int mxcnt = 0, mxseg = 0, wide = 0;
+  const uint32_t segcap = (uint32_t)((size_t)maxn * sizeof(E) / sizeof(uint2));  // segments a row region holds
   const uint32_t nun = *nulist;
   const uint32_t uchunk = (uint32_t)kCellChunk >> g.ubits ? (uint32_t)kCellChunk >> g.ubits : 1u;
   ChunkClaim claim{work, uchunk, 0u};
@@ -103,6 +109,10 @@ __global__ void __launch_bounds__(kCTS, 2) k_search(const double* __restrict__ x
     for (uint32_t ci = cfirst; ci < min(nun, cfirst + uchunk); ++ci) {
       unit_setup(g, ci, urec, cstart, cend, S);
       const Stencil st = S.st;
+      if (sizeof(E) < 4 && S.total > 0xffffu) {  // 16-bit rows cannot index this unit stencil:
+        wide = 1;                                 // the host reruns the search with 32-bit rows
+        continue;
+      }
       int b3[3];
       unit_base(g, S.c3, b3);
       double org[3], M = 0.0;
@@ -119,8 +129,8 @@ __global__ void __launch_bounds__(kCTS, 2) k_search(const double* __restrict__ x
       for (uint32_t t0 = S.sc; t0 < S.ec; t0 += kTgtU) {
         const uint32_t t1 = min(S.ec, t0 + kTgtU);
         for (uint32_t t = t0 + threadIdx.x; t < t1; t += blockDim.x) {
-          tseg[t - t0] = 0;
           tcnt[t - t0] = 0;
+          tseg[t - t0] = 0;
           const double ha = h[t], tha = 2.0 * ha;
           const float2 bd = band32(ha, M);
           const double px = x[t], py = y[t], pz = z[t];
@@ -198,7 +208,6 @@ __global__ void __launch_bounds__(kCTS, 2) k_search(const double* __restrict__ x
             }
           }
           __syncthreads();
-          const uint32_t tile0 = gb >> 5;
           // lane per target: 32 consecutive targets per warp
           for (uint32_t tb = t0 + 32u * warp; tb < t1; tb += 32u * kNWS) {
             const uint32_t t = tb + lane;
@@ -208,8 +217,8 @@ __global__ void __launch_bounds__(kCTS, 2) k_search(const double* __restrict__ x
             const float lo = act ? T.f[3] : -1.0f, hi = act ? T.f[4] : -1.0f;
             const uint32_t selff = T.self - gb;  // >= ntile*32 (wraps) when not in this group
             const uint32_t selfq = selff >> 5, selfbit = 1u << (selff & 31u);
-            uint32_t nsg = act ? tseg[t - t0] : 0u, ncn = act ? tcnt[t - t0] : 0u;
-            uint2* const row = seg + (size_t)(act ? t : 0) * maxs;
+            uint32_t ncn = act ? tcnt[t - t0] : 0u, nsg = act ? tseg[t - t0] : 0u;
+            uint2* const row = reinterpret_cast<uint2*>(nbr + (size_t)(act ? t : 0) * maxn);
             // the block's bounding box and largest band (box-to-box culling)
             float blx = act ? ax : INFINITY, bly = act ? ay : INFINITY, blz = act ? az : INFINITY;
             float bhx = act ? ax : -INFINITY, bhy = act ? ay : -INFINITY, bhz = act ? az : -INFINITY;
@@ -291,39 +300,148 @@ __global__ void __launch_bounds__(kCTS, 2) k_search(const double* __restrict__ x
                   }
                 }
                 if ((uint32_t)q == selfq) in &= ~selfbit;
+                // append the segment (mask, first flat index of the tile); a row region
+                // that would overflow is counted, not written (the host grows it, R23)
                 if (in) {
-                  if (nsg < (uint32_t)maxs) row[nsg] = make_uint2(in, tile0 + (uint32_t)q);
+                  if (nsg < segcap) row[nsg] = make_uint2(in, gb + 32u * (uint32_t)q);
                   ++nsg;
                   ncn += __popc(in);
                 }
               }
             }
             if (act) {
-              tseg[t - t0] = nsg;
               tcnt[t - t0] = ncn;
+              tseg[t - t0] = nsg;
             }
           }
           __syncthreads();
         }
         for (uint32_t t = t0 + threadIdx.x; t < t1; t += blockDim.x) {
-          const uint32_t ns = tseg[t - t0], nc = tcnt[t - t0];
-          nseg[t] = ns;
+          const uint32_t nc = tcnt[t - t0], ns = tseg[t - t0];
           ncount[t] = nc;
-          mxseg = max(mxseg, ns);
+          nseg[t] = ns;
           mxcnt = max(mxcnt, nc);
+          mxseg = max(mxseg, ns);
         }
         __syncthreads();
       }
     }
   }
-  // largest segment list / neighbour count of the launch (capacity check, diagnostics)
+  // largest neighbour count (row capacity, diagnostics) and segment count of the launch;
+  // a unit too large for 16-bit rows
   for (int o = 16; o; o >>= 1) {
-    mxseg = max(mxseg, __shfl_xor_sync(0xffffffffu, mxseg, o));
     mxcnt = max(mxcnt, __shfl_xor_sync(0xffffffffu, mxcnt, o));
+    mxseg = max(mxseg, __shfl_xor_sync(0xffffffffu, mxseg, o));
   }
-  if (lane == 0) {
-    if (mxseg) atomicMax(&maxima[0], mxseg);
-    if (mxcnt) atomicMax(&maxima[1], mxcnt);
+  if (lane == 0 && mxcnt) atomicMax(&maxima[0], mxcnt);
+  if (lane == 0 && mxseg > segcap) atomicOr(&maxima[2], 1u);
+  if (wide && threadIdx.x == 0) atomicOr(&maxima[1], 1u);
+}
+
+// Rows in place: segments (mask, first flat index) -> ascending flat indices.  A warp
+// per row: its segments are loaded into registers (lane k holds segments k, k + 32,
+// k + 64) before any entry is stored, their exclusive prefix is a warp scan, and each
+// segment is then written by the whole warp -- lane b stores the entry of bit b at
+// prefix + popc(mask below b) -- so every store instruction writes one contiguous run
+// of the row (coalesced; per-lane loops over bits scattered 32 rows per instruction,
+// or bank-conflicted in shared memory).  Rows whose count exceeds the stride are left
+// alone (the host grows the stride and reruns the search before anything reads them).
+constexpr int kExpWarps = 8;
+constexpr int kExpChunks = 3;  // segments held in registers: 96 = a 384-entry 16-bit row region
+template <typename E>
+__global__ void __launch_bounds__(32 * kExpWarps) k_expand_rows(unsigned char* __restrict__ rows, int64_t n,
+                                                              const uint32_t* __restrict__ nseg,
+                                                              const uint32_t* __restrict__ ncount, int maxn) {
+  const uint32_t lane = threadIdx.x & 31, lt = (1u << lane) - 1u;
+  const int warp = threadIdx.x >> 5;
+  const size_t rbytes = (size_t)maxn * sizeof(E);
+  const int64_t stride = (int64_t)gridDim.x * kExpWarps;
+  int64_t t = (int64_t)blockIdx.x * kExpWarps + warp;
+  uint32_t ns = t < n ? nseg[t] : 0u, nc = t < n ? ncount[t] : 0u;
+  for (; t < n; t += stride) {
+    const uint32_t cns = ns, cnc = nc;
+    if (t + stride < n) {  // the next row's counts land while this one is rewritten
+      ns = nseg[t + stride];
+      nc = ncount[t + stride];
+    }
+    if (cnc > (uint32_t)maxn) continue;
+    unsigned char* const row = rows + (size_t)t * rbytes;
+    const uint2* const gseg = reinterpret_cast<const uint2*>(row);
+    E* const out = reinterpret_cast<E*>(row);
+    uint2 sg[kExpChunks];
+    uint32_t incl[kExpChunks];
+    const uint32_t nchunk = (cns + 31) / 32;
+    if (nchunk > (uint32_t)kExpChunks) continue;  // grown rows: see k_expand_rows_wide
+#pragma unroll
+    for (int c = 0; c < kExpChunks; ++c) {
+      const uint32_t k = 32u * c + lane;
+      sg[c] = k < cns ? gseg[k] : make_uint2(0u, 0u);
+    }
+    uint32_t carry = 0;
+#pragma unroll
+    for (int c = 0; c < kExpChunks; ++c) {  // exclusive prefix of every segment
+      const uint32_t pc = __popc(sg[c].x);
+      uint32_t v = pc;
+#pragma unroll
+      for (int o = 1; o < 32; o <<= 1) {
+        const uint32_t u = __shfl_up_sync(0xffffffffu, v, o);
+        if (lane >= (uint32_t)o) v += u;
+      }
+      incl[c] = carry + v - pc;
+      carry += __shfl_sync(0xffffffffu, v, 31);
+    }
+    __syncwarp();  // every segment is in registers: the row region may be overwritten
+#pragma unroll
+    for (int c = 0; c < kExpChunks; ++c) {
+      const uint32_t nj = min(32u, cns > 32u * c ? cns - 32u * c : 0u);
+      for (uint32_t j = 0; j < nj; ++j) {
+        const uint32_t m = __shfl_sync(0xffffffffu, sg[c].x, j);
+        const uint32_t fb = __shfl_sync(0xffffffffu, sg[c].y, j);
+        const uint32_t e = __shfl_sync(0xffffffffu, incl[c], j);
+        if (m & (1u << lane)) out[e + __popc(m & lt)] = (E)(fb + lane);
+      }
+    }
+  }
+}
+
+// The same for rows whose segments exceed the registers (a stride grown past 384):
+// segments are staged in shared memory first.
+template <typename E>
+__global__ void __launch_bounds__(32 * kExpWarps) k_expand_rows_wide(unsigned char* __restrict__ rows, int64_t n,
+                                                                   const uint32_t* __restrict__ nseg,
+                                                                   const uint32_t* __restrict__ ncount, int maxn) {
+  extern __shared__ uint2 xseg[];
+  const uint32_t lane = threadIdx.x & 31, lt = (1u << lane) - 1u;
+  const int warp = threadIdx.x >> 5;
+  const size_t rbytes = (size_t)maxn * sizeof(E);
+  uint2* const sseg = xseg + (rbytes / sizeof(uint2)) * warp;
+  for (int64_t t = (int64_t)blockIdx.x * kExpWarps + warp; t < n; t += (int64_t)gridDim.x * kExpWarps) {
+    const uint32_t ns = nseg[t], nc = ncount[t];
+    if (nc > (uint32_t)maxn || (ns + 31) / 32 <= (uint32_t)kExpChunks) continue;
+    unsigned char* const row = rows + (size_t)t * rbytes;
+    E* const out = reinterpret_cast<E*>(row);
+    for (uint32_t k = lane; k < ns; k += 32) sseg[k] = reinterpret_cast<const uint2*>(row)[k];
+    __syncwarp();
+    uint32_t carry = 0;
+    for (uint32_t k0 = 0; k0 < ns; k0 += 32) {
+      const uint2 sg = k0 + lane < ns ? sseg[k0 + lane] : make_uint2(0u, 0u);
+      const uint32_t pc = __popc(sg.x);
+      uint32_t v = pc;
+      for (int o = 1; o < 32; o <<= 1) {
+        const uint32_t u = __shfl_up_sync(0xffffffffu, v, o);
+        if (lane >= (uint32_t)o) v += u;
+      }
+      const uint32_t ex = carry + v - pc;
+      carry += __shfl_sync(0xffffffffu, v, 31);
+      const uint32_t nj = min(32u, ns - k0);
+      for (uint32_t j = 0; j < nj; ++j) {
+        const uint32_t m = __shfl_sync(0xffffffffu, sg.x, j);
+        const uint32_t fb = __shfl_sync(0xffffffffu, sg.y, j);
+        const uint32_t e = __shfl_sync(0xffffffffu, ex, j);
+        if (m & (1u << lane)) out[e + __popc(m & lt)] = (E)(fb + lane);
+      }
+    }
+    __syncwarp();
   }
 }
 
@@ -334,23 +452,58 @@ static bool any_wrap2_s(const sph_ctx* c) {
   return false;
 }
 
-int launch_neighbors(sph_ctx* c) {
-  const bool sym = c->phys.sym != 0;
-  const size_t smem = (kSearchCap + 32) * sizeof(float4) + (sym ? (kSearchCap + 32) * sizeof(float2) : 0);
-  auto kern = any_wrap2_s(c) ? (sym ? k_search<true, true> : k_search<true, false>)
-                             : (sym ? k_search<false, true> : k_search<false, false>);
+template <typename E>
+static void search_t(sph_ctx* c, int gs, size_t smem, bool w2, bool sym) {
+  auto kern = w2 ? (sym ? k_search<true, true, E> : k_search<true, false, E>)
+                 : (sym ? k_search<false, true, E> : k_search<false, false, E>);
   cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-  cudaMemsetAsync(c->s.work + 0, 0, sizeof(uint32_t), c->stream);
+  kern<<<gs, kCTS, smem, c->stream>>>(c->P.x, c->P.y, c->P.z, c->P.h, c->grid, c->s.cell_start,
+                                      c->s.cell_end, c->s.unit_rec, c->s.nunit_list, c->s.work + 0,
+                                      reinterpret_cast<E*>(c->s.nbr), c->s.ncount, c->s.nseg, c->maxn_cap,
+                                      c->s.nbr_max);
+}
+
+template <typename E>
+static void expand_t(sph_ctx* c) {
+  const int64_t blocks = std::min<int64_t>((c->P.n + kExpWarps - 1) / kExpWarps, (int64_t)c->num_sms * 8);
+  const int nb = (int)std::max<int64_t>(blocks, 1);
+  k_expand_rows<E><<<nb, 32 * kExpWarps, 0, c->stream>>>(c->s.nbr, c->P.n, c->s.nseg, c->s.ncount, c->maxn_cap);
+  if ((size_t)c->maxn_cap * sizeof(E) / sizeof(uint2) > 32u * kExpChunks) {  // grown rows
+    const size_t smem = (size_t)kExpWarps * c->maxn_cap * sizeof(E);
+    cudaFuncSetAttribute(k_expand_rows_wide<E>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    k_expand_rows_wide<E><<<nb, 32 * kExpWarps, smem, c->stream>>>(c->s.nbr, c->P.n, c->s.nseg, c->s.ncount,
+                                                                   c->maxn_cap);
+  }
+}
+
+// segments -> rows in place (after the capacity check of the search's maxima)
+int launch_expand_rows(sph_ctx* c) {
+  if (c->wide_rows) expand_t<uint32_t>(c);
+  else expand_t<uint16_t>(c);
+  return 1;
+}
+
+// unit records (union stencils + target ranges) for the search and the three passes
+int launch_unit_prep(sph_ctx* c) {
   const int64_t cells = c->grid.ncell < c->P.n ? c->grid.ncell : c->P.n;
-  // unit records (union stencils + target ranges) for the search and the three passes
   const int gprep = (int)std::min<int64_t>(std::max<int64_t>(cells, 1), (int64_t)c->num_sms * 8);
   k_unit_prep<<<gprep, 128, 0, c->stream>>>(c->grid, c->s.cell_list, c->s.unit_list, c->s.nunit_list,
                                             c->s.cell_start, c->s.cell_end, c->s.cell_hmax, c->s.unit_rec);
+  return 1;
+}
+
+// the search proper into rows of the current type / stride (maxima[0]: largest count,
+// maxima[1]: a unit stencil too large for 16-bit rows)
+int launch_search(sph_ctx* c) {
+  const bool sym = c->phys.sym != 0;
+  const size_t smem = (kSearchCap + 32) * sizeof(float4) + (sym ? (kSearchCap + 32) * sizeof(float2) : 0);
+  cudaMemsetAsync(c->s.work + 0, 0, sizeof(uint32_t), c->stream);
+  cudaMemsetAsync(c->s.nbr_max, 0, 3 * sizeof(unsigned int), c->stream);
+  const int64_t cells = c->grid.ncell < c->P.n ? c->grid.ncell : c->P.n;
   const int gs = (int)std::min<int64_t>(std::max<int64_t>(cells, 1), (int64_t)c->num_sms * 2);
-  kern<<<gs, kCTS, smem, c->stream>>>(c->P.x, c->P.y, c->P.z, c->P.h, c->grid, c->s.cell_start,
-                                      c->s.cell_end, c->s.unit_rec, c->s.nunit_list, c->s.work + 0,
-                                      c->s.seg, c->s.nseg, c->s.ncount, c->maxs, c->s.nbr_max);
-  return 2;
+  if (c->wide_rows) search_t<uint32_t>(c, gs, smem, any_wrap2_s(c), sym);
+  else search_t<uint16_t>(c, gs, smem, any_wrap2_s(c), sym);
+  return 1;
 }
 
 }  // namespace sphb

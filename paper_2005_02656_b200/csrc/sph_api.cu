@@ -233,10 +233,9 @@ sph_status sph_init(const sph_params* prm, int64_t capacity, sph_ctx** out) {
   sph_ctx* c = new sph_ctx();
   c->prm = *prm;
   if (c->prm.max_neighbors < 0) c->prm.max_neighbors = 0;
-  if (c->prm.max_segments <= 0) c->prm.max_segments = 64;
   if (!(c->prm.cell_factor > 0.0)) c->prm.cell_factor = 1.0;
   c->maxn = c->prm.max_neighbors;
-  c->maxs = c->prm.max_segments;
+  c->maxn_cap = c->maxn > 0 ? c->maxn : 384;  // 300 neighbours + headroom; grows on demand
   c->cap = capacity;
   c->stream = (cudaStream_t)prm->stream;
   int dev = 0;
@@ -305,10 +304,10 @@ sph_status sph_init(const sph_params* prm, int64_t capacity, sph_ctx** out) {
   AL(s.mX, cap);
   AL(s.ct, 6 * cap);
   AL(s.mrec, 18 * cap);
-  AL(s.seg, cap * (int64_t)c->maxs);
-  AL(s.nseg, cap);
+  AL(s.nbr, cap * (int64_t)c->maxn_cap * (int64_t)sizeof(uint16_t));
   AL(s.ncount, cap);
-  AL(s.nbr_max, 2);
+  AL(s.nseg, cap);
+  AL(s.nbr_max, 3);
   AL(s.work, 4);
   AL(s.wB, cap);
   AL(s.ih2, cap);
@@ -339,7 +338,6 @@ sph_status sph_init(const sph_params* prm, int64_t capacity, sph_ctx** out) {
   cudaMemsetAsync(s.bad_id, 0xff, sizeof(unsigned long long), c->stream);
   cudaMemsetAsync(s.dts, 0, sizeof(double) * DT_SLOTS, c->stream);
   cudaMemsetAsync(s.ncount, 0, sizeof(uint32_t) * cap, c->stream);
-  cudaMemsetAsync(s.nseg, 0, sizeof(uint32_t) * cap, c->stream);
   {
     double inf = INFINITY;
     unsigned long long bits;
@@ -519,23 +517,46 @@ sph_status sph_find_neighbors(sph_ctx* c) {
     CKL();
     ph.done(k);
   }
-  CK(cudaMemsetAsync(c->s.nbr_max, 0, 2 * sizeof(unsigned int), c->stream));
+  unsigned int mx[3] = {0, 0, 0};
   if (c->P.n) {
     Phase ph(c, SPH_PH_NEIGHBORS);
-    int k = launch_neighbors(c);
+    int k = launch_unit_prep(c) + launch_search(c);
     CKL();
     ph.done(k);
   }
-  unsigned int mx[2] = {0, 0};
   CK(cudaMemcpyAsync(mx, c->s.nbr_max, sizeof(mx), cudaMemcpyDeviceToHost, c->stream));
   CK(cudaStreamSynchronize(c->stream));
-  c->nbr_max = mx[1];
-  if (mx[0] > (unsigned)c->maxs)  // never truncated silently (R23)
-    return fail(c, SPH_ERR_CAPACITY, "a neighbour list needs " + std::to_string(mx[0]) +
-                                         " segments > max_segments = " + std::to_string(c->maxs));
-  if (c->maxn > 0 && mx[1] > (unsigned)c->maxn)
-    return fail(c, SPH_ERR_CAPACITY, "a particle has " + std::to_string(mx[1]) +
-                                         " neighbours > max_neighbors = " + std::to_string(c->maxn));
+  // Rows never truncate (R23): a unit stencil too large for 16-bit entries, or a row
+  // longer than the stride, reallocates the rows and reruns the search (rare: the h
+  // update keeps counts near n_target); max_neighbors > 0 is a hard limit instead.
+  while (c->P.n && (mx[1] || mx[2] || mx[0] > (unsigned)c->maxn_cap)) {
+    if (c->maxn > 0 && mx[0] > (unsigned)c->maxn)
+      return fail(c, SPH_ERR_CAPACITY, "a particle has " + std::to_string(mx[0]) +
+                                           " neighbours > max_neighbors = " + std::to_string(c->maxn));
+    if (mx[1]) c->wide_rows = true;
+    if (mx[0] > (unsigned)c->maxn_cap) c->maxn_cap = (int)(((mx[0] + mx[0] / 8) + 31) / 32 * 32);
+    else if (mx[2]) c->maxn_cap *= 2;  // the segments did not fit the row region
+    CK(cudaFree(c->s.nbr));
+    c->s.nbr = nullptr;
+    const size_t bytes = (size_t)c->cap * c->maxn_cap * (c->wide_rows ? 4 : 2);
+    if (cudaMalloc((void**)&c->s.nbr, bytes) != cudaSuccess) {
+      cudaGetLastError();
+      return fail(c, SPH_ERR_CAPACITY, "neighbour rows: cannot allocate " + std::to_string(bytes) + " bytes");
+    }
+    Phase ph(c, SPH_PH_NEIGHBORS);
+    int k = launch_search(c);
+    CKL();
+    ph.done(k);
+    CK(cudaMemcpyAsync(mx, c->s.nbr_max, sizeof(mx), cudaMemcpyDeviceToHost, c->stream));
+    CK(cudaStreamSynchronize(c->stream));
+  }
+  c->nbr_max = mx[0];
+  if (c->P.n) {  // segments -> flat-index rows, in place
+    Phase ph(c, SPH_PH_NEIGHBORS);
+    int k = launch_expand_rows(c);
+    CKL();
+    ph.done(k);
+  }
   c->stage = 1;
   return SPH_OK;
 }
@@ -568,21 +589,20 @@ sph_status sph_get_neighbors(sph_ctx* c, int64_t* offsets, int64_t* ids, int64_t
   CK(cudaMemcpy(chm.data(), c->s.cell_hmax, sizeof(unsigned long long) * g.ncell,
                 cudaMemcpyDeviceToHost));
   const int64_t chunk = 1 << 14;
-  std::vector<uint2> segs((size_t)chunk * c->maxs);
-  std::vector<uint32_t> nsg(n > 0 ? n : 1);
-  if (n) CK(cudaMemcpy(nsg.data(), c->s.nseg, sizeof(uint32_t) * n, cudaMemcpyDeviceToHost));
+  const size_t esz = c->wide_rows ? 4 : 2;
+  std::vector<unsigned char> rows((size_t)chunk * c->maxn_cap * esz);
   std::vector<int64_t> ucum, ucell;
   int ub3[3] = {-1, -1, -1};
   Stencil st;
   for (int64_t r0 = 0; r0 < n; r0 += chunk) {
     int64_t nr = std::min(chunk, n - r0);
-    CK(cudaMemcpy(segs.data(), c->s.seg + (size_t)r0 * c->maxs, sizeof(uint2) * nr * c->maxs,
-                  cudaMemcpyDeviceToHost));
+    CK(cudaMemcpy(rows.data(), c->s.nbr + (size_t)r0 * c->maxn_cap * esz,
+                  esz * nr * c->maxn_cap, cudaMemcpyDeviceToHost));
     for (int64_t i = 0; i < nr; ++i) {
       const int64_t cell = key_cell_hd(g, keys[r0 + i]);
       int c3[3];
       cell_coords(g, cell, c3);
-      // segments hold (mask, tile) over the target's unit stencil (slots in order, each
+      // rows hold flat indices into the target's unit stencil (slots in order, each
       // slot its cell's range): rebuild the slot prefix when the unit changes
       int b3[3];
       unit_base(g, c3, b3);
@@ -597,16 +617,14 @@ sph_status sph_get_neighbors(sph_ctx* c, int64_t* offsets, int64_t* ids, int64_t
           ucum[k + 1] = ucum[k] + (ce[ucell[k]] - cs[ucell[k]]);
         }
       }
-      int64_t o = offsets[r0 + i];
-      for (uint32_t k = 0; k < nsg[r0 + i]; ++k) {
-        const uint2 sg = segs[(size_t)i * c->maxs + k];
-        for (uint32_t m = sg.x; m; m &= m - 1) {
-          const int64_t e = 32 * (int64_t)sg.y + __builtin_ctz(m);
-          const int slot = (int)(std::upper_bound(ucum.begin(), ucum.end(), e) - ucum.begin()) - 1;
-          ids[o++] = id[cs[ucell[slot]] + (e - ucum[slot])];
-        }
+      for (uint32_t k = 0; k < cnt[r0 + i]; ++k) {
+        const size_t at = (size_t)i * c->maxn_cap + k;
+        const int64_t e = c->wide_rows ? (int64_t)((const uint32_t*)rows.data())[at]
+                                       : (int64_t)((const uint16_t*)rows.data())[at];
+        if (e >= ucum[st.K]) return fail(c, SPH_ERR_STATE, "neighbour row entry outside its unit stencil");
+        const int slot = (int)(std::upper_bound(ucum.begin(), ucum.end(), e) - ucum.begin()) - 1;
+        ids[offsets[r0 + i] + k] = id[cs[ucell[slot]] + (e - ucum[slot])];
       }
-      if (o != offsets[r0 + i + 1]) return fail(c, SPH_ERR_STATE, "neighbour segments disagree with counts");
     }
   }
   return SPH_OK;
@@ -838,7 +856,7 @@ sph_status sph_destroy(sph_ctx* c) {
   Scratch& s = c->s;
   void* ptrs[] = {s.keys, s.keys_alt, s.idx, s.idx_alt, s.hist, s.scan_tmp, s.gather, s.gather_id,
                   s.cell_start, s.cell_end, s.cell_hmax, s.cell_flag, s.cell_rank, s.cell_list,
-                  s.ncell_list, s.unit_flag, s.unit_rank, s.unit_list, s.nunit_list, s.unit_rec, s.seg, s.nseg, s.ncount, s.nbr_max, s.work, s.wB, s.ih2, s.vol, s.rinv, s.X,
+                  s.ncell_list, s.unit_flag, s.unit_rank, s.unit_list, s.nunit_list, s.unit_rec, s.nbr, s.ncount, s.nseg, s.nbr_max, s.work, s.wB, s.ih2, s.vol, s.rinv, s.X,
                   s.mX, s.ct, s.mrec, s.red, s.bbox, s.dts, s.cnt, s.bad_id, s.diag, s.ktable};
   for (void* p : ptrs)
     if (p) cudaFree(p);

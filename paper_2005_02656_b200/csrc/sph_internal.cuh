@@ -1,9 +1,10 @@
 // sph_internal.cuh -- shared definitions of the CUDA path (sm_100a).
 //
 // Layout in HBM: every per-particle quantity is its own fp64
-// array (SoA) in Morton-cell order; neighbour lists are per-target lists of
-// (32-bit mask, tile) segments over the target's unit stencil, fixed stride `maxs`
-// (pairpass.cuh); the search grid is a dense table of cell ranges
+// array (SoA) in Morton-cell order; neighbour lists are rows of flat staging
+// indices into the target's unit stencil (16-bit, or 32-bit when a unit stencil
+// exceeds 65,535 particles), fixed stride `maxn_cap` (pairpass.cuh); the search grid
+// is a dense table of cell ranges
 // [cell_start, cell_end) into the sorted order.
 #pragma once
 
@@ -84,10 +85,10 @@ struct Scratch {
   int4* unit_rec = nullptr;                 // 3 x cap: per unit, its union stencil + target range
   int64_t max_cells = 0;
   // neighbours
-  uint2* seg = nullptr;          // cap * maxs neighbour segments (mask, tile)
-  uint32_t* nseg = nullptr;      // cap: segments per target
+  unsigned char* nbr = nullptr;  // cap * maxn_cap row entries (uint16_t, or uint32_t when wide_rows)
   uint32_t* ncount = nullptr;    // cap: neighbours per target
-  unsigned int* nbr_max = nullptr;  // [0] largest segment count, [1] largest neighbour count
+  uint32_t* nseg = nullptr;      // cap: search segments per target (before the in-place expansion)
+  unsigned int* nbr_max = nullptr;  // [0] largest count, [1] a unit too large for 16 bits, [2] segment overflow
   uint32_t* work = nullptr;              // per cell kernel: next cell chunk (reset per launch)
   // per-particle auxiliaries written by density, read by iad / momentum
   double* wB = nullptr;    // B / h^3
@@ -121,7 +122,8 @@ struct sph_ctx {
   cudaStream_t stream = nullptr;
   int64_t cap = 0;
   int maxn = 0;             // user limit on neighbours per particle (0: none)
-  int maxs = 64;            // segment capacity per particle
+  int maxn_cap = 384;       // row stride (grows on demand up to the user limit)
+  bool wide_rows = false;   // 32-bit row entries
   sph_particles P{};
   bool attached = false;
   int stage = 0;            // 0 none, 1 neighbours, 2 density, 3 iad, 4 momentum
@@ -162,7 +164,9 @@ int scan_u32(sph_ctx* c, const uint32_t* in, uint32_t* out, int64_t n);
 int launch_sort(sph_ctx* c, int nbits, const uint32_t** perm_out);
 int launch_permute(sph_ctx* c, const uint32_t* perm);
 int launch_cells(sph_ctx* c);
-int launch_neighbors(sph_ctx* c);
+int launch_unit_prep(sph_ctx* c);
+int launch_search(sph_ctx* c);
+int launch_expand_rows(sph_ctx* c);
 int launch_density(sph_ctx* c);
 int launch_iad(sph_ctx* c);
 int launch_momentum(sph_ctx* c);

@@ -94,7 +94,7 @@ class Params(C.Structure):
         ("rank", C.c_int), ("nranks", C.c_int), ("nccl_unique_id", C.c_void_p),
         ("stream", C.c_void_p),
         ("kernel_mode", C.c_int), ("table_size", C.c_int), ("symmetric", C.c_int),
-        ("redecomp_every", C.c_int), ("max_segments", C.c_int),
+        ("redecomp_every", C.c_int),
     ]
 
 
@@ -180,7 +180,7 @@ def make_params(d: dict, *, n: float = 6.0, alpha: float = 1.0, omega_mode: int 
                 h_max: float = 0.0, u_floor: float = -np.inf, max_neighbors: int = 0,
                 cell_factor: float = 0.0, rank: int = 0, nranks: int = 1, stream=None,
                 kernel_mode: int = 0, table_size: int = 0, symmetric: int = 0,
-                redecomp_every: int = 1, max_segments: int = 0) -> Params:
+                redecomp_every: int = 1) -> Params:
     p = Params()
     p.abi_version = ABI_VERSION
     p.sinc_n = n
@@ -204,7 +204,6 @@ def make_params(d: dict, *, n: float = 6.0, alpha: float = 1.0, omega_mode: int 
     p.table_size = table_size
     p.symmetric = int(symmetric)
     p.redecomp_every = int(redecomp_every)
-    p.max_segments = int(max_segments)
     return p
 
 
