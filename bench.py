@@ -37,11 +37,24 @@ UNIT = "particle-updates/s"
 # per candidate for the search (3 sub + r^2 + compare).
 FLOPS_PER_PAIR = {"density": 70, "iad": 52, "momentum": 169}
 FLOPS_PER_CANDIDATE = 9
+# Whole-step roofline model: per phase max(bytes / HBM,
+# flops / FP64 peak) with algorithmic bytes / flops; the search at the survey's 6.4
+# candidates per neighbour x 8 flops.  Bytes per particle of the streaming phases from
+# the survey table (bbox+keys 36, sort 200, permute 240, cells 10, update+h 204); the
+# pair passes read 2-byte row entries per pair plus their staged fields per particle.
+MODEL_STREAM_BYTES = {"bbox_keys": 36, "sort": 200, "permute": 240, "cells": 10, "update": 204}
+MODEL_PAIR_BYTES = {"search": 2.0, "density": 2.0, "iad": 2.0, "momentum": 2.0}
+MODEL_PARTICLE_BYTES = {"search": 32 + 8, "density": 32 + 80, "iad": 32 + 56, "momentum": 136 + 40}
+SEARCH_FLOPS_PER_PAIR = 6.4 * 8
 
 
 def workload(name: str, G: int, rank: int):
     from paper_2005_02656_b200 import inputs as I
-    if name == "weak":  # config 5: 292 x 292 x (292 G), slab per rank
+    if name == "weak":  # 300 x 300 x (300 G), slab per rank: config 4 (27M) at N=1, config 5 weak scaling
+        d = I.square_patch_weak(300, G, rank if G > 1 else None)
+        desc = (f"square patch 300x300x{300 * G}, {300 ** 3} particles/GPU (N=1: config 4, the "
+                f"north_star's 27M patch; N>1: config 5 weak scaling, z-stacked per GPU)")
+    elif name == "weak292":  # config 5 as in BASELINE: 292 x 292 x (292 G)
         d = I.square_patch_weak(292, G, rank if G > 1 else None)
         desc = f"config5 weak-scaling square patch 292x292x{292 * G}, {292 ** 3} particles/GPU"
     elif name == "patch27m":  # config 4 (strong scaling): z-slab of the 300^3 patch per rank
@@ -158,9 +171,20 @@ def cpu_baseline(target_seconds: float = 12.0) -> dict:
     o.step(d)
     el = time.perf_counter() - t
     return {"value": d["x"].size / el, "unit": UNIT, "cores": cores, "kind": "oracle",
+            "cpu_model": cpu_model(),
             "sample": f"square patch {n}^3 = {d['x'].size} particles, 1 full step "
                       f"(grid neighbours, density, IAD, momentum, dt, update), {el:.1f} s",
             "seconds": el}
+
+
+def cpu_model() -> str:
+    try:
+        for ln in open("/proc/cpuinfo"):
+            if ln.startswith("model name"):
+                return ln.split(":", 1)[1].strip()
+    except Exception:
+        pass
+    return "unknown"
 
 
 def run_reference(args):
@@ -191,13 +215,15 @@ def run_reference(args):
             "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
             "data": "synthetic", "config": {"workload": workload_label(args)},
             "cpu_baseline": {"value": v, "unit": UNIT, "cores": cores, "kind": "oracle",
+                             "cpu_model": cpu_model(),
                              "sample": f"square patch {n}^3 = {d['x'].size} particles per step"},
             "e2e": {"value": v, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
     print(json.dumps(line), flush=True)
 
 
 def workload_label(args):
-    return {"weak": "config5_weak_square_patch_292^3_per_gpu", "patch27m": "config4_square_patch_300^3",
+    return {"weak": "square_patch_300^3_per_gpu (config4 at N=1, config5 weak)",
+            "weak292": "config5_weak_square_patch_292^3_per_gpu", "patch27m": "config4_square_patch_300^3",
             "patch1m": "config2_square_patch_100^3", "evrard": "config3_evrard_124"}[args.workload]
 
 
@@ -255,6 +281,7 @@ def run_ours(args):
         e2e_ms = max(ee0.elapsed_time(ee1), 1e3 * (time.perf_counter() - t0))
         peak64 = sph.measure_fp64_peak(stream.cuda_stream)
     ms_rank = ms
+    mem_per_particle = (torch.cuda.max_memory_allocated() + sim.library_bytes()) / max(1, n_local)
     ms = max_over_ranks(ms, world)
     e2e_ms = max_over_ranks(e2e_ms, world)
     per_rank = None
@@ -304,6 +331,29 @@ def run_ours(args):
             a = FLOPS_PER_PAIR[ph_name] * pairs / (t * 1e-3) / 1e12
             pair_kernels[ph_name] = {"ms": round(t, 3), "tflops": round(a, 3),
                                      "frac": round(a / peak64, 4) if peak64 else None}
+    # whole-step roofline model (SURVEY §8(d) "headline fraction = sum roofline time / measured")
+    bw = (peaks.get("hbm_gbs") or 6549.1) * 1e9
+    p64 = peak64 * 1e12
+    model = {
+        "bbox+keys": MODEL_STREAM_BYTES["bbox_keys"] * n_local / bw,
+        "sort": MODEL_STREAM_BYTES["sort"] * n_local / bw,
+        "permute": MODEL_STREAM_BYTES["permute"] * n_local / bw,
+        "cells": MODEL_STREAM_BYTES["cells"] * n_local / bw,
+        "update": MODEL_STREAM_BYTES["update"] * n_local / bw,
+    }
+    for ph_name in ("search", "density", "iad", "momentum"):
+        fl = (SEARCH_FLOPS_PER_PAIR if ph_name == "search" else FLOPS_PER_PAIR[ph_name]) * pairs
+        by = MODEL_PAIR_BYTES[ph_name] * pairs + MODEL_PARTICLE_BYTES[ph_name] * n_local
+        model[ph_name] = max(fl / p64, by / bw)
+    model_ms = {k: round(v * 1e3, 3) for k, v in model.items()}
+    step_model_ms = sum(model.values()) * 1e3
+    search_ms = phase_ms.get("neighbors", 0.0) / args.steps
+    roofline_step = {"model_ms_per_step": round(step_model_ms, 3), "measured_ms_per_step": ms_step,
+                     "frac": step_model_ms / ms_step, "model_phases_ms": model_ms,
+                     "search_frac": (model["search"] * 1e3 / search_ms) if search_ms else None,
+                     "peaks": {"fp64_tflops": peak64, "hbm_gbs": bw / 1e9},
+                     "note": "per phase max(algorithmic bytes / HBM, algorithmic flops / FP64 peak); "
+                             "search at 6.4 candidates x 8 flops per neighbour (SURVEY 8(d))"}
     line = {
         "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": max(world, 1),
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms_step,
@@ -325,6 +375,8 @@ def run_ours(args):
                      "flops_per_pair": FLOPS_PER_PAIR["momentum"], "pairs_per_launch": pairs,
                      "avg_launch_ms": mom_ms},
         "pair_kernels_fp64": pair_kernels,
+        "roofline_step": roofline_step,
+        "memory_bytes_per_particle": mem_per_particle,
         "phases_ms_per_step": phases,
         "per_rank": per_rank,
         "gpu_launches": int(sum(phase_launch.values())),
@@ -344,7 +396,7 @@ def main():
     ap.add_argument("--gpus", type=int, default=1)
     ap.add_argument("--steps", type=int, default=10)
     ap.add_argument("--warmup", type=int, default=3)
-    ap.add_argument("--workload", default="weak", choices=["weak", "patch27m", "patch1m", "evrard"])
+    ap.add_argument("--workload", default="weak", choices=["weak", "weak292", "patch27m", "patch1m", "evrard"])
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--kernel-mode", default="poly", choices=["poly", "table", "sin"],

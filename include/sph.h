@@ -161,6 +161,9 @@ sph_status  sph_download(sph_ctx* ctx, sph_particles* host);
 /* Particles currently owned by this rank (== the attached arrays' valid prefix; it changes
  * when particles migrate between ranks) and halo particles held during the current step. */
 sph_status  sph_local_count(const sph_ctx* ctx, int64_t* n_owned, int64_t* n_halo);
+/* Device memory the library holds for this context (scratch, neighbour rows, multi-GPU
+ * buffers), in bytes; the caller's particle arrays are not included. */
+sph_status  sph_memory_bytes(const sph_ctx* ctx, int64_t* bytes);
 /* Conserved sums and counters ("tracking total momentum and energy"), summed over all
  * ranks when nranks > 1 (n_owned is then the global particle count).  Synchronises. */
 sph_status  sph_diagnostics(sph_ctx* ctx, sph_diag* out);

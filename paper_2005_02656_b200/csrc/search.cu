@@ -7,10 +7,11 @@
 // bounding boxes.  LANE PER TARGET: a warp takes 32 consecutive (Z-ordered, so
 // compact) targets, culls the tiles no member can reach with one box-to-box test,
 // and streams the surviving tiles' candidates from shared memory as broadcasts --
-// every lane tests the same candidate against its own target, so a test is ~10
-// instructions with no per-hit bookkeeping: a tile's hits of a target accumulate in
-// ONE 32-bit mask, and the lane appends the segment (mask, tile) to its target's row
-// region (one 8-byte store per non-empty tile).  k_expand_rows then rewrites every
+// every lane tests the same candidate against its own target: one fp32 subtraction
+// against the band's lower edge whose SIGN BIT is the hit (funnel-shifted into a
+// 32-bit tile mask) and a running min |r^2 - lo| that flags the rare ambiguous tile --
+// ~9 instructions per test, no per-hit bookkeeping.  The lane appends the segment
+// (mask, tile) to its target's row region (one 8-byte store per non-empty tile).  k_expand_rows then rewrites every
 // row in place as flat staging indices (pairpass.cuh), a warp per row through shared
 // memory, so the row stores are coalesced (per-bit stores from the lane-per-target
 // loop touched 32 rows per instruction and doubled the search time).
@@ -30,7 +31,7 @@ constexpr int kNWS = kCTS / 32;
 struct TgtW {  // per-target search data (exact-test fp64 + fp32 band + own flat index)
   double pos[3];
   double lim;
-  float f[5];
+  float f[6];   // x, y, z (unit-relative), band lo, band hi, ambiguity width
   uint32_t self;
 };
 
@@ -144,6 +145,8 @@ __global__ void __launch_bounds__(kCTS, 2) k_search(const double* __restrict__ x
           w.f[2] = (float)(pz - org[2]);
           w.f[3] = bd.x;
           w.f[4] = bd.y;
+          // |fl(r2 - lo)| of a candidate inside [lo, hi) is below this (fp32 rounding slack)
+          w.f[5] = bd.y < INFINITY ? (bd.y - bd.x) * (1.0f + 0x1p-20f) + 0x1p-126f : INFINITY;
           // own flat staging index (the unit slot of the target's cell): never its own neighbour
           w.self = 0xffffffffu;
           for (int dz = 0; dz < (g.ubits > 2 ? 2 : 1); ++dz)
@@ -215,6 +218,7 @@ __global__ void __launch_bounds__(kCTS, 2) k_search(const double* __restrict__ x
             const TgtW& T = TW[act ? t - t0 : 0];
             const float ax = T.f[0], ay = T.f[1], az = T.f[2];
             const float lo = act ? T.f[3] : -1.0f, hi = act ? T.f[4] : -1.0f;
+            const float wband = act ? T.f[5] : -1.0f;
             const uint32_t selff = T.self - gb;  // >= ntile*32 (wraps) when not in this group
             const uint32_t selfq = selff >> 5, selfbit = 1u << (selff & 31u);
             uint32_t ncn = act ? tcnt[t - t0] : 0u, nsg = act ? tseg[t - t0] : 0u;
@@ -262,9 +266,20 @@ __global__ void __launch_bounds__(kCTS, 2) k_search(const double* __restrict__ x
                 const int q = 32 * w + __ffs(nm) - 1;
                 nm &= nm - 1;
                 const float4* cq = cand + 32 * q;
-                uint32_t in = 0u, near = 0u;
-#pragma unroll
-                for (int k = 0; k < 32; ++k) {
+                uint32_t in = 0u;
+                // rare: exact fp64 test of candidate b (the oracle's r^2 < (2h)^2, R10)
+                auto exact = [&](uint32_t b) -> bool {
+                  const uint32_t f = gb + 32u * q + b;
+                  const int kq = slot_of(S, f);
+                  const uint32_t j = S.t_start[kq] + (f - S.cum[kq]);
+                  double lim = T.lim;
+                  if constexpr (SYM) {
+                    const double thb = 2.0 * h[j];
+                    lim = fmax(lim, __dmul_rn(thb, thb));
+                  }
+                  return exact_hit(g, x, y, z, j, t, T.pos, lim);
+                };
+                auto r2of = [&](int k) -> float {
                   const float4 c = cq[k];
                   float dx = c.x - ax, dy = c.y - ay, dz = c.z - az;
                   if constexpr (W2) {
@@ -272,31 +287,42 @@ __global__ void __launch_bounds__(kCTS, 2) k_search(const double* __restrict__ x
                     if (st.wrap[1] == 2) dy = wrap1(dy, (float)g.L[1]);
                     if (st.wrap[2] == 2) dz = wrap1(dz, (float)g.L[2]);
                   }
-                  const float r = fmaf(dz, dz, fmaf(dy, dy, dx * dx));
-                  float l2 = lo, h2 = hi;
-                  if constexpr (SYM) {  // either side's support
-                    const float2 cb = candb[32 * q + k];
-                    l2 = fmaxf(l2, cb.x);
-                    h2 = fmaxf(h2, cb.y);
+                  return fmaf(dz, dz, fmaf(dy, dy, dx * dx));
+                };
+                if constexpr (!SYM) {
+                  // hit iff r2 < lo  <=>  fl(r2 - lo) < 0: the sign bit, funnel-shifted in
+                  // (candidate 31 first, so bit k ends at position k); a candidate inside
+                  // [lo, hi) has |fl(r2 - lo)| < wband, caught by the running minimum
+                  float mn = INFINITY;
+#pragma unroll
+                  for (int k = 31; k >= 0; --k) {
+                    const float d = r2of(k) - lo;
+                    in = __funnelshift_l(__float_as_uint(d), in, 1);
+                    mn = fminf(mn, fabsf(d));
                   }
-                  if (r < l2) in |= 1u << k;
-                  if (r < h2) near |= 1u << k;
-                }
-                if (!act) in = near = 0u;  // SYM: a padding lane must not pick up candidate bands
-                uint32_t amb = near & ~in;
-                if (__any_sync(0xffffffffu, amb != 0u)) {  // rare: exact fp64 test inside the band
-                  while (amb) {
-                    const uint32_t b = __ffs(amb) - 1;
-                    amb &= amb - 1;
-                    const uint32_t f = gb + 32u * q + b;
-                    const int kq = slot_of(S, f);
-                    const uint32_t j = S.t_start[kq] + (f - S.cum[kq]);
-                    double lim = T.lim;
-                    if constexpr (SYM) {
-                      const double thb = 2.0 * h[j];
-                      lim = fmax(lim, __dmul_rn(thb, thb));
+                  if (!act) in = 0u;
+                  const bool slow = mn < wband;
+                  if (__any_sync(0xffffffffu, slow) && slow) {
+                    for (int k = 0; k < 32; ++k)
+                      if (fabsf(r2of(k) - lo) < wband) in = exact((uint32_t)k) ? in | (1u << k) : in & ~(1u << k);
+                  }
+                } else {  // symmetric relation: either side's support, per-candidate band
+                  uint32_t near = 0u;
+#pragma unroll
+                  for (int k = 0; k < 32; ++k) {
+                    const float r = r2of(k);
+                    const float2 cb = candb[32 * q + k];
+                    if (r < fmaxf(lo, cb.x)) in |= 1u << k;
+                    if (r < fmaxf(hi, cb.y)) near |= 1u << k;
+                  }
+                  if (!act) in = near = 0u;  // a padding lane must not pick up candidate bands
+                  uint32_t amb = near & ~in;
+                  if (__any_sync(0xffffffffu, amb != 0u)) {
+                    while (amb) {
+                      const uint32_t b = __ffs(amb) - 1;
+                      amb &= amb - 1;
+                      if (exact(b)) in |= 1u << b;
                     }
-                    if (exact_hit(g, x, y, z, j, t, T.pos, lim)) in |= 1u << b;
                   }
                 }
                 if ((uint32_t)q == selfq) in &= ~selfbit;
@@ -339,22 +365,22 @@ __global__ void __launch_bounds__(kCTS, 2) k_search(const double* __restrict__ x
 }
 
 // Rows in place: segments (mask, first flat index) -> ascending flat indices.  A warp
-// per row: its segments are loaded into registers (lane k holds segments k, k + 32,
-// k + 64) before any entry is stored, their exclusive prefix is a warp scan, and each
-// segment is then written by the whole warp -- lane b stores the entry of bit b at
-// prefix + popc(mask below b) -- so every store instruction writes one contiguous run
-// of the row (coalesced; per-lane loops over bits scattered 32 rows per instruction,
-// or bank-conflicted in shared memory).  Rows whose count exceeds the stride are left
-// alone (the host grows the stride and reruns the search before anything reads them).
+// per row: the segments are read into registers (all of them before any entry is
+// written back), their exclusive prefix is a warp scan, each lane expands its own
+// segment into the warp's shared-memory row buffer (a shared-memory scatter: global
+// per-lane scatters touched ~20 sectors per store), and the row goes back to HBM in
+// 16-byte stores.  Rows longer than the stride are left alone (the host grows the
+// stride and reruns the search before anything reads them).
 constexpr int kExpWarps = 8;
-constexpr int kExpChunks = 3;  // segments held in registers: 96 = a 384-entry 16-bit row region
 template <typename E>
 __global__ void __launch_bounds__(32 * kExpWarps) k_expand_rows(unsigned char* __restrict__ rows, int64_t n,
                                                               const uint32_t* __restrict__ nseg,
                                                               const uint32_t* __restrict__ ncount, int maxn) {
-  const uint32_t lane = threadIdx.x & 31, lt = (1u << lane) - 1u;
+  extern __shared__ uint4 xsm[];
+  const uint32_t lane = threadIdx.x & 31;
   const int warp = threadIdx.x >> 5;
-  const size_t rbytes = (size_t)maxn * sizeof(E);
+  const size_t rbytes = (size_t)maxn * sizeof(E);  // a multiple of 16 (stride rounded to 32 entries)
+  E* const sout = reinterpret_cast<E*>(reinterpret_cast<unsigned char*>(xsm) + rbytes * warp);
   const int64_t stride = (int64_t)gridDim.x * kExpWarps;
   int64_t t = (int64_t)blockIdx.x * kExpWarps + warp;
   uint32_t ns = t < n ? nseg[t] : 0u, nc = t < n ? ncount[t] : 0u;
@@ -364,83 +390,29 @@ __global__ void __launch_bounds__(32 * kExpWarps) k_expand_rows(unsigned char* _
       ns = nseg[t + stride];
       nc = ncount[t + stride];
     }
-    if (cnc > (uint32_t)maxn) continue;
+    if (cnc > (uint32_t)maxn || (size_t)cns * sizeof(uint2) > rbytes) continue;
     unsigned char* const row = rows + (size_t)t * rbytes;
     const uint2* const gseg = reinterpret_cast<const uint2*>(row);
-    E* const out = reinterpret_cast<E*>(row);
-    uint2 sg[kExpChunks];
-    uint32_t incl[kExpChunks];
-    const uint32_t nchunk = (cns + 31) / 32;
-    if (nchunk > (uint32_t)kExpChunks) continue;  // grown rows: see k_expand_rows_wide
-#pragma unroll
-    for (int c = 0; c < kExpChunks; ++c) {
-      const uint32_t k = 32u * c + lane;
-      sg[c] = k < cns ? gseg[k] : make_uint2(0u, 0u);
-    }
     uint32_t carry = 0;
-#pragma unroll
-    for (int c = 0; c < kExpChunks; ++c) {  // exclusive prefix of every segment
-      const uint32_t pc = __popc(sg[c].x);
-      uint32_t v = pc;
-#pragma unroll
-      for (int o = 1; o < 32; o <<= 1) {
-        const uint32_t u = __shfl_up_sync(0xffffffffu, v, o);
-        if (lane >= (uint32_t)o) v += u;
-      }
-      incl[c] = carry + v - pc;
-      carry += __shfl_sync(0xffffffffu, v, 31);
-    }
-    __syncwarp();  // every segment is in registers: the row region may be overwritten
-#pragma unroll
-    for (int c = 0; c < kExpChunks; ++c) {
-      const uint32_t nj = min(32u, cns > 32u * c ? cns - 32u * c : 0u);
-      for (uint32_t j = 0; j < nj; ++j) {
-        const uint32_t m = __shfl_sync(0xffffffffu, sg[c].x, j);
-        const uint32_t fb = __shfl_sync(0xffffffffu, sg[c].y, j);
-        const uint32_t e = __shfl_sync(0xffffffffu, incl[c], j);
-        if (m & (1u << lane)) out[e + __popc(m & lt)] = (E)(fb + lane);
-      }
-    }
-  }
-}
-
-// The same for rows whose segments exceed the registers (a stride grown past 384):
-// segments are staged in shared memory first.
-template <typename E>
-__global__ void __launch_bounds__(32 * kExpWarps) k_expand_rows_wide(unsigned char* __restrict__ rows, int64_t n,
-                                                                   const uint32_t* __restrict__ nseg,
-                                                                   const uint32_t* __restrict__ ncount, int maxn) {
-  extern __shared__ uint2 xseg[];
-  const uint32_t lane = threadIdx.x & 31, lt = (1u << lane) - 1u;
-  const int warp = threadIdx.x >> 5;
-  const size_t rbytes = (size_t)maxn * sizeof(E);
-  uint2* const sseg = xseg + (rbytes / sizeof(uint2)) * warp;
-  for (int64_t t = (int64_t)blockIdx.x * kExpWarps + warp; t < n; t += (int64_t)gridDim.x * kExpWarps) {
-    const uint32_t ns = nseg[t], nc = ncount[t];
-    if (nc > (uint32_t)maxn || (ns + 31) / 32 <= (uint32_t)kExpChunks) continue;
-    unsigned char* const row = rows + (size_t)t * rbytes;
-    E* const out = reinterpret_cast<E*>(row);
-    for (uint32_t k = lane; k < ns; k += 32) sseg[k] = reinterpret_cast<const uint2*>(row)[k];
-    __syncwarp();
-    uint32_t carry = 0;
-    for (uint32_t k0 = 0; k0 < ns; k0 += 32) {
-      const uint2 sg = k0 + lane < ns ? sseg[k0 + lane] : make_uint2(0u, 0u);
+    for (uint32_t k0 = 0; k0 < cns; k0 += 32) {
+      const uint32_t k = k0 + lane;
+      const uint2 sg = k < cns ? gseg[k] : make_uint2(0u, 0u);
       const uint32_t pc = __popc(sg.x);
       uint32_t v = pc;
+#pragma unroll
       for (int o = 1; o < 32; o <<= 1) {
         const uint32_t u = __shfl_up_sync(0xffffffffu, v, o);
         if (lane >= (uint32_t)o) v += u;
       }
-      const uint32_t ex = carry + v - pc;
+      uint32_t pos = carry + v - pc;
+      for (uint32_t mm = sg.x; mm; mm &= mm - 1) sout[pos++] = (E)(sg.y + (uint32_t)(__ffs(mm) - 1));
       carry += __shfl_sync(0xffffffffu, v, 31);
-      const uint32_t nj = min(32u, ns - k0);
-      for (uint32_t j = 0; j < nj; ++j) {
-        const uint32_t m = __shfl_sync(0xffffffffu, sg.x, j);
-        const uint32_t fb = __shfl_sync(0xffffffffu, sg.y, j);
-        const uint32_t e = __shfl_sync(0xffffffffu, ex, j);
-        if (m & (1u << lane)) out[e + __popc(m & lt)] = (E)(fb + lane);
-      }
     }
+    __syncwarp();  // every segment was read and expanded: the row region may be overwritten
+    const uint32_t nv = (uint32_t)((cnc * sizeof(E) + 15) / 16);
+    uint4* const dst = reinterpret_cast<uint4*>(row);
+    const uint4* const src = reinterpret_cast<const uint4*>(sout);
+    for (uint32_t k = lane; k < nv; k += 32) dst[k] = src[k];
     __syncwarp();
   }
 }
@@ -465,15 +437,11 @@ static void search_t(sph_ctx* c, int gs, size_t smem, bool w2, bool sym) {
 
 template <typename E>
 static void expand_t(sph_ctx* c) {
+  const size_t smem = (size_t)kExpWarps * c->maxn_cap * sizeof(E);
+  cudaFuncSetAttribute(k_expand_rows<E>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   const int64_t blocks = std::min<int64_t>((c->P.n + kExpWarps - 1) / kExpWarps, (int64_t)c->num_sms * 8);
-  const int nb = (int)std::max<int64_t>(blocks, 1);
-  k_expand_rows<E><<<nb, 32 * kExpWarps, 0, c->stream>>>(c->s.nbr, c->P.n, c->s.nseg, c->s.ncount, c->maxn_cap);
-  if ((size_t)c->maxn_cap * sizeof(E) / sizeof(uint2) > 32u * kExpChunks) {  // grown rows
-    const size_t smem = (size_t)kExpWarps * c->maxn_cap * sizeof(E);
-    cudaFuncSetAttribute(k_expand_rows_wide<E>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    k_expand_rows_wide<E><<<nb, 32 * kExpWarps, smem, c->stream>>>(c->s.nbr, c->P.n, c->s.nseg, c->s.ncount,
-                                                                   c->maxn_cap);
-  }
+  k_expand_rows<E><<<(int)std::max<int64_t>(blocks, 1), 32 * kExpWarps, smem, c->stream>>>(
+      c->s.nbr, c->P.n, c->s.nseg, c->s.ncount, c->maxn_cap);
 }
 
 // segments -> rows in place (after the capacity check of the search's maxima)

@@ -117,6 +117,7 @@ struct Phase {
 template <class T>
 sph_status dalloc(sph_ctx* c, T** p, size_t count) {
   CK(cudaMalloc((void**)p, sizeof(T) * (count ? count : 1)));
+  c->mem_bytes += sizeof(T) * (count ? count : 1);
   return SPH_OK;
 }
 
@@ -305,6 +306,7 @@ sph_status sph_init(const sph_params* prm, int64_t capacity, sph_ctx** out) {
   AL(s.ct, 6 * cap);
   AL(s.mrec, 18 * cap);
   AL(s.nbr, cap * (int64_t)c->maxn_cap * (int64_t)sizeof(uint16_t));
+  c->maxn_cap_alloc = c->maxn_cap;
   AL(s.ncount, cap);
   AL(s.nseg, cap);
   AL(s.nbr_max, 3);
@@ -536,13 +538,18 @@ sph_status sph_find_neighbors(sph_ctx* c) {
     if (mx[1]) c->wide_rows = true;
     if (mx[0] > (unsigned)c->maxn_cap) c->maxn_cap = (int)(((mx[0] + mx[0] / 8) + 31) / 32 * 32);
     else if (mx[2]) c->maxn_cap *= 2;  // the segments did not fit the row region
+    const size_t old_bytes = (size_t)c->cap * c->maxn_cap_alloc * (c->wide_rows_alloc ? 4 : 2);
     CK(cudaFree(c->s.nbr));
     c->s.nbr = nullptr;
+    c->mem_bytes -= old_bytes;
     const size_t bytes = (size_t)c->cap * c->maxn_cap * (c->wide_rows ? 4 : 2);
     if (cudaMalloc((void**)&c->s.nbr, bytes) != cudaSuccess) {
       cudaGetLastError();
       return fail(c, SPH_ERR_CAPACITY, "neighbour rows: cannot allocate " + std::to_string(bytes) + " bytes");
     }
+    c->mem_bytes += bytes;
+    c->maxn_cap_alloc = c->maxn_cap;
+    c->wide_rows_alloc = c->wide_rows;
     Phase ph(c, SPH_PH_NEIGHBORS);
     int k = launch_search(c);
     CKL();
@@ -818,6 +825,12 @@ sph_status sph_diagnostics(sph_ctx* c, sph_diag* out) {
   if (cnt[CNT_NONFINITE]) return fail(c, SPH_ERR_NUMERIC, "non-finite dt encountered");
   if (badid != ~0ull)
     return fail(c, SPH_ERR_NUMERIC, "non-finite state of particle id " + std::to_string(badid));
+  return SPH_OK;
+}
+
+sph_status sph_memory_bytes(const sph_ctx* c, int64_t* bytes) {
+  if (!c || !bytes) return SPH_ERR_CONFIG;
+  *bytes = (int64_t)c->mem_bytes + (c->dist ? dist_memory_bytes(c) : 0);
   return SPH_OK;
 }
 

@@ -582,6 +582,13 @@ bool dist_init(sph_ctx* c, const sph_params* prm) {
   return true;
 }
 
+int64_t dist_memory_bytes(const sph_ctx* c) {
+  const Dist& D = *c->dist;
+  const int64_t cap = c->cap, G = D.G;
+  return (int64_t)(sizeof(unsigned long long) << kBinBits) + 8 * (4 * (G + 1) + G * (G + 1) + G + 16 + kCounters + 2) +
+         cap * (8 + 4 + 4) + D.xcap * (4 + 2 * 8 * 14);
+}
+
 void dist_destroy(sph_ctx* c) {
   Dist* D = c->dist;
   if (!D) return;

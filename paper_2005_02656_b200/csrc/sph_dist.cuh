@@ -42,6 +42,7 @@ inline int64_t dist_n_total(const sph_ctx* c) { return c->dist->n_total; }
 inline int64_t dist_n_halo(const sph_ctx* c) { return c->dist->n_halo; }
 inline unsigned long long* dist_counters(const sph_ctx* c) { return c->dist->cntred_d; }
 void dist_destroy(sph_ctx* c);
+int64_t dist_memory_bytes(const sph_ctx* c);
 bool dist_global_bbox(sph_ctx* c, double* bb_out, bool* bad_any);
 bool dist_splitters(sph_ctx* c);
 bool dist_migrate(sph_ctx* c, int64_t* nleave, int64_t* nrecv);

@@ -124,6 +124,9 @@ struct sph_ctx {
   int maxn = 0;             // user limit on neighbours per particle (0: none)
   int maxn_cap = 384;       // row stride (grows on demand up to the user limit)
   bool wide_rows = false;   // 32-bit row entries
+  int maxn_cap_alloc = 0;   // the stride / width the row buffer was allocated for
+  bool wide_rows_alloc = false;
+  size_t mem_bytes = 0;     // device memory the library allocated (sph_memory_bytes)
   sph_particles P{};
   bool attached = false;
   int stage = 0;            // 0 none, 1 neighbours, 2 density, 3 iad, 4 momentum

@@ -155,6 +155,8 @@ def lib():
         L.sph_measure_fp64_peak.argtypes = [vp, _P]
         L.sph_local_count.argtypes = [vp, C.POINTER(C.c_int64), C.POINTER(C.c_int64)]
         L.sph_local_count.restype = C.c_int
+        L.sph_memory_bytes.argtypes = [vp, C.POINTER(C.c_int64)]
+        L.sph_memory_bytes.restype = C.c_int
         L.sph_nccl_unique_id.argtypes = [vp, C.c_int]
         L.sph_nccl_unique_id.restype = C.c_int
         L.sph_local_comm_id.argtypes = [C.c_int, vp, C.c_int]
@@ -376,6 +378,12 @@ class Simulation:
         out = d.as_dict()
         out["status"] = st
         return out
+
+    def library_bytes(self) -> int:
+        """Device memory held by the library for this context (sph_memory_bytes)."""
+        b = C.c_int64(0)
+        self._check(lib().sph_memory_bytes(self._ctx, C.byref(b)))
+        return b.value
 
     def set_profiling(self, on: bool):
         self._check(lib().sph_set_profiling(self._ctx, int(on)))
