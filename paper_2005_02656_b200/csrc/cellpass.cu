@@ -41,16 +41,27 @@ __device__ __forceinline__ double sinc_dpoly(double t) {
   for (int k = kPolyTerms - 3; k >= 0; --k) p = fma(p, t, c_dpoly[k]);
   return p;
 }
-// Estrin form (dependency depth ~5 instead of 12) for the momentum pass, where four
-// warps per SMSP cannot hide the DFMA latency of a Horner chain (ncu "wait").
+// Even/odd split P(t) = E(t^2) + t O(t^2): two independent Horner chains of depth 6
+// in u = t^2 (dependency depth 8 instead of 12) for the momentum pass, where four
+// warps per SMSP cannot hide a single chain's DFMA latency (ncu "wait").  Every DFMA
+// takes its coefficient as a constant operand, so no register holds a coefficient
+// (an Estrin tree pairs two constants per DFMA and kept ten of them in registers).
 static_assert(kPolyTerms == 13, "Estrin scheme below is written for degree 12");
 __device__ __forceinline__ double sinc_poly_e(double t) {
-  const double* c = c_poly;
-  const double t2 = t * t, t4 = t2 * t2, t8 = t4 * t4;
-  const double q0 = fma(fma(c[3], t, c[2]), t2, fma(c[1], t, c[0]));
-  const double q1 = fma(fma(c[7], t, c[6]), t2, fma(c[5], t, c[4]));
-  const double q2 = fma(fma(c[11], t, c[10]), t2, fma(c[9], t, c[8]));
-  return fma(fma(c[12], t4, q2), t8, fma(q1, t4, q0));
+  const double u = t * t;
+  double e = c_poly[12], o = c_poly[11];
+  e = fma(e, u, c_poly[10]);
+  o = fma(o, u, c_poly[9]);
+  e = fma(e, u, c_poly[8]);
+  o = fma(o, u, c_poly[7]);
+  e = fma(e, u, c_poly[6]);
+  o = fma(o, u, c_poly[5]);
+  e = fma(e, u, c_poly[4]);
+  o = fma(o, u, c_poly[3]);
+  e = fma(e, u, c_poly[2]);
+  o = fma(o, u, c_poly[1]);
+  e = fma(e, u, c_poly[0]);
+  return fma(o, t, e);
 }
 // "inline x*x*x*x..."; N > 0 fixes the exponent at compile time
 template <int N>
@@ -310,6 +321,11 @@ __device__ __forceinline__ void stage2x2(const Grid& g, const CellSm& S, uint32_
   }
 }
 
+// The pass kernels' W2 flag selects the GENERAL variant, which checks the rare cases at
+// run time: periodic dims whose stencil spans every cell (per-pair minimum image) and
+// the symmetric neighbour relation (extra pairs with W(r, h_a) = 0).  The default
+// variant (W2 = false) carries neither test in its pair loop.
+//
 // minimum image only for periodic dims where the stencil spans every cell
 template <bool W2>
 __device__ __forceinline__ void delta3(const Stencil& st, const Grid& g, double& dx, double& dy,
@@ -400,7 +416,7 @@ __global__ void __launch_bounds__(kCTD, 1) k_density_c(
               double dx = p01.x - xa, dy = p01.y - ya, dz = p23.x - za;
               delta3<W2>(*st, *g, dx, dy, dz);
               const double tt = (dx * dx + dy * dy + dz * dz) * ih2a;
-              if (sym) ok = ok && tt < 4.0;  // symmetric extra pair: W(r, h_a) = 0
+              if (W2 && sym) ok = ok && tt < 4.0;  // symmetric extra pair: W(r, h_a) = 0
               const double P = sinc_poly(tt);
               const double Pn1 = ipow<N - 1 < 0 ? 0 : N - 1>(P, n - 1);
               const double dP = sinc_dpoly(tt);
@@ -544,7 +560,7 @@ __global__ void __launch_bounds__(kCTD, 1) k_iad_c(
               double dx = p01.x - xa, dy = p01.y - ya, dz = p23.x - za;
               delta3<W2>(*st, *g, dx, dy, dz);
               const double tt = (dx * dx + dy * dy + dz * dz) * ih2a;
-              if (sym) ok = ok && tt < 4.0;  // symmetric extra pair: W(r, h_a) = 0
+              if (W2 && sym) ok = ok && tt < 4.0;  // symmetric extra pair: W(r, h_a) = 0
               const double S_ = kern_S<KM, N, false>(tt, n, tab, K);
               const double w = p23.y * (ok ? S_ : 0.0);  // (m_b/rho_b) S
               const double wx = w * dx, wy = w * dy;
@@ -705,7 +721,7 @@ __global__ void __launch_bounds__(kCTM, 1) k_momentum_c(
   __shared__ uint32_t s_chunk;
   const int n = N > 0 ? N : ph.n;
   double dtmin = INFINITY;
-  unsigned long long ncoinc = 0;
+  uint32_t ncoinc = 0;
   __shared__ __align__(8) uint64_t mbar;  // staging: bulk copies complete on it
   __shared__ int s_wrap;
   uint32_t mphase = 0;
@@ -802,7 +818,7 @@ __global__ void __launch_bounds__(kCTM, 1) k_momentum_c(
             double alpha;
             int n, K, sym;
             const double* tab;
-            unsigned long long* ncoinc;
+            uint32_t* ncoinc;
             double xa, ya, za, vxa, vya, vza, ih2a, wBa, rinva, Xa, ca, a11, a12, a13, a22, a23, a33;
             double fx, fy, fz, fu, vs;
             __device__ __forceinline__ void begin(uint32_t i) {
@@ -827,7 +843,7 @@ __global__ void __launch_bounds__(kCTM, 1) k_momentum_c(
               *ncoinc += coinc;
               const double ta = r2 * ih2a;
               // symmetric extra pair (r >= 2 h_a): W(r, h_a) = 0, only the h_b terms remain
-              const double Sa = (sym && !(ta < 4.0)) ? 0.0 : kern_S<KM, N, true>(ta, n, tab, K);
+              const double Sa = (W2 && sym && !(ta < 4.0)) ? 0.0 : kern_S<KM, N, true>(ta, n, tab, K);
               const double Wa = wBa * Sa;
               const double tb = r2 * p3.y;
               double Sb = Sa;  // equal h: W(r, h_b) shares the kernel value
@@ -903,7 +919,7 @@ __global__ void __launch_bounds__(kCTM, 1) k_momentum_c(
   dtmin = -wmax(-dtmin);
   if (threadIdx.x == 0) shco = 0;
   __syncthreads();
-  if (ncoinc) atomicAdd(&shco, ncoinc);
+  if (ncoinc) atomicAdd(&shco, (unsigned long long)ncoinc);
   if (lane == 0) shdt[warp] = dtmin;
   __syncthreads();
   if (threadIdx.x == 0) {
@@ -950,7 +966,7 @@ static void density_t(sph_ctx* c) {
 // row type x kernel-mode x exponent x wrap dispatch of a pair pass
 #define SPH_DISPATCH_E(fn, E)                                                         \
   do {                                                                                \
-    const bool w2 = any_wrap2(c);                                                     \
+    const bool w2 = any_wrap2(c) || c->phys.sym; /* the general (rare-case) variant */ \
     const bool n6 = c->phys.n == 6;                                                   \
     switch (c->phys.kmode) {                                                          \
       case SPH_KERNEL_TABLE:                                                          \
