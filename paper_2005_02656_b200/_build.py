@@ -39,10 +39,11 @@ def deps():
 
 
 def build(force: bool = False, verbose: bool = False, csrc: str = CSRC, out: str = LIB) -> str:
+    """SPH_NVCC_EXTRA (env) adds flags, e.g. -D macros of A/B variant builds (tools/)."""
     newest = max(os.path.getmtime(p) for p in deps())
     if not force and os.path.exists(out) and os.path.getmtime(out) >= newest:
         return out
-    cmd = ["nvcc", *NVCC_FLAGS]
+    cmd = ["nvcc", *NVCC_FLAGS, *os.environ.get("SPH_NVCC_EXTRA", "").split()]
     inc, lib = _nccl_paths()
     if inc and lib:
         cmd += ["-DSPH_WITH_NCCL=1", f"-I{inc}", f"-L{lib}", "-l:libnccl.so.2",

@@ -179,6 +179,7 @@ __device__ __forceinline__ void walk_targets_half(uint32_t t0, uint32_t t1,
                                                   uint32_t pend, const uint32_t* cum, uint32_t gb,
                                                   uint32_t* s_next, Body&& body, Finish&& finish) {
   (void)cum;
+  uint32_t par = 0;  // body.fetch / body.begin: double-buffered per-half prefetch slot
   const int lane = threadIdx.x & 31, l16 = lane & 15;
   const unsigned hmask = (threadIdx.x & 16) ? 0xffff0000u : 0x0000ffffu;
   auto claim = [&]() {
@@ -194,6 +195,7 @@ __device__ __forceinline__ void walk_targets_half(uint32_t t0, uint32_t t1,
     f0 = row_chunk(r, c0, nn);
     f1 = row_chunk(r, c0 + 16, nn);
   }
+  body.fetch(t, par, t < t1);
   while (__any_sync(0xffffffffu, t < t1)) {
     const bool act = t < t1;
     const uint32_t i = act ? t - t0 : 0;
@@ -210,7 +212,9 @@ __device__ __forceinline__ void walk_targets_half(uint32_t t0, uint32_t t1,
       f0 = row_chunk(r, cn, nn);
       f1 = row_chunk(r, cn + 16, nn);
     }
-    if (act) body.begin(i);
+    body.fetch(tn, par ^ 1u, tn < t1);  // the next target's record lands while this one runs
+    if (act) body.begin(par);
+    par ^= 1u;
     bool live = act;
 #define SPH_HALF_STEP(R)                                                       \
   {                                                                            \
@@ -649,6 +653,12 @@ __device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t by
                : "memory");
 }
 __device__ __forceinline__ void fence_proxy_async() { asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory"); }
+// cp.async (LDGSTS): 16 bytes global -> shared, L2 only (.cg), grouped per thread
+__device__ __forceinline__ void cp_async16(void* dst, const void* src) {
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(smem_u32(dst)), "l"(src) : "memory");
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;\n" ::: "memory"); }
+__device__ __forceinline__ void cp_async_wait_prev() { asm volatile("cp.async.wait_group 1;\n" ::: "memory"); }
 
 struct MomSrc {  // per-particle arrays staged for the source side of a pair
   const double *x, *y, *z, *vx, *vy, *vz, *m, *ih2, *c, *mX, *mr;
@@ -662,9 +672,12 @@ struct MomOut {
   double *ax, *ay, *az, *du, *vsig;
 };
 // staged field slots (SoA, kMomCap doubles each)
-// staged source fields as double2 pairs (kMomPairs arrays of kMomCap):
+// staged source fields as double2 pairs (one 144-byte record per particle):
 //   0 (x, y)  1 (z, vx)  2 (vy, vz)  3 (m, 1/h^2)  4 (c, m X)  5 (m/rho, C~11)
-//   6 (C~12, C~13)  7 (C~22, C~23)  8 (C~33, -)
+//   6 (C~12, C~13)  7 (C~22, C~23)  8 (C~33, 1/m)
+// The TARGET side of a pair reads the target's own record too: X_a = (m X) (1/m),
+// 1/rho_a = (m/rho) (1/m), and A_ab(h_a) = C_a Delta W(r, h_a) = C~_a Delta S(r/h_a)
+// (C~ = (B/h^3) C), so no per-target table is staged.
 constexpr int kMomPairs = 9;
 
 // Momentum source records: the kMomPairs double2 a pair reads from its source, one
@@ -689,7 +702,7 @@ __global__ void __launch_bounds__(kRecThreads) k_mom_records(MomSrc src, int64_t
       r[5] = make_double2(src.mr[j], src.ct[j]);
       r[6] = make_double2(src.ct[cs + j], src.ct[2 * cs + j]);
       r[7] = make_double2(src.ct[3 * cs + j], src.ct[4 * cs + j]);
-      r[8] = make_double2(src.ct[5 * cs + j], 0.0);
+      r[8] = make_double2(src.ct[5 * cs + j], 1.0 / src.m[j]);  // 1/m: the target side derives X, 1/rho
     }
     __syncthreads();
     const int64_t cnt = min((int64_t)kRecThreads, n - b0) * kMomPairs;
@@ -698,8 +711,6 @@ __global__ void __launch_bounds__(kRecThreads) k_mom_records(MomSrc src, int64_t
     __syncthreads();
   }
 }
-// per-target smem fields
-enum { T_X, T_Y, T_Z, T_VX, T_VY, T_VZ, T_IH2, T_WB, T_RINV, T_XP, T_C, T_A11, T_A12, T_A13, T_A22, T_A23, T_A33, T_N };
 
 template <int N, bool W2, int KM, typename E>
 __global__ void __launch_bounds__(kCTM, 1) k_momentum_c(
@@ -709,9 +720,9 @@ __global__ void __launch_bounds__(kCTM, 1) k_momentum_c(
     const int4* __restrict__ urec, const uint32_t* __restrict__ nulist, uint32_t* __restrict__ work,
     const E* __restrict__ nbr, const uint32_t* __restrict__ ncount, int maxn, Phys ph,
     double* __restrict__ dts, unsigned long long* __restrict__ cnt, const double2* __restrict__ mrec) {
-  extern __shared__ double dsm[];  // kMomCap staged source records + T_N * kTgtU target fields
+  extern __shared__ double dsm[];  // kMomCap staged source records
   double2* const F2 = reinterpret_cast<double2*>(dsm);
-  double* const T = dsm + 2 * kMomPairs * kMomCap;
+  __shared__ double2 tslot[kNWM * 2][2][kMomPairs];  // per half-warp: the current / next target's record
   __shared__ CellSm S;
   __shared__ uint32_t s_n[kTgtU], s_cur[kTgtU];
   __shared__ double acc[5][kTgtU];
@@ -743,23 +754,6 @@ __global__ void __launch_bounds__(kCTM, 1) k_momentum_c(
           const uint32_t i = t - t0;
           s_n[i] = ncount[t];
           s_cur[i] = 0;
-          T[T_X * kTgtU + i] = src.x[t];
-          T[T_Y * kTgtU + i] = src.y[t];
-          T[T_Z * kTgtU + i] = src.z[t];
-          T[T_VX * kTgtU + i] = src.vx[t];
-          T[T_VY * kTgtU + i] = src.vy[t];
-          T[T_VZ * kTgtU + i] = src.vz[t];
-          T[T_IH2 * kTgtU + i] = src.ih2[t];
-          T[T_WB * kTgtU + i] = tg.wB[t];
-          T[T_RINV * kTgtU + i] = tg.rinv[t];
-          T[T_XP * kTgtU + i] = tg.X[t];
-          T[T_C * kTgtU + i] = src.c[t];
-          T[T_A11 * kTgtU + i] = tg.c11[t];
-          T[T_A12 * kTgtU + i] = tg.c12[t];
-          T[T_A13 * kTgtU + i] = tg.c13[t];
-          T[T_A22 * kTgtU + i] = tg.c22[t];
-          T[T_A23 * kTgtU + i] = tg.c23[t];
-          T[T_A33 * kTgtU + i] = tg.c33[t];
           acc[0][i] = 0.0;
           acc[1][i] = 0.0;
           acc[2][i] = 0.0;
@@ -812,22 +806,35 @@ __global__ void __launch_bounds__(kCTM, 1) k_momentum_c(
           }
           struct B {
             const double2* F2;
-            const double* T;
+            const double2* __restrict__ mrec;
+            double2 (*slot)[kMomPairs];  // this half-warp's two prefetch slots
             const Stencil* st;
             const Grid* g;
             double alpha;
             int n, K, sym;
             const double* tab;
             uint32_t* ncoinc;
-            double xa, ya, za, vxa, vya, vza, ih2a, wBa, rinva, Xa, ca, a11, a12, a13, a22, a23, a33;
+            double xa, ya, za, vxa, vya, vza, ih2a, rinva, Xa, ca, a11, a12, a13, a22, a23, a33;
             double fx, fy, fz, fu, vs;
-            __device__ __forceinline__ void begin(uint32_t i) {
-              xa = T[T_X * kTgtU + i]; ya = T[T_Y * kTgtU + i]; za = T[T_Z * kTgtU + i];
-              vxa = T[T_VX * kTgtU + i]; vya = T[T_VY * kTgtU + i]; vza = T[T_VZ * kTgtU + i];
-              ih2a = T[T_IH2 * kTgtU + i]; wBa = T[T_WB * kTgtU + i]; rinva = T[T_RINV * kTgtU + i];
-              Xa = T[T_XP * kTgtU + i]; ca = T[T_C * kTgtU + i];
-              a11 = T[T_A11 * kTgtU + i]; a12 = T[T_A12 * kTgtU + i]; a13 = T[T_A13 * kTgtU + i];
-              a22 = T[T_A22 * kTgtU + i]; a23 = T[T_A23 * kTgtU + i]; a33 = T[T_A33 * kTgtU + i];
+            // target t's record -> prefetch slot p (cp.async, 16 bytes per lane, 9 lanes);
+            // every call commits one group (empty when !valid), so begin's "all but the
+            // newest group" wait always means "this target's record has landed"
+            __device__ __forceinline__ void fetch(uint32_t t, uint32_t p, bool valid) {
+              const uint32_t l16 = threadIdx.x & 15;
+              if (valid && l16 < (uint32_t)kMomPairs) cp_async16(&slot[p][l16], mrec + (size_t)t * kMomPairs + l16);
+              cp_async_commit();
+            }
+            __device__ __forceinline__ void begin(uint32_t p) {
+              cp_async_wait_prev();
+              __syncwarp(0xffffffffu >> 16 << (threadIdx.x & 16));
+              const double2* r = slot[p];
+              const double2 r0 = r[0], r1 = r[1], r2 = r[2], r3 = r[3], r4 = r[4], r5 = r[5], r6 = r[6],
+                            r7 = r[7], r8 = r[8];
+              xa = r0.x; ya = r0.y; za = r1.x; vxa = r1.y; vya = r2.x; vza = r2.y;
+              ih2a = r3.y; ca = r4.x;
+              Xa = r4.y * r8.y;     // (m X) / m
+              rinva = r5.x * r8.y;  // (m / rho) / m
+              a11 = r5.y; a12 = r6.x; a13 = r6.y; a22 = r7.x; a23 = r7.y; a33 = r8.x;  // C~_a
               fx = fy = fz = fu = 0.0;
               vs = -1.0;
             }
@@ -844,11 +851,13 @@ __global__ void __launch_bounds__(kCTM, 1) k_momentum_c(
               const double ta = r2 * ih2a;
               // symmetric extra pair (r >= 2 h_a): W(r, h_a) = 0, only the h_b terms remain
               const double Sa = (W2 && sym && !(ta < 4.0)) ? 0.0 : kern_S<KM, N, true>(ta, n, tab, K);
-              const double Wa = wBa * Sa;
+              const double Wa = Sa;  // with u = C~_a Delta: A_ab(h_a) = Wa u
               const double tb = r2 * p3.y;
-              double Sb = Sa;  // equal h: W(r, h_b) shares the kernel value
-              if (tb != ta) Sb = tb < 4.0 ? kern_S<KM, N, true>(tb, n, tab, K) : 0.0;
-              // R5: A_ab(h_a) = C_a Delta W_ab(h_a) = Wa u;  R4: A_ab(h_b) = C~_b Delta S_b = Sb w
+              // W(r, h_b): evaluated unconditionally (a branch on h_b != h_a cost more than
+              // the second polynomial, A/B measured), zero outside its support
+              const double Sb0 = kern_S<KM, N, true>(tb, n, tab, K);
+              const double Sb = tb < 4.0 ? Sb0 : 0.0;
+              // R5: A_ab(h_a) = C~_a Delta S_a = Wa u;  R4: A_ab(h_b) = C~_b Delta S_b = Sb w
               const double ux = a11 * dx + a12 * dy + a13 * dz;
               const double uy = a12 * dx + a22 * dy + a23 * dz;
               const double uz = a13 * dx + a23 * dy + a33 * dz;
@@ -862,7 +871,11 @@ __global__ void __launch_bounds__(kCTM, 1) k_momentum_c(
               const double vabx = vxa - p1.y, vaby = vya - p2.x, vabz = vza - p2.y;
               const double vdotx = -(vabx * dx + vaby * dy + vabz * dz);  // v_ab . x_ab
               // Eq. 5: w_ab = v_ab . x_ab / |x_ab|, Pi' only when approaching
+#ifdef SPH_MOM_AV_ALWAYS  // A/B build: branch-free w (r2 = 0 only for Delta = 0, where vdotx = 0)
+              const double w = fmin(vdotx, 0.0) * rsqrt(fmax(r2, 1e-300));
+#else
               const double w = vdotx < 0.0 ? vdotx * rsqrt(r2) : 0.0;
+#endif
               const double vsab = ca + cb - 3.0 * w;  // v_sig; w == min(w, 0)
               const double hp = -0.25 * alpha * vsab * w;  // Pi'/2, Eq. 5
               vs = (!coinc && vsab > vs) ? vsab : vs;
@@ -879,7 +892,8 @@ __global__ void __launch_bounds__(kCTM, 1) k_momentum_c(
               fu += mb * fma(0.5 * hp, rinva, Xa) * Wa * vu + 0.5 * hp * mrb * Sb * vw;
             }
           } body;
-          body.F2 = F2; body.T = T; body.st = &st; body.g = &g; body.alpha = ph.alpha; body.n = n;
+          body.F2 = F2; body.mrec = mrec; body.slot = tslot[threadIdx.x >> 4];
+          body.st = &st; body.g = &g; body.alpha = ph.alpha; body.n = n;
           body.K = ph.tableK; body.tab = ph.table; body.sym = ph.sym;
           body.ncoinc = &ncoinc;
           walk_targets_half(t0, t1, nbr, maxn, s_n, s_cur, pend, S.cum, gb, &S.next[gi & 1], body,
@@ -901,7 +915,7 @@ __global__ void __launch_bounds__(kCTM, 1) k_momentum_c(
         for (uint32_t t = t0 + threadIdx.x; t < t1; t += blockDim.x) {
           const uint32_t i = t - t0;
           double vsig = acc[4][i];
-          if (vsig < 0.0) vsig = 2.0 * T[T_C * kTgtU + i];  // no interacting neighbour
+          if (vsig < 0.0) vsig = 2.0 * src.c[t];  // no interacting neighbour
           out.ax[t] = acc[0][i];
           out.ay[t] = acc[1][i];
           out.az[t] = acc[2][i];
@@ -1012,7 +1026,7 @@ int launch_iad(sph_ctx* c) {
 
 template <int N, bool W2, int KM, typename E>
 static void momentum_t(sph_ctx* c) {
-  const size_t smem = ((size_t)2 * kMomPairs * kMomCap + (size_t)T_N * kTgtU) * sizeof(double);
+  const size_t smem = (size_t)2 * kMomPairs * kMomCap * sizeof(double);
   set_smem(k_momentum_c<N, W2, KM, E>, smem);
   sph_particles& P = c->P;
   MomSrc src = {P.x, P.y, P.z, P.vx, P.vy, P.vz, P.m, c->s.ih2, P.c, c->s.mX, c->s.vol, c->s.ct, c->cap};

@@ -25,8 +25,11 @@ constexpr int kSearchTiles = kSearchCap / 32;
 constexpr int kSearchWords = kSearchTiles / 32;  // tile bitmask words
 constexpr int kDensCap = 4096;    // density: staged particles per group, 4 fp64 fields
 constexpr int kIadCap = 4096;     // IAD: the same fields
-constexpr int kMomCap = 992;      // momentum: staged 144-byte records per group (a 48-cell unit in 4 groups)
-constexpr int kCTM = 512;         // momentum CTA: 16 warps, one CTA per SM
+constexpr int kMomCap = 1312;     // momentum: staged 144-byte records per group (a 48-cell unit in 3 groups)
+#ifndef SPH_MOM_THREADS
+#define SPH_MOM_THREADS 512
+#endif
+constexpr int kCTM = SPH_MOM_THREADS;  // momentum CTA: 16 warps, one CTA per SM (A/B builds override)
 constexpr int kCTD = 1024;        // density / IAD CTA: 32 warps, one CTA per SM
 constexpr int kNWM = kCTM / 32;
 constexpr int kNWD = kCTD / 32;
