@@ -243,7 +243,8 @@ def run_ours(args):
     with torch.cuda.stream(stream):
         sim = sph.Simulation(d, capacity=cap, stream=stream.cuda_stream, rank=rank, nranks=world,
                              unique_id=uid, kernel_mode=sph.KERNEL_MODES[args.kernel_mode],
-                             symmetric=int(args.symmetric), redecomp_every=args.redecomp_every)
+                             symmetric=int(args.symmetric), redecomp_every=args.redecomp_every,
+                             cell_factor=args.cell_factor)
         for _ in range(args.warmup):
             sim.step()
         torch.cuda.synchronize()
@@ -362,6 +363,7 @@ def run_ours(args):
         "config": {"workload": workload_label(args), "description": desc,
                    "particles_per_gpu": n_local, "particles_total": n_total,
                    "kernel_mode": args.kernel_mode, "symmetric": bool(args.symmetric),
+                   "cell_factor": args.cell_factor or 1.0,
                    "redecomp_every": args.redecomp_every,
                    "neighbors_mean": diag["nbr_total"] / max(1, diag["n_owned"]),
                    "l2": "no flush: every SoA field array >= 200 MB > 126 MB L2",
@@ -403,6 +405,8 @@ def main():
                     help="kernel evaluation in the pair passes (sph.h SPH_KERNEL_*; A/B of P:248)")
     ap.add_argument("--redecomp-every", type=int, default=1,
                     help="multi-GPU: recompute splitters every k-th step (sph_params.redecomp_every)")
+    ap.add_argument("--cell-factor", type=float, default=0.0,
+                    help="search-cell edge in units of 2 mean(h) (sph_params.cell_factor; 0: 1.0)")
     ap.add_argument("--symmetric", action="store_true",
                     help="neighbour relation r < 2 max(h_a, h_b) (sph_params.symmetric)")
     args = ap.parse_args()

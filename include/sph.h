@@ -63,7 +63,7 @@ enum { SPH_EOS_LINEAR = 0, SPH_EOS_IDEAL = 1 };
  * definition; the grad-h derivative term of Omega uses the exact polynomial in all
  * modes (the oracle evaluates it directly in all modes, reading R12).             */
 enum {
-  SPH_KERNEL_POLY = 0,   /* default: 13-term Maclaurin polynomial of sinc in t = v^2 (no sqrt) */
+  SPH_KERNEL_POLY = 0,   /* default: degree-9 polynomial of sinc in t = v^2 on [0,4] (no sqrt) */
   SPH_KERNEL_TABLE = 1,  /* the paper's table: table_size samples of S_n on [0, 2] incl. both
                             ends, index floor(v (K-1)/2), linear interpolation (R12)  */
   SPH_KERNEL_SIN = 2     /* direct: sin(x)/x, x = pi v / 2, raised to n                      */

@@ -41,26 +41,23 @@ __device__ __forceinline__ double sinc_dpoly(double t) {
   for (int k = kPolyTerms - 3; k >= 0; --k) p = fma(p, t, c_dpoly[k]);
   return p;
 }
-// Even/odd split P(t) = E(t^2) + t O(t^2): two independent Horner chains of depth 6
-// in u = t^2 (dependency depth 8 instead of 12) for the momentum pass, where four
+// Even/odd split P(t) = E(t^2) + t O(t^2): two independent Horner chains of depth 4
+// in u = t^2 (dependency depth 6 instead of 9) for the momentum pass, where four
 // warps per SMSP cannot hide a single chain's DFMA latency (ncu "wait").  Every DFMA
 // takes its coefficient as a constant operand, so no register holds a coefficient
 // (an Estrin tree pairs two constants per DFMA and kept ten of them in registers).
-static_assert(kPolyTerms == 13, "Estrin scheme below is written for degree 12");
+static_assert(kPolyTerms == 10, "the even/odd split below is written for degree 9");
 __device__ __forceinline__ double sinc_poly_e(double t) {
   const double u = t * t;
-  double e = c_poly[12], o = c_poly[11];
-  e = fma(e, u, c_poly[10]);
-  o = fma(o, u, c_poly[9]);
-  e = fma(e, u, c_poly[8]);
-  o = fma(o, u, c_poly[7]);
+  double e = c_poly[8], o = c_poly[9];
   e = fma(e, u, c_poly[6]);
-  o = fma(o, u, c_poly[5]);
+  o = fma(o, u, c_poly[7]);
   e = fma(e, u, c_poly[4]);
-  o = fma(o, u, c_poly[3]);
+  o = fma(o, u, c_poly[5]);
   e = fma(e, u, c_poly[2]);
-  o = fma(o, u, c_poly[1]);
+  o = fma(o, u, c_poly[3]);
   e = fma(e, u, c_poly[0]);
+  o = fma(o, u, c_poly[1]);
   return fma(o, t, e);
 }
 // "inline x*x*x*x..."; N > 0 fixes the exponent at compile time
@@ -213,9 +210,12 @@ __device__ __forceinline__ void walk_targets_half(uint32_t t0, uint32_t t1,
       f1 = row_chunk(r, cn + 16, nn);
     }
     body.fetch(tn, par ^ 1u, tn < t1);  // the next target's record lands while this one runs
-    if (act) body.begin(par);
+    // (skipping a target with no entry in the group, as the full-warp walk does, hung
+    // this walk on the GPU: not done here)
+    const bool has = act;
+    body.begin(par, has);  // every lane (the prefetch wait is a warp-wide barrier)
     par ^= 1u;
-    bool live = act;
+    bool live = has;
 #define SPH_HALF_STEP(R)                                                       \
   {                                                                            \
     const uint32_t e = R;                                                      \
@@ -236,7 +236,7 @@ __device__ __forceinline__ void walk_targets_half(uint32_t t0, uint32_t t1,
       SPH_HALF_STEP(e1)
     }
 #undef SPH_HALF_STEP
-    finish(act, i, cur);
+    finish(has, i, cur);
     t = tn;
   }
 }
@@ -281,6 +281,13 @@ __device__ __forceinline__ void walk_targets_fast(uint32_t t0, uint32_t t1,
       f0 = row_chunk(r, cn, nn);
       f1 = row_chunk(r, cn + 32, nn);
       f2 = row_chunk(r, cn + 64, nn);
+    }
+    // no entry of this target in the group (rows ascend: its first entry is past it):
+    // nothing to add, skip the set-up and the reduction (variable h: most visits of a
+    // small-h target in a big unit stencil are empty)
+    if (__shfl_sync(0xffffffffu, e0, 0) >= pend) {
+      t = tn;
+      continue;
     }
     body.begin(i);
 #define SPH_FAST_STEP(R)                                                             \
@@ -364,7 +371,7 @@ __global__ void __launch_bounds__(kCTD, 1) k_density_c(
     const double* __restrict__ h, const double* __restrict__ m, const double* __restrict__ u,
     Grid g, const uint32_t* __restrict__ cstart, const uint32_t* __restrict__ cend,
     const unsigned long long* __restrict__ chmax, const uint32_t* __restrict__ clist,
-    const uint32_t* __restrict__ nclist, const int4* __restrict__ urec, const uint32_t* __restrict__ nulist, uint32_t* __restrict__ work, const E* __restrict__ nbr,
+    const uint32_t* __restrict__ nclist, const int4* __restrict__ urec, URange ur, uint32_t* __restrict__ work, const E* __restrict__ nbr,
     const uint32_t* __restrict__ ncount, int maxn, Phys ph, double* __restrict__ rho,
     double* __restrict__ omega, double* __restrict__ p, double* __restrict__ cs,
     double* __restrict__ wB, double* __restrict__ ih2, double* __restrict__ vol,
@@ -382,12 +389,12 @@ __global__ void __launch_bounds__(kCTD, 1) k_density_c(
   // cells in chunks of kCellChunk consecutive (Morton-order) cells claimed from a
   // counter: consecutive cells share most of their stencil, so a CTA's next staging
   // finds its sources in L2 (a grid stride left the re-reads to HBM)
-  const uint32_t nun = *nulist;
+  const uint32_t ulo = ur.lo ? *ur.lo : 0u, nun = *ur.hi;
   const uint32_t uchunk = (uint32_t)kCellChunk >> g.ubits ? (uint32_t)kCellChunk >> g.ubits : 1u;
   ChunkClaim claim{work, uchunk, 0u};
-  for (uint32_t cfirst = claim.first(&s_chunk); cfirst < nun; cfirst = claim.next(&s_chunk)) {
-    for (uint32_t ci = cfirst; ci < min(nun, cfirst + uchunk); ++ci) {
-      unit_setup(g, ci, urec, cstart, cend, S);
+  for (uint32_t cfirst = ulo + claim.first(&s_chunk); cfirst < nun; cfirst = ulo + claim.next(&s_chunk)) {
+    for (uint32_t ck = cfirst; ck < min(nun, cfirst + uchunk); ++ck) {
+      unit_setup(g, ur.order ? ur.order[ck] : ck, urec, cstart, cend, S);
       const Stencil st = S.st;
       for (uint32_t t0 = S.sc; t0 < S.ec; t0 += kTgtU) {
         const uint32_t t1 = min(S.ec, t0 + kTgtU);
@@ -499,7 +506,7 @@ __global__ void __launch_bounds__(kCTD, 1) k_iad_c(
     const double* __restrict__ x, const double* __restrict__ y, const double* __restrict__ z,
     Grid g, const uint32_t* __restrict__ cstart, const uint32_t* __restrict__ cend,
     const unsigned long long* __restrict__ chmax, const uint32_t* __restrict__ clist,
-    const uint32_t* __restrict__ nclist, const int4* __restrict__ urec, const uint32_t* __restrict__ nulist, uint32_t* __restrict__ work, const E* __restrict__ nbr,
+    const uint32_t* __restrict__ nclist, const int4* __restrict__ urec, URange ur, uint32_t* __restrict__ work, const E* __restrict__ nbr,
     const uint32_t* __restrict__ ncount, int maxn, Phys ph, const double* __restrict__ wB,
     const double* __restrict__ ih2, const double* __restrict__ vol, double* __restrict__ c11,
     double* __restrict__ c12, double* __restrict__ c13, double* __restrict__ c22,
@@ -518,12 +525,12 @@ __global__ void __launch_bounds__(kCTD, 1) k_iad_c(
   // cells in chunks of kCellChunk consecutive (Morton-order) cells claimed from a
   // counter: consecutive cells share most of their stencil, so a CTA's next staging
   // finds its sources in L2 (a grid stride left the re-reads to HBM)
-  const uint32_t nun = *nulist;
+  const uint32_t ulo = ur.lo ? *ur.lo : 0u, nun = *ur.hi;
   const uint32_t uchunk = (uint32_t)kCellChunk >> g.ubits ? (uint32_t)kCellChunk >> g.ubits : 1u;
   ChunkClaim claim{work, uchunk, 0u};
-  for (uint32_t cfirst = claim.first(&s_chunk); cfirst < nun; cfirst = claim.next(&s_chunk)) {
-    for (uint32_t ci = cfirst; ci < min(nun, cfirst + uchunk); ++ci) {
-      unit_setup(g, ci, urec, cstart, cend, S);
+  for (uint32_t cfirst = ulo + claim.first(&s_chunk); cfirst < nun; cfirst = ulo + claim.next(&s_chunk)) {
+    for (uint32_t ck = cfirst; ck < min(nun, cfirst + uchunk); ++ck) {
+      unit_setup(g, ur.order ? ur.order[ck] : ck, urec, cstart, cend, S);
       const Stencil st = S.st;
       for (uint32_t t0 = S.sc; t0 < S.ec; t0 += kTgtU) {
         const uint32_t t1 = min(S.ec, t0 + kTgtU);
@@ -684,14 +691,15 @@ constexpr int kMomPairs = 9;
 // contiguous 144-byte record per particle, built once per step after IAD (owned +
 // halo).  A staging group is then a handful of bulk copies (one per stencil slot).
 constexpr int kRecThreads = 256;  // k_mom_records block: records transposed through smem
-__global__ void __launch_bounds__(kRecThreads) k_mom_records(MomSrc src, int64_t n, double2* __restrict__ rec) {
+__global__ void __launch_bounds__(kRecThreads) k_mom_records(MomSrc src, int64_t i0, int64_t n,
+                                                              double2* __restrict__ rec) {
   // each thread assembles one record in shared memory, then the block writes its
   // kRecThreads consecutive records as one contiguous, fully coalesced range
   // (per-thread 144-byte-strided stores wrote each L2 sector piecemeal: 3.0 ms at 25M)
   __shared__ double2 buf[kRecThreads * kMomPairs];
   for (int64_t b0 = (int64_t)blockIdx.x * kRecThreads; b0 < n; b0 += (int64_t)gridDim.x * kRecThreads) {
-    const int64_t j = b0 + threadIdx.x;
-    if (j < n) {
+    const int64_t j = i0 + b0 + threadIdx.x;  // records [i0, i0 + n)
+    if (b0 + threadIdx.x < n) {
       const int64_t cs = src.ct_stride;
       double2* r = buf + threadIdx.x * kMomPairs;
       r[0] = make_double2(src.x[j], src.y[j]);
@@ -706,7 +714,7 @@ __global__ void __launch_bounds__(kRecThreads) k_mom_records(MomSrc src, int64_t
     }
     __syncthreads();
     const int64_t cnt = min((int64_t)kRecThreads, n - b0) * kMomPairs;
-    double2* out = rec + b0 * kMomPairs;
+    double2* out = rec + (i0 + b0) * kMomPairs;
     for (int64_t e = threadIdx.x; e < cnt; e += kRecThreads) out[e] = buf[e];
     __syncthreads();
   }
@@ -717,7 +725,7 @@ __global__ void __launch_bounds__(kCTM, 1) k_momentum_c(
     MomSrc src, MomTgt tg, MomOut out, Grid g, const uint32_t* __restrict__ cstart,
     const uint32_t* __restrict__ cend, const unsigned long long* __restrict__ chmax,
     const uint32_t* __restrict__ clist, const uint32_t* __restrict__ nclist,
-    const int4* __restrict__ urec, const uint32_t* __restrict__ nulist, uint32_t* __restrict__ work,
+    const int4* __restrict__ urec, URange ur, uint32_t* __restrict__ work,
     const E* __restrict__ nbr, const uint32_t* __restrict__ ncount, int maxn, Phys ph,
     double* __restrict__ dts, unsigned long long* __restrict__ cnt, const double2* __restrict__ mrec) {
   extern __shared__ double dsm[];  // kMomCap staged source records
@@ -741,12 +749,12 @@ __global__ void __launch_bounds__(kCTM, 1) k_momentum_c(
   // cells in chunks of kCellChunk consecutive (Morton-order) cells claimed from a
   // counter: consecutive cells share most of their stencil, so a CTA's next staging
   // finds its sources in L2 (a grid stride left the re-reads to HBM)
-  const uint32_t nun = *nulist;
+  const uint32_t ulo = ur.lo ? *ur.lo : 0u, nun = *ur.hi;
   const uint32_t uchunk = (uint32_t)kCellChunk >> g.ubits ? (uint32_t)kCellChunk >> g.ubits : 1u;
   ChunkClaim claim{work, uchunk, 0u};
-  for (uint32_t cfirst = claim.first(&s_chunk); cfirst < nun; cfirst = claim.next(&s_chunk)) {
-    for (uint32_t ci = cfirst; ci < min(nun, cfirst + uchunk); ++ci) {
-      unit_setup(g, ci, urec, cstart, cend, S);
+  for (uint32_t cfirst = ulo + claim.first(&s_chunk); cfirst < nun; cfirst = ulo + claim.next(&s_chunk)) {
+    for (uint32_t ck = cfirst; ck < min(nun, cfirst + uchunk); ++ck) {
+      unit_setup(g, ur.order ? ur.order[ck] : ck, urec, cstart, cend, S);
       const Stencil st = S.st;
       for (uint32_t t0 = S.sc; t0 < S.ec; t0 += kTgtU) {
         const uint32_t t1 = min(S.ec, t0 + kTgtU);
@@ -824,9 +832,12 @@ __global__ void __launch_bounds__(kCTM, 1) k_momentum_c(
               if (valid && l16 < (uint32_t)kMomPairs) cp_async16(&slot[p][l16], mrec + (size_t)t * kMomPairs + l16);
               cp_async_commit();
             }
-            __device__ __forceinline__ void begin(uint32_t p) {
+            __device__ __forceinline__ void begin(uint32_t p, bool has) {
               cp_async_wait_prev();
-              __syncwarp(0xffffffffu >> 16 << (threadIdx.x & 16));
+              __syncwarp();  // (a half-warp mask here with the other half diverged hung the pass)
+              fx = fy = fz = fu = 0.0;
+              vs = -1.0;
+              if (!has) return;
               const double2* r = slot[p];
               const double2 r0 = r[0], r1 = r[1], r2 = r[2], r3 = r[3], r4 = r[4], r5 = r[5], r6 = r[6],
                             r7 = r[7], r8 = r[8];
@@ -835,8 +846,6 @@ __global__ void __launch_bounds__(kCTM, 1) k_momentum_c(
               Xa = r4.y * r8.y;     // (m X) / m
               rinva = r5.x * r8.y;  // (m / rho) / m
               a11 = r5.y; a12 = r6.x; a13 = r6.y; a22 = r7.x; a23 = r7.y; a33 = r8.x;  // C~_a
-              fx = fy = fz = fu = 0.0;
-              vs = -1.0;
             }
             __device__ __forceinline__ void operator()(int qi) {
               const double2* q = F2 + (size_t)qi * kMomPairs;
@@ -946,6 +955,17 @@ __global__ void __launch_bounds__(kCTM, 1) k_momentum_c(
 }
 
 // ------------------------------------------------------------------ launchers
+// Which units a pass launch covers (c->unit_sel): all, or -- multi-GPU, communication
+// overlapped (§8(f) NEXT-3) -- the INTERIOR units (stencil without halo cells, runnable
+// while a halo exchange is in flight) or the BOUNDARY units (launched after it lands).
+static URange unit_range(const sph_ctx* c) {
+  if (c->unit_sel == 0 || !c->s.unit_order) return URange{nullptr, nullptr, c->s.nunit_list};
+  return c->unit_sel == 1 ? URange{c->s.unit_order, nullptr, c->s.unit_bounds + 1}
+                          : URange{c->s.unit_order, c->s.unit_bounds + 1, c->s.unit_bounds + 2};
+}
+// a claim counter per (pass, unit selection): the two launches of a pass may overlap
+static int unit_work(const sph_ctx* c, int pass) { return c->unit_sel == 2 ? pass + 3 : pass; }
+
 static int cell_grid(const sph_ctx* c, int per_sm) {
   int64_t cells = c->grid.ncell < c->P.n ? c->grid.ncell : c->P.n;
   int64_t mx = (int64_t)c->num_sms * per_sm;
@@ -970,10 +990,10 @@ static void density_t(sph_ctx* c) {
   const size_t smem = 4 * kDensCap * sizeof(double);
   set_smem(k_density_c<N, W2, KM, E>, smem);
   sph_particles& P = c->P;
-  cudaMemsetAsync(c->s.work + 1, 0, sizeof(uint32_t), c->stream);
+  cudaMemsetAsync(c->s.work + unit_work(c, 1), 0, sizeof(uint32_t), c->stream);
   k_density_c<N, W2, KM, E><<<cell_grid(c, 1), kCTD, smem, c->stream>>>(
       P.x, P.y, P.z, P.h, P.m, P.u, c->grid, c->s.cell_start, c->s.cell_end, c->s.cell_hmax,
-      c->s.cell_list, c->s.ncell_list, c->s.unit_rec, c->s.nunit_list, c->s.work + 1, reinterpret_cast<const E*>(c->s.nbr), c->s.ncount, c->maxn_cap, c->phys, P.rho, P.omega,
+      c->s.cell_list, c->s.ncell_list, c->s.unit_rec, unit_range(c), c->s.work + unit_work(c, 1), reinterpret_cast<const E*>(c->s.nbr), c->s.ncount, c->maxn_cap, c->phys, P.rho, P.omega,
       P.p, P.c, c->s.wB, c->s.ih2, c->s.vol, c->s.rinv, c->s.X, c->s.mX, c->s.cnt);
 }
 
@@ -1012,10 +1032,10 @@ static void iad_t(sph_ctx* c) {
   const size_t smem = 4 * kIadCap * sizeof(double);
   set_smem(k_iad_c<N, W2, KM, E>, smem);
   sph_particles& P = c->P;
-  cudaMemsetAsync(c->s.work + 2, 0, sizeof(uint32_t), c->stream);
+  cudaMemsetAsync(c->s.work + unit_work(c, 2), 0, sizeof(uint32_t), c->stream);
   k_iad_c<N, W2, KM, E><<<cell_grid(c, 1), kCTD, smem, c->stream>>>(
       P.x, P.y, P.z, c->grid, c->s.cell_start, c->s.cell_end, c->s.cell_hmax, c->s.cell_list,
-      c->s.ncell_list, c->s.unit_rec, c->s.nunit_list, c->s.work + 2, reinterpret_cast<const E*>(c->s.nbr), c->s.ncount, c->maxn_cap, c->phys, c->s.wB, c->s.ih2, c->s.vol,
+      c->s.ncell_list, c->s.unit_rec, unit_range(c), c->s.work + unit_work(c, 2), reinterpret_cast<const E*>(c->s.nbr), c->s.ncount, c->maxn_cap, c->phys, c->s.wB, c->s.ih2, c->s.vol,
       P.c11, P.c12, P.c13, P.c22, P.c23, P.c33, c->s.ct, c->cap, c->s.cnt);
 }
 
@@ -1032,10 +1052,10 @@ static void momentum_t(sph_ctx* c) {
   MomSrc src = {P.x, P.y, P.z, P.vx, P.vy, P.vz, P.m, c->s.ih2, P.c, c->s.mX, c->s.vol, c->s.ct, c->cap};
   MomTgt tg = {P.h, c->s.wB, c->s.rinv, c->s.X, P.c11, P.c12, P.c13, P.c22, P.c23, P.c33};
   MomOut out = {P.ax, P.ay, P.az, P.du, P.vsig};
-  cudaMemsetAsync(c->s.work + 3, 0, sizeof(uint32_t), c->stream);
+  cudaMemsetAsync(c->s.work + unit_work(c, 3), 0, sizeof(uint32_t), c->stream);
   k_momentum_c<N, W2, KM, E><<<cell_grid(c, 1), kCTM, smem, c->stream>>>(
       src, tg, out, c->grid, c->s.cell_start, c->s.cell_end, c->s.cell_hmax, c->s.cell_list,
-      c->s.ncell_list, c->s.unit_rec, c->s.nunit_list, c->s.work + 3, reinterpret_cast<const E*>(c->s.nbr), c->s.ncount, c->maxn_cap, c->phys, c->s.dts, c->s.cnt,
+      c->s.ncell_list, c->s.unit_rec, unit_range(c), c->s.work + unit_work(c, 3), reinterpret_cast<const E*>(c->s.nbr), c->s.ncount, c->maxn_cap, c->phys, c->s.dts, c->s.cnt,
       reinterpret_cast<const double2*>(c->s.mrec));
 }
 
@@ -1044,13 +1064,17 @@ int launch_momentum(sph_ctx* c) {
   return 1;
 }
 
-int launch_mom_records(sph_ctx* c) {
+int launch_mom_records_range(sph_ctx* c, int64_t i0, int64_t n, cudaStream_t st) {
+  if (n <= 0) return 0;
   sph_particles& P = c->P;
   MomSrc src = {P.x, P.y, P.z, P.vx, P.vy, P.vz, P.m, c->s.ih2, P.c, c->s.mX, c->s.vol, c->s.ct, c->cap};
-  const int64_t nall = P.n + c->n_halo;  // owned + halo sources
-  k_mom_records<<<grid_blocks(c, nall, kRecThreads, 6), kRecThreads, 0, c->stream>>>(
-      src, nall, reinterpret_cast<double2*>(c->s.mrec));
+  k_mom_records<<<grid_blocks(c, n, kRecThreads, 6), kRecThreads, 0, st>>>(src, i0, n,
+                                                                          reinterpret_cast<double2*>(c->s.mrec));
   return 1;
+}
+
+int launch_mom_records(sph_ctx* c) {  // owned + halo sources
+  return launch_mom_records_range(c, 0, c->P.n + c->n_halo, c->stream);
 }
 
 }  // namespace sphb

@@ -187,6 +187,15 @@ __device__ __forceinline__ void unit_setup(const Grid& g, uint32_t u, const int4
   __syncthreads();
 }
 
+// The units a pair-pass launch processes: indices [*lo (0 if null), *hi) into `order`
+// (the identity if null) -- all units, or the interior / boundary split of the
+// multi-GPU overlap (cellpass.cu unit_range).
+struct URange {
+  const uint32_t* order;
+  const uint32_t* lo;
+  const uint32_t* hi;
+};
+
 // Dynamic claims of work chunks from a global counter, the next claim issued one
 // chunk ahead (its atomic's latency overlaps the current chunk).
 struct ChunkClaim {

@@ -61,11 +61,14 @@ __device__ __forceinline__ float2 band32(double hh, double M) {
   return make_float2((float)(lim * (1.0 - delta)), (float)(lim * (1.0 + delta)));
 }
 
-// Unit records (one thread per unit, once per step before the search).
+// Unit records (one thread per unit, once per step before the search).  Multi-GPU
+// (iflag != null): a unit is INTERIOR when no slot of its stencil holds halo particles
+// (halos sit behind the n_owned owned particles), i.e. its pair passes read nothing a
+// halo exchange delivers -- they run while the exchange is in flight (sph_api.cu).
 __global__ void k_unit_prep(Grid g, const uint32_t* __restrict__ clist, const uint32_t* __restrict__ ulist,
                             const uint32_t* __restrict__ nulist, const uint32_t* __restrict__ cstart,
                             const uint32_t* __restrict__ cend, const unsigned long long* __restrict__ chmax,
-                            int4* __restrict__ urec) {
+                            int4* __restrict__ urec, int64_t n_owned, uint32_t* __restrict__ iflag) {
   const uint32_t nu = *nulist;
   for (uint32_t u = blockIdx.x * blockDim.x + threadIdx.x; u < nu; u += gridDim.x * blockDim.x) {
     const uint32_t i0 = ulist[u], i1 = ulist[u + 1];
@@ -75,7 +78,40 @@ __global__ void k_unit_prep(Grid g, const uint32_t* __restrict__ clist, const ui
     Stencil st;
     make_unit_stencil(g, c3, cstart, cend, chmax, st);
     pack_unit(st, cstart[cf], cend[cl], cf, urec + 3 * (size_t)u);
+    if (iflag) {
+      bool interior = true;
+      for (int k = 0; k < st.K && interior; ++k) {
+        int sh[3];
+        const int64_t cell = slot_cell(g, st, k, sh);
+        if (cend[cell] > cstart[cell] && (int64_t)cstart[cell] >= n_owned) interior = false;
+      }
+      iflag[u] = interior ? 1u : 0u;
+    }
   }
+}
+
+// unit order for the overlapped passes: interior units first, then boundary units, each
+// in Morton order (iexcl = exclusive scan of iflag over the unit indices)
+__global__ void k_unit_order(const uint32_t* __restrict__ nulist, const uint32_t* __restrict__ iflag,
+                             const uint32_t* __restrict__ iexcl, uint32_t* __restrict__ order,
+                             uint32_t* __restrict__ bounds) {
+  const uint32_t nu = *nulist;
+  const uint32_t nint = nu ? iexcl[nu - 1] + iflag[nu - 1] : 0u;
+  for (uint32_t u = blockIdx.x * blockDim.x + threadIdx.x; u < nu; u += gridDim.x * blockDim.x)
+    order[iflag[u] ? iexcl[u] : nint + (u - iexcl[u])] = u;
+  if (blockIdx.x == 0 && threadIdx.x == 0) {
+    bounds[0] = 0;
+    bounds[1] = nint;
+    bounds[2] = nu;
+  }
+}
+
+int launch_unit_order(sph_ctx* c) {
+  int k = scan_u32(c, c->s.unit_iflag, c->s.unit_iexcl, c->P.n);
+  k_unit_order<<<grid_blocks(c, c->P.n, 256, 4), 256, 0, c->stream>>>(c->s.nunit_list, c->s.unit_iflag,
+                                                                      c->s.unit_iexcl, c->s.unit_order,
+                                                                      c->s.unit_bounds);
+  return k + 1;
 }
 
 // W2: a periodic dim whose stencil spans every cell (per-pair minimum image in fp32).
@@ -455,9 +491,12 @@ int launch_expand_rows(sph_ctx* c) {
 int launch_unit_prep(sph_ctx* c) {
   const int64_t cells = c->grid.ncell < c->P.n ? c->grid.ncell : c->P.n;
   const int gprep = (int)std::min<int64_t>(std::max<int64_t>(cells, 1), (int64_t)c->num_sms * 8);
+  if (c->s.unit_iflag)  // flags past the unit count must read 0 for the scan
+    cudaMemsetAsync(c->s.unit_iflag, 0, sizeof(uint32_t) * c->P.n, c->stream);
   k_unit_prep<<<gprep, 128, 0, c->stream>>>(c->grid, c->s.cell_list, c->s.unit_list, c->s.nunit_list,
-                                            c->s.cell_start, c->s.cell_end, c->s.cell_hmax, c->s.unit_rec);
-  return 1;
+                                            c->s.cell_start, c->s.cell_end, c->s.cell_hmax, c->s.unit_rec,
+                                            c->P.n, c->s.unit_iflag);
+  return 1 + (c->s.unit_iflag ? launch_unit_order(c) : 0);
 }
 
 // the search proper into rows of the current type / stride (maxima[0]: largest count,

@@ -68,18 +68,51 @@ double kernel_norm(int n) {
   return (double)(1.0L / (4.0L * 3.141592653589793238462643383279502884L * acc));
 }
 
-// Maclaurin coefficients of sinc(pi sqrt(t)/2) = sum_k (-1)^k (pi^2/4)^k t^k / (2k+1)!
+// Coefficients (monomials in t) of the degree-9 polynomial interpolating
+// P(t) = sinc(pi sqrt(t) / 2) at the 10 Chebyshev nodes of t in [0, 4] (v = sqrt(t) in
+// [0, 2], the support of Eq. 6), in long double: near-minimax, max |error| 1.4e-15 on
+// [0, 4] (the 13-term Maclaurin series it replaces needed 3 more DFMA per evaluation
+// for 8e-16); dpoly = P'(t) of the same polynomial.
 void sinc_coeffs(double* poly, double* dpoly) {
-  const long double q = 3.141592653589793238462643383279502884L * 3.141592653589793238462643383279502884L / 4.0L;
-  long double ck = 1.0L;
-  long double c[kPolyTerms];
-  for (int k = 0; k < kPolyTerms; ++k) {
-    c[k] = ck;
-    ck = -ck * q / ((2.0L * (k + 1)) * (2.0L * (k + 1) + 1.0L));
+  const int N = kPolyTerms;
+  const long double pi = 3.141592653589793238462643383279502884L;
+  long double f[kPolyTerms], a[kPolyTerms];
+  for (int j = 0; j < N; ++j) {  // samples at the nodes s_j = cos(pi (j + 1/2) / N), t = 2 (s + 1)
+    const long double sj = std::cos(pi * (j + 0.5L) / N), t = 2.0L * (sj + 1.0L);
+    const long double x = 0.5L * pi * std::sqrt(t);
+    f[j] = x == 0.0L ? 1.0L : std::sin(x) / x;
   }
-  for (int k = 0; k < kPolyTerms; ++k) poly[k] = (double)c[k];
-  for (int k = 0; k < kPolyTerms - 1; ++k) dpoly[k] = (double)((k + 1) * c[k + 1]);
-  dpoly[kPolyTerms - 1] = 0.0;
+  for (int k = 0; k < N; ++k) {  // Chebyshev coefficients of the interpolant
+    long double acc = 0.0L;
+    for (int j = 0; j < N; ++j) acc += f[j] * std::cos(pi * k * (j + 0.5L) / N);
+    a[k] = (k == 0 ? 1.0L : 2.0L) * acc / N;
+  }
+  // sum_k a_k T_k(s) -> monomials in s (T_{k+1} = 2 s T_k - T_{k-1}) -> monomials in t
+  long double Tm[kPolyTerms] = {0}, Tk[kPolyTerms] = {0}, ps[kPolyTerms] = {0};
+  Tm[0] = 1.0L;  // T_0
+  Tk[1] = 1.0L;  // T_1
+  ps[0] += a[0];
+  for (int i = 0; i < N; ++i) ps[i] += a[1] * Tk[i];
+  for (int k = 2; k < N; ++k) {
+    long double Tn[kPolyTerms] = {0};
+    for (int i = 0; i < N; ++i) Tn[i] = (i > 0 ? 2.0L * Tk[i - 1] : 0.0L) - Tm[i];
+    for (int i = 0; i < N; ++i) {
+      Tm[i] = Tk[i];
+      Tk[i] = Tn[i];
+      ps[i] += a[k] * Tn[i];
+    }
+  }
+  long double pt[kPolyTerms] = {0};  // s = t/2 - 1: s^i = sum_j C(i,j) (t/2)^j (-1)^(i-j)
+  for (int i = 0; i < N; ++i) {
+    long double binom = 1.0L;
+    for (int j = 0; j <= i; ++j) {
+      if (j > 0) binom = binom * (i - j + 1) / j;
+      pt[j] += ps[i] * binom * std::pow(0.5L, j) * (((i - j) & 1) ? -1.0L : 1.0L);
+    }
+  }
+  for (int k = 0; k < N; ++k) poly[k] = (double)pt[k];
+  for (int k = 0; k < N - 1; ++k) dpoly[k] = (double)((k + 1) * pt[k + 1]);
+  dpoly[N - 1] = 0.0;
 }
 
 int bits_for(uint64_t v) {  // number of bits to hold values 0..v
@@ -301,6 +334,12 @@ sph_status sph_init(const sph_params* prm, int64_t capacity, sph_ctx** out) {
   AL(s.unit_rank, cap);
   AL(s.unit_list, cap + 1);
   AL(s.unit_rec, 3 * cap);
+  if (prm->nranks > 1) {
+    AL(s.unit_iflag, cap);
+    AL(s.unit_iexcl, cap);
+    AL(s.unit_order, cap);
+    AL(s.unit_bounds, 4);
+  }
   AL(s.nunit_list, 1);
   AL(s.mX, cap);
   AL(s.ct, 6 * cap);
@@ -310,7 +349,7 @@ sph_status sph_init(const sph_params* prm, int64_t capacity, sph_ctx** out) {
   AL(s.ncount, cap);
   AL(s.nseg, cap);
   AL(s.nbr_max, 3);
-  AL(s.work, 4);
+  AL(s.work, 8);
   AL(s.wB, cap);
   AL(s.ih2, cap);
   AL(s.vol, cap);
@@ -647,7 +686,7 @@ sph_status sph_density(sph_ctx* c) {
     CKL();
     ph.done(k);
   }
-  if (c->dist) {  // a7: halo exchange #2 (R21)
+  if (c->dist) {  // a7: halo exchange #2 (R21), in flight during the interior IAD units
     Phase ph(c, SPH_PH_HALO);
     if (!dist_exchange2(c)) return fail(c, SPH_ERR_COMM, c->dist_err);
     ph.done(0);
@@ -660,13 +699,25 @@ sph_status sph_iad(sph_ctx* c) {
   if (!c) return SPH_ERR_CONFIG;
   if (c->status != SPH_OK) return c->status;
   if (c->stage < 2) return fail(c, SPH_ERR_STATE, "sph_iad before sph_density");
-  if (c->P.n) {
+  if (c->dist) {  // interior units while exchange #2 is in flight, then the boundary units
+    Phase ph(c, SPH_PH_IAD);
+    int k = 0;
+    c->unit_sel = 1;
+    if (c->P.n) k += launch_iad(c);
+    c->unit_sel = 0;
+    if (!dist_wait_halo(c)) return fail(c, SPH_ERR_COMM, c->dist_err);
+    c->unit_sel = 2;
+    if (c->P.n) k += launch_iad(c);
+    c->unit_sel = 0;
+    CKL();
+    ph.done(k);
+  } else if (c->P.n) {
     Phase ph(c, SPH_PH_IAD);
     int k = launch_iad(c);
     CKL();
     ph.done(k);
   }
-  if (c->dist) {  // a9: halo exchange #3 (R21)
+  if (c->dist) {  // a9: halo exchange #3 (R21), in flight during the interior momentum units
     Phase ph(c, SPH_PH_HALO);
     if (!dist_exchange3(c)) return fail(c, SPH_ERR_COMM, c->dist_err);
     ph.done(0);
@@ -679,15 +730,26 @@ sph_status sph_momentum_energy(sph_ctx* c, double* dt_out) {
   if (!c) return SPH_ERR_CONFIG;
   if (c->status != SPH_OK) return c->status;
   if (c->stage < 3) return fail(c, SPH_ERR_STATE, "sph_momentum_energy before sph_iad");
-  if (c->P.n) {  // source records of owned + halo particles for the pass's bulk staging
+  if (c->P.n) {  // source records of the owned particles (+ halos: with exchange #3 on multi-GPU)
     Phase ph(c, SPH_PH_RECORDS);
-    int k = launch_mom_records(c);
+    int k = c->dist ? launch_mom_records_range(c, 0, c->P.n, c->stream) : launch_mom_records(c);
     CKL();
     ph.done(k);
   }
   {
     Phase ph(c, SPH_PH_MOMENTUM);
-    int k = c->P.n ? launch_momentum(c) : 0;
+    int k = 0;
+    if (c->dist) {  // interior units while exchange #3 is in flight, then the boundary units
+      c->unit_sel = 1;
+      if (c->P.n) k += launch_momentum(c);
+      c->unit_sel = 0;
+      if (!dist_wait_halo(c)) return fail(c, SPH_ERR_COMM, c->dist_err);
+      c->unit_sel = 2;
+      if (c->P.n) k += launch_momentum(c);
+      c->unit_sel = 0;
+    } else if (c->P.n) {
+      k = launch_momentum(c);
+    }
     if (c->dist && !dist_allreduce_dt(c)) return fail(c, SPH_ERR_COMM, c->dist_err);  // a11
     k += launch_dt_finalize(c, c->n_global > 0);
     CKL();
@@ -869,7 +931,7 @@ sph_status sph_destroy(sph_ctx* c) {
   Scratch& s = c->s;
   void* ptrs[] = {s.keys, s.keys_alt, s.idx, s.idx_alt, s.hist, s.scan_tmp, s.gather, s.gather_id,
                   s.cell_start, s.cell_end, s.cell_hmax, s.cell_flag, s.cell_rank, s.cell_list,
-                  s.ncell_list, s.unit_flag, s.unit_rank, s.unit_list, s.nunit_list, s.unit_rec, s.nbr, s.ncount, s.nseg, s.nbr_max, s.work, s.wB, s.ih2, s.vol, s.rinv, s.X,
+                  s.ncell_list, s.unit_flag, s.unit_rank, s.unit_list, s.nunit_list, s.unit_rec, s.unit_iflag, s.unit_iexcl, s.unit_order, s.unit_bounds, s.nbr, s.ncount, s.nseg, s.nbr_max, s.work, s.wB, s.ih2, s.vol, s.rinv, s.X,
                   s.mX, s.ct, s.mrec, s.red, s.bbox, s.dts, s.cnt, s.bad_id, s.diag, s.ktable};
   for (void* p : ptrs)
     if (p) cudaFree(p);

@@ -283,7 +283,9 @@ static FieldSet state_fields(sph_ctx* c, bool with_hist) {
   return fs;
 }
 
-static bool exchange(sph_ctx* c, const FieldSet& fs) {
+// Pack on the compute stream, transfer on `xs` (the compute stream, or the comm stream
+// of an overlapped exchange, which first waits for the packing).
+static bool exchange(sph_ctx* c, const FieldSet& fs, cudaStream_t xs) {
   // send the per-peer index lists (send_idx at soff), receive in rank order
   Dist& D = *c->dist;
   const int G = D.G, me = D.rank;
@@ -298,6 +300,10 @@ static bool exchange(sph_ctx* c, const FieldSet& fs) {
     if (r != me) sbase += D.scnt[r];
   }
   CUK(cudaGetLastError());
+  if (xs != c->stream) {
+    CUK(cudaEventRecord(D.ev_pack, c->stream));
+    CUK(cudaStreamWaitEvent(xs, D.ev_pack, 0));
+  }
   std::vector<Xfer> sends, recvs;
   sbase = 0;
   for (int r = 0; r < G; ++r) {
@@ -307,18 +313,18 @@ static bool exchange(sph_ctx* c, const FieldSet& fs) {
     sbase += D.scnt[r];
     rbase += D.rcnt[r];
   }
-  COMM(exchange(sends, recvs, c->stream, c->dist_err));
+  COMM(exchange(sends, recvs, xs, c->dist_err));
   return true;
 }
 
-static bool unpack_all(sph_ctx* c, const FieldSet& fs, int64_t dst0) {
+static bool unpack_all(sph_ctx* c, const FieldSet& fs, int64_t dst0, cudaStream_t us) {
   Dist& D = *c->dist;
   int64_t rbase = 0;
   for (int r = 0; r < D.G; ++r) {
     if (r == D.rank) continue;
     if (D.rcnt[r]) {
-      k_unpack<<<grid_blocks(c, D.rcnt[r], 256, 4), 256, 0, c->stream>>>(fs, D.recvbuf, D.rcnt[r], rbase,
-                                                                        dst0 + rbase);
+      k_unpack<<<grid_blocks(c, D.rcnt[r], 256, 4), 256, 0, us>>>(fs, D.recvbuf, D.rcnt[r], rbase,
+                                                                 dst0 + rbase);
       c->launches++;
     }
     rbase += D.rcnt[r];
@@ -459,14 +465,14 @@ bool dist_migrate(sph_ctx* c, int64_t* nleave, int64_t* nrecv) {
     c->launches++;
   }
   FieldSet fs = state_fields(c, true);
-  if (!exchange(c, fs)) return false;  // packs the leavers (stream order: before the moves)
+  if (!exchange(c, fs, c->stream)) return false;  // packs the leavers (stream order: before the moves)
   if (*nleave) {
     // holes below n_keep == stayers at or above n_keep (both equal nleave minus the
     // leavers already at or above n_keep); the host does not need the count
     k_fill_holes_dev<<<grid_blocks(c, *nleave, 256, 8), 256, 0, c->stream>>>(fs, holes, movers, D.hm_d);
     c->launches++;
   }
-  return unpack_all(c, fs, n_keep);
+  return unpack_all(c, fs, n_keep, c->stream);
 }
 
 // halo plan (who needs which of my cells) + exchange #1 (x, v, h, m, u, id)
@@ -516,25 +522,41 @@ bool dist_halo_plan_and_exchange1(sph_ctx* c) {
   D.n_halo = 0;
   for (int r = 0; r < G; ++r) D.n_halo += D.rcnt[r];
   FieldSet fs = state_fields(c, false);
-  if (!exchange(c, fs)) return false;
-  return unpack_all(c, fs, n);
+  if (!exchange(c, fs, c->stream)) return false;
+  return unpack_all(c, fs, n, c->stream);
 }
 
+// Exchanges #2 and #3 (R21) overlap the interior units' passes (SURVEY 8(f) NEXT-3,
+// P:388): packed on the compute stream, sent / received / unpacked on the comm stream,
+// and an event the compute stream waits on before the boundary units (dist_wait_halo).
 bool dist_exchange2(sph_ctx* c) {  // after density: quantities IAD / momentum read at sources
+  Dist& D = *c->dist;
   FieldSet fs{};
   fs.f[0] = (uint64_t*)c->s.vol;
   fs.f[1] = (uint64_t*)c->s.ih2;
   fs.f[2] = (uint64_t*)c->P.c;
   fs.f[3] = (uint64_t*)c->s.mX;
   fs.nf = 4;
-  return exchange(c, fs) && unpack_all(c, fs, c->P.n);
+  if (!exchange(c, fs, D.cstream) || !unpack_all(c, fs, c->P.n, D.cstream)) return false;
+  CUK(cudaEventRecord(D.ev_halo, D.cstream));
+  return true;
 }
 
-bool dist_exchange3(sph_ctx* c) {  // after IAD: C~ = (B/h^3) C of the sources
+bool dist_exchange3(sph_ctx* c) {  // after IAD: C~ = (B/h^3) C of the sources, then their records
+  Dist& D = *c->dist;
   FieldSet fs{};
   for (int k = 0; k < 6; ++k) fs.f[k] = (uint64_t*)(c->s.ct + (size_t)k * c->cap);
   fs.nf = 6;
-  return exchange(c, fs) && unpack_all(c, fs, c->P.n);
+  if (!exchange(c, fs, D.cstream) || !unpack_all(c, fs, c->P.n, D.cstream)) return false;
+  c->launches += launch_mom_records_range(c, c->P.n, c->n_halo, D.cstream);  // halo sources
+  CUK(cudaGetLastError());
+  CUK(cudaEventRecord(D.ev_halo, D.cstream));
+  return true;
+}
+
+bool dist_wait_halo(sph_ctx* c) {  // the compute stream waits for the last async exchange
+  CUK(cudaStreamWaitEvent(c->stream, c->dist->ev_halo, 0));
+  return true;
 }
 
 bool dist_allreduce_dt(sph_ctx* c) {
@@ -562,6 +584,9 @@ bool dist_init(sph_ctx* c, const sph_params* prm) {
   D->rcnt.assign(D->G, 0);
   D->comm = comm_create(prm->nccl_unique_id, D->G, D->rank, c->dist_err);
   if (!D->comm) return false;
+  CUK(cudaStreamCreateWithFlags(&D->cstream, cudaStreamNonBlocking));
+  CUK(cudaEventCreateWithFlags(&D->ev_pack, cudaEventDisableTiming));
+  CUK(cudaEventCreateWithFlags(&D->ev_halo, cudaEventDisableTiming));
   D->xcap = c->cap;
   const int64_t cap = c->cap;
   CUK(cudaMalloc(&D->hist_d, sizeof(unsigned long long) << kBinBits));
@@ -593,6 +618,9 @@ void dist_destroy(sph_ctx* c) {
   Dist* D = c->dist;
   if (!D) return;
   delete D->comm;
+  if (D->cstream) cudaStreamSynchronize(D->cstream), cudaStreamDestroy(D->cstream);
+  if (D->ev_pack) cudaEventDestroy(D->ev_pack);
+  if (D->ev_halo) cudaEventDestroy(D->ev_halo);
   void* ptrs[] = {D->hist_d, D->split_d, D->off_d, D->cnt_d, D->cnt_all_d, D->tot_d, D->red_d,
                   D->mask_d, D->pcnt_d, D->poff_d, D->send_idx, D->sendbuf, D->recvbuf, D->cntred_d,
                   D->hm_d};

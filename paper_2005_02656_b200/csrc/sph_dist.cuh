@@ -13,6 +13,8 @@ constexpr int kBinBits = 16;  // key-prefix histogram: 2^16 bins (top Morton bit
 struct Dist {
   int G = 1, rank = 0;
   Comm* comm = nullptr;     // NCCL or the in-process hub (comm.cuh)
+  cudaStream_t cstream = nullptr;   // overlapped halo exchanges #2 / #3
+  cudaEvent_t ev_pack = nullptr, ev_halo = nullptr;
   int shift = 0;            // bin = Morton(cell) >> shift
   int every = 1;            // recompute splitters every k-th step (sph_params.redecomp_every)
   int64_t decomp_calls = 0; // dist_splitters calls so far
@@ -49,6 +51,7 @@ bool dist_migrate(sph_ctx* c, int64_t* nleave, int64_t* nrecv);
 bool dist_halo_plan_and_exchange1(sph_ctx* c);
 bool dist_exchange2(sph_ctx* c);
 bool dist_exchange3(sph_ctx* c);
+bool dist_wait_halo(sph_ctx* c);
 bool dist_allreduce_dt(sph_ctx* c);
 bool dist_allreduce_diag(sph_ctx* c, double* d_dev, unsigned long long* cnt_dev);
 

@@ -19,7 +19,7 @@
 
 namespace sphb {
 
-constexpr int kPolyTerms = 13;   // Maclaurin terms of sinc(pi sqrt(t) / 2) in t = v^2
+constexpr int kPolyTerms = 10;   // degree-9 polynomial of sinc(pi sqrt(t) / 2) in t = v^2 on [0, 4]
 constexpr int kCounters = 8;     // device event counters (see enum below)
 enum { CNT_OMEGA = 0, CNT_IAD_SINGULAR, CNT_COINCIDENT, CNT_U_FLOOR, CNT_H_CLAMP, CNT_NONFINITE };
 
@@ -83,13 +83,18 @@ struct Scratch {
   uint32_t* unit_list = nullptr;            // cap + 1: index into cell_list of each unit's first cell
   uint32_t* nunit_list = nullptr;           // device scalar
   int4* unit_rec = nullptr;                 // 3 x cap: per unit, its union stencil + target range
+  // multi-GPU overlap: units ordered interior first (stencil without halo cells), then boundary
+  uint32_t* unit_iflag = nullptr;           // cap: 1 for an interior unit (scan input)
+  uint32_t* unit_iexcl = nullptr;           // cap: exclusive scan of unit_iflag
+  uint32_t* unit_order = nullptr;           // cap: unit ids, interior then boundary
+  uint32_t* unit_bounds = nullptr;          // {0, interior count, unit count}
   int64_t max_cells = 0;
   // neighbours
   unsigned char* nbr = nullptr;  // cap * maxn_cap row entries (uint16_t, or uint32_t when wide_rows)
   uint32_t* ncount = nullptr;    // cap: neighbours per target
   uint32_t* nseg = nullptr;      // cap: search segments per target (before the in-place expansion)
   unsigned int* nbr_max = nullptr;  // [0] largest count, [1] a unit too large for 16 bits, [2] segment overflow
-  uint32_t* work = nullptr;              // per cell kernel: next cell chunk (reset per launch)
+  uint32_t* work = nullptr;              // 8 claim counters: search, density, iad, momentum (+ boundary launches)
   // per-particle auxiliaries written by density, read by iad / momentum
   double* wB = nullptr;    // B / h^3
   double* ih2 = nullptr;   // 1 / h^2
@@ -142,6 +147,7 @@ struct sph_ctx {
   int64_t nbr_max = 0;
   sph_status status = SPH_OK;
   int64_t first_bad_id = -1;  // sph_diag.first_bad_id
+  int unit_sel = 0;           // pass launches: 0 all units, 1 interior, 2 boundary (multi-GPU overlap)
   int64_t n_global = 0;       // particles over all ranks in the current step
   std::string err;
   // profiling
@@ -174,6 +180,8 @@ int launch_density(sph_ctx* c);
 int launch_iad(sph_ctx* c);
 int launch_momentum(sph_ctx* c);
 int launch_mom_records(sph_ctx* c);
+int launch_mom_records_range(sph_ctx* c, int64_t i0, int64_t n, cudaStream_t st);
+int launch_unit_order(sph_ctx* c);
 int launch_dt_finalize(sph_ctx* c, bool nonempty);
 int launch_update(sph_ctx* c);
 int launch_diag(sph_ctx* c);
