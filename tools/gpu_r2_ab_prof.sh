@@ -1,0 +1,13 @@
+set -x
+python -c "import __graft_entry__ as g; g.build()" > /dev/null 2>&1
+timeout 120 python tools/dbg_hang.py > gpurun_out/dbg_hang.log 2>&1 || { cat gpurun_out/dbg_hang.log; exit 3; }
+bash tools/ab_bench.sh ab3 fulltile halftile
+for cf in 1.0 0.7 0.5; do
+  timeout 300 python bench.py --steps 5 --warmup 3 --no-cpu-baseline --workload evrard --cell-factor $cf > gpurun_out/r2_evrard_cf$cf.json 2>/dev/null
+  python -c "import json; d=json.loads(open('gpurun_out/r2_evrard_cf$cf.json').read().strip().splitlines()[-1]); print('evrard cf $cf', d['ms_per_step'], d['value'], d['phases_ms_per_step'])"
+done
+timeout 300 python bench.py --steps 5 --warmup 3 --no-cpu-baseline --workload patch1m > gpurun_out/r2_patch1m.json 2>/dev/null
+python -c "import json; d=json.loads(open('gpurun_out/r2_patch1m.json').read().strip().splitlines()[-1]); print('patch1m', d['ms_per_step'], d['value'], d['phases_ms_per_step'])"
+ncu --metrics gpu__time_duration.sum --clock-control none -c 200 --csv --log-file gpurun_out/r2_launches_v2.csv python bench.py --steps 2 --warmup 3 --no-cpu-baseline > gpurun_out/r2_ncu_launch2.log 2>&1
+ncu --set full --import-source on --clock-control none -k regex:"k_momentum_c|k_search|k_expand_rows|k_density_c|k_iad_c" -s 20 -c 5 -o gpurun_out/r2_full_v2 python bench.py --steps 1 --warmup 3 --no-cpu-baseline > gpurun_out/r2_ncu_full2.log 2>&1
+ls -la gpurun_out | tail -5

@@ -1,13 +1,22 @@
-"""Physics validation: rotating square patch, 100x100x100 =
-10^6 particles (§4.6), integrated with the CUDA path to
-t = 0.5 s, reporting |L_z| against the paper's L_tot = 8.33e9 g cm^2/s (P:285,
-"~0.2% from the parent codes") and the drift of linear momentum and energy.
+"""Physics validation: rotating square patch (§4.6,
+P:265-282) integrated to t = 0.5 s, reporting |L_z| against the paper's
+L_tot = 8.33e9 g cm^2/s ("~0.2% from the parent codes") and the drift of
+linear momentum and total energy, with pass/fail gates.
 
-    python tools/validate_square_patch.py [--n 100] [--t-end 0.5] [--out profiles/r1_validation.json]
+    python tools/validate_square_patch.py [--n 100] [--t-end 0.5] [--symmetric 1]
+                                          [--h-max-factor 2] [--backend gpu|oracle]
+                                          [--out gpurun_out/validation.json]
 
-Pressure-consistent initial masses (reading R16) are used, as the paper derives P0
-from the incompressible Poisson equation.  This is a physics check of
-the built path, not part of the timed benchmark.
+--backend oracle integrates the same initial state with the CPU oracle (test
+infrastructure; oracle/), so a late-time anomaly can be attributed: if the oracle
+shows it too, it is the discretisation (the method as read from the paper), not a
+kernel defect.  --symmetric 1 uses the r < 2 max(h_a, h_b) relation (pairwise
+antisymmetric forces: exact conservation for variable h, reading R24), so its energy
+and momentum drift isolate the gather relation's non-conservation.
+
+Gates (printed and stored): |p| / sum m|v| < 1e-6 at the end (linear momentum), and
+|E - E_10| / E_10 < 0.05 (energy after the start-up impulse of the first 10 steps,
+DESIGN.md §10).  Pressure-consistent initial masses (reading R16) by default.
 """
 import argparse
 import json
@@ -15,55 +24,121 @@ import os
 import sys
 import time
 
+import numpy as np
+
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 sys.path.insert(0, ROOT)
 
 
-def main():
-    import torch
+class GpuRun:
+    def __init__(self, d, kw):
+        import torch
 
-    from paper_2005_02656_b200 import inputs, sph
+        from paper_2005_02656_b200 import sph
+        torch.cuda.set_device(0)
+        self.sim = sph.Simulation(d, **kw)
+
+    def step(self):
+        return self.sim.step(want_dt=True)
+
+    def diag(self):
+        g = self.sim.diagnostics()
+        return list(g["momentum"]), list(g["ang_momentum"]), g["energy"], g
+
+    def state(self):
+        return self.sim.state()
+
+
+class OracleRun:
+    def __init__(self, d, kw):
+        import oracle as O
+        O.build()
+        self.O = O
+        okw = {}
+        if kw.get("symmetric"):
+            okw["symmetric"] = 1
+        if kw.get("h_max"):
+            okw["h_max"] = kw["h_max"]
+        self.o = O.Oracle(O.Params.from_inputs(d, **okw))
+        self.st = {k: np.array(d[k], dtype=np.float64) for k in ("x", "y", "z", "vx", "vy", "vz", "h", "m", "u")}
+        self.st["id"] = np.array(d["id"])
+        self.st["first"] = True
+        self.st["dt_prev"] = 0.0
+
+    def step(self):
+        r = self.o.step(self.st)
+        s = r["state"]
+        s["id"] = self.st["id"]
+        s["rho"] = r["dens"]["rho"]
+        self.st = s
+        return r["dt"]
+
+    def diag(self):
+        v = self.O.Oracle.diagnostics(self.st)
+        return list(v[0:3]), list(v[3:6]), float(v[6]), {}
+
+    def state(self):
+        return self.st
+
+
+def main():
+    from paper_2005_02656_b200 import inputs
     ap = argparse.ArgumentParser()
     ap.add_argument("--n", type=int, default=100)
     ap.add_argument("--t-end", type=float, default=0.5)
     ap.add_argument("--pressure-ics", type=int, default=1)
+    ap.add_argument("--symmetric", type=int, default=0)
+    ap.add_argument("--h-max-factor", type=float, default=0.0, help="clamp h at this x the initial h (0: none)")
+    ap.add_argument("--backend", default="gpu", choices=["gpu", "oracle"])
+    ap.add_argument("--every", type=int, default=250)
     ap.add_argument("--max-steps", type=int, default=20000)
     ap.add_argument("--out", default=os.path.join(ROOT, "gpurun_out", "validation.json"))
     a = ap.parse_args()
-    torch.cuda.set_device(0)
     d = inputs.square_patch(a.n, pressure_ics=bool(a.pressure_ics))
-    sim = sph.Simulation(d)
-    d0 = sim.diagnostics()
+    kw = {"symmetric": a.symmetric}
+    if a.h_max_factor > 0:
+        kw["h_max"] = float(a.h_max_factor * d["h"][0])
+    run = (GpuRun if a.backend == "gpu" else OracleRun)(d, kw)
+    p0, L0, E0, _ = run.diag()
     hist = []
-    t, steps = 0.0, 0
+    t, steps, E10 = 0.0, 0, None
     t0 = time.time()
+    m_scale = float(np.sum(d["m"] * (np.abs(d["vx"]) + np.abs(d["vy"]))))
     while t < a.t_end and steps < a.max_steps:
-        dt = sim.step(want_dt=True)
+        dt = run.step()
         t += dt
         steps += 1
-        if steps % 250 == 0 or t >= a.t_end:
-            g = sim.diagnostics()
-            s = sim.state()
+        if steps == 10:
+            E10 = run.diag()[2]
+        if steps % a.every == 0 or t >= a.t_end:
+            p, L, E, _ = run.diag()
+            s = run.state()
             ke = 0.5 * float((s["m"] * (s["vx"] ** 2 + s["vy"] ** 2 + s["vz"] ** 2)).sum())
-            hist.append({"step": steps, "t": t, "Lz": g["ang_momentum"][2], "E": g["energy"],
-                         "KE": ke, "IE": g["energy"] - ke, "rho_min": float(s["rho"].min()),
-                         "rho_max": float(s["rho"].max()), "p": g["momentum"], "dt": dt})
-            print(json.dumps(hist[-1]), flush=True)
-    g = sim.diagnostics()
-    Lz0, Lz = d0["ang_momentum"][2], g["ang_momentum"][2]
-    m_scale = sum(abs(v) for v in d["m"] * (abs(d["vx"]) + abs(d["vy"])))
+            rec = {"step": steps, "t": t, "Lz": L[2], "E": E, "KE": ke, "IE": E - ke,
+                   "p_rel": [v / m_scale for v in p], "dt": dt}
+            if "rho" in s:
+                rec["rho_min"], rec["rho_max"] = float(np.min(s["rho"])), float(np.max(s["rho"]))
+            hist.append(rec)
+            print(json.dumps(rec), flush=True)
+    p, L, E, g = run.diag()
+    E10 = E10 if E10 is not None else E0
     res = {
-        "config": f"square patch {a.n}^3, pressure-consistent ICs={bool(a.pressure_ics)}",
+        "backend": a.backend,
+        "config": f"square patch {a.n}^3, pressure-consistent ICs={bool(a.pressure_ics)}, "
+                  f"symmetric={a.symmetric}, h_max={kw.get('h_max', 0)}",
         "steps": steps, "t": t, "wall_s": time.time() - t0,
-        "Lz_t0": Lz0, "Lz_end": Lz, "abs_Lz_end": abs(Lz),
-        "paper_Ltot_t0.5": 8.33e9, "rel_to_paper": abs(Lz) / 8.33e9 - 1.0,
-        "Lz_drift_rel": (Lz - Lz0) / abs(Lz0),
-        "momentum_end": g["momentum"], "momentum_rel_to_sum_m_abs_v": [p / m_scale for p in g["momentum"]],
-        "E_t0": d0["energy"], "E_end": g["energy"], "E_drift_rel": (g["energy"] - d0["energy"]) / d0["energy"],
+        "Lz_t0": L0[2], "Lz_end": L[2], "abs_Lz_end": abs(L[2]),
+        "paper_Ltot_t0.5": 8.33e9, "rel_to_paper": abs(L[2]) / 8.33e9 - 1.0,
+        "Lz_drift_rel": (L[2] - L0[2]) / abs(L0[2]),
+        "momentum_rel_to_sum_m_abs_v": [v / m_scale for v in p],
+        "E_t0": E0, "E_step10": E10, "E_end": E, "E_drift_rel_after_startup": (E - E10) / E10,
         "counters": {k: g[k] for k in ("omega_clamped", "iad_singular", "coincident_pairs", "u_floored",
-                                        "h_clamped")},
+                                        "h_clamped")} if g else {},
         "history": hist,
     }
+    res["gate_momentum"] = bool(max(abs(v) for v in res["momentum_rel_to_sum_m_abs_v"]) < 1e-6)
+    res["gate_energy"] = bool(abs(res["E_drift_rel_after_startup"]) < 0.05)
+    res["gate_Lz_0.5pct"] = bool(abs(res["rel_to_paper"]) < 0.005)
     os.makedirs(os.path.dirname(a.out), exist_ok=True)
     json.dump(res, open(a.out, "w"), indent=1)
     print(json.dumps({k: v for k, v in res.items() if k != "history"}), flush=True)
