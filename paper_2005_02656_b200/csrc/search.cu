@@ -28,10 +28,8 @@ namespace sphb {
 constexpr int kCTS = 320;             // search CTA: 10 warps = one 32-target block each per round
 constexpr int kNWS = kCTS / 32;
 
-struct TgtW {  // per-target search data (exact-test fp64 + fp32 band + own flat index)
-  double pos[3];
-  double lim;
-  float f[6];   // x, y, z (unit-relative), band lo, band hi, ambiguity width
+struct TgtW {  // per-target search data (fp32 band + own flat index; the rare exact test
+  float f[6];   // re-reads the fp64 position) -- x, y, z (unit-relative), band lo, hi, width
   uint32_t self;
 };
 
@@ -132,7 +130,8 @@ __global__ void __launch_bounds__(kCTS, 2) k_search(const double* __restrict__ x
   extern __shared__ float4 cand[];  // kSearchCap + 32 (last tile padded with sentinels)
   float2* const candb = reinterpret_cast<float2*>(cand + kSearchCap + 32);  // SYM: per-candidate band
   __shared__ CellSm S;
-  __shared__ float4 tlo[kSearchTiles], thi[kSearchTiles];  // per staged tile: fp32 bounding box
+  // per staged HALF tile (16 candidates): fp32 bounding box; .w of thi: SYM largest band
+  __shared__ float4 tlo[2 * kSearchTiles], thi[2 * kSearchTiles];
   __shared__ uint32_t tcnt[kTgtU], tseg[kTgtU];            // per target: neighbours / segments so far
   __shared__ TgtW TW[kTgtU];
   __shared__ uint32_t s_chunk;
@@ -168,14 +167,10 @@ __global__ void __launch_bounds__(kCTS, 2) k_search(const double* __restrict__ x
         for (uint32_t t = t0 + threadIdx.x; t < t1; t += blockDim.x) {
           tcnt[t - t0] = 0;
           tseg[t - t0] = 0;
-          const double ha = h[t], tha = 2.0 * ha;
+          const double ha = h[t];
           const float2 bd = band32(ha, M);
           const double px = x[t], py = y[t], pz = z[t];
           TgtW& w = TW[t - t0];
-          w.pos[0] = px;
-          w.pos[1] = py;
-          w.pos[2] = pz;
-          w.lim = __dmul_rn(tha, tha);
           w.f[0] = (float)(px - org[0]);
           w.f[1] = (float)(py - org[1]);
           w.f[2] = (float)(pz - org[2]);
@@ -222,8 +217,8 @@ __global__ void __launch_bounds__(kCTS, 2) k_search(const double* __restrict__ x
             if constexpr (SYM) candb[q] = make_float2(-1.0f, -1.0f);
           }
           __syncthreads();
-          // tile bounding boxes (staged candidates are Z-ordered within each cell, so a
-          // tile is a compact block); one warp per tile
+          // half-tile bounding boxes (staged candidates are Z-ordered within each cell, so
+          // 16 consecutive candidates are a compact block); one warp per tile
           for (int q = warp; q < ntile; q += kNWS) {
             const float4 v = cand[32 * q + lane];
             const bool ok = v.x != INFINITY;
@@ -232,7 +227,7 @@ __global__ void __launch_bounds__(kCTS, 2) k_search(const double* __restrict__ x
             float hb = -1.0f;  // SYM: largest candidate band of the tile
             if constexpr (SYM) hb = ok ? candb[32 * q + lane].y : -1.0f;
 #pragma unroll
-            for (int o = 16; o; o >>= 1) {
+            for (int o = 8; o; o >>= 1) {  // within each 16-lane half
               if constexpr (SYM) hb = fmaxf(hb, __shfl_xor_sync(0xffffffffu, hb, o));
               lx = fminf(lx, __shfl_xor_sync(0xffffffffu, lx, o));
               ly = fminf(ly, __shfl_xor_sync(0xffffffffu, ly, o));
@@ -241,9 +236,9 @@ __global__ void __launch_bounds__(kCTS, 2) k_search(const double* __restrict__ x
               hy = fmaxf(hy, __shfl_xor_sync(0xffffffffu, hy, o));
               hz = fmaxf(hz, __shfl_xor_sync(0xffffffffu, hz, o));
             }
-            if (lane == 0) {
-              tlo[q] = make_float4(lx, ly, lz, 0.f);
-              thi[q] = make_float4(hx, hy, hz, hb);
+            if ((lane & 15) == 0) {
+              tlo[2 * q + (lane >> 4)] = make_float4(lx, ly, lz, 0.f);
+              thi[2 * q + (lane >> 4)] = make_float4(hx, hy, hz, hb);
             }
           }
           __syncthreads();
@@ -277,12 +272,13 @@ __global__ void __launch_bounds__(kCTS, 2) k_search(const double* __restrict__ x
             // expression: rounding is monotone, so the gap never exceeds |c - a| of a
             // member pair, box d2 <= r2_32, and box d2 >= every hi excludes hits and
             // ambiguous candidates alike (lists stay exact).
-            uint32_t need[kSearchWords];
+            // half tiles any member can reach (one bit per 16 candidates)
+            uint32_t need[2 * kSearchWords];
 #pragma unroll
-            for (int w = 0; w < kSearchWords; ++w) {
-              const int q = 32 * w + lane;
+            for (int w = 0; w < 2 * kSearchWords; ++w) {
+              const int q = 32 * w + lane;  // half-tile index
               bool nd = false;
-              if (q < ntile) {
+              if (q < 2 * ntile) {
                 if constexpr (W2) {
                   nd = true;
                 } else {
@@ -296,11 +292,15 @@ __global__ void __launch_bounds__(kCTS, 2) k_search(const double* __restrict__ x
               need[w] = __ballot_sync(0xffffffffu, nd);
             }
 #pragma unroll 1
-            for (int w = 0; w < kSearchWords; ++w) {
-              uint32_t nm = need[w];
+            for (int w = 0; w < 2 * kSearchWords; ++w) {
+              // tiles of this word (16 per word) with any half needed: bit pairs (lo, hi)
+              const uint32_t hw = need[w];
+              uint32_t nm = (hw | (hw >> 1)) & 0x55555555u;
               while (nm) {
-                const int q = 32 * w + __ffs(nm) - 1;
+                const int b2 = __ffs(nm) - 1;  // even bit: the tile's low half
                 nm &= nm - 1;
+                const int q = 16 * w + (b2 >> 1);
+                const bool need_lo = (hw >> b2) & 1u, need_hi = (hw >> (b2 + 1)) & 1u;
                 const float4* cq = cand + 32 * q;
                 uint32_t in = 0u;
                 // rare: exact fp64 test of candidate b (the oracle's r^2 < (2h)^2, R10)
@@ -308,12 +308,14 @@ __global__ void __launch_bounds__(kCTS, 2) k_search(const double* __restrict__ x
                   const uint32_t f = gb + 32u * q + b;
                   const int kq = slot_of(S, f);
                   const uint32_t j = S.t_start[kq] + (f - S.cum[kq]);
-                  double lim = T.lim;
+                  const double tha = 2.0 * h[t];
+                  double lim = __dmul_rn(tha, tha);
                   if constexpr (SYM) {
                     const double thb = 2.0 * h[j];
                     lim = fmax(lim, __dmul_rn(thb, thb));
                   }
-                  return exact_hit(g, x, y, z, j, t, T.pos, lim);
+                  const double pos[3] = {x[t], y[t], z[t]};
+                  return exact_hit(g, x, y, z, j, t, pos, lim);
                 };
                 auto r2of = [&](int k) -> float {
                   const float4 c = cq[k];
@@ -329,12 +331,26 @@ __global__ void __launch_bounds__(kCTS, 2) k_search(const double* __restrict__ x
                   // hit iff r2 < lo  <=>  fl(r2 - lo) < 0: the sign bit, funnel-shifted in
                   // (candidate 31 first, so bit k ends at position k); a candidate inside
                   // [lo, hi) has |fl(r2 - lo)| < wband, caught by the running minimum
+                  // (a half tile no member can reach is skipped: its 16 bits stay 0)
                   float mn = INFINITY;
+                  if (need_hi) {
 #pragma unroll
-                  for (int k = 31; k >= 0; --k) {
-                    const float d = r2of(k) - lo;
-                    in = __funnelshift_l(__float_as_uint(d), in, 1);
-                    mn = fminf(mn, fabsf(d));
+                    for (int k = 31; k >= 16; --k) {
+                      const float d = r2of(k) - lo;
+                      in = __funnelshift_l(__float_as_uint(d), in, 1);
+                      mn = fminf(mn, fabsf(d));
+                    }
+                  }
+                  in <<= need_hi ? 0 : 16;
+                  if (need_lo) {
+#pragma unroll
+                    for (int k = 15; k >= 0; --k) {
+                      const float d = r2of(k) - lo;
+                      in = __funnelshift_l(__float_as_uint(d), in, 1);
+                      mn = fminf(mn, fabsf(d));
+                    }
+                  } else {
+                    in <<= 16;
                   }
                   if (!act) in = 0u;
                   const bool slow = mn < wband;
@@ -401,22 +417,26 @@ __global__ void __launch_bounds__(kCTS, 2) k_search(const double* __restrict__ x
 }
 
 // Rows in place: segments (mask, first flat index) -> ascending flat indices.  A warp
-// per row: the segments are read into registers (all of them before any entry is
-// written back), their exclusive prefix is a warp scan, each lane expands its own
-// segment into the warp's shared-memory row buffer (a shared-memory scatter: global
-// per-lane scatters touched ~20 sectors per store), and the row goes back to HBM in
-// 16-byte stores.  Rows longer than the stride are left alone (the host grows the
-// stride and reruns the search before anything reads them).
+// per row: its segments and their exclusive prefix (a warp scan) are staged in shared
+// memory (all of them before any entry is written back), then the warp writes each
+// segment with ONE LANE PER BIT (lane b stores the entry of bit b at prefix +
+// popc(mask below b)): consecutive shared-memory addresses, no bank conflicts, and
+// the instruction count is per segment, not per entry of the longest segment (a lane
+// per segment walking its own bits ran max-popcount iterations at ~31 % lane use).
+// The row goes back to HBM in 16-byte stores.  Rows longer than the stride are left
+// alone (the host grows the stride and reruns the search before anything reads them).
 constexpr int kExpWarps = 8;
 template <typename E>
 __global__ void __launch_bounds__(32 * kExpWarps) k_expand_rows(unsigned char* __restrict__ rows, int64_t n,
                                                               const uint32_t* __restrict__ nseg,
                                                               const uint32_t* __restrict__ ncount, int maxn) {
   extern __shared__ uint4 xsm[];
-  const uint32_t lane = threadIdx.x & 31;
+  const uint32_t lane = threadIdx.x & 31, lt = (1u << lane) - 1u;
   const int warp = threadIdx.x >> 5;
   const size_t rbytes = (size_t)maxn * sizeof(E);  // a multiple of 16 (stride rounded to 32 entries)
-  E* const sout = reinterpret_cast<E*>(reinterpret_cast<unsigned char*>(xsm) + rbytes * warp);
+  const uint32_t segcap = (uint32_t)(rbytes / sizeof(uint2));
+  uint4* const sseg = xsm + (size_t)warp * (segcap + rbytes / 16);  // (mask, base, prefix, -) per segment
+  E* const sout = reinterpret_cast<E*>(sseg + segcap);
   const int64_t stride = (int64_t)gridDim.x * kExpWarps;
   int64_t t = (int64_t)blockIdx.x * kExpWarps + warp;
   uint32_t ns = t < n ? nseg[t] : 0u, nc = t < n ? ncount[t] : 0u;
@@ -426,7 +446,7 @@ __global__ void __launch_bounds__(32 * kExpWarps) k_expand_rows(unsigned char* _
       ns = nseg[t + stride];
       nc = ncount[t + stride];
     }
-    if (cnc > (uint32_t)maxn || (size_t)cns * sizeof(uint2) > rbytes) continue;
+    if (cnc > (uint32_t)maxn || cns > segcap) continue;
     unsigned char* const row = rows + (size_t)t * rbytes;
     const uint2* const gseg = reinterpret_cast<const uint2*>(row);
     uint32_t carry = 0;
@@ -440,11 +460,16 @@ __global__ void __launch_bounds__(32 * kExpWarps) k_expand_rows(unsigned char* _
         const uint32_t u = __shfl_up_sync(0xffffffffu, v, o);
         if (lane >= (uint32_t)o) v += u;
       }
-      uint32_t pos = carry + v - pc;
-      for (uint32_t mm = sg.x; mm; mm &= mm - 1) sout[pos++] = (E)(sg.y + (uint32_t)(__ffs(mm) - 1));
+      if (k < cns) sseg[k] = make_uint4(sg.x, sg.y, carry + v - pc, 0u);
       carry += __shfl_sync(0xffffffffu, v, 31);
     }
-    __syncwarp();  // every segment was read and expanded: the row region may be overwritten
+    __syncwarp();  // every segment was read: the row region may be overwritten
+#pragma unroll 4
+    for (uint32_t j = 0; j < cns; ++j) {
+      const uint4 sg = sseg[j];  // broadcast
+      if (sg.x & (1u << lane)) sout[sg.z + __popc(sg.x & lt)] = (E)(sg.y + lane);
+    }
+    __syncwarp();
     const uint32_t nv = (uint32_t)((cnc * sizeof(E) + 15) / 16);
     uint4* const dst = reinterpret_cast<uint4*>(row);
     const uint4* const src = reinterpret_cast<const uint4*>(sout);
@@ -473,7 +498,8 @@ static void search_t(sph_ctx* c, int gs, size_t smem, bool w2, bool sym) {
 
 template <typename E>
 static void expand_t(sph_ctx* c) {
-  const size_t smem = (size_t)kExpWarps * c->maxn_cap * sizeof(E);
+  const size_t rbytes = (size_t)c->maxn_cap * sizeof(E);
+  const size_t smem = (size_t)kExpWarps * (rbytes / sizeof(uint2) * sizeof(uint4) + rbytes);
   cudaFuncSetAttribute(k_expand_rows<E>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   const int64_t blocks = std::min<int64_t>((c->P.n + kExpWarps - 1) / kExpWarps, (int64_t)c->num_sms * 8);
   k_expand_rows<E><<<(int)std::max<int64_t>(blocks, 1), 32 * kExpWarps, smem, c->stream>>>(
