@@ -437,8 +437,9 @@ __global__ void __launch_bounds__(32 * kExpWarps) k_expand_rows(unsigned char* _
   const uint32_t segcap = (uint32_t)(rbytes / sizeof(uint2));
   uint4* const sseg = xsm + (size_t)warp * (segcap + rbytes / 16);  // (mask, base, prefix, -) per segment
   E* const sout = reinterpret_cast<E*>(sseg + segcap);
-  const int64_t stride = (int64_t)gridDim.x * kExpWarps;
-  int64_t t = (int64_t)blockIdx.x * kExpWarps + warp;
+  const int nw = blockDim.x >> 5;  // kExpWarps, fewer for long rows (shared-memory budget)
+  const int64_t stride = (int64_t)gridDim.x * nw;
+  int64_t t = (int64_t)blockIdx.x * nw + warp;
   uint32_t ns = t < n ? nseg[t] : 0u, nc = t < n ? ncount[t] : 0u;
   for (; t < n; t += stride) {
     const uint32_t cns = ns, cnc = nc;
@@ -497,20 +498,24 @@ static void search_t(sph_ctx* c, int gs, size_t smem, bool w2, bool sym) {
 }
 
 template <typename E>
-static void expand_t(sph_ctx* c) {
+static bool expand_t(sph_ctx* c) {
   const size_t rbytes = (size_t)c->maxn_cap * sizeof(E);
-  const size_t smem = (size_t)kExpWarps * (rbytes / sizeof(uint2) * sizeof(uint4) + rbytes);
+  const size_t per_warp = rbytes / sizeof(uint2) * sizeof(uint4) + rbytes;
+  const size_t budget = 200 * 1024;  // dynamic shared memory per block
+  const int nw = (int)std::min<size_t>(kExpWarps, budget / per_warp);
+  if (nw < 1) return false;  // a row stride beyond ~4,000 16-bit entries
+  const size_t smem = (size_t)nw * per_warp;
   cudaFuncSetAttribute(k_expand_rows<E>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-  const int64_t blocks = std::min<int64_t>((c->P.n + kExpWarps - 1) / kExpWarps, (int64_t)c->num_sms * 8);
-  k_expand_rows<E><<<(int)std::max<int64_t>(blocks, 1), 32 * kExpWarps, smem, c->stream>>>(
+  const int64_t blocks = std::min<int64_t>((c->P.n + nw - 1) / nw, (int64_t)c->num_sms * 8);
+  k_expand_rows<E><<<(int)std::max<int64_t>(blocks, 1), 32 * nw, smem, c->stream>>>(
       c->s.nbr, c->P.n, c->s.nseg, c->s.ncount, c->maxn_cap);
+  return true;
 }
 
 // segments -> rows in place (after the capacity check of the search's maxima)
 int launch_expand_rows(sph_ctx* c) {
-  if (c->wide_rows) expand_t<uint32_t>(c);
-  else expand_t<uint16_t>(c);
-  return 1;
+  const bool ok = c->wide_rows ? expand_t<uint32_t>(c) : expand_t<uint16_t>(c);
+  return ok ? 1 : -1;
 }
 
 // unit records (union stencils + target ranges) for the search and the three passes

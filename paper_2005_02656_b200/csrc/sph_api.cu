@@ -32,7 +32,8 @@ sph_status fail(sph_ctx* c, sph_status st, const std::string& msg) {
   do {                                                                                        \
     cudaError_t e_ = cudaGetLastError();                                                      \
     if (e_ != cudaSuccess)                                                                    \
-      return fail(c, SPH_ERR_CUDA, std::string("kernel launch: ") + cudaGetErrorString(e_));  \
+      return fail(c, SPH_ERR_CUDA, std::string("kernel launch (sph_api.cu:") +               \
+                                       std::to_string(__LINE__) + "): " + cudaGetErrorString(e_)); \
   } while (0)
 
 // ---- B_n of Eq. 6: 1 / (4 pi int_0^2 [sinc(pi v/2)]^n v^2 dv).
@@ -574,6 +575,9 @@ sph_status sph_find_neighbors(sph_ctx* c) {
     if (c->maxn > 0 && mx[0] > (unsigned)c->maxn)
       return fail(c, SPH_ERR_CAPACITY, "a particle has " + std::to_string(mx[0]) +
                                            " neighbours > max_neighbors = " + std::to_string(c->maxn));
+    if (getenv("SPH_DEBUG_ROWS"))
+      fprintf(stderr, "sph: rows grow (max count %u, wide %u, segment overflow %u, stride %d)\n", mx[0], mx[1],
+              mx[2], c->maxn_cap);
     if (mx[1]) c->wide_rows = true;
     if (mx[0] > (unsigned)c->maxn_cap) c->maxn_cap = (int)(((mx[0] + mx[0] / 8) + 31) / 32 * 32);
     else if (mx[2]) c->maxn_cap *= 2;  // the segments did not fit the row region
@@ -600,6 +604,9 @@ sph_status sph_find_neighbors(sph_ctx* c) {
   if (c->P.n) {  // segments -> flat-index rows, in place
     Phase ph(c, SPH_PH_NEIGHBORS);
     int k = launch_expand_rows(c);
+    if (k < 0)
+      return fail(c, SPH_ERR_CAPACITY, "neighbour rows of " + std::to_string(c->maxn_cap) +
+                                           " entries exceed the row-expansion buffer");
     CKL();
     ph.done(k);
   }
