@@ -68,15 +68,19 @@ __global__ void __launch_bounds__(kRedThreads) k_bbox(const double* __restrict__
   }
 }
 
+// one warp per reduced value: lanes stride over the block partials, then a fixed
+// shuffle tree (deterministic order; a single thread looping over ~600 partials cost
+// ~0.1 ms of dependent L2 loads per step)
 __global__ void k_bbox_final(const double* __restrict__ part, int nblk, double* __restrict__ out) {
-  int k = threadIdx.x;
+  const int k = threadIdx.x >> 5, lane = threadIdx.x & 31;
   if (k >= kBB) return;
-  double r = part[k];
-  for (int b = 1; b < nblk; ++b) {  // fixed order: deterministic
-    double q = part[(int64_t)b * kBB + k];
+  double r = k < 3 ? INFINITY : (k == 7 ? 0.0 : -INFINITY);
+  for (int b = lane; b < nblk; b += 32) {
+    const double q = part[(int64_t)b * kBB + k];
     r = k < 3 ? fmin(r, q) : (k == 7 ? r + q : fmax(r, q));
   }
-  out[k] = r;
+  r = k < 3 ? warp_min(r) : (k == 7 ? warp_sum(r) : warp_max(r));
+  if (lane == 0) out[k] = r;
 }
 
 int launch_bbox(sph_ctx* c) {
@@ -84,7 +88,7 @@ int launch_bbox(sph_ctx* c) {
   int nb = grid_blocks(c, n, kRedThreads, 4);
   k_bbox<<<nb, kRedThreads, 0, c->stream>>>(c->P.x, c->P.y, c->P.z, c->P.h, c->P.m, c->P.id, n,
                                               c->s.red, c->s.bad_id);
-  k_bbox_final<<<1, 32, 0, c->stream>>>(c->s.red, nb, c->s.bbox);
+  k_bbox_final<<<1, 32 * kBB, 0, c->stream>>>(c->s.red, nb, c->s.bbox);
   return 2;
 }
 
