@@ -847,7 +847,9 @@ __global__ void __launch_bounds__(kCTM, 1) k_momentum_c(
               rinva = r5.x * r8.y;  // (m / rho) / m
               a11 = r5.y; a12 = r6.x; a13 = r6.y; a22 = r7.x; a23 = r7.y; a33 = r8.x;  // C~_a
             }
-            __device__ __forceinline__ void operator()(int qi) {
+            // pair (a, b = staged entry qi): the Eq. 2 / Eq. 3 contributions and v_sig
+            __device__ __forceinline__ void eval(int qi, double& gx, double& gy, double& gz, double& gu,
+                                                 double& vsab, bool& coinc) const {
               const double2* q = F2 + (size_t)qi * kMomPairs;
               const double2 p0 = q[0], p1 = q[1], p3 = q[3];
               double dx = p0.x - xa, dy = p0.y - ya, dz = p1.x - za;
@@ -855,8 +857,7 @@ __global__ void __launch_bounds__(kCTM, 1) k_momentum_c(
               const double r2 = dx * dx + dy * dy + dz * dz;
               // coincident pair: Delta = 0 zeroes every term below; it is only
               // kept out of v_sig and counted (no branch)
-              const bool coinc = r2 == 0.0;
-              *ncoinc += coinc;
+              coinc = r2 == 0.0;
               const double ta = r2 * ih2a;
               // symmetric extra pair (r >= 2 h_a): W(r, h_a) = 0, only the h_b terms remain
               const double Sa = (W2 && sym && !(ta < 4.0)) ? 0.0 : kern_S<KM, N, true>(ta, n, tab, K);
@@ -885,20 +886,34 @@ __global__ void __launch_bounds__(kCTM, 1) k_momentum_c(
 #else
               const double w = vdotx < 0.0 ? vdotx * rsqrt(r2) : 0.0;
 #endif
-              const double vsab = ca + cb - 3.0 * w;  // v_sig; w == min(w, 0)
+              vsab = ca + cb - 3.0 * w;  // v_sig; w == min(w, 0)
               const double hp = -0.25 * alpha * vsab * w;  // Pi'/2, Eq. 5
-              vs = (!coinc && vsab > vs) ? vsab : vs;
               // Eq. 2 with R2 and Eq. 4: a += -m_b (X_a A_a + X_b A_b) - g,
               //   g = (Pi'/2) (m_b/rho_a A_a + m_b/rho_b A_b), folded onto u and w
               const double ka = mb * fma(hp, rinva, Xa) * Wa;
               const double kb = fma(hp, mrb, mXb) * Sb;
-              fx -= fma(ka, ux, kb * wx);
-              fy -= fma(ka, uy, kb * wy);
-              fz -= fma(ka, uz, kb * wz);
+              gx = fma(ka, ux, kb * wx);
+              gy = fma(ka, uy, kb * wy);
+              gz = fma(ka, uz, kb * wz);
               // Eq. 3 with R1, R3: du += m_b X_a v_ab.A_a + (1/2) v_ab.g
               const double vu = vabx * ux + vaby * uy + vabz * uz;
               const double vw = vabx * wx + vaby * wy + vabz * wz;
-              fu += mb * fma(0.5 * hp, rinva, Xa) * Wa * vu + 0.5 * hp * mrb * Sb * vw;
+              gu = mb * fma(0.5 * hp, rinva, Xa) * Wa * vu + 0.5 * hp * mrb * Sb * vw;
+            }
+            __device__ __forceinline__ void add(double gx, double gy, double gz, double gu, double vsab,
+                                                bool coinc) {
+              *ncoinc += coinc;  // coincident pair: kept out of v_sig, counted
+              vs = (!coinc && vsab > vs) ? vsab : vs;
+              fx -= gx;
+              fy -= gy;
+              fz -= gz;
+              fu += gu;
+            }
+            __device__ __forceinline__ void operator()(int qi) {
+              double gx, gy, gz, gu, v;
+              bool co;
+              eval(qi, gx, gy, gz, gu, v, co);
+              add(gx, gy, gz, gu, v, co);
             }
           } body;
           body.F2 = F2; body.mrec = mrec; body.slot = tslot[threadIdx.x >> 4];

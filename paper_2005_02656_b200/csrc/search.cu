@@ -176,8 +176,10 @@ __global__ void __launch_bounds__(kCTS, 2) k_search(const double* __restrict__ x
           w.f[2] = (float)(pz - org[2]);
           w.f[3] = bd.x;
           w.f[4] = bd.y;
-          // |fl(r2 - lo)| of a candidate inside [lo, hi) is below this (fp32 rounding slack)
-          w.f[5] = bd.y < INFINITY ? (bd.y - bd.x) * (1.0f + 0x1p-20f) + 0x1p-126f : INFINITY;
+          // |d| (the fused fl(r2 - lo) below) of a candidate inside [lo, hi) is below this:
+          // hi - lo plus 2^-20 hi for the three roundings of the fused chain (<= 3u max(lo, r2)
+          // on each side of the test)
+          w.f[5] = bd.y < INFINITY ? (bd.y - bd.x) * (1.0f + 0x1p-20f) + 0x1p-20f * bd.y + 0x1p-126f : INFINITY;
           // own flat staging index (the unit slot of the target's cell): never its own neighbour
           w.self = 0xffffffffu;
           for (int dz = 0; dz < (g.ubits > 2 ? 2 : 1); ++dz)
@@ -327,16 +329,27 @@ __global__ void __launch_bounds__(kCTS, 2) k_search(const double* __restrict__ x
                   }
                   return fmaf(dz, dz, fmaf(dy, dy, dx * dx));
                 };
+                // r2 - lo in one fused chain (three FFMA, no separate subtract)
+                auto dof = [&](int k) -> float {
+                  const float4 c = cq[k];
+                  float dx = c.x - ax, dy = c.y - ay, dz = c.z - az;
+                  if constexpr (W2) {
+                    if (st.wrap[0] == 2) dx = wrap1(dx, (float)g.L[0]);
+                    if (st.wrap[1] == 2) dy = wrap1(dy, (float)g.L[1]);
+                    if (st.wrap[2] == 2) dz = wrap1(dz, (float)g.L[2]);
+                  }
+                  return fmaf(dz, dz, fmaf(dy, dy, fmaf(dx, dx, -lo)));
+                };
                 if constexpr (!SYM) {
-                  // hit iff r2 < lo  <=>  fl(r2 - lo) < 0: the sign bit, funnel-shifted in
-                  // (candidate 31 first, so bit k ends at position k); a candidate inside
-                  // [lo, hi) has |fl(r2 - lo)| < wband, caught by the running minimum
+                  // hit iff d = r2 - lo < 0: the sign bit, funnel-shifted in (candidate 31
+                  // first, so bit k ends at position k); a candidate inside [lo, hi) has
+                  // |d| < wband, caught by the running minimum
                   // (a half tile no member can reach is skipped: its 16 bits stay 0)
                   float mn = INFINITY;
                   if (need_hi) {
 #pragma unroll
                     for (int k = 31; k >= 16; --k) {
-                      const float d = r2of(k) - lo;
+                      const float d = dof(k);
                       in = __funnelshift_l(__float_as_uint(d), in, 1);
                       mn = fminf(mn, fabsf(d));
                     }
@@ -345,7 +358,7 @@ __global__ void __launch_bounds__(kCTS, 2) k_search(const double* __restrict__ x
                   if (need_lo) {
 #pragma unroll
                     for (int k = 15; k >= 0; --k) {
-                      const float d = r2of(k) - lo;
+                      const float d = dof(k);
                       in = __funnelshift_l(__float_as_uint(d), in, 1);
                       mn = fminf(mn, fabsf(d));
                     }
@@ -356,7 +369,7 @@ __global__ void __launch_bounds__(kCTS, 2) k_search(const double* __restrict__ x
                   const bool slow = mn < wband;
                   if (__any_sync(0xffffffffu, slow) && slow) {
                     for (int k = 0; k < 32; ++k)
-                      if (fabsf(r2of(k) - lo) < wband) in = exact((uint32_t)k) ? in | (1u << k) : in & ~(1u << k);
+                      if (fabsf(dof(k)) < wband) in = exact((uint32_t)k) ? in | (1u << k) : in & ~(1u << k);
                   }
                 } else {  // symmetric relation: either side's support, per-candidate band
                   uint32_t near = 0u;
