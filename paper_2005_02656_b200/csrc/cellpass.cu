@@ -500,6 +500,21 @@ __global__ void __launch_bounds__(kCTD, 1) k_density_c(
   }
 }
 
+struct MomSrc {  // per-particle arrays staged for the source side of a pair
+  const double *x, *y, *z, *vx, *vy, *vz, *m, *ih2, *c, *mX, *mr;
+  const double* ct;  // 6 x stride: C~ = (B/h^3) C
+  int64_t ct_stride;
+};
+constexpr int kMomPairs = 9;  // 144-byte momentum source record: 9 double2 (layout below)
+// The IAD epilogue writes the records of its targets (owned particles) straight from
+// the values it has just computed (C~) or staged (x, 1/h^2): the separate record pass
+// then covers halos only.  Build with -DSPH_SEPARATE_RECORDS for the A/B baseline.
+#ifdef SPH_SEPARATE_RECORDS
+constexpr bool kIadRecords = false;
+#else
+constexpr bool kIadRecords = true;
+#endif
+
 // ------------------------------------------------------------------ a8 IAD
 template <int N, bool W2, int KM, typename E>
 __global__ void __launch_bounds__(kCTD, 1) k_iad_c(
@@ -511,7 +526,7 @@ __global__ void __launch_bounds__(kCTD, 1) k_iad_c(
     const double* __restrict__ ih2, const double* __restrict__ vol, double* __restrict__ c11,
     double* __restrict__ c12, double* __restrict__ c13, double* __restrict__ c22,
     double* __restrict__ c23, double* __restrict__ c33, double* __restrict__ ct,
-    int64_t ct_stride, unsigned long long* __restrict__ cnt) {
+    int64_t ct_stride, unsigned long long* __restrict__ cnt, MomSrc rs, double2* __restrict__ mrec) {
   extern __shared__ double dsm[];
   double2* s01 = reinterpret_cast<double2*>(dsm);
   double2* s23 = s01 + kIadCap;
@@ -625,6 +640,25 @@ __global__ void __launch_bounds__(kCTD, 1) k_iad_c(
           // C~ = (B/h^3) C, staged by the momentum pass (A_ab(h_b) = C~_b Delta S_b)
           ct[0 * ct_stride + t] = s * i11; ct[1 * ct_stride + t] = s * i12; ct[2 * ct_stride + t] = s * i13;
           ct[3 * ct_stride + t] = s * i22; ct[4 * ct_stride + t] = s * i23; ct[5 * ct_stride + t] = s * i33;
+          if (mrec) {  // the target's momentum source record (k_mom_records' layout), staged
+            double2* r = s01 + (size_t)i * kMomPairs;  // staging buffer is free after the groups
+            const double mm = rs.m[t];
+            r[0] = make_double2(tx[i], ty[i]);
+            r[1] = make_double2(tz[i], rs.vx[t]);
+            r[2] = make_double2(rs.vy[t], rs.vz[t]);
+            r[3] = make_double2(mm, tih2[i]);
+            r[4] = make_double2(rs.c[t], rs.mX[t]);
+            r[5] = make_double2(rs.mr[t], s * i11);
+            r[6] = make_double2(s * i12, s * i13);
+            r[7] = make_double2(s * i22, s * i23);
+            r[8] = make_double2(s * i33, 1.0 / mm);
+          }
+        }
+        if (mrec) {  // the sub-block's records leave in coalesced 16-byte stores
+          __syncthreads();
+          const uint32_t nr = (t1 - t0) * kMomPairs;
+          double2* const out = mrec + (size_t)t0 * kMomPairs;
+          for (uint32_t e = threadIdx.x; e < nr; e += blockDim.x) out[e] = s01[e];
         }
         __syncthreads();
       }
@@ -667,11 +701,6 @@ __device__ __forceinline__ void cp_async16(void* dst, const void* src) {
 __device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;\n" ::: "memory"); }
 __device__ __forceinline__ void cp_async_wait_prev() { asm volatile("cp.async.wait_group 1;\n" ::: "memory"); }
 
-struct MomSrc {  // per-particle arrays staged for the source side of a pair
-  const double *x, *y, *z, *vx, *vy, *vz, *m, *ih2, *c, *mX, *mr;
-  const double* ct;  // 6 x stride: C~ = (B/h^3) C
-  int64_t ct_stride;
-};
 struct MomTgt {
   const double *h, *wB, *rinv, *X, *c11, *c12, *c13, *c22, *c23, *c33;
 };
@@ -684,12 +713,12 @@ struct MomOut {
 //   6 (C~12, C~13)  7 (C~22, C~23)  8 (C~33, 1/m)
 // The TARGET side of a pair reads the target's own record too: X_a = (m X) (1/m),
 // 1/rho_a = (m/rho) (1/m), and A_ab(h_a) = C_a Delta W(r, h_a) = C~_a Delta S(r/h_a)
-// (C~ = (B/h^3) C), so no per-target table is staged.
-constexpr int kMomPairs = 9;
+// (C~ = (B/h^3) C), so no per-target table is staged.  (kMomPairs = 9 is defined
+// above the IAD kernel, whose epilogue writes the owned particles' records.)
 
 // Momentum source records: the kMomPairs double2 a pair reads from its source, one
-// contiguous 144-byte record per particle, built once per step after IAD (owned +
-// halo).  A staging group is then a handful of bulk copies (one per stencil slot).
+// contiguous 144-byte record per particle, built once per step by the IAD epilogue
+// (owned) and k_mom_records (halo).  A staging group is then a handful of bulk copies (one per stencil slot).
 constexpr int kRecThreads = 256;  // k_mom_records block: records transposed through smem
 __global__ void __launch_bounds__(kRecThreads) k_mom_records(MomSrc src, int64_t i0, int64_t n,
                                                               double2* __restrict__ rec) {
@@ -1051,7 +1080,9 @@ static void iad_t(sph_ctx* c) {
   k_iad_c<N, W2, KM, E><<<cell_grid(c, 1), kCTD, smem, c->stream>>>(
       P.x, P.y, P.z, c->grid, c->s.cell_start, c->s.cell_end, c->s.cell_hmax, c->s.cell_list,
       c->s.ncell_list, c->s.unit_rec, unit_range(c), c->s.work + unit_work(c, 2), reinterpret_cast<const E*>(c->s.nbr), c->s.ncount, c->maxn_cap, c->phys, c->s.wB, c->s.ih2, c->s.vol,
-      P.c11, P.c12, P.c13, P.c22, P.c23, P.c33, c->s.ct, c->cap, c->s.cnt);
+      P.c11, P.c12, P.c13, P.c22, P.c23, P.c33, c->s.ct, c->cap, c->s.cnt,
+      MomSrc{P.x, P.y, P.z, P.vx, P.vy, P.vz, P.m, c->s.ih2, P.c, c->s.mX, c->s.vol, c->s.ct, c->cap},
+      kIadRecords ? reinterpret_cast<double2*>(c->s.mrec) : nullptr);
 }
 
 int launch_iad(sph_ctx* c) {
@@ -1088,8 +1119,13 @@ int launch_mom_records_range(sph_ctx* c, int64_t i0, int64_t n, cudaStream_t st)
   return 1;
 }
 
-int launch_mom_records(sph_ctx* c) {  // owned + halo sources
-  return launch_mom_records_range(c, 0, c->P.n + c->n_halo, c->stream);
+int launch_mom_records_owned(sph_ctx* c) {  // multi-GPU: halo records come with exchange #3
+  return kIadRecords ? 0 : launch_mom_records_range(c, 0, c->P.n, c->stream);
+}
+
+int launch_mom_records(sph_ctx* c) {  // the sources the IAD epilogue did not write
+  return kIadRecords ? launch_mom_records_range(c, c->P.n, c->n_halo, c->stream)
+                     : launch_mom_records_range(c, 0, c->P.n + c->n_halo, c->stream);
 }
 
 }  // namespace sphb

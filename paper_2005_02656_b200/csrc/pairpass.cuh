@@ -30,7 +30,10 @@ constexpr int kMomCap = 1312;     // momentum: staged 144-byte records per group
 #define SPH_MOM_THREADS 512
 #endif
 constexpr int kCTM = SPH_MOM_THREADS;  // momentum CTA: 16 warps, one CTA per SM (A/B builds override)
-constexpr int kCTD = 1024;        // density / IAD CTA: 32 warps, one CTA per SM
+#ifndef SPH_DENS_THREADS
+#define SPH_DENS_THREADS 1024
+#endif
+constexpr int kCTD = SPH_DENS_THREADS;  // density / IAD CTA: 32 warps, one CTA per SM (A/B builds override)
 constexpr int kNWM = kCTM / 32;
 constexpr int kNWD = kCTD / 32;
 constexpr uint32_t kSent = 0xffffffffu;  // past-the-end row entry

@@ -737,9 +737,9 @@ sph_status sph_momentum_energy(sph_ctx* c, double* dt_out) {
   if (!c) return SPH_ERR_CONFIG;
   if (c->status != SPH_OK) return c->status;
   if (c->stage < 3) return fail(c, SPH_ERR_STATE, "sph_momentum_energy before sph_iad");
-  if (c->P.n) {  // source records of the owned particles (+ halos: with exchange #3 on multi-GPU)
+  if (c->P.n) {  // source records not written by the IAD epilogue (multi-GPU halos: with exchange #3)
     Phase ph(c, SPH_PH_RECORDS);
-    int k = c->dist ? launch_mom_records_range(c, 0, c->P.n, c->stream) : launch_mom_records(c);
+    int k = c->dist ? launch_mom_records_owned(c) : launch_mom_records(c);
     CKL();
     ph.done(k);
   }

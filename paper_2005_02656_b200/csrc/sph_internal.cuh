@@ -180,6 +180,7 @@ int launch_density(sph_ctx* c);
 int launch_iad(sph_ctx* c);
 int launch_momentum(sph_ctx* c);
 int launch_mom_records(sph_ctx* c);
+int launch_mom_records_owned(sph_ctx* c);
 int launch_mom_records_range(sph_ctx* c, int64_t i0, int64_t n, cudaStream_t st);
 int launch_unit_order(sph_ctx* c);
 int launch_dt_finalize(sph_ctx* c, bool nonempty);
