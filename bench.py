@@ -315,11 +315,12 @@ def run_ours(args):
         pass
     phases = {k: round(v / args.steps, 4) for k, v in phase_ms.items() if v}
     # DRAM bytes per launch of the dominant kernel from the committed ncu --set full capture
-    # (profiles/r1_ncu_traffic.json; only for the workload it was captured on)
-    traffic = None
+    # (profiles/r2_ncu_traffic.json; only for the workload and GPU count it was captured on)
+    traffic, traffic_src = None, "profiles/r2_ncu_traffic.json (dram__bytes_read+write, 1 launch)"
     try:
-        tr = json.load(open(os.path.join(ROOT, "profiles", "r1_ncu_traffic.json")))
-        if args.workload == "weak" and world == 1:
+        tr = json.load(open(os.path.join(ROOT, "profiles", "r2_ncu_traffic.json")))
+        if (args.workload == tr.get("workload") and world == 1 and not args.symmetric
+                and args.kernel_mode == "poly"):
             k = tr["kernels"]["k_momentum_c"]
             traffic = k["dram_read_bytes"] + k["dram_write_bytes"]
     except Exception:
@@ -372,7 +373,7 @@ def run_ours(args):
                      "peak": peak64, "unit": "TFLOP/s",
                      "peak_source": "measured live: DFMA kernel (sph_measure_fp64_peak)",
                      "frac": achieved / peak64 if peak64 else None, "traffic": traffic,
-                     "traffic_source": "profiles/r1_ncu_traffic.json (dram__bytes_read+write, 1 launch)",
+                     "traffic_source": traffic_src if traffic is not None else None,
                      "algorithmic_bytes": 4.0 * pairs + 136.0 * n_local,
                      "flops_per_pair": FLOPS_PER_PAIR["momentum"], "pairs_per_launch": pairs,
                      "avg_launch_ms": mom_ms},
