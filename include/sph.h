@@ -63,7 +63,8 @@ enum { SPH_EOS_LINEAR = 0, SPH_EOS_IDEAL = 1 };
  * definition; the grad-h derivative term of Omega uses the exact polynomial in all
  * modes (the oracle evaluates it directly in all modes, reading R12).             */
 enum {
-  SPH_KERNEL_POLY = 0,   /* default: degree-9 polynomial of sinc in t = v^2 on [0,4] (no sqrt) */
+  SPH_KERNEL_POLY = 0,   /* default: degree-8 polynomial of sinc in t = v^2 on [0,4] (no sqrt;
+                          |error| <= 5e-14 on sinc, 3e-13 on sinc^6)                      */
   SPH_KERNEL_TABLE = 1,  /* the paper's table: table_size samples of S_n on [0, 2] incl. both
                             ends, index floor(v (K-1)/2), linear interpolation (R12)  */
   SPH_KERNEL_SIN = 2     /* direct: sin(x)/x, x = pi v / 2, raised to n                      */
@@ -134,6 +135,11 @@ enum {
 };
 
 int         sph_abi_version(void);
+/* The polynomial SPH_KERNEL_POLY evaluates in place of sinc(pi v / 2) of Eq. 6 (the
+ * paper's lookup table): P(t) = sum_k coef[k] t^k, t = v^2 in
+ * [0, 4].  Writes min(cap, n) coefficients to the HOST array coef (may be NULL when
+ * cap = 0) and returns n.  Pure host computation: no context or device needed. */
+int         sph_poly_coefficients(double* coef, int cap);
 /* Create a context: validates params, computes B_n, allocates scratch for `capacity`
  * particles.  *out is NULL on error (the status says why). */
 sph_status  sph_init(const sph_params* params, int64_t capacity, sph_ctx** out);

@@ -46,18 +46,14 @@ __device__ __forceinline__ double sinc_dpoly(double t) {
 // warps per SMSP cannot hide a single chain's DFMA latency (ncu "wait").  Every DFMA
 // takes its coefficient as a constant operand, so no register holds a coefficient
 // (an Estrin tree pairs two constants per DFMA and kept ten of them in registers).
-static_assert(kPolyTerms == 10, "the even/odd split below is written for degree 9");
 __device__ __forceinline__ double sinc_poly_e(double t) {
   const double u = t * t;
-  double e = c_poly[8], o = c_poly[9];
-  e = fma(e, u, c_poly[6]);
-  o = fma(o, u, c_poly[7]);
-  e = fma(e, u, c_poly[4]);
-  o = fma(o, u, c_poly[5]);
-  e = fma(e, u, c_poly[2]);
-  o = fma(o, u, c_poly[3]);
-  e = fma(e, u, c_poly[0]);
-  o = fma(o, u, c_poly[1]);
+  constexpr int te = (kPolyTerms - 1) & ~1, to = (kPolyTerms - 2) | 1;  // top even / odd index
+  double e = c_poly[te], o = c_poly[to];
+#pragma unroll
+  for (int k = te - 2; k >= 0; k -= 2) e = fma(e, u, c_poly[k]);
+#pragma unroll
+  for (int k = to - 2; k >= 1; k -= 2) o = fma(o, u, c_poly[k]);
   return fma(o, t, e);
 }
 // "inline x*x*x*x..."; N > 0 fixes the exponent at compile time

@@ -19,7 +19,10 @@
 
 namespace sphb {
 
-constexpr int kPolyTerms = 10;   // degree-9 polynomial of sinc(pi sqrt(t) / 2) in t = v^2 on [0, 4]
+#ifndef SPH_POLY_TERMS
+#define SPH_POLY_TERMS 9
+#endif
+constexpr int kPolyTerms = SPH_POLY_TERMS;  // degree-8 polynomial of sinc(pi sqrt(t) / 2) in t = v^2 on [0, 4]
 constexpr int kCounters = 8;     // device event counters (see enum below)
 enum { CNT_OMEGA = 0, CNT_IAD_SINGULAR, CNT_COINCIDENT, CNT_U_FLOOR, CNT_H_CLAMP, CNT_NONFINITE };
 

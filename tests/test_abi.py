@@ -46,6 +46,43 @@ def test_library_loads_and_reports_abi(libpath):
         assert hasattr(L, s)
 
 
+def test_kernel_polynomial_within_its_stated_bound(libpath):
+    """SPH_KERNEL_POLY's P(t) against sinc(pi sqrt(t)/2) computed here by numpy (not by
+    the library or the oracle), on a dense grid of the support t in [0, 4]: the bounds
+    sph.h / DESIGN §6 state (5e-14 on sinc, 3e-13 on sinc^6, 2e-12 on the derivative
+    the grad-h term uses), and P(0) = 1, P(4) = sinc(pi) = 0 up to that error."""
+    from paper_2005_02656_b200 import sph
+    L = sph.lib()
+    L.sph_poly_coefficients.argtypes = [ctypes.POINTER(ctypes.c_double), ctypes.c_int]
+    n = L.sph_poly_coefficients(None, 0)
+    assert 8 <= n <= 16
+    c = (ctypes.c_double * n)()
+    assert L.sph_poly_coefficients(c, n) == n
+    import numpy as np
+    c = np.array(c[:])
+    t = np.linspace(0.0, 4.0, 200001)
+    p = np.zeros_like(t)
+    dp = np.zeros_like(t)
+    for k in range(n - 1, -1, -1):
+        p = p * t + c[k]
+    for k in range(n - 1, 0, -1):
+        dp = dp * t + k * c[k]
+    x = 0.5 * np.pi * np.sqrt(t)
+    s = np.sinc(x / np.pi)  # sin(x)/x
+    # d/dt sinc(pi sqrt(t)/2) = (x cos x - sin x) / x^2 * pi / (4 sqrt t); below t = 0.05
+    # that form cancels, so the Taylor series in u = x^2 = pi^2 t / 4 is used there
+    ds = np.zeros_like(t)
+    big = t > 0.05
+    ds[big] = (x[big] * np.cos(x[big]) - np.sin(x[big])) / x[big] ** 2 * np.pi / (4.0 * np.sqrt(t[big]))
+    u = np.pi ** 2 * t[~big] / 4.0
+    fact = [1.0, 6.0, 120.0, 5040.0, 362880.0, 39916800.0, 6227020800.0, 1307674368000.0]
+    ds[~big] = np.pi ** 2 / 4.0 * sum(k * (-1) ** k * u ** (k - 1) / fact[k] for k in range(1, 8))
+    assert np.abs(p - s).max() <= 6e-14
+    assert np.abs(p ** 6 - s ** 6).max() <= 4e-13
+    assert np.abs(dp - ds).max() <= 3e-12
+    assert abs(p[0] - 1.0) <= 6e-14 and abs(p[-1]) <= 6e-14
+
+
 def test_init_rejects_bad_params_without_gpu(libpath):
     """Validation happens before any device call: a bad exponent / ABI is SPH_ERR_CONFIG."""
     from paper_2005_02656_b200 import inputs, sph

@@ -6,6 +6,8 @@ linear momentum and total energy, with pass/fail gates.
     python tools/validate_square_patch.py [--n 100] [--t-end 0.5] [--symmetric 1]
                                           [--h-max-factor 2] [--backend gpu|oracle]
                                           [--out gpurun_out/validation.json]
+    python -m torch.distributed.run --nproc-per-node 4 --master-addr 127.0.0.1 \
+           tools/validate_square_patch.py ...     # the same run decomposed over 4 GPUs
 
 --backend oracle integrates the same initial state with the CPU oracle (test
 infrastructure; oracle/), so a late-time anomaly can be attributed: if the oracle
@@ -31,12 +33,24 @@ sys.path.insert(0, ROOT)
 
 
 class GpuRun:
+    """One GPU, or -- under torchrun (WORLD_SIZE > 1) -- one rank of the SFC-decomposed
+    run: each rank attaches a round-robin subset (the first step migrates), dt and the
+    diagnostics are global (allreduced in the library), KE is summed over ranks."""
+
     def __init__(self, d, kw):
+        import numpy as np
         import torch
 
-        from paper_2005_02656_b200 import sph
-        torch.cuda.set_device(0)
-        self.sim = sph.Simulation(d, **kw)
+        from paper_2005_02656_b200 import dist, inputs, sph
+        self.world, self.rank, local = dist.init("nccl")
+        torch.cuda.set_device(local)
+        if self.world > 1:
+            uid = dist.share_unique_id(self.rank, self.world)
+            mine = inputs.subset(d, np.arange(self.rank, d["x"].size, self.world))
+            cap = int(d["x"].size * 1.2 / self.world) + 200000
+            self.sim = sph.Simulation(mine, capacity=cap, rank=self.rank, nranks=self.world, unique_id=uid, **kw)
+        else:
+            self.sim = sph.Simulation(d, **kw)
 
     def step(self):
         return self.sim.step(want_dt=True)
@@ -47,6 +61,16 @@ class GpuRun:
 
     def state(self):
         return self.sim.state()
+
+    def kinetic(self, s):
+        ke = 0.5 * float((s["m"] * (s["vx"] ** 2 + s["vy"] ** 2 + s["vz"] ** 2)).sum())
+        if self.world > 1:
+            import torch
+            import torch.distributed as tdist
+            t = torch.tensor([ke], dtype=torch.float64, device="cuda")
+            tdist.all_reduce(t)
+            ke = float(t.item())
+        return ke
 
 
 class OracleRun:
@@ -79,6 +103,11 @@ class OracleRun:
 
     def state(self):
         return self.st
+
+    rank, world = 0, 1
+
+    def kinetic(self, s):
+        return 0.5 * float((s["m"] * (s["vx"] ** 2 + s["vy"] ** 2 + s["vz"] ** 2)).sum())
 
 
 def main():
@@ -113,17 +142,21 @@ def main():
         if steps % a.every == 0 or t >= a.t_end:
             p, L, E, _ = run.diag()
             s = run.state()
-            ke = 0.5 * float((s["m"] * (s["vx"] ** 2 + s["vy"] ** 2 + s["vz"] ** 2)).sum())
+            ke = run.kinetic(s)
             rec = {"step": steps, "t": t, "Lz": L[2], "E": E, "KE": ke, "IE": E - ke,
                    "p_rel": [v / m_scale for v in p], "dt": dt}
-            if "rho" in s:
+            if "rho" in s and run.world == 1:
                 rec["rho_min"], rec["rho_max"] = float(np.min(s["rho"])), float(np.max(s["rho"]))
             hist.append(rec)
-            print(json.dumps(rec), flush=True)
+            if run.rank == 0:
+                print(json.dumps(rec), flush=True)
     p, L, E, g = run.diag()
     E10 = E10 if E10 is not None else E0
+    if run.rank != 0:
+        return
     res = {
         "backend": a.backend,
+        "gpus": run.world,
         "config": f"square patch {a.n}^3, pressure-consistent ICs={bool(a.pressure_ics)}, "
                   f"symmetric={a.symmetric}, h_max={kw.get('h_max', 0)}",
         "steps": steps, "t": t, "wall_s": time.time() - t0,
