@@ -5,7 +5,7 @@ python -c "import __graft_entry__ as g; g.build()" > /dev/null 2>&1
 timeout 900 python tools/validate_square_patch.py --n 100 --out gpurun_out/r2_val_mgpu1_100.json > gpurun_out/r2_val_mgpu1_100.log 2>&1
 for G in 2 4; do
   timeout 1200 python -m torch.distributed.run --nnodes=1 --nproc-per-node $G --master-addr 127.0.0.1 --master-port 2971$G \
-    tools/validate_square_patch.py --n 100 --out gpurun_out/r2_val_mgpu${G}_100.json > gpurun_out/r2_val_mgpu${G}_100.log 2>&1
+    tools/validate_square_patch.py --side 100 --out gpurun_out/r2_val_mgpu${G}_100.json > gpurun_out/r2_val_mgpu${G}_100.log 2>&1
 done
 python - <<'PY'
 import json

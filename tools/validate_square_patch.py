@@ -113,7 +113,9 @@ class OracleRun:
 def main():
     from paper_2005_02656_b200 import inputs
     ap = argparse.ArgumentParser()
-    ap.add_argument("--n", type=int, default=100)
+    # --side: the same option under a name torchrun's argument parser does not take
+    # for an abbreviation of its own (--n would match --nnodes / --nproc-per-node)
+    ap.add_argument("--n", "--side", dest="n", type=int, default=100)
     ap.add_argument("--t-end", type=float, default=0.5)
     ap.add_argument("--pressure-ics", type=int, default=1)
     ap.add_argument("--symmetric", type=int, default=0)
