@@ -23,10 +23,14 @@ __device__ __forceinline__ int qidx(const uint32_t* cum, uint32_t gb, uint32_t e
 
 __constant__ double c_poly[kPolyTerms];   // sinc(pi sqrt(t)/2) = sum c_poly[k] t^k
 __constant__ double c_dpoly[kPolyTerms];  // derivative in t
+__constant__ double c_dpoly4[kPolyTerms]; // 4 x the derivative (exact scaling; density at n = 6)
 
 void set_poly_constants(const double* poly, const double* dpoly) {
+  double d4[kPolyTerms];
+  for (int k = 0; k < kPolyTerms; ++k) d4[k] = 4.0 * dpoly[k];
   cudaMemcpyToSymbol(c_poly, poly, sizeof(double) * kPolyTerms);
   cudaMemcpyToSymbol(c_dpoly, dpoly, sizeof(double) * kPolyTerms);
+  cudaMemcpyToSymbol(c_dpoly4, d4, sizeof(double) * kPolyTerms);
 }
 
 __device__ __forceinline__ double sinc_poly(double t) {  // Horner
@@ -39,6 +43,12 @@ __device__ __forceinline__ double sinc_dpoly(double t) {
   double p = c_dpoly[kPolyTerms - 2];
 #pragma unroll
   for (int k = kPolyTerms - 3; k >= 0; --k) p = fma(p, t, c_dpoly[k]);
+  return p;
+}
+__device__ __forceinline__ double sinc_dpoly4(double t) {
+  double p = c_dpoly4[kPolyTerms - 2];
+#pragma unroll
+  for (int k = kPolyTerms - 3; k >= 0; --k) p = fma(p, t, c_dpoly4[k]);
   return p;
 }
 // Even/odd split P(t) = E(t^2) + t O(t^2): two independent Horner chains of depth 4
@@ -63,6 +73,9 @@ __device__ __forceinline__ double ipow(double s, int n) {
     double s2 = s * s;
     double s4 = s2 * s2;
     return s4 * s2;
+  } else if constexpr (N == 5) {
+    double s2 = s * s;
+    return s2 * s2 * s;
   } else if constexpr (N > 0) {
     double r = s;
 #pragma unroll
@@ -345,6 +358,10 @@ __device__ __forceinline__ void delta3(const Stencil& st, const Grid& g, double&
 }
 
 // ------------------------------------------------------------------ a6 density + Omega + EOS
+// n = 6 with the polynomial: the grad-h summand 3 S + v S'(v) = 3 P^5 (P + 4 t P') is
+// accumulated divided by 3 (one FMA on 4 P', whose coefficients are exact multiples)
+template <int KM, int N>
+__host__ __device__ constexpr bool fold3() { return KM == SPH_KERNEL_POLY && N == 6; }
 struct DensBody {
   const double2 *s01, *s23;
   const double *tx, *ty, *tz, *tih2;
@@ -426,13 +443,17 @@ __global__ void __launch_bounds__(kCTD, 1) k_density_c(
               if (W2 && sym) ok = ok && tt < 4.0;  // symmetric extra pair: W(r, h_a) = 0
               const double P = sinc_poly(tt);
               const double Pn1 = ipow<N - 1 < 0 ? 0 : N - 1>(P, n - 1);
-              const double dP = sinc_dpoly(tt);
               const double mj = p23.y;
               double a, b;
-              if constexpr (KM == SPH_KERNEL_POLY) {
+              if constexpr (fold3<KM, N>()) {  // b / 3 = P^5 (P + 4 t P'): 2n = 12 = 3 x 4, 4 P' exact
+                a = Pn1 * P;
+                b = Pn1 * fma(tt, sinc_dpoly4(tt), P);
+              } else if constexpr (KM == SPH_KERNEL_POLY) {
+                const double dP = sinc_dpoly(tt);
                 a = Pn1 * P;
                 b = Pn1 * (3.0 * P + (2.0 * n) * tt * dP);  // 3 S + v S'(v)
               } else {  // S from the selected mode; v S'(v) from the exact polynomial (R12)
+                const double dP = sinc_dpoly(tt);
                 const double S_ = kern_S<KM, N, false>(tt, n, tab, K);
                 a = S_;
                 b = fma(3.0, S_, Pn1 * (2.0 * n) * tt * dP);
@@ -464,7 +485,8 @@ __global__ void __launch_bounds__(kCTD, 1) k_density_c(
           const double ih2a = ih * ih;
           const double wBa = ph.B * ih * ih2a;               // B / h^3
           const double r = wBa * (ma + acc0[i]);             // Eq. 1 incl. self (R11)
-          const double dsum = -wBa * ih * (3.0 * ma + acc1[i]);  // sum m dW/dh
+          // sum m dW/dh (acc1 holds sum m (3 S + v S') / 3 when fold3)
+          const double dsum = fold3<KM, N>() ? -wBa * ih * (3.0 * (ma + acc1[i])) : -wBa * ih * (3.0 * ma + acc1[i]);
           double om = ph.omega_mode ? 1.0 : 1.0 + ha / (3.0 * r) * dsum;  // R8
           if (om < 0.1) {
             om = 0.1;
@@ -872,9 +894,8 @@ __global__ void __launch_bounds__(kCTM, 1) k_momentum_c(
               rinva = r5.x * r8.y;  // (m / rho) / m
               a11 = r5.y; a12 = r6.x; a13 = r6.y; a22 = r7.x; a23 = r7.y; a33 = r8.x;  // C~_a
             }
-            // pair (a, b = staged entry qi): the Eq. 2 / Eq. 3 contributions and v_sig
-            __device__ __forceinline__ void eval(int qi, double& gx, double& gy, double& gz, double& gu,
-                                                 double& vsab, bool& coinc) const {
+            // pair (a, b = staged entry qi): accumulate the Eq. 2 / Eq. 3 terms and v_sig
+            __device__ __forceinline__ void operator()(int qi) {
               const double2* q = F2 + (size_t)qi * kMomPairs;
               const double2 p0 = q[0], p1 = q[1], p3 = q[3];
               double dx = p0.x - xa, dy = p0.y - ya, dz = p1.x - za;
@@ -882,7 +903,8 @@ __global__ void __launch_bounds__(kCTM, 1) k_momentum_c(
               const double r2 = dx * dx + dy * dy + dz * dz;
               // coincident pair: Delta = 0 zeroes every term below; it is only
               // kept out of v_sig and counted (no branch)
-              coinc = r2 == 0.0;
+              const bool coinc = r2 == 0.0;
+              *ncoinc += coinc;
               const double ta = r2 * ih2a;
               // symmetric extra pair (r >= 2 h_a): W(r, h_a) = 0, only the h_b terms remain
               const double Sa = (W2 && sym && !(ta < 4.0)) ? 0.0 : kern_S<KM, N, true>(ta, n, tab, K);
@@ -911,34 +933,24 @@ __global__ void __launch_bounds__(kCTM, 1) k_momentum_c(
 #else
               const double w = vdotx < 0.0 ? vdotx * rsqrt(r2) : 0.0;
 #endif
-              vsab = ca + cb - 3.0 * w;  // v_sig; w == min(w, 0)
+              const double vsab = ca + cb - 3.0 * w;  // v_sig; w == min(w, 0)
               const double hp = -0.25 * alpha * vsab * w;  // Pi'/2, Eq. 5
               // Eq. 2 with R2 and Eq. 4: a += -m_b (X_a A_a + X_b A_b) - g,
               //   g = (Pi'/2) (m_b/rho_a A_a + m_b/rho_b A_b), folded onto u and w
-              const double ka = mb * fma(hp, rinva, Xa) * Wa;
+              vs = (!coinc && vsab > vs) ? vsab : vs;  // a coincident pair stays out of v_sig
+              // accumulated straight into the sums (two FMA per component, no product
+              // temporaries): ka = m_b W_a (X_a + (Pi'/2) / rho_a), kb = (m_b X_b + (Pi'/2) m_b/rho_b) S_b
+              const double mbW = mb * Wa;
+              const double ka = mbW * fma(hp, rinva, Xa);
               const double kb = fma(hp, mrb, mXb) * Sb;
-              gx = fma(ka, ux, kb * wx);
-              gy = fma(ka, uy, kb * wy);
-              gz = fma(ka, uz, kb * wz);
+              fx = fma(-ka, ux, fma(-kb, wx, fx));
+              fy = fma(-ka, uy, fma(-kb, wy, fy));
+              fz = fma(-ka, uz, fma(-kb, wz, fz));
               // Eq. 3 with R1, R3: du += m_b X_a v_ab.A_a + (1/2) v_ab.g
               const double vu = vabx * ux + vaby * uy + vabz * uz;
               const double vw = vabx * wx + vaby * wy + vabz * wz;
-              gu = mb * fma(0.5 * hp, rinva, Xa) * Wa * vu + 0.5 * hp * mrb * Sb * vw;
-            }
-            __device__ __forceinline__ void add(double gx, double gy, double gz, double gu, double vsab,
-                                                bool coinc) {
-              *ncoinc += coinc;  // coincident pair: kept out of v_sig, counted
-              vs = (!coinc && vsab > vs) ? vsab : vs;
-              fx -= gx;
-              fy -= gy;
-              fz -= gz;
-              fu += gu;
-            }
-            __device__ __forceinline__ void operator()(int qi) {
-              double gx, gy, gz, gu, v;
-              bool co;
-              eval(qi, gx, gy, gz, gu, v, co);
-              add(gx, gy, gz, gu, v, co);
+              const double hh = 0.5 * hp;
+              fu = fma(mbW * fma(hh, rinva, Xa), vu, fma(hh * mrb * Sb, vw, fu));
             }
           } body;
           body.F2 = F2; body.mrec = mrec; body.slot = tslot[threadIdx.x >> 4];
