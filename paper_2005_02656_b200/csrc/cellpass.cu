@@ -633,6 +633,13 @@ __global__ void __launch_bounds__(kCTD, 1) k_iad_c(
         for (uint32_t t = t0 + threadIdx.x; t < t1; t += blockDim.x) {
           const uint32_t i = t - t0;
           const double s = wB[t];
+          // the record's per-particle fields, loaded first: their latency overlaps the
+          // inverse below (the ct stores would otherwise order them after it)
+          double rvx = 0.0, rvy = 0.0, rvz = 0.0, rm = 1.0, rc = 0.0, rmX = 0.0, rmr = 0.0;
+          if (mrec) {
+            rvx = rs.vx[t]; rvy = rs.vy[t]; rvz = rs.vz[t]; rm = rs.m[t];
+            rc = rs.c[t]; rmX = rs.mX[t]; rmr = rs.mr[t];
+          }
           const double a11 = acc[0][i] * s, a12 = acc[1][i] * s, a13 = acc[2][i] * s,
                        a22 = acc[3][i] * s, a23 = acc[4][i] * s, a33 = acc[5][i] * s;
           const double det = a11 * (a22 * a33 - a23 * a23) - a12 * (a12 * a33 - a23 * a13) +
@@ -660,16 +667,15 @@ __global__ void __launch_bounds__(kCTD, 1) k_iad_c(
           ct[3 * ct_stride + t] = s * i22; ct[4 * ct_stride + t] = s * i23; ct[5 * ct_stride + t] = s * i33;
           if (mrec) {  // the target's momentum source record (k_mom_records' layout), staged
             double2* r = s01 + (size_t)i * kMomPairs;  // staging buffer is free after the groups
-            const double mm = rs.m[t];
             r[0] = make_double2(tx[i], ty[i]);
-            r[1] = make_double2(tz[i], rs.vx[t]);
-            r[2] = make_double2(rs.vy[t], rs.vz[t]);
-            r[3] = make_double2(mm, tih2[i]);
-            r[4] = make_double2(rs.c[t], rs.mX[t]);
-            r[5] = make_double2(rs.mr[t], s * i11);
+            r[1] = make_double2(tz[i], rvx);
+            r[2] = make_double2(rvy, rvz);
+            r[3] = make_double2(rm, tih2[i]);
+            r[4] = make_double2(rc, rmX);
+            r[5] = make_double2(rmr, s * i11);
             r[6] = make_double2(s * i12, s * i13);
             r[7] = make_double2(s * i22, s * i23);
-            r[8] = make_double2(s * i33, 1.0 / mm);
+            r[8] = make_double2(s * i33, 1.0 / rm);
           }
         }
         if (mrec) {  // the sub-block's records leave in coalesced 16-byte stores

@@ -47,7 +47,7 @@ class GpuRun:
         if self.world > 1:
             uid = dist.share_unique_id(self.rank, self.world)
             mine = inputs.subset(d, np.arange(self.rank, d["x"].size, self.world))
-            cap = int(d["x"].size * 1.2 / self.world) + 200000
+            cap = int(d["x"].size * 2.2 / self.world) + 200000  # first step: own + arrivals + halos
             self.sim = sph.Simulation(mine, capacity=cap, rank=self.rank, nranks=self.world, unique_id=uid, **kw)
         else:
             self.sim = sph.Simulation(d, **kw)
@@ -121,11 +121,15 @@ def main():
     ap.add_argument("--symmetric", type=int, default=0)
     ap.add_argument("--h-max-factor", type=float, default=0.0, help="clamp h at this x the initial h (0: none)")
     ap.add_argument("--backend", default="gpu", choices=["gpu", "oracle"])
+    ap.add_argument("--perturb", type=float, default=0.0,
+                    help="scale x by (1 + eps) before the run: the late-time sensitivity check")
     ap.add_argument("--every", type=int, default=250)
     ap.add_argument("--max-steps", type=int, default=20000)
     ap.add_argument("--out", default=os.path.join(ROOT, "gpurun_out", "validation.json"))
     a = ap.parse_args()
     d = inputs.square_patch(a.n, pressure_ics=bool(a.pressure_ics))
+    if a.perturb:
+        d["x"] = d["x"] * (1.0 + a.perturb)
     kw = {"symmetric": a.symmetric}
     if a.h_max_factor > 0:
         kw["h_max"] = float(a.h_max_factor * d["h"][0])
@@ -160,7 +164,7 @@ def main():
         "backend": a.backend,
         "gpus": run.world,
         "config": f"square patch {a.n}^3, pressure-consistent ICs={bool(a.pressure_ics)}, "
-                  f"symmetric={a.symmetric}, h_max={kw.get('h_max', 0)}",
+                  f"symmetric={a.symmetric}, h_max={kw.get('h_max', 0)}, x perturbed by {a.perturb}",
         "steps": steps, "t": t, "wall_s": time.time() - t0,
         "Lz_t0": L0[2], "Lz_end": L[2], "abs_Lz_end": abs(L[2]),
         "paper_Ltot_t0.5": 8.33e9, "rel_to_paper": abs(L[2]) / 8.33e9 - 1.0,
