@@ -519,7 +519,15 @@ static bool expand_t(sph_ctx* c) {
   if (nw < 1) return false;  // a row stride beyond ~4,000 16-bit entries
   const size_t smem = (size_t)nw * per_warp;
   cudaFuncSetAttribute(k_expand_rows<E>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-  const int64_t blocks = std::min<int64_t>((c->P.n + nw - 1) / nw, (int64_t)c->num_sms * 8);
+  // one wave of resident blocks (a grid-stride loop): num_sms x 8 left a partial second
+  // wave when registers allow only 6 blocks per SM
+  int per_sm = 0;
+  if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_expand_rows<E>, 32 * nw, smem) != cudaSuccess ||
+      per_sm < 1) {
+    cudaGetLastError();
+    per_sm = 1;
+  }
+  const int64_t blocks = std::min<int64_t>((c->P.n + nw - 1) / nw, (int64_t)c->num_sms * per_sm);
   k_expand_rows<E><<<(int)std::max<int64_t>(blocks, 1), 32 * nw, smem, c->stream>>>(
       c->s.nbr, c->P.n, c->s.nseg, c->s.ncount, c->maxn_cap);
   return true;
