@@ -25,7 +25,10 @@
 
 namespace sphb {
 
-constexpr int kCTS = 320;             // search CTA: 10 warps = one 32-target block each per round
+#ifndef SPH_SEARCH_THREADS
+#define SPH_SEARCH_THREADS 320
+#endif
+constexpr int kCTS = SPH_SEARCH_THREADS;  // search CTA: 10 warps = one 32-target block each per round
 constexpr int kNWS = kCTS / 32;
 
 struct TgtW {  // per-target search data (fp32 band + own flat index; the rare exact test
