@@ -250,12 +250,20 @@ __device__ __forceinline__ void walk_targets_half(uint32_t t0, uint32_t t1,
   }
 }
 
-// Lean full-warp walk (density, IAD): the ring of three row chunks is consumed in
-// place -- each step refills the register it just used with the chunk three steps
+// Lean full-warp walk (density, IAD): the ring of RING row chunks is consumed in
+// place -- each step refills the register it just used with the chunk RING steps
 // ahead (a shifted ring makes every move wait for the latest load) -- through a
 // running row pointer, and the body runs on every lane with a validity flag instead
 // of a divergent branch (ncu: per-step bookkeeping was as large as the pair math).
-template <typename E, class Body, class Finish>
+// RING row chunks in flight per warp (4: density -0.1 ms, IAD -0.2 to -0.5 ms vs 3,
+// profiles/r2_ab14_*; IAD stays at its 64-register cap without spills)
+#ifndef SPH_DENS_RING
+#define SPH_DENS_RING 4
+#endif
+#ifndef SPH_IAD_RING
+#define SPH_IAD_RING 4
+#endif
+template <int RING, typename E, class Body, class Finish>
 __device__ __forceinline__ void walk_targets_fast(uint32_t t0, uint32_t t1,
                                                   const E* __restrict__ nbr, int maxn,
                                                   const uint32_t* s_n, const uint32_t* s_cur,
@@ -268,28 +276,30 @@ __device__ __forceinline__ void walk_targets_fast(uint32_t t0, uint32_t t1,
     return __shfl_sync(0xffffffffu, v, 0);
   };
   uint32_t t = claim();
-  uint32_t f0 = kSent, f1 = kSent, f2 = kSent;
+  uint32_t f0 = kSent, f1 = kSent, f2 = kSent, f3 = kSent;
   if (t < t1) {
     const uint32_t c0 = s_cur[t - t0] + lane, nn = s_n[t - t0];
     const E* r = nbr + (size_t)t * maxn;
     f0 = row_chunk(r, c0, nn);
     f1 = row_chunk(r, c0 + 32, nn);
     f2 = row_chunk(r, c0 + 64, nn);
+    if constexpr (RING > 3) f3 = row_chunk(r, c0 + 96, nn);
   }
   while (t < t1) {
     const uint32_t i = t - t0, n = s_n[i];
     uint32_t cur = s_cur[i];
     const uint32_t lim = n - cur;  // valid positions: offset < lim from cur
-    const E* rp = nbr + (size_t)t * maxn + cur + lane + 96;
-    uint32_t off = lane + 96;
-    uint32_t e0 = f0, e1 = f1, e2 = f2;
+    const E* rp = nbr + (size_t)t * maxn + cur + lane + 32 * RING;
+    uint32_t off = lane + 32 * RING;
+    uint32_t e0 = f0, e1 = f1, e2 = f2, e3 = f3;
     const uint32_t tn = claim();
-    if (tn < t1) {  // the next target's first three chunks
+    if (tn < t1) {  // the next target's first RING chunks
       const uint32_t cn = s_cur[tn - t0] + lane, nn = s_n[tn - t0];
       const E* r = nbr + (size_t)tn * maxn;
       f0 = row_chunk(r, cn, nn);
       f1 = row_chunk(r, cn + 32, nn);
       f2 = row_chunk(r, cn + 64, nn);
+      if constexpr (RING > 3) f3 = row_chunk(r, cn + 96, nn);
     }
     // no entry of this target in the group (rows ascend: its first entry is past it):
     // nothing to add, skip the set-up and the reduction (variable h: most visits of a
@@ -316,6 +326,7 @@ __device__ __forceinline__ void walk_targets_fast(uint32_t t0, uint32_t t1,
       SPH_FAST_STEP(e0)
       SPH_FAST_STEP(e1)
       SPH_FAST_STEP(e2)
+      if constexpr (RING > 3) SPH_FAST_STEP(e3)
     }
 #undef SPH_FAST_STEP
     finish(i, cur);
@@ -466,7 +477,7 @@ __global__ void __launch_bounds__(kCTD, 1) k_density_c(
           body.tx = tx; body.ty = ty; body.tz = tz; body.tih2 = tih2;
           body.st = &st; body.g = &g; body.n = n; body.K = ph.tableK; body.tab = ph.table;
           body.sym = ph.sym;
-          walk_targets_fast(t0, t1, nbr, maxn, s_n, s_cur, pend, S.cum, gb, &S.next[gi & 1], body,
+          walk_targets_fast<SPH_DENS_RING>(t0, t1, nbr, maxn, s_n, s_cur, pend, S.cum, gb, &S.next[gi & 1], body,
                             [&](uint32_t i, uint32_t c2) {
                               double v[2] = {body.sr, body.sd};
                               warp_multi_sum<2>(v);
@@ -620,7 +631,7 @@ __global__ void __launch_bounds__(kCTD, 1) k_iad_c(
           body.tx = tx; body.ty = ty; body.tz = tz; body.tih2 = tih2;
           body.st = &st; body.g = &g; body.n = n; body.K = ph.tableK; body.tab = ph.table;
           body.sym = ph.sym;
-          walk_targets_fast(t0, t1, nbr, maxn, s_n, s_cur, pend, S.cum, gb, &S.next[gi & 1], body,
+          walk_targets_fast<SPH_IAD_RING>(t0, t1, nbr, maxn, s_n, s_cur, pend, S.cum, gb, &S.next[gi & 1], body,
                             [&](uint32_t i, uint32_t c2) {
                               double v[8] = {body.t11, body.t12, body.t13, body.t22,
                                              body.t23, body.t33, 0.0, 0.0};
