@@ -178,6 +178,10 @@ __device__ __forceinline__ void walk_targets(uint32_t t0, uint32_t t1, const E* 
 // shifted ring (e0 = e1; e1 = e2 <- load) made every step wait for the load it had
 // just issued (ncu: long_sb on the ring move), and a momentum step is long enough
 // that two chunks of prefetch cover the load latency.
+#ifndef SPH_MOM_RING
+#define SPH_MOM_RING 2
+#endif
+constexpr int kMomRing = SPH_MOM_RING;  // row chunks in flight per half-warp (momentum)
 template <typename E, class Body, class Finish>
 __device__ __forceinline__ void walk_targets_half(uint32_t t0, uint32_t t1,
                                                   const E* __restrict__ nbr, int maxn,
@@ -194,12 +198,13 @@ __device__ __forceinline__ void walk_targets_half(uint32_t t0, uint32_t t1,
     return __shfl_sync(0xffffffffu, v, lane & 16);
   };
   uint32_t t = claim();
-  uint32_t f0 = kSent, f1 = kSent;
+  uint32_t f0 = kSent, f1 = kSent, f2 = kSent;
   if (t < t1) {
     const uint32_t c0 = s_cur[t - t0] + l16, nn = s_n[t - t0];
     const E* r = nbr + (size_t)t * maxn;
     f0 = row_chunk(r, c0, nn);
     f1 = row_chunk(r, c0 + 16, nn);
+    if constexpr (kMomRing > 2) f2 = row_chunk(r, c0 + 32, nn);
   }
   body.fetch(t, par, t < t1);
   while (__any_sync(0xffffffffu, t < t1)) {
@@ -207,16 +212,17 @@ __device__ __forceinline__ void walk_targets_half(uint32_t t0, uint32_t t1,
     const uint32_t i = act ? t - t0 : 0;
     const uint32_t n = act ? s_n[i] : 0;
     uint32_t cur = act ? s_cur[i] : 0;
-    uint32_t off = cur + l16 + 32;  // row position of the next chunk to load (two ahead)
+    uint32_t off = cur + l16 + 16 * kMomRing;  // row position of the next chunk to load (kMomRing ahead)
     const E* rp = nbr + (size_t)(act ? t : 0) * maxn + off;
-    uint32_t e0 = f0, e1 = f1;
+    uint32_t e0 = f0, e1 = f1, e2 = f2;
     const uint32_t tn = claim();
-    f0 = f1 = kSent;
+    f0 = f1 = f2 = kSent;
     if (tn < t1) {
       const uint32_t cn = s_cur[tn - t0] + l16, nn = s_n[tn - t0];
       const E* r = nbr + (size_t)tn * maxn;
       f0 = row_chunk(r, cn, nn);
       f1 = row_chunk(r, cn + 16, nn);
+      if constexpr (kMomRing > 2) f2 = row_chunk(r, cn + 32, nn);
     }
     body.fetch(tn, par ^ 1u, tn < t1);  // the next target's record lands while this one runs
     // (skipping a target with no entry in the group, as the full-warp walk does, hung
@@ -243,6 +249,7 @@ __device__ __forceinline__ void walk_targets_half(uint32_t t0, uint32_t t1,
     for (;;) {
       SPH_HALF_STEP(e0)
       SPH_HALF_STEP(e1)
+      if constexpr (kMomRing > 2) SPH_HALF_STEP(e2)
     }
 #undef SPH_HALF_STEP
     finish(has, i, cur);
