@@ -171,3 +171,17 @@ def test_nonfinite_input_and_dt_reported(S, O):
     with pytest.raises(S.SphError) as e:
         sim.step()
     assert e.value.status == 1
+
+
+def test_wide_rows_unit_stencil_over_65535(S, O, monkeypatch, capfd):
+    """A unit stencil above 65,535 particles cannot be addressed by 16-bit flat indices:
+    the search reports it, the library reallocates 32-bit rows and reruns (R23: rows
+    are never truncated), and every output -- lists, rho, C, a, du, the update -- still
+    matches the oracle.  cell_factor 20 puts a 68,000-particle cloud (~60 neighbours
+    each) in one unit, so the 32-bit instantiations of the search, the row expansion
+    and the three pair passes all run."""
+    monkeypatch.setenv("SPH_DEBUG_ROWS", "1")
+    d = I.random_cloud(68000, box=10.0, h0=0.3, hspread=0.1, periodic=(0, 0, 0), seed=11)
+    per_call_parity(S, O, d, cell_factor=20.0)
+    err = capfd.readouterr().err
+    assert "wide 1" in err, err[-500:]
