@@ -185,3 +185,14 @@ def test_wide_rows_unit_stencil_over_65535(S, O, monkeypatch, capfd):
     per_call_parity(S, O, d, cell_factor=20.0)
     err = capfd.readouterr().err
     assert "wide 1" in err, err[-500:]
+
+
+def test_rows_grow_past_initial_stride(S, O, monkeypatch, capfd):
+    """~700 neighbours per particle: longer than the initial 384-entry row stride, so the
+    search reports the overflow, the rows are reallocated at the larger stride and the
+    search reruns (R23: never truncated); every output matches the oracle."""
+    monkeypatch.setenv("SPH_DEBUG_ROWS", "1")
+    d = I.random_cloud(6000, box=10.0, h0=1.5, hspread=0.1, periodic=(1, 1, 1), seed=5)
+    per_call_parity(S, O, d)
+    err = capfd.readouterr().err
+    assert "rows grow (max count" in err, err[-500:]
