@@ -19,7 +19,10 @@ constexpr int kCT = 256;          // search CTA threads
 constexpr int kNW = kCT / 32;
 constexpr int kTgtU = 416;        // targets per sub-block (a whole 2x2x1 unit, <= 9x9x5 at config 5)
 constexpr int kSlots = kKMax;     // slot tables: every stencil the grid chooser admits
-constexpr int kCellChunk = 4;     // consecutive cells per claim (L2 reuse of shared stencils)
+#ifndef SPH_CELL_CHUNK
+#define SPH_CELL_CHUNK 4
+#endif
+constexpr int kCellChunk = SPH_CELL_CHUNK;  // consecutive cells per claim (L2 reuse of shared stencils)
 constexpr int kSearchCap = 4096;  // staged candidates per group (float4): a unit stencil in one group
 constexpr int kSearchTiles = kSearchCap / 32;
 constexpr int kSearchWords = kSearchTiles / 32;  // tile bitmask words
